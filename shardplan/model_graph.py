@@ -1,0 +1,5 @@
+"""`shardplan.model_graph` -> `paper_2604_26334_b200.planning.graph` (drop-in shim)."""
+from paper_2604_26334_b200.planning.graph import *  # noqa: F401,F403
+from paper_2604_26334_b200.planning import graph as _impl
+
+globals().update({k: v for k, v in vars(_impl).items() if not k.startswith("__")})

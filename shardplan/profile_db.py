@@ -1,0 +1,5 @@
+"""`shardplan.profile_db` -> `paper_2604_26334_b200.planning.costdb` (drop-in shim)."""
+from paper_2604_26334_b200.planning.costdb import *  # noqa: F401,F403
+from paper_2604_26334_b200.planning import costdb as _impl
+
+globals().update({k: v for k, v in vars(_impl).items() if not k.startswith("__")})
