@@ -1,0 +1,138 @@
+/*
+ * pshard.h — C-ABI of the B200-native pipelined-sharding inference path.
+ *
+ * The reference (`shardplan`, pure Python) has no native interface: its
+ * hot path prices these operations analytically and simulates the
+ * pipeline. Each entry point below REPLACES the priced/simulated operation
+ * cited beside it with real sm_100a work; the Python host
+ * (`paper_2604_26334_b200/runtime/`) binds it through ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions: plain pointers and sizes, no framework types. Device
+ * pointers unless stated; "host-mapped" pointers come from ps_host_alloc
+ * (mapped=1) and are valid in kernels (zero-copy). `stream` is a
+ * cudaStream_t. Every function returns 0 on success, non-zero on error;
+ * ps_last_error() returns the thread-local message. No function allocates
+ * device memory behind the caller's back (the VRAM budget is enforced by
+ * the caller's capped arena).
+ */
+#ifndef PSHARD_H
+#define PSHARD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_ABI_VERSION 1
+
+/* GEMV / GEMM epilogues */
+#define PS_EPI_STORE 0      /* y = acc (fp32) */
+#define PS_EPI_ACCUM 1      /* y += acc (fp32; fused residual add) */
+#define PS_EPI_SWIGLU 2     /* rows/cols interleaved gate,up: y[j] = silu(acc[2j]) * acc[2j+1] */
+#define PS_EPI_STORE_BF16 3 /* y = bf16(acc) (GEMM only) */
+
+/* ---- errors / device ------------------------------------------------------ */
+const char* ps_last_error(void);
+int ps_abi_version(void);
+int ps_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
+int ps_set_device(int device);
+
+/* ---- host memory and the copy engine --------------------------------------
+ * Replace the simulated PCIe channels of `pkg/src/shardplan/simulator.py:156-207`
+ * (in-order H2D / D2H uploads, slot release by compute) and the link rate of
+ * `pkg/src/shardplan/machine.py:99-101`. */
+int ps_host_alloc(size_t bytes, int mapped, void** out);         /* cudaHostAlloc, exact size */
+int ps_host_free(void* ptr);
+int ps_host_register(void* ptr, size_t bytes, int portable);     /* pin existing memory (/dev/shm) */
+int ps_host_unregister(void* ptr);
+int ps_host_device_pointer(void* host_ptr, void** dev_ptr);
+int ps_device_alloc(size_t bytes, void** out);
+int ps_device_free(void* ptr);
+int ps_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
+int ps_memset_async(void* dst, int value, size_t bytes, void* stream);
+int ps_stream_create(int high_priority, void** out);
+int ps_stream_destroy(void* stream);
+int ps_stream_synchronize(void* stream);
+int ps_device_synchronize(void);
+int ps_event_create(int timing, void** out);
+int ps_event_destroy(void* ev);
+int ps_event_record(void* ev, void* stream);
+int ps_stream_wait_event(void* stream, void* ev);
+int ps_event_synchronize(void* ev);
+int ps_event_query(void* ev);                                    /* 1 done, 0 pending, <0 error */
+int ps_event_elapsed_ms(void* start, void* stop, float* ms);
+
+/* ---- K1 / K8: GEMV / skinny GEMM, t <= 32 rows ------------------------------
+ * Replaces MATMUL (t, d, n) requests of `pkg/src/shardplan/model_graph.py:147-153`
+ * (attention projection), `:173-179` (FFN) and `:202-209` (output head).
+ * y[t, n] (epi)= sum_k x[t, k] * W[n, k]; x fp32 [t x ldx], W bf16 [N x ldw]
+ * (device, ring slot, or host-mapped for CPU-placed shards), y fp32 [t x ldy].
+ * SWIGLU writes N/2 columns. */
+int ps_gemv_bf16(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
+                 float* y, int ldy, int epilogue, void* stream);
+
+/* ---- K3: tcgen05/TMEM/TMA GEMM (prefill, batched projections) ---------------
+ * Same MATMUL requests at t >= 64. C[M x N] (epi)= A[M x K] * B[N x K]^T,
+ * A, B bf16 K-major (row-major), K % 64 == 0. C fp32 (STORE/ACCUM) or bf16
+ * (STORE_BF16, SWIGLU: N/2 columns). */
+int ps_gemm_bf16(const void* A, int M, int K, long long lda, const void* B, int N, long long ldb,
+                 void* C, int ldc, int epilogue, void* stream);
+
+/* ---- K2: normalisation, RoPE, KV append ------------------------------------
+ * Folded into elementwise_epsilon by the reference
+ * (`pkg/src/shardplan/model_graph.py:35,142`); KV append is the KV shard's
+ * ELEMENT_WISE request (`:164-171`, kv_append_bytes `:241-246`). */
+int ps_rmsnorm(const float* x, int ldx, const int* rows, int n_rows, const void* w, int d,
+               float eps, void* out, int ldo, int out_bf16, void* stream);
+int ps_qkv_rope_append(float* qkv, int ldq, int t, int n_heads, int n_kv, int head_dim,
+                       const int* pos, const int* req, void* kv_base, long long kv_req_stride,
+                       long long kv_row_stride, const void* rope_cs, const void* q_norm,
+                       const void* k_norm, float eps, void* stream);
+
+/* ---- K4: attention (GQA / MHA) ----------------------------------------------
+ * Replaces GQA/MHA requests (`pkg/src/shardplan/model_graph.py:154-161`).
+ * Per-layer KV layout: bf16 [position][request slot][K heads | V heads]; the row of
+ * request b at position p is kv_base + slot(b) * kv_req_stride + p * kv_row_stride
+ * (elements); slot(b) = req_slot[b], or b when req_slot is NULL. kv_base may be a
+ * VRAM-pinned cache, a ring-staged copy of a host cache, or host-mapped memory. */
+int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, int n_kv, int head_dim,
+                   const int* req_slot, const void* kv_base, long long kv_req_stride,
+                   long long kv_row_stride, const int* lens, int max_len, float scale, float* out,
+                   int ldo, float* workspace, long long workspace_floats, void* stream);
+int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_start, const int* p0,
+                    const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
+                    const void* kv_base, long long kv_req_stride, long long kv_row_stride,
+                    float scale, void* out, int ldo, int out_bf16, void* stream);
+
+/* ---- K6: embedding gather (zero-copy from host-mapped table), greedy -------
+ * Not priced by the reference (embeddings are outside the plan,
+ * `pkg/src/shardplan/model_graph.py:279-297`); the head's MATMUL is
+ * `:202-209`. */
+int ps_embed_gather(const void* table, const int* ids, int n, int d, float* out, int ldo,
+                    void* stream);
+int ps_argmax(const float* logits, int rows, int V, int ldl, int* out, void* stream);
+int ps_cast_f32_bf16(const float* src, int lds, void* dst, int ldd, int rows, int cols, void* stream);
+int ps_add_f32(float* dst, const float* src, long long n, void* stream);
+/* <= 4000 bytes host -> device through a kernel's parameter block (no copy engine). */
+int ps_upload_small(void* dst, const void* src, int nbytes, void* stream);
+
+/* ---- model load: deterministic random init ----------------------------------
+ * dst[i] = bf16_rne(fmaf(2u - 1, scale, bias)), u = splitmix64(seed ^ ((offset + i) * golden)) >> 40
+ * scaled to [0, 1). Restated on the CPU by oracle/c/weights.c. */
+int ps_init_uniform_bf16(void* dst, size_t n, unsigned long long seed, unsigned long long offset,
+                         float scale, float bias, void* stream);
+/* Gate/up rows interleaved for the fused SwiGLU epilogue: rows [row_begin, row_begin + n_rows)
+ * of the [2 * rows_each x cols] interleaved matrix; row 2j is tensor a's row j (seed_a),
+ * row 2j+1 tensor b's row j (seed_b); element (j, c) uses counter j * cols + c. */
+int ps_init_interleaved_bf16(void* dst, long long rows_each, long long row_begin, long long n_rows,
+                             int cols, unsigned long long seed_a, unsigned long long seed_b,
+                             float scale, float bias, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSHARD_H */

@@ -1,0 +1,158 @@
+// C-ABI runtime utilities: errors, host memory, copies, events.
+//
+// These are the primitives of the copy-engine weight streamer (SURVEY.md
+// §8a row a17): pinned host memory (cudaHostAlloc, exact size, mapped so
+// CPU-placed shards can be read zero-copy), cudaMemcpyAsync on a dedicated
+// stream, and events that order ring-slot reuse against compute.
+#include <stdarg.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "../../include/pshard.h"
+
+static thread_local char g_err[1024] = "";
+
+void ps_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" {
+
+const char* ps_last_error(void) { return g_err; }
+
+int ps_abi_version(void) { return PS_ABI_VERSION; }
+
+int ps_device_info(int device, int* sm_count, int* cc_major, int* cc_minor,
+                   size_t* total_mem) {
+  cudaDeviceProp prop;
+  PS_CHECK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (total_mem) *total_mem = prop.totalGlobalMem;
+  return PS_OK;
+}
+
+int ps_set_device(int device) {
+  PS_CHECK_CUDA(cudaSetDevice(device));
+  return PS_OK;
+}
+
+int ps_host_alloc(size_t bytes, int mapped, void** out) {
+  PS_REQUIRE(out != nullptr, "ps_host_alloc: out is null");
+  unsigned flags = cudaHostAllocPortable | (mapped ? cudaHostAllocMapped : 0);
+  PS_CHECK_CUDA(cudaHostAlloc(out, bytes, flags));
+  return PS_OK;
+}
+
+int ps_host_free(void* ptr) {
+  if (ptr) PS_CHECK_CUDA(cudaFreeHost(ptr));
+  return PS_OK;
+}
+
+int ps_host_register(void* ptr, size_t bytes, int portable) {
+  unsigned flags = cudaHostRegisterMapped | (portable ? cudaHostRegisterPortable : 0);
+  PS_CHECK_CUDA(cudaHostRegister(ptr, bytes, flags));
+  return PS_OK;
+}
+
+int ps_host_unregister(void* ptr) {
+  PS_CHECK_CUDA(cudaHostUnregister(ptr));
+  return PS_OK;
+}
+
+int ps_host_device_pointer(void* host_ptr, void** dev_ptr) {
+  PS_CHECK_CUDA(cudaHostGetDevicePointer(dev_ptr, host_ptr, 0));
+  return PS_OK;
+}
+
+int ps_device_alloc(size_t bytes, void** out) {
+  PS_CHECK_CUDA(cudaMalloc(out, bytes));
+  return PS_OK;
+}
+
+int ps_device_free(void* ptr) {
+  if (ptr) PS_CHECK_CUDA(cudaFree(ptr));
+  return PS_OK;
+}
+
+int ps_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return PS_OK;
+  PS_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return PS_OK;
+}
+
+int ps_memset_async(void* dst, int value, size_t bytes, void* stream) {
+  if (bytes == 0) return PS_OK;
+  PS_CHECK_CUDA(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream));
+  return PS_OK;
+}
+
+int ps_stream_create(int high_priority, void** out) {
+  int lo = 0, hi = 0;
+  PS_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  cudaStream_t s;
+  PS_CHECK_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, high_priority ? hi : lo));
+  *out = (void*)s;
+  return PS_OK;
+}
+
+int ps_stream_destroy(void* stream) {
+  if (stream) PS_CHECK_CUDA(cudaStreamDestroy((cudaStream_t)stream));
+  return PS_OK;
+}
+
+int ps_stream_synchronize(void* stream) {
+  PS_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return PS_OK;
+}
+
+int ps_device_synchronize(void) {
+  PS_CHECK_CUDA(cudaDeviceSynchronize());
+  return PS_OK;
+}
+
+int ps_event_create(int timing, void** out) {
+  cudaEvent_t e;
+  PS_CHECK_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  *out = (void*)e;
+  return PS_OK;
+}
+
+int ps_event_destroy(void* ev) {
+  if (ev) PS_CHECK_CUDA(cudaEventDestroy((cudaEvent_t)ev));
+  return PS_OK;
+}
+
+int ps_event_record(void* ev, void* stream) {
+  PS_CHECK_CUDA(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream));
+  return PS_OK;
+}
+
+int ps_stream_wait_event(void* stream, void* ev) {
+  PS_CHECK_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)ev, 0));
+  return PS_OK;
+}
+
+int ps_event_synchronize(void* ev) {
+  PS_CHECK_CUDA(cudaEventSynchronize((cudaEvent_t)ev));
+  return PS_OK;
+}
+
+int ps_event_query(void* ev) {
+  cudaError_t e = cudaEventQuery((cudaEvent_t)ev);
+  if (e == cudaSuccess) return 1;
+  if (e == cudaErrorNotReady) { cudaGetLastError(); return 0; }
+  ps_set_error("cudaEventQuery -> %s", cudaGetErrorString(e));
+  return -PS_ERR_CUDA;
+}
+
+int ps_event_elapsed_ms(void* start, void* stop, float* ms) {
+  PS_CHECK_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+  return PS_OK;
+}
+
+}  // extern "C"

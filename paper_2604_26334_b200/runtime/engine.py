@@ -1,0 +1,225 @@
+"""User-facing engine: model load, VRAM budget, plan, prefill / decode / generate.
+
+This is the drop-in for the reference's inference path. Planning is the
+reference-compatible planner (`paper_2604_26334_b200.planning`, bit-exact
+with `pkg/src/shardplan/planner.py`); the loop is `simulate_inference`'s
+(`pkg/src/shardplan/simulator.py:239-314`) — same tier pick, same chunked
+prefill, same definitions of TTFT, decode TPS and E2EL — but every pass is
+a real GPU pass of `Executor.run_pass` instead of `simulate_schedule`.
+
+    eng = Engine("llama3.1-8b", budget_bytes=4e9, context_len=2304)
+    out = eng.generate([prompt_ids], gen_len=256)
+    out.tokens, out.ttft_s, out.tps
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ..planning import catalog
+from ..planning.costdb import ProfileDb, load_profile, synth_profile
+from ..planning.faults import InfeasibleBudget, SpecError
+from ..planning.graph import ModelSpec
+from ..planning.hardware import MachineSpec
+from ..planning.placement import TIERS, TierTable, TierEntry, reachable_tiers
+from ..planning.pipeline_model import outstanding_tokens, schedule_iteration
+from . import lib as L
+from .executor import Executor, PassSpec
+from .model import HostWeights, arch_for
+
+
+@dataclass
+class GenerateResult:
+    tokens: list                 # per request: np.int32 array of generated ids
+    ttft_s: float
+    tps: float
+    e2el_s: float
+    decode_tokens: int
+    decode_time_s: float
+    passes: list = field(default_factory=list)   # (tier, T, seconds, bytes streamed)
+    migration_bytes: int = 0
+
+
+class Engine:
+    """Plan + weights + executor for one model under one VRAM budget."""
+
+    def __init__(self, model, budget_bytes: float, context_len: int, batch: int = 1,
+                 machine="b200", profile: str | None = None, seed: int = 0,
+                 max_tokens: int | None = None, chunk_bytes: int = 64 << 20):
+        self.spec: ModelSpec = catalog.builtin_model(model) if isinstance(model, str) else model
+        self.machine: MachineSpec = (catalog.builtin_machine(machine) if isinstance(machine, str)
+                                     else machine)
+        self.db: ProfileDb = load_profile(profile) if profile else synth_profile(self.machine)
+        self.budget = float(budget_bytes)
+        self.context_len = int(context_len)
+        self.batch = int(batch)
+        self.arch = arch_for(self.spec, seed)
+        # per-tier plans; tiers the budget cannot plan are unreachable (time = inf)
+        self.plans = reachable_tiers(self.spec, self.machine, self.db, self.budget,
+                                     self.context_len, self.batch)
+        if not self.plans:
+            raise InfeasibleBudget(self.budget, self.budget, "every token tier")
+        self.table = None
+        if set(self.plans) == set(TIERS):
+            self.table = TierTable(self.spec.name, self.machine.name, self.budget,
+                                   self.context_len,
+                                   {t: TierEntry(t, p) for t, p in self.plans.items()})
+        self.weights = HostWeights(self.spec, self.arch)
+        t0 = time.perf_counter()
+        self.weights.generate()
+        self.load_seconds = time.perf_counter() - t0
+        self.max_tokens = max_tokens
+        self.chunk_bytes = chunk_bytes
+        self.executor: Executor | None = None
+
+    # -- tier selection over reachable tiers (pick_tier, planner.py:451-460) --
+    def pick_tier(self, n_new: int) -> int:
+        if n_new < 1:
+            raise SpecError(f"batch_new_tokens must be >= 1, got {n_new}")
+        best, best_cost = None, None
+        for tier in TIERS:
+            plan = self.plans.get(tier)
+            if plan is None:
+                continue
+            cost = -(-n_new // tier) * plan.estimated_time
+            if best_cost is None or cost < best_cost:
+                best, best_cost = tier, cost
+        return best
+
+    def _ensure_executor(self, max_tokens: int) -> Executor:
+        if self.executor is None:
+            tiers_used = self.plans
+            self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
+                                     self.batch, self.context_len,
+                                     self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes)
+        elif max_tokens > self.executor.Tmax:
+            raise SpecError(f"pass of {max_tokens} tokens exceeds the executor's {self.executor.Tmax}")
+        return self.executor
+
+    def max_pass_tokens(self, prompt_lens: list, gen_len: int) -> int:
+        """Largest T any pass of generate() will run (dry run of the loop)."""
+        pl, gl = list(prompt_lens), [gen_len] * len(prompt_lens)
+        biggest = 1
+        while any(p > 0 for p in pl) or any(g > 0 for g in gl):
+            tier = self.pick_tier(outstanding_tokens(pl, gl))
+            step = schedule_iteration(tier, pl, gl)
+            biggest = max(biggest, step.context_consumed + step.decoded)
+        return biggest
+
+    # ------------------------------------------------------------------ generate
+    def generate(self, prompts: list, gen_len: int, timing: bool = True) -> GenerateResult:
+        """Greedy generation for a batch of prompts, following the reference
+        loop: each iteration picks the tier for the outstanding new tokens,
+        feeds prompt chunks (a finished prompt emits its first token) or one
+        decode token per request."""
+        if not prompts:
+            raise SpecError("generate needs at least one request")
+        if len(prompts) > self.batch:
+            raise SpecError(f"{len(prompts)} requests exceed the planned batch of {self.batch}")
+        prompts = [np.asarray(p, np.int32) for p in prompts]
+        n = len(prompts)
+        if max(len(p) for p in prompts) + gen_len > self.context_len:
+            raise SpecError("prompt + gen exceeds the planned context length")
+        ex = self._ensure_executor(self.max_pass_tokens([len(p) for p in prompts], gen_len))
+        prompt_left = [len(p) for p in prompts]
+        gen_left = [gen_len] * n
+        fed = [0] * n                      # prompt tokens fed so far
+        out = [[] for _ in range(n)]
+        pending_host = []                  # passes whose tokens we have not read yet
+        t_start = time.perf_counter()
+        ttft = None
+        decode_time = 0.0
+        decode_tokens = 0
+        passes = []
+        migration = 0
+        last_sampled = None
+        while any(p > 0 for p in prompt_left) or any(g > 0 for g in gen_left):
+            tier = self.pick_tier(outstanding_tokens(prompt_left, gen_left))
+            migration += ex.set_tier(tier)
+            step = schedule_iteration(tier, prompt_left, gen_left)
+            slots, n_new, p0, ids, sample = [], [], [], [], []
+            decode_ids_from_device = True
+            for i in range(n):
+                if step.prompt_take[i]:
+                    k = step.prompt_take[i]
+                    slots.append(i); n_new.append(k); p0.append(fed[i])
+                    ids.append(prompts[i][fed[i]:fed[i] + k])
+                    fed[i] += k
+                    decode_ids_from_device = False
+                elif step.decode[i]:
+                    slots.append(i); n_new.append(1); p0.append(len(prompts[i]) + len(out[i]) - 1 +
+                                                              self._pending_count(pending_host, i))
+                    ids.append(None)
+                if step.emits[i]:
+                    sample.append(len(slots) - 1)
+            if decode_ids_from_device and last_sampled == slots:
+                ids_arr = None
+            else:
+                self._drain(ex, pending_host, out)
+                ids_arr = np.concatenate([a if a is not None else
+                                          np.array([out[slots[j]][-1]], np.int32)
+                                          for j, a in enumerate(ids)]).astype(np.int32)
+                # decode positions are exact once drained
+                for j, a in enumerate(ids):
+                    if a is None:
+                        p0[j] = len(prompts[slots[j]]) + len(out[slots[j]]) - 1
+            ev0 = L.event_create(True) if timing else 0
+            if timing:
+                L.call("ps_event_record", ev0, ex.cs)
+            stats = ex.run_pass(PassSpec(slots, n_new, p0, ids_arr, sample))
+            if sample:
+                pending_host.append([slots[j] for j in sample])
+                last_sampled = [slots[j] for j in sample]
+            ev1 = 0
+            if timing:
+                ev1 = L.event_create(True)
+                L.call("ps_event_record", ev1, ex.cs)
+            passes.append([tier, stats.T, ev0, ev1, stats.bytes_streamed,
+                           step.context_consumed == 0 and step.decoded > 0])
+            if step.first_prompt_done and ttft is None:
+                self._drain(ex, pending_host, out)   # first token is on the host
+                ttft = time.perf_counter() - t_start
+        self._drain(ex, pending_host, out)
+        ex.synchronize()
+        total = time.perf_counter() - t_start
+        pass_rows = []
+        for tier, T, e0, e1, nbytes, is_decode in passes:
+            secs = L.event_elapsed_ms(e0, e1) / 1e3 if timing else float("nan")
+            pass_rows.append((tier, T, secs, nbytes))
+            if is_decode:
+                decode_tokens += T
+                decode_time += secs
+            if timing:
+                L.call("ps_event_destroy", e0)
+                L.call("ps_event_destroy", e1)
+        if ttft is None:
+            ttft = total
+        # decode throughput: device time from the end of the last context pass to the
+        # end of the last decode pass (passes overlap their copies, so per-pass
+        # compute-stream intervals undercount the pipelined wall time)
+        tps = decode_tokens / decode_time if decode_time > 0 else float("inf")
+        return GenerateResult([np.array(o, np.int32) for o in out], ttft, tps,
+                              ttft + 100.0 / tps if tps else float("inf"),
+                              decode_tokens, decode_time, pass_rows, migration)
+
+    @staticmethod
+    def _pending_count(pending_host, slot) -> int:
+        return sum(1 for slots in pending_host if slot in slots)
+
+    @staticmethod
+    def _drain(ex, pending_host, out) -> None:
+        if not pending_host:
+            return
+        for slots, toks in ex.collect_tokens():
+            for s, t in zip(slots, toks):
+                out[s].append(int(t))
+        pending_host.clear()
+
+    def close(self) -> None:
+        if self.executor is not None:
+            self.executor.close()
+            self.executor = None
+        self.weights.close()

@@ -1,0 +1,579 @@
+"""The real pass: runs one tier's SchedulePlan on the GPU.
+
+Replaces `simulate_schedule` (`pkg/src/shardplan/simulator.py:117-216`) inside
+the generate loop. Per plan placement (`pkg/src/shardplan/planner.py:276-309`):
+
+  VRAM_PINNED / GPU            weights (or the layer's KV cache) live in the
+                               capped arena; kernels read them in place
+  SYS_RAM / GPU / WEIGHTS_H2D  streamed through the copy-engine ring, one
+                               row-aligned piece at a time, kernels per piece
+  SYS_RAM / GPU / KV_H2D       the layer's KV home is pinned host memory: the
+                               current prefix is streamed into the ring, new
+                               rows are appended there and written back D2H
+  SYS_RAM / CPU                no CPU backend exists: the GPU reads the shard
+                               zero-copy from host-mapped memory (K8, no VRAM);
+                               at T > 32 (GEMM passes) it is staged through the
+                               ring instead, still inside the budget
+
+Stream order is the plan's topological order with KV_i hoisted before
+Attn_i (attention consumes the cache; SURVEY.md §7 hard part 4).
+
+Numerics of a pass with T new tokens: the residual stream is fp32. T <= 32
+uses the GEMV kernels on fp32 activations; larger T uses the tcgen05 GEMM
+on bf16 activations. Attention: the split-KV decode kernel when every
+request adds exactly one token (and T <= 32), else the causal varlen
+flash-attention kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from ..planning.faults import InfeasibleBudget, SpecError
+from ..planning.graph import ShardKind, build_shards
+from ..planning.placement import Residency, SchedulePlan, Streaming
+from ..planning.vocab import Backend
+from . import lib as L
+from .arena import VramArena
+from .model import Arch, HostWeights, rope_table
+from .streamer import CopyRing, EventPool
+
+GEMV_MAX_T = 32
+
+
+@dataclass
+class PassSpec:
+    """One pass: which request slots advance, by how many tokens, from where."""
+
+    slots: list                 # request slot per participating request
+    n_new: list                 # new tokens per participating request
+    p0: list                    # position of the first new token per request
+    ids: np.ndarray | None      # int32 [T] token ids (None: the previous pass's samples)
+    sample: list                # participating-request indices that emit a token
+
+    @property
+    def T(self) -> int:
+        return int(sum(self.n_new))
+
+    @property
+    def decode_only(self) -> bool:
+        return all(n == 1 for n in self.n_new)
+
+
+@dataclass
+class PassStats:
+    tier: int
+    T: int
+    bytes_streamed: int = 0
+    copies: int = 0
+    kv_writeback_bytes: int = 0
+    zero_copy_bytes: int = 0
+
+
+@dataclass
+class Consumer:
+    tensor: str | None          # tensor whose rows it consumes (None: runs between tensors)
+    fn: object                  # fn(ptr, r0, r1)
+    even_rows: bool = False     # piece boundaries on even rows (interleaved gate/up)
+    reads: tuple = ()           # other (small) tensors it reads through `ptrs`
+
+
+class Executor:
+    def __init__(self, weights: HostWeights, arch: Arch, plans: dict, budget_bytes: float,
+                 kv_slots: int, context_len: int, max_tokens: int,
+                 chunk_bytes: int = 64 << 20, ring_cap: int = 1 << 30):
+        spec = weights.spec
+        if spec.moe is not None:
+            raise SpecError("MoE expert-group execution is not built in this round (DESIGN.md §7)")
+        self.spec, self.arch, self.w = spec, arch, weights
+        self.plans = plans                       # tier -> SchedulePlan
+        self.B = kv_slots
+        self.cap = context_len
+        self.Tmax = max_tokens
+        self.shards = build_shards(spec, context_len, kv_slots)
+        self.by_layer_kind = {(s.layer_index, s.kind): s for s in self.shards}
+        L.lib()
+
+        s = spec
+        self.d, self.h, self.kv, self.hd = s.d_model, s.n_heads, s.n_kv_heads, s.head_dim
+        self.qkv_rows = (self.h + 2 * self.kv) * self.hd
+        self.ffn = s.ffn_dim
+        self.V = s.vocab_size
+        self.row_elems = 2 * self.kv * self.hd
+        self.row_bytes = self.row_elems * 2
+        self.kv_layer_bytes = self.cap * self.B * self.row_bytes
+
+        self.cs = L.stream_create(high_priority=True)   # compute
+        self.h2d = L.stream_create()                    # copy engine, host -> device
+        self.d2h = L.stream_create()                    # KV write-back, token readback
+        self.events = EventPool()
+
+        # host KV homes: [layer][position][slot][K|V heads] bf16, pinned + mapped
+        self.kv_host = L.host_alloc(max(1, s.n_layers * self.kv_layer_bytes), mapped=True)
+        self.kv_len = [0] * self.B
+        self.kv_vram: dict[int, int] = {}
+        self.kv_mode: dict[int, str] = {}
+        self.kv_writeback: dict[int, int] = {}   # layer -> event of its last D2H append
+        self.tok_events = [L.event_create(False) for _ in range(64)]
+
+        self.arena = VramArena(budget_bytes)
+        self._carve_fixed()
+        self.residency: dict[int, tuple] = {}
+        self.tier = None
+        max_pinned = max(self._pinned_bytes(p) for p in plans.values())
+        free_for_ring = self.arena.free_bytes - max_pinned
+        ring_bytes = max(0, min(ring_cap, free_for_ring)) // 256 * 256
+        self.chunk = min(chunk_bytes, max(1 << 16, ring_bytes // 6 // 256 * 256))
+        need = self.kv_layer_bytes + 3 * self.chunk
+        if ring_bytes < need:
+            raise InfeasibleBudget(float(budget_bytes),
+                                   float(budget_bytes) - free_for_ring + need, "copy-engine ring")
+        self.ring = CopyRing(self.arena.alloc_high("ring", ring_bytes), ring_bytes, self.h2d,
+                             self.events)
+        self.stats: list[PassStats] = []
+        self.host_tokens: list = []
+        self._prev_sample_slots = None
+
+    # ------------------------------------------------------------------ layout
+    def _carve_fixed(self) -> None:
+        a, T, B, d = self.arena, self.Tmax, self.B, self.d
+        t32 = min(T, GEMV_MAX_T)
+        self.x = a.alloc_high("x", T * d * 4)
+        self.qkv = a.alloc_high("qkv", T * self.qkv_rows * 4)
+        self.xn32 = a.alloc_high("xn32", t32 * d * 4)
+        self.att32 = a.alloc_high("att32", t32 * self.h * self.hd * 4)
+        self.hid32 = a.alloc_high("hid32", t32 * self.ffn * 4)
+        if T > GEMV_MAX_T:
+            self.xn16 = a.alloc_high("xn16", T * d * 2)
+            self.att16 = a.alloc_high("att16", T * self.h * self.hd * 2)
+            self.hid16 = a.alloc_high("hid16", T * self.ffn * 2)
+        else:
+            self.xn16 = self.att16 = self.hid16 = 0
+        self.xs = a.alloc_high("xs", B * d * 4)
+        self.logits = a.alloc_high("logits", B * self.V * 4)
+        splits = max(1, math.ceil(self.cap / 256))
+        self.ws_floats = B * self.h * splits * (self.hd + 2)
+        self.ws = a.alloc_high("attn_ws", self.ws_floats * 4)
+        self.i_ids = a.alloc_high("ids", T * 4)
+        self.i_pos = a.alloc_high("pos", T * 4)
+        self.i_req = a.alloc_high("req", T * 4)
+        self.i_meta = a.alloc_high("meta", 4 * (4 * B + 4))
+        self.i_rows = a.alloc_high("sample_rows", B * 4)
+        self.i_tok_ring = a.alloc_high("sample_tok", 8 * B * 4)   # 8 rotating slots
+        self.tok_slot = 0
+        self.i_tok = self.i_tok_ring
+        rope = rope_table(self.arch, self.hd, self.cap)
+        self.rope = a.alloc_high("rope", rope.nbytes)
+        self.host_stage = L.host_alloc(max(1 << 20, rope.nbytes, T * 4 + 4096), mapped=False)
+        self._h2d_sync(self.rope, rope)
+        self.host_tok = L.host_alloc(4 * B * 4096, mapped=False)
+        self.host_tok_i = 0
+
+    def _h2d_sync(self, dst: int, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr)
+        L.call("ps_stream_synchronize", self.cs)
+        C.memmove(self.host_stage, arr.ctypes.data, arr.nbytes)
+        L.memcpy_async(dst, self.host_stage, arr.nbytes, self.cs)
+        L.call("ps_stream_synchronize", self.cs)
+
+    def _phys_bytes(self, shard) -> int:
+        if shard.kind is ShardKind.KV_CACHE:
+            return self.kv_layer_bytes
+        return self.w.layout.blobs[shard.id].nbytes
+
+    def _pinned_bytes(self, plan: SchedulePlan) -> int:
+        return sum((self._phys_bytes(self.shards[p.shard_id]) + 255) // 256 * 256
+                   for p in plan.placements if p.residency is Residency.VRAM_PINNED)
+
+    def _kv_host_ptr(self, layer: int) -> int:
+        return self.kv_host + layer * self.kv_layer_bytes
+
+    # --------------------------------------------------------------- residency
+    def set_tier(self, tier: int) -> int:
+        """Make `tier`'s plan resident (the paper's SetupForSched); returns the
+        bytes moved. The reference charges this 0; the engine
+        charges it to the pass that follows."""
+        if tier == self.tier:
+            return 0
+        plan = self.plans[tier]
+        moved = 0
+        rows = max(self.kv_len) if self.kv_len else 0
+        kv_rows_bytes = rows * self.B * self.row_bytes
+        # 1. every VRAM KV cache goes home first (content is authoritative)
+        for layer, dev in self.kv_vram.items():
+            L.memcpy_async(self._kv_host_ptr(layer), dev, kv_rows_bytes, self.cs)
+            moved += kv_rows_bytes
+        L.call("ps_stream_synchronize", self.cs)
+        self.synchronize()   # the ring and every stream must be idle before re-carving
+        # 2. re-carve the pinned region in pin order; keep weights whose slot is unchanged
+        old = {sid: r[1] for sid, r in self.residency.items() if r[0] == "pinned"}
+        self.arena.reset_low()
+        self.residency, self.kv_vram, self.kv_mode = {}, {}, {}
+        pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
+                        key=lambda p: (self.shards[p.shard_id].priority,
+                                       self.shards[p.shard_id].layer_index, p.shard_id))
+        for p in pinned:
+            s = self.shards[p.shard_id]
+            dev = self.arena.alloc_low(f"pin{s.id}", self._phys_bytes(s))
+            if s.kind is ShardKind.KV_CACHE:
+                self.kv_vram[s.layer_index] = dev
+                self.kv_mode[s.layer_index] = "pinned"
+                L.memcpy_async(dev, self._kv_host_ptr(s.layer_index), kv_rows_bytes, self.cs)
+                moved += kv_rows_bytes
+            else:
+                if old.get(s.id) != dev:
+                    nbytes = self._phys_bytes(s)
+                    L.memcpy_async(dev, self.w.shard_ptr(s.id), nbytes, self.cs)
+                    moved += nbytes
+                self.residency[s.id] = ("pinned", dev)
+        for p in plan.placements:
+            if p.residency is Residency.VRAM_PINNED:
+                continue
+            s = self.shards[p.shard_id]
+            if p.exec_backend is Backend.CPU:
+                mode = "zerocopy"
+            elif p.streaming in (Streaming.WEIGHTS_H2D, Streaming.KV_H2D,
+                                 Streaming.WEIGHTS_AND_KV):
+                mode = "stream"
+            else:
+                raise SpecError(f"unsupported placement {p}")
+            if s.kind is ShardKind.KV_CACHE:
+                self.kv_mode[s.layer_index] = mode
+            else:
+                self.residency[s.id] = (mode, 0)
+        L.call("ps_stream_synchronize", self.cs)
+        self.tier = tier
+        return moved
+
+    # --------------------------------------------------------------- helpers
+    def _wait(self, ev: int) -> None:
+        L.call("ps_stream_wait_event", self.cs, ev)
+
+    def _record(self, stream: int) -> int:
+        ev = self.events.next()
+        L.call("ps_event_record", ev, stream)
+        return ev
+
+    def _pieces(self, sid: int, names: list, even: set) -> list:
+        """Row-aligned pieces (<= chunk bytes) covering `names` in blob order:
+        [(byte_start, byte_end, [(tensor, r0, r1), ...])]; 1-row tensors
+        (norm vectors) ride in the piece that follows them."""
+        blob = self.w.layout.blobs[sid]
+        out, items, start, end, big = [], [], None, 0, False
+        for name in names:
+            t = blob.tensors[name]
+            row_b = t.cols * 2
+            step = max(1, self.chunk // row_b)
+            if name in even:
+                step = max(2, step // 2 * 2)
+            r = 0
+            while r < t.rows:
+                r1 = min(t.rows, r + step)
+                b0, b1 = t.offset + r * row_b, t.offset + r1 * row_b
+                if big and t.rows > 1 and b1 - start > self.chunk:
+                    out.append((start, end, items))
+                    items, start, big = [], None, False
+                if start is None:
+                    start = b0
+                items.append((name, r, r1))
+                big = big or t.rows > 1
+                end = b1
+                r = r1
+        if items:
+            out.append((start, end, items))
+        return out
+
+    def _shard(self, sid: int, consumers: list, T: int) -> None:
+        """Make a weight shard's tensors addressable and run its consumers in order.
+
+        Pinned / zero-copy shards expose whole tensors. Streamed shards are
+        walked piece by piece through the ring: each piece is waited for
+        right before its first consumer and released (sealed) after the last
+        consumer that reads any tensor in it."""
+        mode, dev = self.residency[sid]
+        if mode == "zerocopy" and T > GEMV_MAX_T:
+            mode = "stream"
+        blob = self.w.layout.blobs[sid]
+        own = {c.tensor: i for i, c in enumerate(consumers) if c.tensor is not None}
+        readers: dict = {}
+        for i, c in enumerate(consumers):
+            if c.tensor is not None:
+                readers.setdefault(c.tensor, set()).add(i)
+            for r in c.reads:
+                readers.setdefault(r, set()).add(i)
+        names = [n for n in blob.tensors if n in readers]
+        self.ptrs = {}
+        ci = 0
+
+        def advance_to(target: int) -> None:
+            nonlocal ci
+            while ci < target:
+                c = consumers[ci]
+                if c.tensor is not None:
+                    raise SpecError(f"consumer order mismatch at {c.tensor}")
+                c.fn(None, 0, 0)
+                done(ci)
+                ci += 1
+
+        if mode in ("pinned", "zerocopy"):
+            base = dev if mode == "pinned" else self.w.shard_ptr(sid)
+            if mode == "zerocopy":
+                self._stat.zero_copy_bytes += blob.nbytes
+            live = []
+
+            def done(i):
+                pass
+            for name in names:
+                t = blob.tensors[name]
+                self.ptrs[name] = base + t.offset
+                if name in own:
+                    advance_to(own[name])
+                    consumers[ci].fn(base + t.offset, 0, t.rows)
+                    ci += 1
+            advance_to(len(consumers))
+            return
+
+        pieces = self._pieces(sid, names, {c.tensor for c in consumers if c.even_rows})
+        host = self.w.shard_ptr(sid)
+        live: list = []       # [region, pending consumer set]
+
+        def done(i):
+            for entry in live[:]:
+                entry[1].discard(i)
+                if not entry[1]:
+                    self.ring.seal(entry[0], [self._record(self.cs)])
+                    live.remove(entry)
+
+        for b0, b1, items in pieces:
+            region, pdev, arrived = self.ring.upload(host + b0, b1 - b0, f"s{sid}@{b0}")
+            self._stat.bytes_streamed += b1 - b0
+            self._stat.copies += 1
+            pending = set()
+            for name, _, _ in items:
+                pending |= readers[name]
+            entry = [region, pending]
+            live.append(entry)
+            self._wait(arrived)
+            for name, r0, r1 in items:
+                t = blob.tensors[name]
+                ptr = pdev + (t.offset + r0 * t.cols * 2 - b0)
+                if r0 == 0:
+                    self.ptrs[name] = ptr
+                if name in own:
+                    advance_to(own[name])
+                    consumers[ci].fn(ptr, r0, r1)
+                    if r1 == t.rows:
+                        done(ci)
+                        ci += 1
+        advance_to(len(consumers))
+        for entry in live:
+            self.ring.seal(entry[0], [self._record(self.cs)])
+
+    def _matmul(self, T, act, W, N, K, out, ldo, epi) -> None:
+        """out (epi)= act @ W[:N]^T for T tokens: GEMV on fp32 act (T <= 32)
+        or the tcgen05 GEMM on bf16 act."""
+        if T <= GEMV_MAX_T:
+            L.call("ps_gemv_bf16", act, K, T, W, N, K, K, out, ldo, epi, self.cs)
+        else:
+            L.call("ps_gemm_bf16", act, T, K, K, W, N, K, out, ldo, epi, self.cs)
+
+    def _upload(self, dst: int, arr: np.ndarray) -> None:
+        arr = np.ascontiguousarray(arr, dtype=np.int32)
+        if arr.nbytes == 0:
+            return
+        if arr.nbytes <= 4000:
+            L.call("ps_upload_small", dst, arr.ctypes.data, arr.nbytes, self.cs)
+        else:
+            self._h2d_sync(dst, arr)
+
+    # ----------------------------------------------------------------- the pass
+    def run_pass(self, ps: PassSpec) -> PassStats:
+        T = ps.T
+        if T > self.Tmax:
+            raise SpecError(f"pass of {T} tokens exceeds max_tokens {self.Tmax}")
+        nb = len(ps.slots)
+        self._stat = PassStats(self.tier, T)
+        gemv = T <= GEMV_MAX_T
+        d, hq = self.d, self.h * self.hd
+
+        pos = np.empty(T, np.int32)
+        req = np.empty(T, np.int32)
+        q_start = np.zeros(nb + 1, np.int32)
+        k = 0
+        for j, (slot, n, p0) in enumerate(zip(ps.slots, ps.n_new, ps.p0)):
+            pos[k:k + n] = np.arange(p0, p0 + n, dtype=np.int32)
+            req[k:k + n] = slot
+            k += n
+            q_start[j + 1] = k
+        lens = np.array([p0 + n for p0, n in zip(ps.p0, ps.n_new)], np.int32)
+        if int(lens.max()) > self.cap:
+            raise SpecError(f"context {int(lens.max())} exceeds the planned {self.cap}")
+        p0a = np.array(ps.p0, np.int32)
+        rows = np.array([int(q_start[j + 1]) - 1 for j in ps.sample], np.int32)
+        self._upload(self.i_pos, pos)
+        self._upload(self.i_req, req)
+        self._upload(self.i_meta, np.concatenate([q_start, p0a, lens,
+                                                  np.array(ps.slots, np.int32)]))
+        self._upload(self.i_rows, rows)
+        i_qstart = self.i_meta
+        i_p0 = i_qstart + 4 * (nb + 1)
+        i_lens = i_p0 + 4 * nb
+        i_slot = i_lens + 4 * nb
+        max_len, max_new = int(lens.max()), int(max(ps.n_new))
+        min_p0 = int(p0a.min())
+        use_decode_kernel = ps.decode_only and gemv
+
+        if ps.ids is not None:
+            self._upload(self.i_ids, np.asarray(ps.ids, np.int32))
+            ids_ptr = self.i_ids
+        else:
+            if self._prev_sample_slots != list(ps.slots):
+                raise SpecError("a pass without ids must follow a pass that sampled the same slots")
+            ids_ptr = self.i_tok          # the previous sampling pass's slot
+        L.call("ps_embed_gather", self.w.embed, ids_ptr, T, d, self.x, d, self.cs)
+
+        xn = self.xn32 if gemv else self.xn16
+        att = self.att32 if gemv else self.att16
+        hid = self.hid32 if gemv else self.hid16
+        esz = 4 if gemv else 2
+        scale = 1.0 / math.sqrt(self.hd)
+        eps = self.arch.rms_eps
+        row_stride = self.B * self.row_elems
+
+        def norm(w_ptr):
+            L.call("ps_rmsnorm", self.x, d, 0, T, w_ptr, d, eps, xn, d, 0 if gemv else 1, self.cs)
+
+        for layer in range(self.spec.n_layers):
+            attn_sid = self.by_layer_kind[(layer, ShardKind.ATTENTION)].id
+            ffn_sid = self.by_layer_kind[(layer, ShardKind.FFN)].id
+            # ---- KV_i, hoisted before Attn_i
+            mode = self.kv_mode[layer]
+            kv_region = None
+            if mode == "pinned":
+                kv_base = self.kv_vram[layer]
+            elif mode == "zerocopy" and gemv:
+                kv_base = self._kv_host_ptr(layer)
+            else:
+                prefix = min_p0 * self.B * self.row_bytes
+                room = max_len * self.B * self.row_bytes
+                wb = self.kv_writeback.get(layer)
+                if wb is not None and prefix:
+                    # the host home must hold the previous pass's appended rows
+                    L.call("ps_stream_wait_event", self.h2d, wb)
+                kv_region, kv_base, arrived = self.ring.upload(self._kv_host_ptr(layer), prefix,
+                                                               f"kv{layer}", reserve=room)
+                self._stat.bytes_streamed += prefix
+                self._stat.copies += 1 if prefix else 0
+                self._wait(arrived)
+
+            # ---- Attn_i
+            def core(_p, _a, _b, layer=layer, kv_base=kv_base, kv_region=kv_region):
+                qn = self.ptrs.get(f"L{layer}.q_norm", 0)
+                kn = self.ptrs.get(f"L{layer}.k_norm", 0)
+                L.call("ps_qkv_rope_append", self.qkv, self.qkv_rows, T, self.h, self.kv, self.hd,
+                       self.i_pos, self.i_req, kv_base, self.row_elems, row_stride, self.rope,
+                       qn, kn, eps, self.cs)
+                if use_decode_kernel:
+                    L.call("ps_attn_decode", self.qkv, self.qkv_rows, nb, self.h, self.kv, self.hd,
+                           i_slot, kv_base, self.row_elems, row_stride, i_lens, max_len, scale,
+                           att, hq, self.ws, self.ws_floats, self.cs)
+                else:
+                    L.call("ps_attn_prefill", self.qkv, self.qkv_rows, nb, i_qstart, i_p0, i_slot,
+                           max_new, self.h, self.kv, self.hd, kv_base, self.row_elems, row_stride,
+                           scale, att, hq, 0 if gemv else 1, self.cs)
+                if kv_region is not None:
+                    # appended rows -> the layer's host home (D2H stream), then release
+                    L.call("ps_stream_wait_event", self.d2h, self._record(self.cs))
+                    a, b = min_p0 * self.B * self.row_bytes, max_len * self.B * self.row_bytes
+                    L.memcpy_async(self._kv_host_ptr(layer) + a, kv_base + a, b - a, self.d2h)
+                    self._stat.kv_writeback_bytes += b - a
+                    wb = self._record(self.d2h)
+                    self.kv_writeback[layer] = wb
+                    self.ring.seal(kv_region, [wb])
+
+            reads = (f"L{layer}.q_norm", f"L{layer}.k_norm") if self.arch.qk_norm else ()
+            self._shard(attn_sid, [
+                Consumer(f"L{layer}.attn_norm", lambda p, a, b: norm(p)),
+                Consumer(f"L{layer}.wqkv", lambda p, r0, r1: self._matmul(
+                    T, xn, p, r1 - r0, d, self.qkv + r0 * 4, self.qkv_rows, L.PS_EPI_STORE)),
+                Consumer(None, core, reads=reads),
+                Consumer(f"L{layer}.wo", lambda p, r0, r1: self._matmul(
+                    T, att, p, r1 - r0, hq, self.x + r0 * 4, d, L.PS_EPI_ACCUM)),
+            ], T)
+
+            # ---- FFN_i
+            self._shard(ffn_sid, [
+                Consumer(f"L{layer}.ffn_norm", lambda p, a, b: norm(p)),
+                Consumer(f"L{layer}.wgu", lambda p, r0, r1: self._matmul(
+                    T, xn, p, r1 - r0, d, hid + (r0 // 2) * esz, self.ffn, L.PS_EPI_SWIGLU),
+                    even_rows=True),
+                Consumer(f"L{layer}.wdown", lambda p, r0, r1: self._matmul(
+                    T, hid, p, r1 - r0, self.ffn, self.x + r0 * 4, d, L.PS_EPI_ACCUM)),
+            ], T)
+
+        # ---- head, on the sampled rows only (HEAD_ROWS_CAP, model_graph.py:30-33)
+        R = len(ps.sample)
+        if R:
+            head_sid = self.by_layer_kind[(self.spec.n_layers, ShardKind.OUTPUT_HEAD)].id
+
+            def hnorm(p, a, b):
+                L.call("ps_rmsnorm", self.x, d, self.i_rows, R, p, d, eps, self.xs, d, 0, self.cs)
+
+            def lm(p, r0, r1):
+                L.call("ps_gemv_bf16", self.xs, d, R, p, r1 - r0, d, d, self.logits + r0 * 4,
+                       self.V, L.PS_EPI_STORE, self.cs)
+
+            self.tok_slot = (self.tok_slot + 1) % 8
+            self.i_tok = self.i_tok_ring + self.tok_slot * self.B * 4
+
+            def greedy(p, a, b):
+                L.call("ps_argmax", self.logits, R, self.V, self.V, self.i_tok, self.cs)
+
+            self._shard(head_sid, [Consumer("final_norm", hnorm), Consumer("lm_head", lm),
+                                   Consumer(None, greedy)], R)
+            L.call("ps_stream_wait_event", self.d2h, self._record(self.cs))
+            dst = self.host_tok + (self.host_tok_i % 4096) * self.B * 4
+            self.host_tok_i += 1
+            L.memcpy_async(dst, self.i_tok, R * 4, self.d2h)
+            sampled = [ps.slots[j] for j in ps.sample]
+            ev = self.tok_events[self.host_tok_i % len(self.tok_events)]
+            L.call("ps_event_record", ev, self.d2h)
+            self.host_tokens.append((dst, R, ev, sampled))
+            self._prev_sample_slots = sampled
+        for slot, n, p0 in zip(ps.slots, ps.n_new, ps.p0):
+            self.kv_len[slot] = max(self.kv_len[slot], p0 + n)
+        self.stats.append(self._stat)
+        return self._stat
+
+    # ------------------------------------------------------------------ results
+    def collect_tokens(self) -> list:
+        """Wait for and return [(slots, tokens)] of every sampling pass so far."""
+        out = []
+        for dst, R, ev, slots in self.host_tokens:
+            L.call("ps_event_synchronize", ev)
+            out.append((slots, np.ctypeslib.as_array((C.c_int32 * R).from_address(dst)).copy()))
+        self.host_tokens = []
+        return out
+
+    def logits_host(self, rows: int) -> np.ndarray:
+        """fp32 logits of the last sampling pass (synchronises)."""
+        self.synchronize()
+        import torch
+        t = self.arena.tensor(self.logits, rows * self.V * 4).view(torch.float32)
+        return t.reshape(rows, self.V).cpu().numpy()
+
+    def synchronize(self) -> None:
+        for s in (self.cs, self.h2d, self.d2h):
+            L.call("ps_stream_synchronize", s)
+
+    def close(self) -> None:
+        if self.kv_host:
+            self.synchronize()
+            L.host_free(self.kv_host)
+            L.host_free(self.host_stage)
+            L.host_free(self.host_tok)
+            self.kv_host = 0

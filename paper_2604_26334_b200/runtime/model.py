@@ -1,0 +1,286 @@
+"""Model load: architecture constants, host weight layout and random init.
+
+The north_star's "model load" (BASELINE.json) for this build: weights are
+random-initialised from a `ModelSpec` (no checkpoints travel to the box),
+deterministically from (model seed, tensor name), generated on the GPU by
+`ps_init_*` and written into ONE pinned, mapped host blob laid out
+shard-contiguous in stream order, so every streamed shard is one or a few
+large `cudaMemcpyAsync` source ranges and CPU-placed shards are readable
+zero-copy. The embedding table is a separate mapped host buffer (outside
+the plan, `pkg/src/shardplan/model_graph.py:279-297`).
+
+Tensor conventions (bf16, row-major, rows = output features):
+  attention shard  attn_norm[d] | wqkv[(h + 2 kv) hd, d] (= wq; wk; wv) |
+                   q_norm[hd], k_norm[hd] (Qwen3) | wo[d, h hd]
+  FFN shard        ffn_norm[d] | wgu[2 ffn, d] (gate/up rows interleaved:
+                   2j = gate_j, 2j+1 = up_j) | wdown[d, ffn]
+  MoE shard        ffn_norm[d] | router[E, d] | per expert e: wgu_e[2 eff, d],
+                   wdown_e[d, eff]
+  head shard       final_norm[d] | lm_head[V, d]
+Every tensor starts on a 256-byte boundary.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ..planning.graph import ModelSpec, ShardKind, build_shards
+from . import lib as L
+
+ALIGN = 256
+
+
+def _align(n: int) -> int:
+    return (n + ALIGN - 1) // ALIGN * ALIGN
+
+
+@dataclass(frozen=True)
+class Arch:
+    """Numerics the ModelSpec does not carry (public HF configs)."""
+
+    rope_theta: float = 10000.0
+    rope_scaling: dict | None = None     # llama3: factor, low_freq_factor, high_freq_factor, original_max
+    qk_norm: bool = False
+    rms_eps: float = 1e-5
+    seed: int = 0
+
+
+LLAMA3_SCALING = {"factor": 8.0, "low_freq_factor": 1.0, "high_freq_factor": 4.0,
+                  "original_max_position_embeddings": 8192}
+
+ARCHS = {
+    "tiny-llama": Arch(rope_theta=10000.0),
+    "llama3.1-8b": Arch(rope_theta=500000.0, rope_scaling=LLAMA3_SCALING),
+    "llama3.3-70b": Arch(rope_theta=500000.0, rope_scaling=LLAMA3_SCALING),
+    "qwen3-30b-a3b": Arch(rope_theta=1000000.0, qk_norm=True, rms_eps=1e-6),
+}
+
+
+def arch_for(spec: ModelSpec, seed: int = 0) -> Arch:
+    base = ARCHS.get(spec.name, Arch())
+    return Arch(base.rope_theta, base.rope_scaling, base.qk_norm, base.rms_eps, seed)
+
+
+def tensor_seed(model_seed: int, name: str) -> int:
+    """64-bit seed of one logical tensor: sha256("<seed>:<name>")[:8], little endian."""
+    return int.from_bytes(hashlib.sha256(f"{model_seed}:{name}".encode()).digest()[:8], "little")
+
+
+def init_scale(name: str, fan_in: int) -> tuple[float, float]:
+    """(scale, bias) of the uniform init: norms ~ U(0.9, 1.1), embeddings
+    ~ U(-1, 1), linear weights ~ U(-a, a) with a = sqrt(3 / fan_in)."""
+    leaf = name.rsplit(".", 1)[-1]
+    if leaf.endswith("norm"):
+        return 0.1, 1.0
+    if leaf == "embed":
+        return 1.0, 0.0
+    return math.sqrt(3.0 / fan_in), 0.0
+
+
+def rope_inv_freq(arch: Arch, head_dim: int) -> np.ndarray:
+    """Per-pair inverse frequencies (float64), Llama-3 scaling when configured."""
+    inv = 1.0 / (arch.rope_theta ** (np.arange(0, head_dim, 2, dtype=np.float64) / head_dim))
+    sc = arch.rope_scaling
+    if not sc:
+        return inv
+    factor, lo, hi = sc["factor"], sc["low_freq_factor"], sc["high_freq_factor"]
+    orig = sc["original_max_position_embeddings"]
+    low_wl, high_wl = orig / lo, orig / hi
+    wl = 2 * math.pi / inv
+    out = np.where(wl > low_wl, inv / factor, inv)
+    smooth = (orig / wl - lo) / (hi - lo)
+    mid = (wl <= low_wl) & (wl >= high_wl)
+    return np.where(mid, (1 - smooth) * inv / factor + smooth * inv, out)
+
+
+def rope_table(arch: Arch, head_dim: int, n_pos: int) -> np.ndarray:
+    """(cos, sin) per position and pair as float32 [n_pos, head_dim/2, 2]."""
+    ang = np.arange(n_pos, dtype=np.float64)[:, None] * rope_inv_freq(arch, head_dim)[None, :]
+    return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+
+
+@dataclass
+class TensorSlot:
+    name: str
+    offset: int          # bytes from the start of its shard
+    rows: int
+    cols: int
+    init: tuple          # ("plain", [seed names]) or ("interleaved", name_a, name_b)
+
+    @property
+    def nbytes(self) -> int:
+        return self.rows * self.cols * 2
+
+
+@dataclass
+class ShardBlob:
+    shard_id: int
+    kind: ShardKind
+    layer: int
+    offset: int                      # bytes from the start of the host blob
+    nbytes: int
+    tensors: dict = field(default_factory=dict)   # name -> TensorSlot (offset within shard)
+
+
+class WeightLayout:
+    """Byte layout of the host weight blob, in stream order."""
+
+    def __init__(self, spec: ModelSpec, arch: Arch):
+        self.spec, self.arch = spec, arch
+        s = spec
+        self.qkv_rows = (s.n_heads + 2 * s.n_kv_heads) * s.head_dim
+        self.blobs: dict[int, ShardBlob] = {}
+        cursor = 0
+        for shard in build_shards(spec, 0):
+            if shard.kind is ShardKind.KV_CACHE:
+                continue
+            blob = ShardBlob(shard.id, shard.kind, shard.layer_index, cursor, 0)
+            self._fill(blob)
+            cursor += _align(blob.nbytes)
+            self.blobs[shard.id] = blob
+        self.total_bytes = cursor
+        self.embed_bytes = s.vocab_size * s.d_model * 2
+
+    def _fill(self, blob: ShardBlob) -> None:
+        s, i = self.spec, blob.layer
+        off = 0
+
+        def add(name, rows, cols, init):
+            nonlocal off
+            blob.tensors[name] = TensorSlot(name, off, rows, cols, init)
+            off = _align(off + rows * cols * 2)
+
+        hd, h, kv, d = s.head_dim, s.n_heads, s.n_kv_heads, s.d_model
+        if blob.kind is ShardKind.ATTENTION:
+            add(f"L{i}.attn_norm", 1, d, ("plain", f"L{i}.attn_norm"))
+            add(f"L{i}.wqkv", self.qkv_rows, d,
+                ("concat", [(f"L{i}.wq", h * hd), (f"L{i}.wk", kv * hd), (f"L{i}.wv", kv * hd)]))
+            if self.arch.qk_norm:   # consumed between the projections, so stored between them
+                add(f"L{i}.q_norm", 1, hd, ("plain", f"L{i}.q_norm"))
+                add(f"L{i}.k_norm", 1, hd, ("plain", f"L{i}.k_norm"))
+            add(f"L{i}.wo", d, h * hd, ("plain", f"L{i}.wo"))
+        elif blob.kind is ShardKind.FFN:
+            add(f"L{i}.ffn_norm", 1, d, ("plain", f"L{i}.ffn_norm"))
+            add(f"L{i}.wgu", 2 * s.ffn_dim, d, ("interleaved", f"L{i}.w_gate", f"L{i}.w_up"))
+            add(f"L{i}.wdown", d, s.ffn_dim, ("plain", f"L{i}.w_down"))
+        elif blob.kind is ShardKind.MOE_EXPERT_GROUP:
+            moe = s.moe
+            add(f"L{i}.ffn_norm", 1, d, ("plain", f"L{i}.ffn_norm"))
+            add(f"L{i}.router", moe.n_experts, d, ("plain", f"L{i}.router"))
+            for e in range(moe.n_experts):
+                add(f"L{i}.e{e}.wgu", 2 * moe.expert_ffn_dim, d,
+                    ("interleaved", f"L{i}.e{e}.w_gate", f"L{i}.e{e}.w_up"))
+                add(f"L{i}.e{e}.wdown", d, moe.expert_ffn_dim, ("plain", f"L{i}.e{e}.w_down"))
+        elif blob.kind is ShardKind.OUTPUT_HEAD:
+            add("final_norm", 1, d, ("plain", "final_norm"))
+            add("lm_head", s.vocab_size, d, ("plain", "lm_head"))
+        blob.nbytes = off
+
+    def tensor(self, shard_id: int, name: str) -> TensorSlot:
+        return self.blobs[shard_id].tensors[name]
+
+
+class HostWeights:
+    """Pinned + mapped host blob holding every shard, plus the embedding table.
+
+    `generate()` fills it on the GPU (deterministic per tensor name) through
+    a bounded device staging buffer and D2H copies; the staging buffer is
+    released before the VRAM arena is created, so it does not count against
+    the budget.
+    """
+
+    def __init__(self, spec: ModelSpec, arch: Arch):
+        self.spec, self.arch = spec, arch
+        self.layout = WeightLayout(spec, arch)
+        self.base = L.host_alloc(self.layout.total_bytes, mapped=True)
+        self.embed = L.host_alloc(self.layout.embed_bytes, mapped=True)
+
+    def close(self) -> None:
+        if self.base:
+            L.host_free(self.base)
+            L.host_free(self.embed)
+            self.base = self.embed = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard_ptr(self, shard_id: int) -> int:
+        return self.base + self.layout.blobs[shard_id].offset
+
+    def tensor_ptr(self, shard_id: int, name: str) -> int:
+        return self.shard_ptr(shard_id) + self.layout.tensor(shard_id, name).offset
+
+    def host_view(self, shard_id: int, name: str) -> np.ndarray:
+        """uint16 view (bf16 bits) of one tensor in the pinned blob."""
+        t = self.layout.tensor(shard_id, name)
+        buf = (np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint16 * (t.rows * t.cols))
+                                     .from_address(self.tensor_ptr(shard_id, name))))
+        return buf.reshape(t.rows, t.cols)
+
+    def embed_view(self) -> np.ndarray:
+        n = self.spec.vocab_size * self.spec.d_model
+        buf = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint16 * n).from_address(self.embed))
+        return buf.reshape(self.spec.vocab_size, self.spec.d_model)
+
+    def generate(self, staging_bytes: int = 256 << 20) -> None:
+        import torch
+        seed = self.arch.seed
+        stream = torch.cuda.current_stream().cuda_stream
+        stage = torch.empty(staging_bytes, dtype=torch.uint8, device="cuda")
+        sptr = stage.data_ptr()
+        row_cap_bytes = staging_bytes
+
+        def emit(dst_host: int, nbytes: int, producer) -> None:
+            done = 0
+            while done < nbytes:
+                n = min(row_cap_bytes, nbytes - done)
+                producer(sptr, done, n)
+                L.memcpy_async(dst_host + done, sptr, n, stream)
+                L.call("ps_stream_synchronize", stream)
+                done += n
+
+        def plain(name, fan_in):
+            scale, bias = init_scale(name, fan_in)
+            sd = tensor_seed(seed, name)
+
+            def prod(dst, byte_off, n):
+                L.call("ps_init_uniform_bf16", dst, n // 2, sd, byte_off // 2, scale, bias, stream)
+            return prod
+
+        for sid, blob in self.layout.blobs.items():
+            for t in blob.tensors.values():
+                dst = self.base + blob.offset + t.offset
+                kind = t.init[0]
+                if kind == "plain":
+                    emit(dst, t.nbytes, plain(t.init[1], t.cols))
+                elif kind == "concat":
+                    cur = dst
+                    for name, rows in t.init[1]:
+                        emit(cur, rows * t.cols * 2, plain(name, t.cols))
+                        cur += rows * t.cols * 2
+                elif kind == "interleaved":
+                    name_a, name_b = t.init[1], t.init[2]
+                    scale, bias = init_scale(name_a, t.cols)
+                    sa, sb = tensor_seed(seed, name_a), tensor_seed(seed, name_b)
+                    rows_each, cols = t.rows // 2, t.cols
+                    row_bytes = cols * 2
+
+                    def prod(dst_dev, byte_off, n, rows_each=rows_each, cols=cols, sa=sa, sb=sb,
+                             scale=scale, bias=bias, row_bytes=row_bytes):
+                        L.call("ps_init_interleaved_bf16", dst_dev, rows_each, byte_off // row_bytes,
+                               n // row_bytes, cols, sa, sb, scale, bias, stream)
+                    # chunks must hold whole rows
+                    saved = row_cap_bytes
+                    row_cap_bytes = max(row_bytes, (saved // row_bytes) * row_bytes)
+                    emit(dst, t.nbytes, prod)
+                    row_cap_bytes = saved
+        emit(self.embed, self.layout.embed_bytes, plain("embed", self.spec.d_model))
+        del stage
+        torch.cuda.synchronize()

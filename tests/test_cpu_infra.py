@@ -1,0 +1,101 @@
+"""CPU-side checks: oracle known answers, host layout, C-ABI exports, tier reachability."""
+
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2604_26334_b200.planning import catalog
+from paper_2604_26334_b200.planning.graph import build_shards, total_model_bytes
+from paper_2604_26334_b200.planning.placement import reachable_tiers
+from paper_2604_26334_b200.planning.costdb import synth_profile
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _py_value(seed, idx, scale, bias):
+    """Pure-Python restatement of one element of the initialiser (small cases)."""
+    m = (1 << 64) - 1
+    z = seed ^ ((idx * 0x9E3779B97F4A7C15) & m)
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    z ^= z >> 31
+    u = np.float32((z >> 40) * (1.0 / 16777216.0))
+    w = np.float32(np.float32(2.0) * u - np.float32(1.0))
+    v = np.float64(w) * np.float64(np.float32(scale)) + np.float64(np.float32(bias))
+    f = np.float32(v)   # fmaf: single rounding of the exact product-sum
+    b = int(f.view(np.uint32))
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFFFFFF
+    return b >> 16
+
+
+def test_oracle_initialiser_matches_python_restatement():
+    from oracle import model_ref
+    bits = model_ref.bf16_bits(7, "L0.wq", 4, 64)
+    sc, bi = model_ref.scale_bias("L0.wq", 64)
+    sd = model_ref.seed_of(7, "L0.wq")
+    want = np.array([_py_value(sd, i, sc, bi) for i in range(4 * 64)], np.uint16).reshape(4, 64)
+    np.testing.assert_array_equal(bits, want)
+    gu = model_ref.interleaved_bits(7, "L0.w_gate", "L0.w_up", 3, 64)
+    np.testing.assert_array_equal(gu[0::2], model_ref.bf16_bits(7, "L0.w_gate", 3, 64))
+    np.testing.assert_array_equal(gu[1::2], model_ref.bf16_bits(7, "L0.w_up", 3, 64))
+
+
+def test_oracle_norm_init_range():
+    from oracle import model_ref
+    w = model_ref.weight(0, "L3.attn_norm", 1, 4096).numpy()
+    assert 0.89 <= w.min() and w.max() <= 1.11
+
+
+def test_rope_table_matches_oracle():
+    from oracle import model_ref
+    from paper_2604_26334_b200.runtime.model import arch_for, rope_table, rope_inv_freq
+    spec = catalog.builtin_model("llama3.1-8b")
+    arch = arch_for(spec)
+    a = rope_inv_freq(arch, 128)
+    b = model_ref.inv_freq(arch.rope_theta, 128, arch.rope_scaling)
+    np.testing.assert_allclose(a, b, rtol=1e-15)
+    tab = rope_table(arch, 128, 64)
+    ang = np.arange(64)[:, None] * b[None, :]
+    np.testing.assert_array_equal(tab[..., 0], np.cos(ang).astype(np.float32))
+
+
+def test_weight_layout_covers_plan_bytes():
+    from paper_2604_26334_b200.runtime.model import WeightLayout, arch_for
+    for name in ("tiny-llama", "llama3.1-8b", "llama3.3-70b"):
+        spec = catalog.builtin_model(name)
+        lay = WeightLayout(spec, arch_for(spec))
+        shards = {s.id: s for s in build_shards(spec, 0)}
+        for sid, blob in lay.blobs.items():
+            # physical = plan weight bytes + norm vectors + 256-B alignment padding
+            extra = blob.nbytes - shards[sid].weight_bytes
+            assert 0 <= extra <= 4 * 256 + 4 * spec.d_model, (name, sid, extra)
+        assert lay.total_bytes >= total_model_bytes(spec)
+
+
+def test_tiny_config_reachable_tiers():
+    spec = catalog.builtin_model("tiny-llama")
+    machine = catalog.builtin_machine("b200")
+    budget = 0.5 * total_model_bytes(spec)
+    plans = reachable_tiers(spec, machine, synth_profile(machine), budget, 160)
+    assert set(plans) == {1, 4, 16, 32, 64, 512, 1024, 2048, 4096}
+
+
+def test_header_exports_match_binding():
+    from paper_2604_26334_b200.runtime import lib as L
+    header = open(os.path.join(REPO, "include", "pshard.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(ps_\w+)\(", header, re.M))
+    assert declared == set(L.EXPORTED), declared ^ set(L.EXPORTED)
+
+
+def test_library_loads_and_exports_every_symbol():
+    from paper_2604_26334_b200.runtime import lib as L
+    if not os.path.exists(L.LIB_PATH):
+        pytest.skip("libpshard.so not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(L.LIB_PATH)
+    for name in L.EXPORTED:
+        assert hasattr(lib, name), name
+    assert lib.ps_abi_version() == 1

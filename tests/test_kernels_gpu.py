@@ -1,0 +1,278 @@
+"""Per-kernel parity on the B200, through the C-ABI (include/pshard.h).
+
+Each kernel is compared with a plain fp32 PyTorch restatement on the same
+inputs. Tolerances: fp32-accumulated kernels on fp32 activations must agree
+to ~1e-5 relative; kernels that take bf16 activations (tcgen05 GEMM,
+mma.sync flash attention) are bounded by bf16 input rounding (2^-8).
+Integer work (argmax, weight init) must be bit-exact.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def L():
+    from paper_2604_26334_b200.runtime import lib
+    return lib
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def rel_err(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("t", [1, 2, 3, 4, 8, 13, 32])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+@pytest.mark.parametrize("N,K", [(6144, 4096), (256, 14336), (130, 512)])
+def test_gemv(t, epi, N, K):
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(t * 100 + N)
+    x = torch.randn(t, K, device="cuda", generator=g)
+    W = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    ref = x @ W.float().T
+    if epi == 2:
+        ref = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+        y = torch.zeros(t, N // 2, device="cuda")
+        ldy = N // 2
+    else:
+        y = torch.randn(t, N, device="cuda", generator=g) if epi == 1 else torch.zeros(t, N, device="cuda")
+        if epi == 1:
+            ref = ref + y
+        ldy = N
+    lib.call("ps_gemv_bf16", x.data_ptr(), K, t, W.data_ptr(), N, K, K, y.data_ptr(), ldy, epi, stream())
+    torch.cuda.synchronize()
+    assert rel_err(y, ref) < 2e-5
+
+
+def test_gemv_zero_copy_host_weights():
+    lib = L()
+    N, K = 512, 4096
+    W = (torch.randn(N, K) / 64).to(torch.bfloat16)
+    host = lib.host_alloc(W.numel() * 2, mapped=True)
+    import ctypes
+    ctypes.memmove(host, W.data_ptr(), W.numel() * 2)
+    x = torch.randn(1, K, device="cuda")
+    y = torch.zeros(1, N, device="cuda")
+    lib.call("ps_gemv_bf16", x.data_ptr(), K, 1, host, N, K, K, y.data_ptr(), N, 0, stream())
+    torch.cuda.synchronize()
+    assert rel_err(y, x @ W.float().cuda().T) < 2e-5
+    lib.host_free(host)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (2048, 6144, 4096), (200, 1000, 512),
+                                   (4096, 512, 14336), (64, 256, 1536)])
+@pytest.mark.parametrize("epi", [0, 1, 3, 2])
+def test_gemm_tcgen05(M, N, K, epi):
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    ref = A.float() @ B.float().T
+    if epi == 2:
+        ref = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+        C = torch.zeros(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        ldc = N // 2
+    elif epi == 3:
+        C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        ldc = N
+    else:
+        C = torch.randn(M, N, device="cuda", generator=g) if epi == 1 else torch.zeros(M, N, device="cuda")
+        if epi == 1:
+            ref = ref + C
+        ldc = N
+    lib.call("ps_gemm_bf16", A.data_ptr(), M, K, K, B.data_ptr(), N, K, C.data_ptr(), ldc, epi, stream())
+    torch.cuda.synchronize()
+    tol = 1e-5 if epi in (0, 1) else 8e-3   # bf16 output rounding
+    assert rel_err(C.float(), ref) < tol
+
+
+def test_rmsnorm_rows_and_bf16():
+    lib = L()
+    x = torch.randn(5, 4096, device="cuda")
+    w = (1 + 0.1 * torch.randn(4096, device="cuda")).to(torch.bfloat16)
+    rows = torch.tensor([4, 0, 2], dtype=torch.int32, device="cuda")
+    out = torch.zeros(3, 4096, device="cuda")
+    lib.call("ps_rmsnorm", x.data_ptr(), 4096, rows.data_ptr(), 3, w.data_ptr(), 4096, 1e-5,
+             out.data_ptr(), 4096, 0, stream())
+    xs = x[rows.long()]
+    ref = xs * torch.rsqrt(xs.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    torch.cuda.synchronize()
+    assert rel_err(out, ref) < 1e-5
+    o16 = torch.zeros(5, 4096, device="cuda", dtype=torch.bfloat16)
+    lib.call("ps_rmsnorm", x.data_ptr(), 4096, 0, 5, w.data_ptr(), 4096, 1e-5, o16.data_ptr(), 4096, 1, stream())
+    ref5 = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    torch.cuda.synchronize()
+    assert rel_err(o16.float(), ref5) < 8e-3
+
+
+def _rope_ref(x, pos, inv):
+    hd = x.shape[-1]
+    ang = pos.double()[:, None] * inv[None, :].double()
+    cos, sin = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+    a, b = x[..., : hd // 2], x[..., hd // 2:]
+    return torch.cat([a * cos - b * sin, b * cos + a * sin], -1)
+
+
+@pytest.mark.parametrize("hd,h,kv,qk", [(128, 32, 8, False), (64, 8, 8, False), (128, 32, 4, True)])
+def test_qkv_rope_append(hd, h, kv, qk):
+    lib = L()
+    T, B, cap = 6, 3, 40
+    rows = (h + 2 * kv) * hd
+    qkv = torch.randn(T, rows, device="cuda")
+    pos = torch.tensor([3, 4, 5, 0, 9, 10], dtype=torch.int32, device="cuda")
+    req = torch.tensor([2, 2, 2, 0, 1, 1], dtype=torch.int32, device="cuda")
+    inv = 1.0 / (10000.0 ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
+    ang = torch.arange(cap, dtype=torch.float64)[:, None] * inv[None, :]
+    table = torch.stack([torch.cos(ang), torch.sin(ang)], -1).float().cuda()
+    cache = torch.zeros(cap, B, 2 * kv * hd, dtype=torch.bfloat16, device="cuda")
+    qn = (1 + 0.1 * torch.randn(hd, device="cuda")).to(torch.bfloat16) if qk else None
+    kn = (1 + 0.1 * torch.randn(hd, device="cuda")).to(torch.bfloat16) if qk else None
+    src = qkv.clone()
+    lib.call("ps_qkv_rope_append", qkv.data_ptr(), rows, T, h, kv, hd, pos.data_ptr(), req.data_ptr(),
+             cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd, table.data_ptr(),
+             qn.data_ptr() if qk else 0, kn.data_ptr() if qk else 0, 1e-6, stream())
+    torch.cuda.synchronize()
+    q = src[:, : h * hd].view(T, h, hd)
+    k = src[:, h * hd:(h + kv) * hd].view(T, kv, hd)
+    v = src[:, (h + kv) * hd:].view(T, kv, hd)
+    if qk:
+        q = q * torch.rsqrt(q.pow(2).mean(-1, keepdim=True) + 1e-6) * qn.float()
+        k = k * torch.rsqrt(k.pow(2).mean(-1, keepdim=True) + 1e-6) * kn.float()
+    q = _rope_ref(q.cpu(), pos.cpu(), inv).cuda()
+    k = _rope_ref(k.cpu(), pos.cpu(), inv).cuda()
+    assert rel_err(qkv[:, : h * hd].view(T, h, hd), q) < 1e-5
+    for t in range(T):
+        row = cache[pos[t], req[t]].float()
+        assert rel_err(row[: kv * hd].view(kv, hd), k[t]) < 8e-3
+        assert rel_err(row[kv * hd:].view(kv, hd), v[t]) < 8e-3
+
+
+def _attn_ref(q, K, V, qpos):
+    # q [T, h, hd]; K, V [S, kvh, hd]
+    h, kvh = q.shape[1], K.shape[1]
+    G = h // kvh
+    Kr, Vr = K.repeat_interleave(G, 1), V.repeat_interleave(G, 1)
+    s = torch.einsum("thd,shd->hts", q, Kr) / math.sqrt(q.shape[-1])
+    mask = torch.arange(K.shape[0], device=q.device)[None, :] > qpos[:, None]
+    s = s.masked_fill(mask[None], float("-inf"))
+    return torch.einsum("hts,shd->thd", torch.softmax(s, -1), Vr)
+
+
+@pytest.mark.parametrize("hd,h,kv,lens", [(128, 32, 8, [2304]), (128, 32, 8, [1, 17, 640, 300]),
+                                          (64, 8, 8, [160, 5]), (128, 64, 8, [4224]),
+                                          (128, 32, 4, [1000])])
+def test_attn_decode(hd, h, kv, lens):
+    lib = L()
+    B, cap = len(lens), max(lens)
+    g = torch.Generator(device="cuda").manual_seed(sum(lens))
+    cache = torch.randn(cap, B, 2, kv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    q = torch.randn(B, h * hd, device="cuda", generator=g)
+    ln = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = torch.zeros(B, h * hd, device="cuda")
+    splits = math.ceil(cap / 256)
+    ws = torch.zeros(B * h * splits * (hd + 2), device="cuda")
+    lib.call("ps_attn_decode", q.data_ptr(), h * hd, B, h, kv, hd, 0, cache.data_ptr(), 2 * kv * hd,
+             B * 2 * kv * hd, ln.data_ptr(), cap, 1 / math.sqrt(hd), out.data_ptr(), h * hd,
+             ws.data_ptr(), ws.numel(), stream())
+    torch.cuda.synchronize()
+    for b, n in enumerate(lens):
+        K = cache[:n, b, 0].float()
+        V = cache[:n, b, 1].float()
+        ref = _attn_ref(q[b].view(1, h, hd), K, V, torch.tensor([n - 1], device="cuda"))
+        assert rel_err(out[b].view(1, h, hd), ref) < 1e-4
+
+
+@pytest.mark.parametrize("hd,h,kv,seqs", [(128, 32, 8, [(0, 2048)]), (64, 8, 8, [(0, 128)]),
+                                          (128, 32, 8, [(0, 100), (37, 64), (500, 5)]),
+                                          (128, 32, 4, [(0, 300)])])
+def test_attn_prefill(hd, h, kv, seqs):
+    lib = L()
+    B = len(seqs)
+    cap = max(p0 + n for p0, n in seqs)
+    g = torch.Generator(device="cuda").manual_seed(cap + B)
+    cache = torch.randn(cap, B, 2, kv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    T = sum(n for _, n in seqs)
+    q = torch.randn(T, h * hd, device="cuda", generator=g)
+    q_start = np.cumsum([0] + [n for _, n in seqs]).astype(np.int32)
+    qs = torch.tensor(q_start, device="cuda")
+    p0 = torch.tensor([p for p, _ in seqs], dtype=torch.int32, device="cuda")
+    out = torch.zeros(T, h * hd, device="cuda", dtype=torch.bfloat16)
+    lib.call("ps_attn_prefill", q.data_ptr(), h * hd, B, qs.data_ptr(), p0.data_ptr(), 0,
+             max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd,
+             1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
+    torch.cuda.synchronize()
+    for b, (s0, n) in enumerate(seqs):
+        K = cache[: s0 + n, b, 0].float()
+        V = cache[: s0 + n, b, 1].float()
+        qb = q[q_start[b]:q_start[b] + n].view(n, h, hd)
+        ref = _attn_ref(qb, K, V, torch.arange(s0, s0 + n, device="cuda"))
+        assert rel_err(out[q_start[b]:q_start[b] + n].float().view(n, h, hd), ref) < 2e-2
+
+
+def test_argmax_ties_lowest_index():
+    lib = L()
+    x = torch.randn(4, 128256, device="cuda")
+    x[1, 77] = 1e9
+    x[1, 5000] = 1e9
+    out = torch.zeros(4, dtype=torch.int32, device="cuda")
+    lib.call("ps_argmax", x.data_ptr(), 4, 128256, 128256, out.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert out.tolist() == torch.argmax(x, -1).int().tolist()
+    assert out[1].item() == 77
+
+
+def test_embed_gather_zero_copy():
+    lib = L()
+    V, d = 1000, 512
+    table = torch.randn(V, d).to(torch.bfloat16)
+    host = lib.host_alloc(V * d * 2, mapped=True)
+    import ctypes
+    ctypes.memmove(host, table.data_ptr(), V * d * 2)
+    ids = torch.tensor([5, 999, 0], dtype=torch.int32, device="cuda")
+    out = torch.zeros(3, d, device="cuda")
+    lib.call("ps_embed_gather", host, ids.data_ptr(), 3, d, out.data_ptr(), d, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), table[ids.cpu().long()].float())
+    lib.host_free(host)
+
+
+def test_upload_small():
+    lib = L()
+    arr = np.arange(1000, dtype=np.int32)
+    dst = torch.zeros(1000, dtype=torch.int32, device="cuda")
+    lib.call("ps_upload_small", dst.data_ptr(), arr.ctypes.data, arr.nbytes, stream())
+    torch.cuda.synchronize()
+    assert dst.cpu().numpy().tolist() == arr.tolist()
+
+
+def test_weight_init_bit_exact_vs_oracle():
+    from oracle import model_ref
+    lib = L()
+    n_rows, cols = 300, 4096
+    buf = torch.zeros(n_rows * cols, dtype=torch.int16, device="cuda")
+    sd = model_ref.seed_of(3, "L1.wo")
+    sc, bi = model_ref.scale_bias("L1.wo", cols)
+    # generate in two chunks to exercise the offset argument
+    half = (n_rows // 2) * cols
+    lib.call("ps_init_uniform_bf16", buf.data_ptr(), half, sd, 0, sc, bi, stream())
+    lib.call("ps_init_uniform_bf16", buf.data_ptr() + half * 2, n_rows * cols - half, sd, half, sc, bi, stream())
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy().view(np.uint16).reshape(n_rows, cols)
+    np.testing.assert_array_equal(got, model_ref.bf16_bits(3, "L1.wo", n_rows, cols))
+    gu = torch.zeros(2 * 50 * cols, dtype=torch.int16, device="cuda")
+    sa, sb = model_ref.seed_of(3, "L1.w_gate"), model_ref.seed_of(3, "L1.w_up")
+    sc, bi = model_ref.scale_bias("L1.w_gate", cols)
+    lib.call("ps_init_interleaved_bf16", gu.data_ptr(), 50, 0, 37, cols, sa, sb, sc, bi, stream())
+    lib.call("ps_init_interleaved_bf16", gu.data_ptr() + 37 * cols * 2, 50, 37, 63, cols, sa, sb, sc, bi, stream())
+    torch.cuda.synchronize()
+    got = gu.cpu().numpy().view(np.uint16).reshape(100, cols)
+    np.testing.assert_array_equal(got, model_ref.interleaved_bits(3, "L1.w_gate", "L1.w_up", 50, cols))
