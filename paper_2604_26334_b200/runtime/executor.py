@@ -124,16 +124,9 @@ class Executor:
         self._carve_fixed()
         self.residency: dict[int, tuple] = {}
         self.tier = None
-        max_pinned = max(self._pinned_bytes(p) for p in plans.values())
-        free_for_ring = self.arena.free_bytes - max_pinned
-        ring_bytes = max(0, min(ring_cap, free_for_ring)) // 256 * 256
-        self.chunk = min(chunk_bytes, max(1 << 16, ring_bytes // 6 // 256 * 256))
-        need = self.kv_layer_bytes + 3 * self.chunk
-        if ring_bytes < need:
-            raise InfeasibleBudget(float(budget_bytes),
-                                   float(budget_bytes) - free_for_ring + need, "copy-engine ring")
-        self.ring = CopyRing(self.arena.alloc_high("ring", ring_bytes), ring_bytes, self.h2d,
-                             self.events)
+        self.chunk_cap, self.ring_cap = chunk_bytes, ring_cap
+        self.fixed_high = self.arena.high          # the ring is carved below this per tier
+        self.ring = None
         self.stats: list[PassStats] = []
         self.host_tokens: list = []
         self._prev_sample_slots = None
@@ -245,9 +238,34 @@ class Executor:
                 self.kv_mode[s.layer_index] = mode
             else:
                 self.residency[s.id] = (mode, 0)
+        self._carve_ring(tier)
         L.call("ps_stream_synchronize", self.cs)
         self.tier = tier
         return moved
+
+    def _carve_ring(self, tier: int) -> None:
+        """The staging ring takes what the tier's pinned set leaves (<= ring_cap).
+
+        A tier that streams nothing (every shard pinned or zero-copy) needs no
+        ring; one that streams needs room for a layer's KV prefix plus a few
+        pieces, else the budget is infeasible for this executor."""
+        self.arena.high = self.fixed_high
+        self.arena.high_marks.pop("ring", None)
+        free = self.arena.free_bytes
+        ring_bytes = max(0, min(self.ring_cap, free)) // 256 * 256
+        self.chunk = min(self.chunk_cap, max(1 << 16, ring_bytes // 6 // 256 * 256))
+        staged = ("stream", "zerocopy") if tier > GEMV_MAX_T else ("stream",)
+        streams = any(m in staged for m, _ in self.residency.values()) or \
+            any(m in staged for m in self.kv_mode.values())
+        need = self.kv_layer_bytes + 3 * self.chunk
+        if streams and ring_bytes < need:
+            raise InfeasibleBudget(float(self.arena.capacity),
+                                   float(self.arena.capacity - free + need), "copy-engine ring")
+        if ring_bytes == 0:
+            self.ring = None
+            return
+        self.ring = CopyRing(self.arena.alloc_high("ring", ring_bytes), ring_bytes, self.h2d,
+                             self.events)
 
     # --------------------------------------------------------------- helpers
     def _wait(self, ev: int) -> None:

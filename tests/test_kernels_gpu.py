@@ -91,7 +91,7 @@ def test_gemm_tcgen05(M, N, K, epi):
         ldc = N
     lib.call("ps_gemm_bf16", A.data_ptr(), M, K, K, B.data_ptr(), N, K, C.data_ptr(), ldc, epi, stream())
     torch.cuda.synchronize()
-    tol = 1e-5 if epi in (0, 1) else 8e-3   # bf16 output rounding
+    tol = 4e-5 if epi in (0, 1) else 8e-3   # fp32 accumulation order / bf16 output rounding
     assert rel_err(C.float(), ref) < tol
 
 

@@ -5,4 +5,4 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gp
 timeout 900 python -m pytest tests/test_kernels_gpu.py -q -m gpu -p no:cacheprovider 2>&1 | tail -60 > gpurun_out/kernels.log
 timeout 600 python -m pytest tests/test_engine_gpu.py -q -m gpu -p no:cacheprovider -x 2>&1 | tail -60 > gpurun_out/engine.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-tail -3 gpurun_out/kernels.log gpurun_out/engine.log gpurun_out/smoke.log
+for f in kernels engine smoke; do echo == $f; tail -n 3 gpurun_out/$f.log; done
