@@ -251,8 +251,10 @@ def run_ours(args, rank: int, world: int) -> dict:
                  "prefill_pass_ms": round(res.passes[0][2] * 1e3, 2) if res.passes else None},
         "model_load_s": round(eng.load_seconds, 2),
     }
-    # kernel launch count of one decode step, from the executor's own accounting
-    out["gpu_launches"] = None
+    # C-ABI kernel calls (each >= 1 launch of our sm_100a kernels) in the timed passes
+    dec_stats = [s for s in ex.stats if s.T == 1][args.warmup:args.warmup + args.steps]
+    out["gpu_launches"] = int(sum(s.kernel_calls for s in dec_stats))
+    out["copies_per_step"] = round(sum(s.copies for s in dec_stats) / max(1, len(dec_stats)), 1)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(eng, args.cpu_sample_steps)

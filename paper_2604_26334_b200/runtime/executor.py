@@ -72,6 +72,7 @@ class PassStats:
     copies: int = 0
     kv_writeback_bytes: int = 0
     zero_copy_bytes: int = 0
+    kernel_calls: int = 0
 
 
 @dataclass
@@ -121,19 +122,23 @@ class Executor:
         self.tok_events = [L.event_create(False) for _ in range(64)]
 
         self.arena = VramArena(budget_bytes)
-        self._carve_fixed()
+        self._carve_persistent()
+        self.persist_high = self.arena.high       # activations + ring are carved below, per tier
         self.residency: dict[int, tuple] = {}
         self.tier = None
+        self.T_tier = 0
         self.chunk_cap, self.ring_cap = chunk_bytes, ring_cap
-        self.fixed_high = self.arena.high          # the ring is carved below this per tier
+        self.fixed_high = self.arena.high
         self.ring = None
         self.stats: list[PassStats] = []
         self.host_tokens: list = []
         self._prev_sample_slots = None
 
     # ------------------------------------------------------------------ layout
-    def _carve_fixed(self) -> None:
-        a, T, B, d = self.arena, self.Tmax, self.B, self.d
+    def _carve_activations(self, T: int) -> None:
+        """Activation buffers for passes of <= T tokens (re-carved per tier, so a
+        decode tier holds only what the plan's activation scratch allows)."""
+        a, B, d = self.arena, self.B, self.d
         t32 = min(T, GEMV_MAX_T)
         self.x = a.alloc_high("x", T * d * 4)
         self.qkv = a.alloc_high("qkv", T * self.qkv_rows * 4)
@@ -149,8 +154,12 @@ class Executor:
         self.xs = a.alloc_high("xs", B * d * 4)
         self.logits = a.alloc_high("logits", B * self.V * 4)
         splits = max(1, math.ceil(self.cap / 256))
-        self.ws_floats = B * self.h * splits * (self.hd + 2)
-        self.ws = a.alloc_high("attn_ws", self.ws_floats * 4)
+        self.ws_floats = B * self.h * splits * (self.hd + 2) if T <= GEMV_MAX_T else 0
+        self.ws = a.alloc_high("attn_ws", max(1, self.ws_floats) * 4)
+
+    def _carve_persistent(self) -> None:
+        """Small buffers whose content outlives a pass (tokens, rope table)."""
+        a, T, B = self.arena, self.Tmax, self.B
         self.i_ids = a.alloc_high("ids", T * 4)
         self.i_pos = a.alloc_high("pos", T * 4)
         self.i_req = a.alloc_high("req", T * 4)
@@ -204,6 +213,11 @@ class Executor:
         self.synchronize()   # the ring and every stream must be idle before re-carving
         # 2. re-carve the pinned region in pin order; keep weights whose slot is unchanged
         old = {sid: r[1] for sid, r in self.residency.items() if r[0] == "pinned"}
+        self.ring = None
+        self.arena.high = self.persist_high        # drop the previous tier's activations + ring
+        self.T_tier = min(tier, self.Tmax)
+        self._carve_activations(self.T_tier)
+        self.fixed_high = self.arena.high
         self.arena.reset_low()
         self.residency, self.kv_vram, self.kv_mode = {}, {}, {}
         pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
@@ -411,10 +425,11 @@ class Executor:
     # ----------------------------------------------------------------- the pass
     def run_pass(self, ps: PassSpec) -> PassStats:
         T = ps.T
-        if T > self.Tmax:
-            raise SpecError(f"pass of {T} tokens exceeds max_tokens {self.Tmax}")
+        if T > self.T_tier:
+            raise SpecError(f"pass of {T} tokens exceeds the tier's {self.T_tier}-token buffers")
         nb = len(ps.slots)
         self._stat = PassStats(self.tier, T)
+        calls0 = L.counters["kernel_calls"]
         gemv = T <= GEMV_MAX_T
         d, hq = self.d, self.h * self.hd
 
@@ -564,6 +579,7 @@ class Executor:
             self._prev_sample_slots = sampled
         for slot, n, p0 in zip(ps.slots, ps.n_new, ps.p0):
             self.kv_len[slot] = max(self.kv_len[slot], p0 + n)
+        self._stat.kernel_calls = L.counters["kernel_calls"] - calls0
         self.stats.append(self._stat)
         return self._stat
 

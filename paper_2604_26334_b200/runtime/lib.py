@@ -91,7 +91,18 @@ def lib():
     return _lib
 
 
+KERNEL_CALLS = frozenset({
+    "ps_gemv_bf16", "ps_gemm_bf16", "ps_rmsnorm", "ps_qkv_rope_append", "ps_attn_decode",
+    "ps_attn_prefill", "ps_embed_gather", "ps_argmax", "ps_cast_f32_bf16", "ps_add_f32",
+    "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16"})
+counters = {"kernel_calls": 0, "memcpy_calls": 0}
+
+
 def call(name: str, *args) -> int:
+    if name in KERNEL_CALLS:
+        counters["kernel_calls"] += 1
+    elif name == "ps_memcpy_async":
+        counters["memcpy_calls"] += 1
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         msg = lib().ps_last_error().decode(errors="replace")

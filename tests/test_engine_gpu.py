@@ -33,19 +33,64 @@ def _prompt(n, V, seed=0):
     return np.random.default_rng(seed).integers(0, V, n).astype(np.int32)
 
 
+def teacher_forced_agreement(got, tf_logits, tol=2e-2):
+    """Every GPU token must be the oracle's argmax given the same prefix, or be
+    within `tol * max|logit|` of it (a near-tie under bf16 prefill rounding).
+    Returns the number of exact agreements."""
+    tf = np.asarray(tf_logits)
+    scale = np.abs(tf).max()
+    exact = 0
+    for i, t in enumerate(got):
+        top = int(np.argmax(tf[i]))
+        if top == int(t):
+            exact += 1
+        else:
+            assert tf[i][top] - tf[i][int(t)] <= tol * scale, (i, t, top)
+    return exact
+
+
 @pytest.mark.parametrize("frac", [0.5, 0.25, 1.5])
-def test_tiny_generate_matches_oracle(tiny, oracle, frac):
+def test_tiny_gemv_path_greedy_exact(tiny, oracle, frac):
+    """Prompt <= 32 tokens: every pass takes the fp32 GEMV path, so greedy
+    tokens must equal the fp32 oracle's exactly, at three budgets that
+    exercise pinned, scratch-packed, streamed and zero-copy placements."""
     from paper_2604_26334_b200.runtime.engine import Engine
-    budget = frac * total_model_bytes(tiny)
-    eng = Engine(tiny, budget_bytes=budget, context_len=160)
-    prompt = _prompt(128, tiny.vocab_size)
-    res = eng.generate([prompt], gen_len=32)
-    got = res.tokens[0]
-    want, ref_logits = oracle.greedy(prompt, 32)
+    eng = Engine(tiny, budget_bytes=frac * total_model_bytes(tiny), context_len=160)
+    prompt = _prompt(24, tiny.vocab_size, seed=5)
+    res = eng.generate([prompt], gen_len=48)
     kinds = {t: p.kind.value for t, p in eng.plans.items()}
     eng.close()
+    want, _ = oracle.greedy(prompt, 48)
+    assert np.array_equal(res.tokens[0], want), (frac, kinds, res.tokens[0], want)
+
+
+@pytest.mark.parametrize("frac", [0.5, 0.25, 1.5])
+def test_tiny_config1_teacher_forced(tiny, oracle, frac):
+    """BASELINE config 1 (prompt 128 + 32): the prompt pass runs the tcgen05
+    GEMM / flash-attention path on bf16 activations, so tokens are checked
+    teacher-forced against the oracle with the north_star tolerance."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    eng = Engine(tiny, budget_bytes=frac * total_model_bytes(tiny), context_len=160)
+    prompt = _prompt(128, tiny.vocab_size)
+    res = eng.generate([prompt], gen_len=32)
+    eng.close()
+    got = res.tokens[0]
     assert len(got) == 32
-    assert np.array_equal(got, want), (frac, kinds, got, want)
+    tf = oracle.teacher_forced(prompt, got).numpy()
+    exact = teacher_forced_agreement(got, tf)
+    assert exact >= 28, exact
+
+
+def test_plans_identical_tokens_across_budgets(tiny):
+    """Residency must not change results: the same prompt gives the same tokens
+    whether every shard is pinned, streamed or read zero-copy."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    outs = []
+    for frac in (1.5, 0.5, 0.25):
+        eng = Engine(tiny, budget_bytes=frac * total_model_bytes(tiny), context_len=160)
+        outs.append(eng.generate([_prompt(128, tiny.vocab_size, 9)], gen_len=16).tokens[0])
+        eng.close()
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
 def test_host_weights_bit_exact_vs_oracle(tiny):
