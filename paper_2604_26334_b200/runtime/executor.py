@@ -371,14 +371,20 @@ class Executor:
 
         pieces = self._pieces(sid, names, {c.tensor for c in consumers if c.even_rows})
         host = self.w.shard_ptr(sid)
-        live: list = []       # [region, pending consumer set]
+        # A piece is released once nothing enqueued later reads it: matrix rows as
+        # soon as their consumer has been enqueued for them ("rows" token), small
+        # tensors (norms, q/k norms) when every consumer that reads them is done.
+        live: list = []       # [region, pending tokens]
+
+        def discharge(entry, token):
+            entry[1].discard(token)
+            if not entry[1] and entry in live:
+                self.ring.seal(entry[0], [self._record(self.cs)])
+                live.remove(entry)
 
         def done(i):
             for entry in live[:]:
-                entry[1].discard(i)
-                if not entry[1]:
-                    self.ring.seal(entry[0], [self._record(self.cs)])
-                    live.remove(entry)
+                discharge(entry, i)
 
         for b0, b1, items in pieces:
             region, pdev, arrived = self.ring.upload(host + b0, b1 - b0, f"s{sid}@{b0}")
@@ -386,7 +392,10 @@ class Executor:
             self._stat.copies += 1
             pending = set()
             for name, _, _ in items:
-                pending |= readers[name]
+                rows_consumer = own.get(name) if blob.tensors[name].rows > 1 else None
+                if rows_consumer is not None:
+                    pending.add(("rows", name))
+                pending |= {i for i in readers[name] if i != rows_consumer}
             entry = [region, pending]
             live.append(entry)
             self._wait(arrived)
@@ -398,6 +407,8 @@ class Executor:
                 if name in own:
                     advance_to(own[name])
                     consumers[ci].fn(ptr, r0, r1)
+                    if t.rows > 1:
+                        discharge(entry, ("rows", name))
                     if r1 == t.rows:
                         done(ci)
                         ci += 1
