@@ -73,6 +73,10 @@ int ps_event_elapsed_ms(void* start, void* stop, float* ms);
  * SWIGLU writes N/2 columns. */
 int ps_gemv_bf16(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
                  float* y, int ldy, int epilogue, void* stream);
+/* Same, with the work decomposition forced (tuning / tests): rows per warp (2|4),
+ * ksplit warps per row group (1|2|4|8, 0 = auto), grid cap (0 = 148 x 6 CTAs). */
+int ps_gemv_bf16_cfg(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
+                     float* y, int ldy, int epilogue, void* stream, int rows, int ksplit, int grid_cap);
 
 /* ---- K3: tcgen05/TMEM/TMA GEMM (prefill, batched projections) ---------------
  * Same MATMUL requests at t >= 64. C[M x N] (epi)= A[M x K] * B[N x K]^T,

@@ -4,10 +4,16 @@
 // (`pkg/src/shardplan/model_graph.py:147-153,173-179,202-209`) at t <= 32
 // new tokens. y[t, n] = sum_k x[t, k] * W[n, k], W row-major [N x K] bf16,
 // fp32 accumulation. HBM-bound on resident or ring-staged weights: every
-// weight byte is read exactly once with 128-bit non-allocating loads, each
-// lane keeping UNROLL x ROWS loads in flight, and each warp reduces its
-// rows with shuffles. The same kernel reads host-mapped weights (K8,
-// zero-copy over PCIe) when W points into cudaHostAllocMapped memory.
+// weight byte is read exactly once with 128-bit non-allocating loads.
+//
+// Work decomposition: a CTA of 8 warps owns tiles of rows; inside a tile
+// the 8 warps form (8 / KSPLIT) row groups of ROWS rows, and the KSPLIT
+// warps of a group split K (partials reduced through shared memory). The
+// host picks KSPLIT so one launch puts enough 16-byte loads in flight to
+// cover HBM latency even for the ~50 MB ring pieces of a decode pass, and
+// sizes the grid to the resident-CTA capacity (148 SMs x 6), looping over
+// tiles (grid-stride) so warps do not retire after one short burst.
+// The same kernel reads host-mapped weights (K8, zero-copy over PCIe).
 //
 // Epilogues: STORE (y = acc), ACCUM (y += acc, fused residual add),
 // SWIGLU (rows interleaved gate/up: y[t, j] = silu(acc[2j]) * acc[2j+1]).
@@ -17,174 +23,231 @@
 namespace ps {
 
 constexpr int GEMV_WARPS = 8;
+constexpr int GEMV_CTAS_PER_SM = 6;
 
-template <int T, int ROWS, int EPI>
+template <int T, int ROWS, int KSPLIT, int EPI>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
-gemv_bf16_kernel(const float* __restrict__ x, int ldx, const __nv_bfloat16* __restrict__ W,
-                 int N, int K, long long ldw, float* __restrict__ y, int ldy) {
+gemv_bf16_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W,
+                 int N, int K, long long ldw, int kpart, float* __restrict__ y, int ldy) {
+  constexpr int GROUPS = GEMV_WARPS / KSPLIT;
+  constexpr int UNROLL = (T == 1) ? 8 : (T <= 4 ? 4 : 2);   // 16-byte loads in flight per row
+  constexpr int STEP = 256;  // 32 lanes x 8 bf16
+  __shared__ float part[GEMV_WARPS][ROWS * T];
+
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int row0 = (blockIdx.x * GEMV_WARPS + warp) * ROWS;
-  if (row0 >= N) return;
+  const int grp = warp / KSPLIT, kp = warp - grp * KSPLIT;
+  const int k_begin = kp * kpart;
+  const int k_end = min(K, k_begin + kpart);
+  const int rows_per_tile = GROUPS * ROWS;
+  const int n_tiles = (N + rows_per_tile - 1) / rows_per_tile;
 
-  float acc[ROWS][T];
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int row0 = tile * rows_per_tile + grp * ROWS;
+    float acc[ROWS][T];
 #pragma unroll
-  for (int r = 0; r < ROWS; ++r)
+    for (int r = 0; r < ROWS; ++r)
 #pragma unroll
-    for (int t = 0; t < T; ++t) acc[r][t] = 0.f;
+      for (int t = 0; t < T; ++t) acc[r][t] = 0.f;
+    const __nv_bfloat16* wrow[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) wrow[r] = W + (long long)min(row0 + r, N - 1) * ldw;
 
-  const __nv_bfloat16* wrow[ROWS];
+    // bursts of UNROLL steps: all loads of a burst are issued (predicated) before use
+    for (int kb = k_begin + lane * 8; kb < k_end; kb += UNROLL * STEP) {
+      uint4 wv[UNROLL][ROWS];
 #pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    int rr = row0 + r < N ? row0 + r : N - 1;  // clamp; result discarded
-    wrow[r] = W + (long long)rr * ldw;
-  }
-
-  constexpr int UNROLL = (T <= 2) ? 4 : 2;
-  constexpr int STEP = 256;  // 32 lanes x 8 bf16
-  int k = lane * 8;
-  // main body: UNROLL steps per iteration, all weight loads issued first
-  for (; k + (UNROLL - 1) * STEP < K; k += UNROLL * STEP) {
-    uint4 wv[UNROLL][ROWS];
+      for (int u = 0; u < UNROLL; ++u)
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u)
+        for (int r = 0; r < ROWS; ++r)
+          wv[u][r] = (kb + u * STEP < k_end) ? ld_stream(wrow[r] + kb + u * STEP) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r) wv[u][r] = ld_stream(wrow[r] + k + u * STEP);
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-#pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const float4* xp = reinterpret_cast<const float4*>(x + (long long)t * ldx + k + u * STEP);
-        float4 a = __ldg(xp), b = __ldg(xp + 1);
-#pragma unroll
-        for (int r = 0; r < ROWS; ++r) {
-          uint4 w = wv[u][r];
-          float s = acc[r][t];
-          s = fmaf(a.x, bf16_lo(w.x), s); s = fmaf(a.y, bf16_hi(w.x), s);
-          s = fmaf(a.z, bf16_lo(w.y), s); s = fmaf(a.w, bf16_hi(w.y), s);
-          s = fmaf(b.x, bf16_lo(w.z), s); s = fmaf(b.y, bf16_hi(w.z), s);
-          s = fmaf(b.z, bf16_lo(w.w), s); s = fmaf(b.w, bf16_hi(w.w), s);
-          acc[r][t] = s;
-        }
-      }
-    }
-  }
-  // tail: single steps (K is a multiple of 8)
-  for (; k < K; k += STEP) {
-    uint4 wv[ROWS];
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) wv[r] = ld_stream(wrow[r] + k);
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const float4* xp = reinterpret_cast<const float4*>(x + (long long)t * ldx + k);
-      float4 a = __ldg(xp), b = __ldg(xp + 1);
-#pragma unroll
-      for (int r = 0; r < ROWS; ++r) {
-        uint4 w = wv[r];
-        float s = acc[r][t];
-        s = fmaf(a.x, bf16_lo(w.x), s); s = fmaf(a.y, bf16_hi(w.x), s);
-        s = fmaf(a.z, bf16_lo(w.y), s); s = fmaf(a.w, bf16_hi(w.y), s);
-        s = fmaf(b.x, bf16_lo(w.z), s); s = fmaf(b.y, bf16_hi(w.z), s);
-        s = fmaf(b.z, bf16_lo(w.w), s); s = fmaf(b.w, bf16_hi(w.w), s);
-        acc[r][t] = s;
-      }
-    }
-  }
-
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r)
-#pragma unroll
-    for (int t = 0; t < T; ++t) acc[r][t] = warp_sum(acc[r][t]);
-
-  // lanes t < T write token t (spreads the stores over lanes)
-  if (EPI == PS_EPI_SWIGLU) {
-#pragma unroll
-    for (int r = 0; r < ROWS; r += 2) {
-      int j = (row0 + r) >> 1;
-      if (row0 + r + 1 < N) {
-#pragma unroll
-        for (int t = 0; t < T; ++t)
-          if (lane == (t & 31)) y[(long long)t * ldy + j] = silu(acc[r][t]) * acc[r + 1][t];
-      }
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      if (row0 + r < N) {
+      for (int u = 0; u < UNROLL; ++u) {
+        const int k = kb + u * STEP;
+        if (k >= k_end) break;
 #pragma unroll
         for (int t = 0; t < T; ++t) {
-          if (lane == (t & 31)) {
-            float* dst = y + (long long)t * ldy + row0 + r;
-            if (EPI == PS_EPI_ACCUM) *dst += acc[r][t];
-            else *dst = acc[r][t];
+          if (t < tt) {
+            const float4* xp = reinterpret_cast<const float4*>(x + (long long)t * ldx + k);
+            float4 a = __ldg(xp), b = __ldg(xp + 1);
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+              uint4 w = wv[u][r];
+              float s = acc[r][t];
+              s = fmaf(a.x, bf16_lo(w.x), s); s = fmaf(a.y, bf16_hi(w.x), s);
+              s = fmaf(a.z, bf16_lo(w.y), s); s = fmaf(a.w, bf16_hi(w.y), s);
+              s = fmaf(b.x, bf16_lo(w.z), s); s = fmaf(b.y, bf16_hi(w.z), s);
+              s = fmaf(b.z, bf16_lo(w.w), s); s = fmaf(b.w, bf16_hi(w.w), s);
+              acc[r][t] = s;
+            }
           }
         }
       }
     }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[r][t] = warp_sum(acc[r][t]);
+
+    if (KSPLIT > 1) {
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+          for (int t = 0; t < T; ++t) part[warp][r * T + t] = acc[r][t];
+      }
+      __syncthreads();
+      if (kp == 0) {
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < KSPLIT; ++j) s += part[warp + j][r * T + t];
+            acc[r][t] = s;
+          }
+      }
+    }
+    if (kp == 0) {
+      if (EPI == PS_EPI_SWIGLU) {
+#pragma unroll
+        for (int r = 0; r < ROWS; r += 2) {
+          if (row0 + r + 1 < N) {
+#pragma unroll
+            for (int t = 0; t < T; ++t)
+              if (t < tt && lane == t) y[(long long)t * ldy + ((row0 + r) >> 1)] = silu(acc[r][t]) * acc[r + 1][t];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          if (row0 + r < N) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+              if (t < tt && lane == t) {
+                float* dst = y + (long long)t * ldy + row0 + r;
+                if (EPI == PS_EPI_ACCUM) *dst += acc[r][t];
+                else *dst = acc[r][t];
+              }
+            }
+          }
+        }
+      }
+    }
+    if (KSPLIT > 1) __syncthreads();  // part[] is reused by the next tile
   }
 }
 
+static int g_sm_count = 0;
+
+static int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+
+// Grid = min(tiles, resident CTA capacity of this instantiation): every CTA is
+// resident from the start, so the grid-stride tile loop has no second wave.
+template <int T, int ROWS, int KSPLIT, int EPI>
+static void launch4(int n_tiles, int grid_cap, cudaStream_t s, const float* x, int ldx, int tt,
+                    const __nv_bfloat16* W, int N, int K, long long ldw, int kpart, float* y, int ldy) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_bf16_kernel<T, ROWS, KSPLIT, EPI>,
+                                                  GEMV_WARPS * 32, 0);
+    if (per_sm <= 0) per_sm = 1;
+  }
+  int cap = grid_cap > 0 ? grid_cap : per_sm * sm_count();
+  dim3 grid(n_tiles < cap ? n_tiles : cap);
+  gemv_bf16_kernel<T, ROWS, KSPLIT, EPI><<<grid, GEMV_WARPS * 32, 0, s>>>(x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+}
+
+template <int T, int ROWS, int KSPLIT>
+static void launch3(int epi, int n_tiles, int grid_cap, cudaStream_t s, const float* x, int ldx, int tt,
+                    const __nv_bfloat16* W, int N, int K, long long ldw, int kpart, float* y, int ldy) {
+  if (epi == PS_EPI_STORE)
+    launch4<T, ROWS, KSPLIT, PS_EPI_STORE>(n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+  else if (epi == PS_EPI_ACCUM)
+    launch4<T, ROWS, KSPLIT, PS_EPI_ACCUM>(n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+  else
+    launch4<T, ROWS, KSPLIT, PS_EPI_SWIGLU>(n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+}
+
 template <int T, int ROWS>
-static int launch_gemv(const float* x, int ldx, const __nv_bfloat16* W, int N, int K,
-                       long long ldw, float* y, int ldy, int epi, cudaStream_t s) {
-  int rows_per_block = GEMV_WARPS * ROWS;
-  dim3 grid((N + rows_per_block - 1) / rows_per_block);
-  dim3 block(GEMV_WARPS * 32);
-  switch (epi) {
-    case PS_EPI_STORE:
-      gemv_bf16_kernel<T, ROWS, PS_EPI_STORE><<<grid, block, 0, s>>>(x, ldx, W, N, K, ldw, y, ldy);
-      break;
-    case PS_EPI_ACCUM:
-      gemv_bf16_kernel<T, ROWS, PS_EPI_ACCUM><<<grid, block, 0, s>>>(x, ldx, W, N, K, ldw, y, ldy);
-      break;
-    case PS_EPI_SWIGLU:
-      gemv_bf16_kernel<T, ROWS, PS_EPI_SWIGLU><<<grid, block, 0, s>>>(x, ldx, W, N, K, ldw, y, ldy);
-      break;
-    default:
-      ps_set_error("ps_gemv_bf16: unsupported epilogue %d", epi);
-      return PS_ERR_ARG;
+static void launch_ks(int ksplit, int epi, int n_tiles, int grid_cap, cudaStream_t s, const float* x, int ldx,
+                      int tt, const __nv_bfloat16* W, int N, int K, long long ldw, int kpart, float* y, int ldy) {
+  switch (ksplit) {
+    case 1: launch3<T, ROWS, 1>(epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy); break;
+    case 2: launch3<T, ROWS, 2>(epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy); break;
+    case 4: launch3<T, ROWS, 4>(epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy); break;
+    default: launch3<T, ROWS, 8>(epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy); break;
+  }
+}
+
+// One launch for tt <= 8 tokens; rows/ksplit/grid chosen (or forced for tuning).
+static int gemv_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw,
+                       float* y, int ldy, int epi, cudaStream_t s, int rows, int ksplit, int grid_cap) {
+  const int ROWS = 2;
+  if (rows != 2 && rows != 4) rows = ROWS;
+  if (tt > 1) rows = 2;
+  if (ksplit <= 0) {
+    // enough warps to fill every SM (64 resident), keeping >= 512 columns per warp
+    long long want = (long long)sm_count() * 64;
+    long long row_groups = (N + rows - 1) / rows;
+    ksplit = 1;
+    while (ksplit < 8 && row_groups * ksplit < want && K / (ksplit * 2) >= 256) ksplit *= 2;
+  }
+  int kpart = ((K + ksplit - 1) / ksplit + 255) / 256 * 256;
+  int rows_per_tile = (GEMV_WARPS / ksplit) * rows;
+  int n_tiles = (N + rows_per_tile - 1) / rows_per_tile;
+  if (tt == 1) {
+    if (rows == 4) launch_ks<1, 4>(ksplit, epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+    else launch_ks<1, 2>(ksplit, epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+  } else if (tt == 2) {
+    launch_ks<2, 2>(ksplit, epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+  } else if (tt <= 4) {
+    launch_ks<4, 2>(ksplit, epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+  } else {
+    launch_ks<8, 2>(ksplit, epi, n_tiles, grid_cap, s, x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
   }
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
 
-}  // namespace ps
-
-extern "C" int ps_gemv_bf16(const float* x, int ldx, int t, const void* W, int N, int K,
-                            long long ldw, float* y, int ldy, int epilogue, void* stream) {
-  using namespace ps;
+static int gemv_checked(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw, float* y,
+                        int ldy, int epilogue, void* stream, int rows, int ksplit, int grid_cap) {
   PS_REQUIRE(t >= 1 && t <= 32, "ps_gemv_bf16: t=%d outside [1, 32]", t);
   PS_REQUIRE(K % 8 == 0 && ldw % 8 == 0 && ldx % 4 == 0, "ps_gemv_bf16: K/ldw must be multiples of 8, ldx of 4");
   PS_REQUIRE(((uintptr_t)W & 15) == 0 && ((uintptr_t)x & 15) == 0, "ps_gemv_bf16: W and x must be 16-byte aligned");
+  PS_REQUIRE(epilogue == PS_EPI_STORE || epilogue == PS_EPI_ACCUM || epilogue == PS_EPI_SWIGLU,
+             "ps_gemv_bf16: unsupported epilogue %d", epilogue);
   PS_REQUIRE(epilogue != PS_EPI_SWIGLU || N % 2 == 0, "ps_gemv_bf16: SWIGLU needs an even N");
   if (N <= 0) return PS_OK;
   auto Wb = static_cast<const __nv_bfloat16*>(W);
   cudaStream_t s = (cudaStream_t)stream;
-  int rc;
-  if (t == 1) rc = launch_gemv<1, 2>(x, ldx, Wb, N, K, ldw, y, ldy, epilogue, s);
-  else if (t == 2) rc = launch_gemv<2, 2>(x, ldx, Wb, N, K, ldw, y, ldy, epilogue, s);
-  else if (t <= 4) {
-    // pad to 4 rows by launching per exact size class
-    if (t == 4) rc = launch_gemv<4, 2>(x, ldx, Wb, N, K, ldw, y, ldy, epilogue, s);
-    else rc = launch_gemv<3, 2>(x, ldx, Wb, N, K, ldw, y, ldy, epilogue, s);
-  } else {
-    // t in (4, 32]: chunks of 8 tokens
-    rc = PS_OK;
-    for (int t0 = 0; t0 < t && rc == PS_OK; t0 += 8) {
-      int tt = t - t0 < 8 ? t - t0 : 8;
-      const float* xs = x + (long long)t0 * ldx;
-      float* ys = y + (long long)t0 * ldy;
-      switch (tt) {
-        case 8: rc = launch_gemv<8, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        case 7: rc = launch_gemv<7, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        case 6: rc = launch_gemv<6, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        case 5: rc = launch_gemv<5, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        case 4: rc = launch_gemv<4, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        case 3: rc = launch_gemv<3, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        case 2: rc = launch_gemv<2, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-        default: rc = launch_gemv<1, 2>(xs, ldx, Wb, N, K, ldw, ys, ldy, epilogue, s); break;
-      }
-    }
+  for (int t0 = 0; t0 < t; t0 += 8) {  // tokens in chunks of 8 (W re-read per chunk)
+    int tt = t - t0 < 8 ? t - t0 : 8;
+    int rc = gemv_launch(x + (long long)t0 * ldx, ldx, tt, Wb, N, K, ldw, y + (long long)t0 * ldy, ldy, epilogue,
+                         s, rows, ksplit, grid_cap);
+    if (rc) return rc;
   }
-  return rc;
+  return PS_OK;
+}
+
+}  // namespace ps
+
+extern "C" int ps_gemv_bf16(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
+                            float* y, int ldy, int epilogue, void* stream) {
+  return ps::gemv_checked(x, ldx, t, W, N, K, ldw, y, ldy, epilogue, stream, 0, 0, 0);
+}
+
+extern "C" int ps_gemv_bf16_cfg(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
+                                float* y, int ldy, int epilogue, void* stream, int rows, int ksplit,
+                                int grid_cap) {
+  return ps::gemv_checked(x, ldx, t, W, N, K, ldw, y, ldy, epilogue, stream, rows, ksplit, grid_cap);
 }

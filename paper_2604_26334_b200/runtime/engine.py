@@ -109,6 +109,13 @@ class Engine:
             biggest = max(biggest, step.context_consumed + step.decoded)
         return biggest
 
+    def prepare(self, prompt_lens: list, gen_len: int) -> int:
+        """Create the executor and make the decode tier resident, as a serving
+        engine sits between requests; returns the bytes moved. TTFT measured
+        after this includes the switch into the prefill tier and back."""
+        ex = self._ensure_executor(self.max_pass_tokens(prompt_lens, gen_len))
+        return ex.set_tier(self.pick_tier(len(prompt_lens)))
+
     # ------------------------------------------------------------------ generate
     def generate(self, prompts: list, gen_len: int, timing: bool = True) -> GenerateResult:
         """Greedy generation for a batch of prompts, following the reference
