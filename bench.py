@@ -37,6 +37,21 @@ GB = 1e9
 MODEL, BUDGET, PROMPT, GEN = "llama3.1-8b", 4e9, 2048, 256
 METRIC = "decode tokens/s at 4 GB VRAM budget (Llama-3.1-8B bf16, prompt 2048 + 256)"
 
+# BASELINE.json configs: model, budget (bytes), prompt, gen, batch, description
+CONFIGS = {
+    1: ("tiny-llama", None, 128, 32, 1,
+        "BASELINE configs[0]: tiny Llama-style decoder (4L, d=512, 8 heads), prompt 128 + 32, "
+        "VRAM budget = 50% of weights"),
+    2: ("llama3.1-8b", 4e9, 2048, 256, 1,
+        "BASELINE configs[1]: Llama-3.1-8B bf16, prompt 2048 + 256 decode, batch 1, VRAM budget 4 GB"),
+    3: ("qwen3-30b-a3b", 8e9, 1024, 256, 1,
+        "BASELINE configs[2]: Qwen3-30B-A3B bf16, prompt 1024 + 256, VRAM budget 8 GB"),
+    4: ("llama3.1-8b", 8e9, 512, 128, 32,
+        "BASELINE configs[3]: Llama-3.1-8B batched mode, batch 32, prompt 512 + 128, VRAM 8 GB per GPU"),
+    5: ("llama3.3-70b", 24e9, 4096, 128, 1,
+        "BASELINE configs[4]: Llama-3.3-70B bf16, prompt 4096 + 128, VRAM budget 24 GB"),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -44,13 +59,29 @@ def parse():
     ap.add_argument("--steps", type=int, default=32)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--model", default=MODEL)
-    ap.add_argument("--budget-gb", type=float, default=BUDGET / GB)
-    ap.add_argument("--prompt", type=int, default=PROMPT)
-    ap.add_argument("--gen", type=int, default=GEN)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (1-based); 2 is the headline")
+    ap.add_argument("--model")
+    ap.add_argument("--budget-gb", type=float)
+    ap.add_argument("--prompt", type=int)
+    ap.add_argument("--gen", type=int)
+    ap.add_argument("--batch", type=int)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
-    return ap.parse_args()
+    args = ap.parse_args()
+    model, budget, prompt, gen, batch, desc = CONFIGS[args.config]
+    args.model = args.model or model
+    if args.budget_gb is None:
+        if budget is None:   # 50 % of the plan's weight bytes
+            from paper_2604_26334_b200.planning import catalog
+            from paper_2604_26334_b200.planning.graph import total_model_bytes
+            budget = 0.5 * total_model_bytes(catalog.builtin_model(args.model))
+        args.budget_gb = budget / GB
+    args.prompt = args.prompt or prompt
+    args.gen = args.gen or gen
+    args.batch = args.batch or batch
+    args.workload = desc
+    return args
 
 
 class ClockSampler:
@@ -189,11 +220,13 @@ def run_ours(args, rank: int, world: int) -> dict:
     except Exception:
         pass
     h2d_peak = measure_h2d(L)
+    B = args.batch
     ctx = args.prompt + args.gen
     gen = min(args.gen, args.warmup + args.steps + 1)
-    eng = Engine(args.model, budget_bytes=args.budget_gb * GB, context_len=ctx, batch=1)
-    prompt = np.random.default_rng(rank).integers(0, eng.spec.vocab_size, args.prompt).astype(np.int32)
-    eng.prepare([args.prompt], gen)        # decode tier resident before the request arrives
+    eng = Engine(args.model, budget_bytes=args.budget_gb * GB, context_len=ctx, batch=B)
+    rng = np.random.default_rng(rank)
+    prompts = [rng.integers(0, eng.spec.vocab_size, args.prompt).astype(np.int32) for _ in range(B)]
+    eng.prepare([args.prompt] * B, gen)    # decode tier resident before the requests arrive
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -201,41 +234,45 @@ def run_ours(args, rank: int, world: int) -> dict:
     torch.cuda.synchronize()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
         t0 = time.perf_counter()
-        res = eng.generate([prompt], gen_len=gen)
+        res = eng.generate(prompts, gen_len=gen)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     if dist:
         dist.barrier()
-    decode = [p for p in res.passes if p[1] == 1]
+    ex = eng.executor
+    decode = [p for p in res.passes if p[1] == B and p[0] == eng.pick_tier(B)]
+    dec_stats = [s for s in ex.stats if s.T == B and s.tier == eng.pick_tier(B)]
     timed = decode[args.warmup:args.warmup + args.steps]
+    timed_stats = dec_stats[args.warmup:args.warmup + args.steps]
     t_steps = sum(p[2] for p in timed)
     streamed = sum(p[3] for p in timed) / max(1, len(timed))
-    tps = len(timed) / t_steps
     t_max = t_steps
     if dist:
         t = torch.tensor([t_steps], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
-    value = world * len(timed) / t_max
+    value = world * B * len(timed) / t_max
     # end to end through the public API: all decode passes, host wall clock, tokens read back
     e2e_decode_wall = wall - res.ttft_s
-    e2e = (gen - 1) / e2e_decode_wall
-    ex = eng.executor
-    kv_wb = sum(s.kv_writeback_bytes for s in ex.stats[-len(timed):]) / max(1, len(timed))
+    e2e = B * (gen - 1) / e2e_decode_wall
+    kv_wb = sum(s.kv_writeback_bytes for s in timed_stats) / max(1, len(timed_stats))
     achieved = streamed / (t_steps / len(timed)) / GB
-    plan1 = eng.plans[1]
+    plan_dec = eng.plans[eng.pick_tier(B)]
+    metric = (f"decode tokens/s at {args.budget_gb:g} GB VRAM budget ({args.model} bf16, "
+              f"batch {B}, prompt {args.prompt} + {args.gen})")
     out = {
-        "metric": METRIC, "value": round(value, 4), "unit": "tokens/s", "n_gpus": world,
+        "metric": metric if args.config != 2 else METRIC, "value": round(value, 4),
+        "unit": "tokens/s", "n_gpus": world,
         "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(t_max / len(timed) * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "ttft_ms": round(res.ttft_s * 1e3, 2),
-        "config": {"workload": "BASELINE configs[1]: Llama-3.1-8B bf16, prompt 2048 + 256 decode, "
-                               "batch 1, VRAM budget 4 GB (random-init weights)",
-                   "model": args.model, "global_batch": world, "seq_len": ctx,
-                   "prompt": args.prompt, "gen": args.gen, "budget_gb": args.budget_gb,
+        "config": {"workload": args.workload + " (random-init weights)",
+                   "model": args.model, "global_batch": world * B, "seq_len": ctx,
+                   "prompt": args.prompt, "gen": args.gen, "budget_gb": round(args.budget_gb, 4),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "plan_tier1": plan1.kind.value, "l2": "inputs larger than L2 (13 GB streamed per step)"},
+                   "decode_tier": eng.pick_tier(B), "decode_plan": plan_dec.kind.value,
+                   "l2": f"inputs larger than L2 ({streamed / GB:.2f} GB streamed per step)"},
         "roofline": {"bound": "h2d", "achieved": round(achieved, 2), "peak": round(h2d_peak, 2),
                      "unit": "GB/s", "frac": round(achieved / h2d_peak, 4),
                      "traffic": None, "algorithmic_bytes_per_step": int(streamed),
@@ -243,7 +280,7 @@ def run_ours(args, rank: int, world: int) -> dict:
                      "what": "copy-engine weight stream (dominant stage of every decode step)"},
         "kernel_roofline": gemv_kernel_roofline(L, peaks),
         "e2e": {"value": round(e2e, 4), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(streamed), "d2h_bytes_per_step": int(kv_wb + 4),
+                "h2d_bytes_per_step": int(streamed), "d2h_bytes_per_step": int(kv_wb + 4 * B),
                 "how": "Engine.generate() on a host prompt; wall clock over all decode passes, "
                        "each token read back to pinned host memory"},
         "gpu_launches": None,
@@ -253,9 +290,10 @@ def run_ours(args, rank: int, world: int) -> dict:
         "model_load_s": round(eng.load_seconds, 2),
     }
     # C-ABI kernel calls (each >= 1 launch of our sm_100a kernels) in the timed passes
-    dec_stats = [s for s in ex.stats if s.T == 1][args.warmup:args.warmup + args.steps]
-    out["gpu_launches"] = int(sum(s.kernel_calls for s in dec_stats))
-    out["copies_per_step"] = round(sum(s.copies for s in dec_stats) / max(1, len(dec_stats)), 1)
+    out["gpu_launches"] = int(sum(s.kernel_calls for s in timed_stats))
+    out["copies_per_step"] = round(sum(s.copies for s in timed_stats) / max(1, len(timed_stats)), 1)
+    out["prefill_passes"] = [{"tier": p[0], "tokens": p[1], "ms": round(p[2] * 1e3, 2),
+                              "streamed_gb": round(p[3] / GB, 3)} for p in res.passes if p[1] != B][:4]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(eng, args.cpu_sample_steps)
