@@ -215,10 +215,10 @@ class Executor:
         old = {sid: r[1] for sid, r in self.residency.items() if r[0] == "pinned"}
         self.ring = None
         self.arena.high = self.persist_high        # drop the previous tier's activations + ring
+        self.arena.reset_low()                     # ... and its pinned region
         self.T_tier = min(tier, self.Tmax)
         self._carve_activations(self.T_tier)
         self.fixed_high = self.arena.high
-        self.arena.reset_low()
         self.residency, self.kv_vram, self.kv_mode = {}, {}, {}
         pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
                         key=lambda p: (self.shards[p.shard_id].priority,
