@@ -111,6 +111,29 @@ int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_start, cons
                     const void* kv_base, long long kv_req_stride, long long kv_row_stride,
                     float scale, void* out, int ldo, int out_bf16, void* stream);
 
+/* ---- K5: MoE router + routed experts ------------------------------------------
+ * Replace MOE_ROUTE (t, d, E) and the expert MATMUL (t*k, d, mats*eff) of
+ * `pkg/src/shardplan/model_graph.py:181-200`. Everything stays on the device:
+ * route_topk (softmax, top-k with ties to the lower id, optional renormalisation)
+ * -> plan (pairs grouped by expert, int buffer of ps_moe_plan_ints() ints)
+ * -> expert_gu (h = silu(x Wg^T) * (x Wu^T)) -> expert_down -> combine (y += sum_j w_j out_j).
+ * Expert e's gate/up rows live at expert_base + e * expert_stride + gu_off
+ * ([2*eff x d], gate/up interleaved) and its down matrix at ... + down_off ([d x eff]);
+ * expert_base may be host-mapped (zero-copy: only routed experts cross the link).
+ * [e_lo, e_hi) restricts the experts processed (a ring piece holding those experts). */
+int ps_moe_route_topk(const float* logits, int ldl, int T, int E, int k, int renorm, int* ids,
+                      float* w, void* stream);
+int ps_moe_plan_ints(int P, int E, long long* n_ints);
+int ps_moe_plan(const int* ids, int P, int E, int* plan, void* stream);
+int ps_moe_expert_gu(const void* x, int ldx, int x_bf16, const int* plan, int E, int P, int k,
+                     const void* expert_base, long long expert_stride, long long gu_off, int eff,
+                     int d, float* h, int e_lo, int e_hi, void* stream);
+int ps_moe_expert_down(const float* h, const int* plan, int E, int P, const void* expert_base,
+                       long long expert_stride, long long down_off, int eff, int d, float* out,
+                       int e_lo, int e_hi, void* stream);
+int ps_moe_combine(const float* out, const int* plan, int E, int P, const float* w, int T, int k,
+                   int d, float* y, int ldy, void* stream);
+
 /* ---- K6: embedding gather (zero-copy from host-mapped table), greedy -------
  * Not priced by the reference (embeddings are outside the plan,
  * `pkg/src/shardplan/model_graph.py:279-297`); the head's MATMUL is

@@ -140,6 +140,7 @@ class RefModel:
 
         self.embed = load("embed", V, d)
         self.layers = []
+        self.moe = hp.get("moe")
         for i in range(L):
             lw = {
                 "attn_norm": load(f"L{i}.attn_norm", 1, d)[0],
@@ -148,10 +149,16 @@ class RefModel:
                 "wv": load(f"L{i}.wv", kv * hd, d),
                 "wo": load(f"L{i}.wo", d, h * hd),
                 "ffn_norm": load(f"L{i}.ffn_norm", 1, d)[0],
-                "w_gate": load(f"L{i}.w_gate", ffn, d),
-                "w_up": load(f"L{i}.w_up", ffn, d),
-                "w_down": load(f"L{i}.w_down", d, ffn),
             }
+            if self.moe:
+                E, eff = self.moe["n_experts"], self.moe["expert_ffn_dim"]
+                lw["router"] = load(f"L{i}.router", E, d)
+                lw["experts"] = [(load(f"L{i}.e{e}.w_gate", eff, d), load(f"L{i}.e{e}.w_up", eff, d),
+                                  load(f"L{i}.e{e}.w_down", d, eff)) for e in range(E)]
+            else:
+                lw["w_gate"] = load(f"L{i}.w_gate", ffn, d)
+                lw["w_up"] = load(f"L{i}.w_up", ffn, d)
+                lw["w_down"] = load(f"L{i}.w_down", d, ffn)
             if self.qk_norm:
                 lw["q_norm"] = load(f"L{i}.q_norm", 1, hd)[0]
                 lw["k_norm"] = load(f"L{i}.k_norm", 1, hd)[0]
@@ -190,6 +197,21 @@ class RefModel:
 
     def _w(self, t: torch.Tensor) -> torch.Tensor:
         return t.float() if self.lazy else t
+
+    def _moe(self, f, lw):
+        """Qwen3-MoE block: softmax router, top-k, renormalised weights
+        (norm_topk_prob), sum of the selected SwiGLU experts."""
+        k = self.moe["top_k"]
+        probs = torch.softmax(f @ self._w(lw["router"]).T, dim=-1)
+        w, ids = torch.topk(probs, k, dim=-1)
+        w = w / w.sum(-1, keepdim=True)
+        out = torch.zeros_like(f)
+        for t in range(f.shape[0]):
+            for j in range(k):
+                wg, wu, wd = (self._w(m) for m in lw["experts"][int(ids[t, j])])
+                h = torch.nn.functional.silu(f[t] @ wg.T) * (f[t] @ wu.T)
+                out[t] += w[t, j] * (h @ wd.T)
+        return out
 
     def _rms(self, x, w):
         return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + self.eps) * w
@@ -235,8 +257,11 @@ class RefModel:
             o = torch.einsum("hts,shd->thd", torch.softmax(scores, -1), Vv).reshape(T, -1)
             x = x + o @ self._w(lw["wo"]).T
             f = self._rms(x, self._w(lw["ffn_norm"]))
-            g, u = f @ self._w(lw["w_gate"]).T, f @ self._w(lw["w_up"]).T
-            x = x + (torch.nn.functional.silu(g) * u) @ self._w(lw["w_down"]).T
+            if self.moe:
+                x = x + self._moe(f, lw)
+            else:
+                g, u = f @ self._w(lw["w_gate"]).T, f @ self._w(lw["w_up"]).T
+                x = x + (torch.nn.functional.silu(g) * u) @ self._w(lw["w_down"]).T
         return self._rms(x, self._w(self.final_norm)) @ self._w(self.lm_head).T
 
     @torch.no_grad()
@@ -266,4 +291,7 @@ def hp_from_spec(spec, arch) -> dict:
     return {"n_layers": spec.n_layers, "d_model": spec.d_model, "n_heads": spec.n_heads,
             "n_kv_heads": spec.n_kv_heads, "head_dim": spec.head_dim, "ffn_dim": spec.ffn_dim,
             "vocab_size": spec.vocab_size, "rope_theta": arch.rope_theta,
-            "rope_scaling": arch.rope_scaling, "qk_norm": arch.qk_norm, "rms_eps": arch.rms_eps}
+            "rope_scaling": arch.rope_scaling, "qk_norm": arch.qk_norm, "rms_eps": arch.rms_eps,
+            "moe": None if spec.moe is None else {
+                "n_experts": spec.moe.n_experts, "top_k": spec.moe.top_k,
+                "expert_ffn_dim": spec.moe.expert_ffn_dim}}

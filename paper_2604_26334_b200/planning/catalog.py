@@ -83,6 +83,8 @@ _B200_MODELS = {
     "qwen3-30b-a3b": _model("qwen3-30b-a3b", 48, 2048, 32, 4, 128, 6144, 151936, 40960,
                             moe=(128, 8, 768)),
     "llama3.3-70b": _model("llama3.3-70b", 80, 8192, 64, 8, 128, 28672, 128256, 131072),
+    # test-scale Qwen3-MoE-style decoder (q/k norm, 16 experts, top-4)
+    "tiny-moe": _model("tiny-moe", 2, 256, 4, 2, 64, 512, 1000, 512, moe=(16, 4, 128)),
 }
 
 # Measured on this pool's B200s: HBM copy 6544.3 GB/s and sustained bf16

@@ -88,8 +88,7 @@ class Executor:
                  kv_slots: int, context_len: int, max_tokens: int,
                  chunk_bytes: int = 64 << 20, ring_cap: int = 1 << 30):
         spec = weights.spec
-        if spec.moe is not None:
-            raise SpecError("MoE expert-group execution is not built in this round (DESIGN.md §7)")
+        self.moe = spec.moe
         self.spec, self.arch, self.w = spec, arch, weights
         self.plans = plans                       # tier -> SchedulePlan
         self.B = kv_slots
@@ -102,7 +101,7 @@ class Executor:
         s = spec
         self.d, self.h, self.kv, self.hd = s.d_model, s.n_heads, s.n_kv_heads, s.head_dim
         self.qkv_rows = (self.h + 2 * self.kv) * self.hd
-        self.ffn = s.ffn_dim
+        self.ffn = s.ffn_dim if s.moe is None else 8   # MoE layers use the expert buffers below
         self.V = s.vocab_size
         self.row_elems = 2 * self.kv * self.hd
         self.row_bytes = self.row_elems * 2
@@ -156,6 +155,17 @@ class Executor:
         splits = max(1, math.ceil(self.cap / 256))
         self.ws_floats = B * self.h * splits * (self.hd + 2) if T <= GEMV_MAX_T else 0
         self.ws = a.alloc_high("attn_ws", max(1, self.ws_floats) * 4)
+        if self.moe is not None:
+            E, k, eff = self.moe.n_experts, self.moe.top_k, self.moe.expert_ffn_dim
+            P = T * k
+            n_ints = C.c_longlong()
+            L.call("ps_moe_plan_ints", P, E, C.byref(n_ints))
+            self.m_logits = a.alloc_high("moe_logits", T * E * 4)
+            self.m_ids = a.alloc_high("moe_ids", P * 4)
+            self.m_w = a.alloc_high("moe_w", P * 4)
+            self.m_plan = a.alloc_high("moe_plan", n_ints.value * 4)
+            self.m_h = a.alloc_high("moe_h", P * eff * 4)
+            self.m_out = a.alloc_high("moe_out", P * d * 4)
 
     def _carve_persistent(self) -> None:
         """Small buffers whose content outlives a pass (tokens, rope table)."""
@@ -416,6 +426,69 @@ class Executor:
         for entry in live:
             self.ring.seal(entry[0], [self._record(self.cs)])
 
+    def _moe(self, sid: int, layer: int, T: int, gemv: bool, xn: int, norm) -> None:
+        """One MoE expert group: router -> top-k -> routed experts -> weighted sum.
+
+        Pinned groups run in place. A streamed (or CPU-placed) group in a GEMV
+        pass (t <= 32) is read zero-copy from the host blob, so only the
+        routed experts cross the link; in a GEMM pass every expert is touched,
+        and the group streams through the ring in whole-expert pieces, the
+        expert kernels running per piece over the experts it holds."""
+        moe, d = self.moe, self.d
+        E, k, eff = moe.n_experts, moe.top_k, moe.expert_ffn_dim
+        P = T * k
+        blob = self.w.layout.blobs[sid]
+        t_norm = blob.tensors[f"L{layer}.ffn_norm"]
+        t_router = blob.tensors[f"L{layer}.router"]
+        e0 = blob.tensors[f"L{layer}.e0.wgu"]
+        stride = blob.tensors[f"L{layer}.e1.wgu"].offset - e0.offset if E > 1 else blob.nbytes
+        down_off = blob.tensors[f"L{layer}.e0.wdown"].offset - e0.offset
+        mode, dev = self.residency[sid]
+        if mode == "zerocopy" and not gemv:
+            mode = "stream"
+        elif mode == "stream" and gemv:
+            mode = "zerocopy"
+
+        def route(base):
+            norm(base + t_norm.offset)
+            self._matmul(T, xn, base + t_router.offset, E, d, self.m_logits, E, L.PS_EPI_STORE)
+            L.call("ps_moe_route_topk", self.m_logits, E, T, E, k, 1, self.m_ids, self.m_w, self.cs)
+            L.call("ps_moe_plan", self.m_ids, P, E, self.m_plan, self.cs)
+
+        def experts(ebase, lo, hi):
+            L.call("ps_moe_expert_gu", xn, d, 0 if gemv else 1, self.m_plan, E, P, k, ebase, stride, 0,
+                   eff, d, self.m_h, lo, hi, self.cs)
+            L.call("ps_moe_expert_down", self.m_h, self.m_plan, E, P, ebase, stride, down_off, eff, d,
+                   self.m_out, lo, hi, self.cs)
+
+        if mode in ("pinned", "zerocopy"):
+            base = dev if mode == "pinned" else self.w.shard_ptr(sid)
+            route(base)
+            experts(base + e0.offset, 0, E)
+            if mode == "zerocopy":
+                touched = min(E, P)
+                self._stat.zero_copy_bytes += e0.offset + touched * stride
+        else:
+            host = self.w.shard_ptr(sid)
+            per_piece = max(1, (self.chunk - e0.offset) // stride)
+            lo = 0
+            first = True
+            while lo < E:
+                hi = min(E, lo + (per_piece if not first else max(1, per_piece)))
+                b0 = 0 if first else e0.offset + lo * stride
+                b1 = e0.offset + hi * stride
+                region, pdev, arrived = self.ring.upload(host + b0, b1 - b0, f"moe{sid}@{lo}")
+                self._stat.bytes_streamed += b1 - b0
+                self._stat.copies += 1
+                self._wait(arrived)
+                if first:
+                    route(pdev)
+                experts(pdev + e0.offset - b0, lo, hi)
+                self.ring.seal(region, [self._record(self.cs)])
+                first = False
+                lo = hi
+        L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
+
     def _matmul(self, T, act, W, N, K, out, ldo, epi) -> None:
         """out (epi)= act @ W[:N]^T for T tokens: GEMV on fp32 act (T <= 32)
         or the tcgen05 GEMM on bf16 act."""
@@ -493,7 +566,8 @@ class Executor:
 
         for layer in range(self.spec.n_layers):
             attn_sid = self.by_layer_kind[(layer, ShardKind.ATTENTION)].id
-            ffn_sid = self.by_layer_kind[(layer, ShardKind.FFN)].id
+            ffn_sid = self.by_layer_kind[(layer, ShardKind.FFN if self.moe is None
+                                          else ShardKind.MOE_EXPERT_GROUP)].id
             # ---- KV_i, hoisted before Attn_i
             mode = self.kv_mode[layer]
             kv_region = None
@@ -549,7 +623,10 @@ class Executor:
                     T, att, p, r1 - r0, hq, self.x + r0 * 4, d, L.PS_EPI_ACCUM)),
             ], T)
 
-            # ---- FFN_i
+            # ---- FFN_i or MoE_i
+            if self.moe is not None:
+                self._moe(ffn_sid, layer, T, gemv, xn, norm)
+                continue
             self._shard(ffn_sid, [
                 Consumer(f"L{layer}.ffn_norm", lambda p, a, b: norm(p)),
                 Consumer(f"L{layer}.wgu", lambda p, r0, r1: self._matmul(

@@ -52,6 +52,12 @@ _SIGS = {
     "ps_attn_decode": [_p, _i, _i, _i, _i, _i, _p, _p, _ll, _ll, _p, _i, _f, _p, _i, _p, _ll, _p],
     "ps_attn_prefill": [_p, _i, _i, _p, _p, _p, _i, _i, _i, _i, _p, _ll, _ll, _f, _p, _i, _i, _p],
     "ps_upload_small": [_p, _p, _i, _p],
+    "ps_moe_route_topk": [_p, _i, _i, _i, _i, _i, _p, _p, _p],
+    "ps_moe_plan_ints": [_i, _i, C.POINTER(_ll)],
+    "ps_moe_plan": [_p, _i, _i, _p, _p],
+    "ps_moe_expert_gu": [_p, _i, _i, _p, _i, _i, _i, _p, _ll, _ll, _i, _i, _p, _i, _i, _p],
+    "ps_moe_expert_down": [_p, _p, _i, _i, _p, _ll, _ll, _i, _i, _p, _i, _i, _p],
+    "ps_moe_combine": [_p, _p, _i, _i, _p, _i, _i, _i, _p, _i, _p],
     "ps_embed_gather": [_p, _p, _i, _i, _p, _i, _p],
     "ps_argmax": [_p, _i, _i, _i, _p, _p],
     "ps_cast_f32_bf16": [_p, _i, _p, _i, _i, _i, _p],
@@ -95,7 +101,8 @@ def lib():
 KERNEL_CALLS = frozenset({
     "ps_gemv_bf16", "ps_gemm_bf16", "ps_rmsnorm", "ps_qkv_rope_append", "ps_attn_decode",
     "ps_attn_prefill", "ps_embed_gather", "ps_argmax", "ps_cast_f32_bf16", "ps_add_f32",
-    "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16"})
+    "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_gemv_bf16_cfg",
+    "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine"})
 counters = {"kernel_calls": 0, "memcpy_calls": 0}
 
 

@@ -57,6 +57,7 @@ ARCHS = {
     "llama3.1-8b": Arch(rope_theta=500000.0, rope_scaling=LLAMA3_SCALING),
     "llama3.3-70b": Arch(rope_theta=500000.0, rope_scaling=LLAMA3_SCALING),
     "qwen3-30b-a3b": Arch(rope_theta=1000000.0, qk_norm=True, rms_eps=1e-6),
+    "tiny-moe": Arch(rope_theta=1000000.0, qk_norm=True, rms_eps=1e-6),
 }
 
 

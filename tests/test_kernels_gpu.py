@@ -276,3 +276,70 @@ def test_weight_init_bit_exact_vs_oracle():
     torch.cuda.synchronize()
     got = gu.cpu().numpy().view(np.uint16).reshape(100, cols)
     np.testing.assert_array_equal(got, model_ref.interleaved_bits(3, "L1.w_gate", "L1.w_up", 50, cols))
+
+
+def _moe_ref(x, router, Wgu, Wd, k):
+    """fp32 Qwen3-MoE block: softmax, top-k, renormalise, SwiGLU experts."""
+    probs = torch.softmax(x @ router.T, -1)
+    w, ids = torch.topk(probs, k, -1)
+    w = w / w.sum(-1, keepdim=True)
+    out = torch.zeros_like(x)
+    for t in range(x.shape[0]):
+        for j in range(k):
+            e = int(ids[t, j])
+            gu = Wgu[e] @ x[t]
+            h = torch.nn.functional.silu(gu[0::2]) * gu[1::2]
+            out[t] += w[t, j] * (Wd[e] @ h)
+    return out, ids, w
+
+
+@pytest.mark.parametrize("T,zero_copy,x_bf16", [(1, True, False), (3, False, False), (40, False, True)])
+def test_moe_pipeline(T, zero_copy, x_bf16):
+    lib = L()
+    E, k, d, eff = 16, 4, 256, 128
+    g = torch.Generator(device="cuda").manual_seed(T)
+    x = torch.randn(T, d, device="cuda", generator=g)
+    router = (torch.randn(E, d, device="cuda", generator=g) / 8).to(torch.bfloat16)
+    Wgu = (torch.randn(E, 2 * eff, d, device="cuda", generator=g) / 16).to(torch.bfloat16)
+    Wd = (torch.randn(E, d, eff, device="cuda", generator=g) / 11).to(torch.bfloat16)
+    # expert blob: [wgu_e | wdown_e] per expert
+    blob = torch.cat([torch.cat([Wgu[e].reshape(-1), Wd[e].reshape(-1)]) for e in range(E)]).contiguous()
+    stride = (2 * eff * d + d * eff) * 2
+    base = blob.data_ptr()
+    host = None
+    if zero_copy:
+        import ctypes
+        host = lib.host_alloc(blob.numel() * 2, mapped=True)
+        cpu = blob.cpu()
+        ctypes.memmove(host, cpu.data_ptr(), blob.numel() * 2)
+        base = host
+    s = stream()
+    logits = x @ router.float().T
+    P = T * k
+    ids = torch.zeros(P, dtype=torch.int32, device="cuda")
+    w = torch.zeros(P, device="cuda")
+    import ctypes
+    n = ctypes.c_longlong()
+    lib.call("ps_moe_plan_ints", P, E, ctypes.byref(n))
+    plan = torch.zeros(n.value, dtype=torch.int32, device="cuda")
+    h = torch.zeros(P, eff, device="cuda")
+    out = torch.zeros(P, d, device="cuda")
+    y = torch.randn(T, d, device="cuda", generator=g)
+    y0 = y.clone()
+    lib.call("ps_moe_route_topk", logits.data_ptr(), E, T, E, k, 1, ids.data_ptr(), w.data_ptr(), s)
+    lib.call("ps_moe_plan", ids.data_ptr(), P, E, plan.data_ptr(), s)
+    xin = x.to(torch.bfloat16) if x_bf16 else x
+    # process experts in two ranges, as a ring piece split would
+    for lo, hi in ((0, 7), (7, E)):
+        lib.call("ps_moe_expert_gu", xin.data_ptr(), d, 1 if x_bf16 else 0, plan.data_ptr(), E, P, k,
+                 base, stride, 0, eff, d, h.data_ptr(), lo, hi, s)
+        lib.call("ps_moe_expert_down", h.data_ptr(), plan.data_ptr(), E, P, base, stride, 2 * eff * d * 2,
+                 eff, d, out.data_ptr(), lo, hi, s)
+    lib.call("ps_moe_combine", out.data_ptr(), plan.data_ptr(), E, P, w.data_ptr(), T, k, d, y.data_ptr(), d, s)
+    torch.cuda.synchronize()
+    ref, rid, rw = _moe_ref(xin.float(), router.float(), Wgu.float(), Wd.float(), k)
+    assert torch.equal(ids.view(T, k).long(), rid)
+    assert rel_err(w.view(T, k), rw) < 1e-5
+    assert rel_err(y - y0, ref) < 1e-4
+    if host:
+        lib.host_free(host)
