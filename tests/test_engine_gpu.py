@@ -158,7 +158,9 @@ def test_tiny_moe_prefill_ring_teacher_forced():
     from paper_2604_26334_b200.runtime.model import arch_for
     spec = catalog.builtin_model("tiny-moe")
     ref = RefModel(hp_from_spec(spec, arch_for(spec)), seed=0)
-    eng = Engine(spec, budget_bytes=0.3 * total_model_bytes(spec), context_len=160, chunk_bytes=1 << 20)
+    # at 100 % of weights the tier-512 plan pins layer 0's expert group and places
+    # layer 1's on the CPU -> staged through the ring in the 128-token GEMM pass
+    eng = Engine(spec, budget_bytes=1.0 * total_model_bytes(spec), context_len=160, chunk_bytes=1 << 20)
     prompt = _prompt(128, spec.vocab_size, seed=4)
     res = eng.generate([prompt], gen_len=8)
     eng.close()

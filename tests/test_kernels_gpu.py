@@ -314,7 +314,8 @@ def test_moe_pipeline(T, zero_copy, x_bf16):
         ctypes.memmove(host, cpu.data_ptr(), blob.numel() * 2)
         base = host
     s = stream()
-    logits = x @ router.float().T
+    xin = x.to(torch.bfloat16) if x_bf16 else x
+    logits = xin.float() @ router.float().T
     P = T * k
     ids = torch.zeros(P, dtype=torch.int32, device="cuda")
     w = torch.zeros(P, device="cuda")
