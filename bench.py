@@ -245,7 +245,9 @@ def run_ours(args, rank: int, world: int) -> dict:
     timed = decode[args.warmup:args.warmup + args.steps]
     timed_stats = dec_stats[args.warmup:args.warmup + args.steps]
     t_steps = sum(p[2] for p in timed)
-    streamed = sum(p[3] for p in timed) / max(1, len(timed))
+    # bytes that crossed the host link per step: copy-engine pieces + zero-copy reads
+    streamed = sum(p[3] + p[4] for p in timed) / max(1, len(timed))
+    zero_copy = sum(p[4] for p in timed) / max(1, len(timed))
     t_max = t_steps
     if dist:
         t = torch.tensor([t_steps], device="cuda")
@@ -293,7 +295,9 @@ def run_ours(args, rank: int, world: int) -> dict:
     out["gpu_launches"] = int(sum(s.kernel_calls for s in timed_stats))
     out["copies_per_step"] = round(sum(s.copies for s in timed_stats) / max(1, len(timed_stats)), 1)
     out["prefill_passes"] = [{"tier": p[0], "tokens": p[1], "ms": round(p[2] * 1e3, 2),
-                              "streamed_gb": round(p[3] / GB, 3)} for p in res.passes if p[1] != B][:4]
+                              "streamed_gb": round(p[3] / GB, 3), "zero_copy_gb": round(p[4] / GB, 3)}
+                             for p in res.passes if p[1] != B][:4]
+    out["roofline"]["zero_copy_bytes_per_step"] = int(zero_copy)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(eng, args.cpu_sample_steps)

@@ -185,7 +185,7 @@ class Engine:
                 ev1 = L.event_create(True)
                 L.call("ps_event_record", ev1, ex.cs)
             passes.append([tier, stats.T, ev0, ev1, stats.bytes_streamed,
-                           step.context_consumed == 0 and step.decoded > 0])
+                           step.context_consumed == 0 and step.decoded > 0, stats.zero_copy_bytes])
             if step.first_prompt_done and ttft is None:
                 self._drain(ex, pending_host, out)   # first token is on the host
                 ttft = time.perf_counter() - t_start
@@ -193,9 +193,10 @@ class Engine:
         ex.synchronize()
         total = time.perf_counter() - t_start
         pass_rows = []
-        for tier, T, e0, e1, nbytes, is_decode in passes:
+        for tier, T, e0, e1, nbytes, is_decode, zc in passes:
             secs = L.event_elapsed_ms(e0, e1) / 1e3 if timing else float("nan")
-            pass_rows.append((tier, T, secs, nbytes))
+            # (tier, tokens, seconds, bytes via the copy engine, bytes read zero-copy)
+            pass_rows.append((tier, T, secs, nbytes, zc))
             if is_decode:
                 decode_tokens += T
                 decode_time += secs
