@@ -248,12 +248,10 @@ def run_ours(args, rank: int, world: int) -> dict:
     # bytes that crossed the host link per step: copy-engine pieces + zero-copy reads
     streamed = sum(p[3] + p[4] for p in timed) / max(1, len(timed))
     zero_copy = sum(p[4] for p in timed) / max(1, len(timed))
-    t_max = t_steps
-    if dist:
-        t = torch.tensor([t_steps], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-    value = world * B * len(timed) / t_max
+    # replicas: sum of tokens over ranks / max over ranks of device seconds (no data collective)
+    from paper_2604_26334_b200.runtime.replicas import aggregate
+    agg = aggregate(B * len(timed), t_steps, device="cuda")
+    t_max, value = agg["seconds_max"], agg["value"]
     # end to end through the public API: all decode passes, host wall clock, tokens read back
     e2e_decode_wall = wall - res.ttft_s
     e2e = B * (gen - 1) / e2e_decode_wall
