@@ -541,7 +541,9 @@ class Executor:
         i_lens = i_p0 + 4 * nb
         i_slot = i_lens + 4 * nb
         max_len, max_new = int(lens.max()), int(max(ps.n_new))
-        min_p0 = int(p0a.min())
+        min_p0, max_p0 = int(p0a.min()), int(p0a.max())
+        idle = [min(self.kv_len[b], max_len) for b in range(self.B) if b not in set(ps.slots)]
+        upload_rows = max([max_p0] + idle)
         use_decode_kernel = ps.decode_only and gemv
 
         if ps.ids is not None:
@@ -576,7 +578,12 @@ class Executor:
             elif mode == "zerocopy" and gemv:
                 kv_base = self._kv_host_ptr(layer)
             else:
-                prefix = min_p0 * self.B * self.row_bytes
+                # Rows [min p0, max len) of EVERY slot are written back below, so the
+                # upload must cover every valid row in that window: participants'
+                # existing rows (< max p0) and the valid rows of slots that sit this
+                # pass out. Rows past a slot's own length may hold anything: they are
+                # never read before that slot writes them.
+                prefix = upload_rows * self.B * self.row_bytes
                 room = max_len * self.B * self.row_bytes
                 wb = self.kv_writeback.get(layer)
                 if wb is not None and prefix:
