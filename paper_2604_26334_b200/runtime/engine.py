@@ -117,7 +117,8 @@ class Engine:
         return ex.set_tier(self.pick_tier(len(prompt_lens)))
 
     # ------------------------------------------------------------------ generate
-    def generate(self, prompts: list, gen_len: int, timing: bool = True) -> GenerateResult:
+    def generate(self, prompts: list, gen_len: int, timing: bool = True,
+                 on_pass=None) -> GenerateResult:
         """Greedy generation for a batch of prompts, following the reference
         loop: each iteration picks the tier for the outstanding new tokens,
         feeds prompt chunks (a finished prompt emits its first token) or one
@@ -176,6 +177,8 @@ class Engine:
             ev0 = L.event_create(True) if timing else 0
             if timing:
                 L.call("ps_event_record", ev0, ex.cs)
+            if on_pass is not None:
+                on_pass(len(passes), tier, ex)       # e.g. attach / detach a tracer
             stats = ex.run_pass(PassSpec(slots, n_new, p0, ids_arr, sample))
             if sample:
                 pending_host.append([slots[j] for j in sample])

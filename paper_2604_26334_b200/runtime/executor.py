@@ -129,6 +129,7 @@ class Executor:
         self.chunk_cap, self.ring_cap = chunk_bytes, ring_cap
         self.fixed_high = self.arena.high
         self.ring = None
+        self.tracer = None                          # runtime.tracer.Tracer when attached
         self.stats: list[PassStats] = []
         self.host_tokens: list = []
         self._prev_sample_slots = None
@@ -290,6 +291,7 @@ class Executor:
             return
         self.ring = CopyRing(self.arena.alloc_high("ring", ring_bytes), ring_bytes, self.h2d,
                              self.events)
+        self.ring.tracer = self.tracer
 
     # --------------------------------------------------------------- helpers
     def _wait(self, ev: int) -> None:
@@ -357,7 +359,7 @@ class Executor:
                 c = consumers[ci]
                 if c.tensor is not None:
                     raise SpecError(f"consumer order mismatch at {c.tensor}")
-                c.fn(None, 0, 0)
+                self._traced("core", c.fn, None, 0, 0)
                 done(ci)
                 ci += 1
 
@@ -374,7 +376,7 @@ class Executor:
                 self.ptrs[name] = base + t.offset
                 if name in own:
                     advance_to(own[name])
-                    consumers[ci].fn(base + t.offset, 0, t.rows)
+                    self._traced(name, consumers[ci].fn, base + t.offset, 0, t.rows)
                     ci += 1
             advance_to(len(consumers))
             return
@@ -416,7 +418,7 @@ class Executor:
                     self.ptrs[name] = ptr
                 if name in own:
                     advance_to(own[name])
-                    consumers[ci].fn(ptr, r0, r1)
+                    self._traced(name, consumers[ci].fn, ptr, r0, r1)
                     if t.rows > 1:
                         discharge(entry, ("rows", name))
                     if r1 == t.rows:
@@ -425,6 +427,19 @@ class Executor:
         advance_to(len(consumers))
         for entry in live:
             self.ring.seal(entry[0], [self._record(self.cs)])
+
+    def _traced(self, name, fn, *args) -> None:
+        if self.tracer is None:
+            fn(*args)
+            return
+        ev0 = self.tracer.begin(self.cs)
+        fn(*args)
+        self.tracer.end(name or "?", "compute", ev0, self.cs)
+
+    def attach_tracer(self, tracer) -> None:
+        self.tracer = tracer
+        if self.ring is not None:
+            self.ring.tracer = tracer
 
     def _moe(self, sid: int, layer: int, T: int, gemv: bool, xn: int, norm) -> None:
         """One MoE expert group: router -> top-k -> routed experts -> weighted sum.
@@ -463,8 +478,8 @@ class Executor:
 
         if mode in ("pinned", "zerocopy"):
             base = dev if mode == "pinned" else self.w.shard_ptr(sid)
-            route(base)
-            experts(base + e0.offset, 0, E)
+            self._traced(f"L{layer}.router+topk", route, base)
+            self._traced(f"L{layer}.experts", experts, base + e0.offset, 0, E)
             if mode == "zerocopy":
                 touched = min(E, P)
                 self._stat.zero_copy_bytes += e0.offset + touched * stride
@@ -482,8 +497,8 @@ class Executor:
                 self._stat.copies += 1
                 self._wait(arrived)
                 if first:
-                    route(pdev)
-                experts(pdev + e0.offset - b0, lo, hi)
+                    self._traced(f"L{layer}.router+topk", route, pdev)
+                self._traced(f"L{layer}.experts[{lo}:{hi})", experts, pdev + e0.offset - b0, lo, hi)
                 self.ring.seal(region, [self._record(self.cs)])
                 first = False
                 lo = hi
@@ -614,7 +629,10 @@ class Executor:
                     # appended rows -> the layer's host home (D2H stream), then release
                     L.call("ps_stream_wait_event", self.d2h, self._record(self.cs))
                     a, b = min_p0 * self.B * self.row_bytes, max_len * self.B * self.row_bytes
+                    ev0 = self.tracer.begin(self.d2h) if self.tracer else None
                     L.memcpy_async(self._kv_host_ptr(layer) + a, kv_base + a, b - a, self.d2h)
+                    if ev0 is not None:
+                        self.tracer.end(f"kv{layer} write-back", "d2h", ev0, self.d2h)
                     self._stat.kv_writeback_bytes += b - a
                     wb = self._record(self.d2h)
                     self.kv_writeback[layer] = wb

@@ -61,6 +61,7 @@ class CopyRing:
         self.live: deque[Region] = deque()
         self.bytes_copied = 0
         self.copies = 0
+        self.tracer = None
 
     def _reserve(self, nbytes: int, tag: str) -> Region:
         n = (nbytes + 255) // 256 * 256
@@ -93,7 +94,11 @@ class CopyRing:
         max(nbytes, reserve) bytes. Returns (region, device address, arrived event)."""
         region = self._reserve(max(nbytes, reserve), tag)
         dst = self.base + region.start
+        tr = self.tracer
+        ev0 = tr.begin(self.stream) if tr is not None and nbytes else None
         L.memcpy_async(dst, src_host, nbytes, self.stream)
+        if ev0 is not None:
+            tr.end(f"{tag} ({nbytes >> 20} MiB)", "h2d", ev0, self.stream)
         ev = self.events.next()
         L.call("ps_event_record", ev, self.stream)
         self.bytes_copied += nbytes
