@@ -84,6 +84,11 @@ int ps_gemv_bf16_cfg(const float* x, int ldx, int t, const void* W, int N, int K
  * (STORE_BF16, SWIGLU: N/2 columns). */
 int ps_gemm_bf16(const void* A, int M, int K, long long lda, const void* B, int N, long long ldb,
                  void* C, int ldc, int epilogue, void* stream);
+/* Same, kernel forced (tuning / tests): 0 = auto (M > 128 -> 2), 1 = one 128 x 256 tile
+ * per CTA, 2 = persistent CTA-pair kernel (tcgen05.mma.cta_group::2, 256 x 256 tiles,
+ * double-buffered TMEM accumulator). */
+int ps_gemm_bf16_cfg(const void* A, int M, int K, long long lda, const void* B, int N, long long ldb,
+                     void* C, int ldc, int epilogue, void* stream, int variant);
 
 /* ---- K2: normalisation, RoPE, KV append ------------------------------------
  * Folded into elementwise_epsilon by the reference

@@ -47,6 +47,7 @@ _SIGS = {
     "ps_gemv_bf16": [_p, _i, _i, _p, _i, _i, _ll, _p, _i, _i, _p],
     "ps_gemv_bf16_cfg": [_p, _i, _i, _p, _i, _i, _ll, _p, _i, _i, _p, _i, _i, _i],
     "ps_gemm_bf16": [_p, _i, _i, _ll, _p, _i, _ll, _p, _i, _i, _p],
+    "ps_gemm_bf16_cfg": [_p, _i, _i, _ll, _p, _i, _ll, _p, _i, _i, _p, _i],
     "ps_rmsnorm": [_p, _i, _p, _i, _p, _i, _f, _p, _i, _i, _p],
     "ps_qkv_rope_append": [_p, _i, _i, _i, _i, _i, _p, _p, _p, _ll, _ll, _p, _p, _p, _f, _p],
     "ps_attn_decode": [_p, _i, _i, _i, _i, _i, _p, _p, _ll, _ll, _p, _i, _f, _p, _i, _p, _ll, _p],

@@ -69,9 +69,16 @@ def test_gemv_zero_copy_host_weights():
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (2048, 6144, 4096), (200, 1000, 512),
-                                   (4096, 512, 14336), (64, 256, 1536)])
+                                   (4096, 512, 14336), (64, 256, 1536), (16384, 768, 512),
+                                   (300, 28672, 256), (1, 256, 64), (257, 130, 128)])
 @pytest.mark.parametrize("epi", [0, 1, 3, 2])
-def test_gemm_tcgen05(M, N, K, epi):
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_gemm_tcgen05(M, N, K, epi, variant):
+    """variant 0 = auto, 1 = one 128x256 tile per CTA, 2 = persistent CTA-pair
+    (cta_group::2) kernel; the pair kernel's tails (M or N not a tile multiple,
+    a pair whose second CTA is entirely out of bounds) are covered."""
+    if variant == 1 and M > 4096:
+        pytest.skip("1-CTA kernel: covered at smaller M")
     lib = L()
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
@@ -89,7 +96,8 @@ def test_gemm_tcgen05(M, N, K, epi):
         if epi == 1:
             ref = ref + C
         ldc = N
-    lib.call("ps_gemm_bf16", A.data_ptr(), M, K, K, B.data_ptr(), N, K, C.data_ptr(), ldc, epi, stream())
+    lib.call("ps_gemm_bf16_cfg", A.data_ptr(), M, K, K, B.data_ptr(), N, K, C.data_ptr(), ldc, epi,
+             stream(), variant)
     torch.cuda.synchronize()
     tol = 4e-5 if epi in (0, 1) else 8e-3   # fp32 accumulation order / bf16 output rounding
     assert rel_err(C.float(), ref) < tol
