@@ -73,8 +73,11 @@ int ps_event_elapsed_ms(void* start, void* stop, float* ms);
  * SWIGLU writes N/2 columns. */
 int ps_gemv_bf16(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
                  float* y, int ldy, int epilogue, void* stream);
-/* Same, with the work decomposition forced (tuning / tests): rows per warp (2|4),
- * ksplit warps per row group (1|2|4|8, 0 = auto), grid cap (0 = 148 x 6 CTAs). */
+/* Device-resident W runs the bulk-copy kernel (8-stage cp.async.bulk ring per SM,
+ * gemv_tma.cu); host-mapped W (zero-copy) runs the register-burst kernel (gemv.cu).
+ * _cfg forces the kernel (tuning / tests): rows = 0 -> bulk-copy kernel with
+ * grid_cap CTAs (0 = one per SM); rows = 2|4 -> register-burst kernel with rows per
+ * warp, ksplit warps per row group (1|2|4|8, 0 = auto), grid cap (0 = resident CTAs). */
 int ps_gemv_bf16_cfg(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw,
                      float* y, int ldy, int epilogue, void* stream, int rows, int ksplit, int grid_cap);
 

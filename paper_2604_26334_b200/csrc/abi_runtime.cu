@@ -7,6 +7,9 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "../../include/pshard.h"
 
@@ -18,6 +21,38 @@ void ps_set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+
+// Host ranges visible to kernels (mapped cudaHostAlloc / cudaHostRegister). The
+// GEMV dispatcher reads weights that live here with the register-burst kernel
+// (zero-copy over PCIe) instead of the bulk-copy kernel.
+namespace {
+std::mutex g_host_mu;
+std::vector<std::pair<uintptr_t, size_t>> g_host_ranges;
+
+void host_range_add(const void* p, size_t n) {
+  std::lock_guard<std::mutex> g(g_host_mu);
+  g_host_ranges.emplace_back(reinterpret_cast<uintptr_t>(p), n);
+}
+
+void host_range_remove(const void* p) {
+  std::lock_guard<std::mutex> g(g_host_mu);
+  for (size_t i = 0; i < g_host_ranges.size(); ++i)
+    if (g_host_ranges[i].first == reinterpret_cast<uintptr_t>(p)) {
+      g_host_ranges.erase(g_host_ranges.begin() + i);
+      return;
+    }
+}
+}  // namespace
+
+namespace ps {
+bool is_host_ptr(const void* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  std::lock_guard<std::mutex> g(g_host_mu);
+  for (const auto& r : g_host_ranges)
+    if (a >= r.first && a < r.first + r.second) return true;
+  return false;
+}
+}  // namespace ps
 
 extern "C" {
 
@@ -45,21 +80,27 @@ int ps_host_alloc(size_t bytes, int mapped, void** out) {
   PS_REQUIRE(out != nullptr, "ps_host_alloc: out is null");
   unsigned flags = cudaHostAllocPortable | (mapped ? cudaHostAllocMapped : 0);
   PS_CHECK_CUDA(cudaHostAlloc(out, bytes, flags));
+  if (mapped) host_range_add(*out, bytes);
   return PS_OK;
 }
 
 int ps_host_free(void* ptr) {
-  if (ptr) PS_CHECK_CUDA(cudaFreeHost(ptr));
+  if (ptr) {
+    host_range_remove(ptr);
+    PS_CHECK_CUDA(cudaFreeHost(ptr));
+  }
   return PS_OK;
 }
 
 int ps_host_register(void* ptr, size_t bytes, int portable) {
   unsigned flags = cudaHostRegisterMapped | (portable ? cudaHostRegisterPortable : 0);
   PS_CHECK_CUDA(cudaHostRegister(ptr, bytes, flags));
+  host_range_add(ptr, bytes);
   return PS_OK;
 }
 
 int ps_host_unregister(void* ptr) {
+  host_range_remove(ptr);
   PS_CHECK_CUDA(cudaHostUnregister(ptr));
   return PS_OK;
 }

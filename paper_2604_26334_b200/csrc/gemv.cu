@@ -23,7 +23,6 @@
 namespace ps {
 
 constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_CTAS_PER_SM = 6;
 
 template <int T, int ROWS, int KSPLIT, int EPI>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
@@ -219,6 +218,12 @@ static int gemv_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, 
   return PS_OK;
 }
 
+bool is_host_ptr(const void* p);
+int gemv_tma_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
+                    int ldy, int epi, cudaStream_t s, int grid_cap);
+
+// rows == 0 selects the bulk-copy kernel (gemv_tma.cu) for device-resident weights;
+// host-mapped weights (zero-copy, K8) and rows = 2 | 4 use the register-burst kernel.
 static int gemv_checked(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw, float* y,
                         int ldy, int epilogue, void* stream, int rows, int ksplit, int grid_cap) {
   PS_REQUIRE(t >= 1 && t <= 32, "ps_gemv_bf16: t=%d outside [1, 32]", t);
@@ -232,6 +237,12 @@ static int gemv_checked(const float* x, int ldx, int t, const void* W, int N, in
   cudaStream_t s = (cudaStream_t)stream;
   for (int t0 = 0; t0 < t; t0 += 8) {  // tokens in chunks of 8 (W re-read per chunk)
     int tt = t - t0 < 8 ? t - t0 : 8;
+    if ((rows == 0 && !is_host_ptr(W)) || rows == -1) {  // -1: bulk-copy kernel even on host memory
+      int rc = gemv_tma_launch(x + (long long)t0 * ldx, ldx, tt, Wb, N, K, ldw, y + (long long)t0 * ldy, ldy,
+                               epilogue, s, grid_cap);
+      if (rc) return rc;
+      continue;
+    }
     int rc = gemv_launch(x + (long long)t0 * ldx, ldx, tt, Wb, N, K, ldw, y + (long long)t0 * ldy, ldy, epilogue,
                          s, rows, ksplit, grid_cap);
     if (rc) return rc;

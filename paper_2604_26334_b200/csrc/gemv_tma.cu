@@ -1,0 +1,271 @@
+// K1: decode GEMV streamed through shared memory by the bulk-copy (TMA) engine.
+//
+// Prices the same MATMUL requests as gemv.cu (`pkg/src/shardplan/model_graph.py:147-153,
+// 173-179,202-209`) at t <= 8 tokens per launch: y[t, n] (epi)= sum_k x[t, k] W[n, k],
+// W bf16 row-major [N x ldw], x / y fp32, fp32 accumulation.
+//
+// Why a second GEMV: the register-burst kernel (gemv.cu) keeps its bytes in
+// flight in registers, so occupancy caps it near 65-78 % of HBM. Here one
+// producer lane per CTA keeps an 8-stage x 16 KB ring of cp.async.bulk copies
+// in flight (128 KB per SM, no register cost) and 8 consumer warps read the
+// weights from shared memory.
+//
+// Decomposition (persistent, one CTA per SM): CTA b owns the contiguous row
+// range [b*R, (b+1)*R) (R even, so SwiGLU gate/up pairs never straddle CTAs)
+// and walks it K-chunk-outer: for each chunk of KC <= 2048 columns every
+// consumer thread holds its 8 columns of x (x t tokens) in registers and the
+// ring streams the range's rows in blocks of RS rows (RS*KC*2 <= 16 KB, one
+// bulk copy per row segment). Per stage each thread forms RS x t partial dot
+// products, the 32 values are reduce-scattered across the warp with 31
+// shuffles, summed over the 8 warps through shared memory and accumulated
+// into a per-row fp32 accumulator in shared memory; the epilogue (store /
+// accumulate / SwiGLU) runs once per row after the last chunk. The summation
+// order is fixed: results are deterministic.
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "mbarrier.cuh"
+#include "../../include/pshard.h"
+
+namespace ps {
+
+constexpr int GT_STAGES = 8;
+constexpr int GT_STAGE_BYTES = 16384;
+constexpr int GT_CONSUMERS = 8;                      // consumer warps
+constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp
+
+// Per token count: columns per consumer thread (x kept in registers: CPT * T floats)
+// and rows per stage (RS * KC * 2 = 16 KB, KC = 256 * CPT columns per chunk).
+template <int T> struct GtShape {
+  static constexpr int CPT = T == 4 ? 16 : 8;
+  static constexpr int KC = GT_CONSUMERS * 32 * CPT;
+  static constexpr int RS = GT_STAGE_BYTES / (KC * 2);
+  static constexpr int V = RS * T;  // partial sums reduced per stage
+};
+
+// 8 bf16 weights x 8 fp32 activations, packed fp32x2 FMA (two partial sums).
+__device__ __forceinline__ float2 dot8x2(uint4 w, const float2* x, float2 s) {
+  s = __ffma2_rn(x[0], make_float2(bf16_lo(w.x), bf16_hi(w.x)), s);
+  s = __ffma2_rn(x[1], make_float2(bf16_lo(w.y), bf16_hi(w.y)), s);
+  s = __ffma2_rn(x[2], make_float2(bf16_lo(w.z), bf16_hi(w.z)), s);
+  s = __ffma2_rn(x[3], make_float2(bf16_lo(w.w), bf16_hi(w.w)), s);
+  return s;
+}
+
+// Reduce-scatter N values over the lanes that differ in bit O and below: after the
+// call lane l holds the warp sum of one value (index fixed by l's high bits).
+template <int N, int O, int V>
+__device__ __forceinline__ void warp_reduce_scatter(float (&v)[V], int lane) {
+  if constexpr (O >= 1) {
+    if constexpr (N > 1) {
+      const bool upper = (lane & O) != 0;
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        const float send = upper ? v[i] : v[i + N / 2];
+        const float keep = upper ? v[i + N / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+      }
+      warp_reduce_scatter<N / 2, O / 2, V>(v, lane);
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+      warp_reduce_scatter<1, O / 2, V>(v, lane);
+    }
+  }
+}
+
+template <int T, int EPI>
+__global__ void __launch_bounds__(GT_THREADS, 1)
+gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W, int N, int K,
+                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages) {
+  using S = GtShape<T>;
+  constexpr int CPT = S::CPT, KC = S::KC, RS = S::RS, V = S::V;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * GT_STAGE_BYTES);
+  uint64_t* empty = full + stages;
+  float* red = reinterpret_cast<float*>(empty + stages);  // [2][GT_CONSUMERS][32]
+  float* acc = red + 2 * GT_CONSUMERS * 32;                   // [rows_per_cta][T]
+
+  const int r0 = blockIdx.x * rows_per_cta;
+  if (r0 >= N) return;  // whole CTA, before any barrier
+  const int r1 = min(N, r0 + rows_per_cta);
+  const int nrows = r1 - r0;
+  const int nchunks = (K + KC - 1) / KC;
+  const int nblocks = (nrows + RS - 1) / RS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], GT_CONSUMERS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < nrows * T; i += GT_THREADS) acc[i] = 0.f;
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        const int kc = min(KC, K - c * KC);
+        for (int b = 0; b < nblocks; ++b) {
+          const int rb = r0 + b * RS;
+          const int nr = min(RS, r1 - rb);
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], (uint32_t)(nr * kc * 2));
+          uint8_t* dst = ring + s * GT_STAGE_BYTES;
+          for (int r = 0; r < nr; ++r)
+            bulk_load(dst + r * KC * 2, W + (long long)(rb + r) * ldw + (long long)c * KC, (uint32_t)(kc * 2),
+                      &full[s]);
+          if (++s == stages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  const int j = threadIdx.x - 32;  // consumer thread 0..255
+  const int cw = warp - 1;
+  // value index this lane holds after the reduce-scatter, and whether it writes it
+  int my_idx = 0;
+  {
+    int n = V;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+      if (n > 1) { if (lane & o) my_idx += n / 2; n >>= 1; }
+  }
+  const bool writer = (lane & ((32 / V) - 1)) == 0;
+  int it = 0, s = 0;
+  uint32_t ph = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int kc = min(KC, K - c * KC);
+    float2 xr[T][CPT / 2];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+#pragma unroll
+      for (int h = 0; h < CPT / 8; ++h) {
+        const int col = (h * GT_CONSUMERS * 32 + j) * 8;   // 8-column groups, consecutive threads adjacent
+        if (col < kc && t < tt) {
+          const float4* xp = reinterpret_cast<const float4*>(x + (long long)t * ldx + (long long)c * KC + col);
+          float4 a = __ldg(xp), b = __ldg(xp + 1);
+          xr[t][h * 4 + 0] = make_float2(a.x, a.y); xr[t][h * 4 + 1] = make_float2(a.z, a.w);
+          xr[t][h * 4 + 2] = make_float2(b.x, b.y); xr[t][h * 4 + 3] = make_float2(b.z, b.w);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) xr[t][h * 4 + i] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+    for (int b = 0; b < nblocks; ++b, ++it) {
+      const int rb = r0 + b * RS;
+      const int nr = min(RS, r1 - rb);
+      mbar_wait(&full[s], ph);
+      const uint8_t* stage = ring + s * GT_STAGE_BYTES;
+      float v[V];
+#pragma unroll
+      for (int r = 0; r < RS; ++r) {
+        uint4 w[CPT / 8];
+#pragma unroll
+        for (int h = 0; h < CPT / 8; ++h) {
+          const int col = (h * GT_CONSUMERS * 32 + j) * 8;
+          w[h] = (r < nr && col < kc) ? *reinterpret_cast<const uint4*>(stage + (r * KC + col) * 2)
+                                      : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int h = 0; h < CPT / 8; ++h) p = dot8x2(w[h], &xr[t][h * 4], p);
+          v[r * T + t] = p.x + p.y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading the stage
+      if (++s == stages) { s = 0; ph ^= 1; }
+      // reduce-scatter V values over the warp, then butterfly the rest: lane l ends
+      // with the warp sum of value my_idx
+      warp_reduce_scatter<V, 16, V>(v, lane);
+      const int buf = it & 1;
+      if (writer) red[(buf * GT_CONSUMERS + cw) * 32 + my_idx] = v[0];
+      named_sync(1, GT_CONSUMERS * 32);
+      if (j < V) {
+        const int r = j / T, t = j - (j / T) * T;
+        if (r < nr) {
+          float sum = 0.f;
+#pragma unroll
+          for (int w = 0; w < GT_CONSUMERS; ++w) sum += red[(buf * GT_CONSUMERS + w) * 32 + j];
+          acc[(rb - r0 + r) * T + t] += sum;
+        }
+      }
+    }
+  }
+  named_sync(1, GT_CONSUMERS * 32);
+  for (int idx = j; idx < nrows * T; idx += GT_CONSUMERS * 32) {
+    const int r = idx / T, t = idx - (idx / T) * T;
+    if (t >= tt) continue;
+    const int row = r0 + r;
+    if (EPI == PS_EPI_SWIGLU) {
+      if ((r & 1) == 0 && row + 1 < N)
+        y[(long long)t * ldy + (row >> 1)] = silu(acc[idx]) * acc[idx + T];
+    } else if (EPI == PS_EPI_ACCUM) {
+      y[(long long)t * ldy + row] += acc[idx];
+    } else {
+      y[(long long)t * ldy + row] = acc[idx];
+    }
+  }
+}
+
+static int g_tma_sms = 0;
+static int g_tma_stages = 0;
+
+template <int T, int EPI>
+static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
+                      int ldy, cudaStream_t s, int grid_cap) {
+  if (!g_tma_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_tma_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_tma_sms <= 0) g_tma_sms = 148;
+  }
+  const int pairs = (N + 1) / 2;
+  int grid = grid_cap > 0 ? grid_cap : g_tma_sms;
+  if (grid > pairs) grid = pairs;
+  if (g_tma_stages == 0) {  // PS_GEMV_STAGES: ring depth override for tuning sweeps
+    const char* e = getenv("PS_GEMV_STAGES");
+    int v = e ? atoi(e) : GT_STAGES;
+    g_tma_stages = v < 2 ? 2 : (v > 12 ? 12 : v);
+  }
+  const int stages = g_tma_stages;
+  // the per-row accumulators share shared memory with the ring
+  const int max_rows = ((232448 - stages * (GT_STAGE_BYTES + 16) - 2 * GT_CONSUMERS * 32 * 4) / (T * 4)) & ~1;
+  int rows_per_cta = 2 * ((pairs + grid - 1) / grid);
+  if (rows_per_cta > max_rows) rows_per_cta = max_rows;
+  grid = (N + rows_per_cta - 1) / rows_per_cta;
+  const size_t smem = (size_t)stages * (GT_STAGE_BYTES + 16) + 2 * GT_CONSUMERS * 32 * 4 + (size_t)rows_per_cta * T * 4;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  gemv_tma_kernel<T, EPI><<<grid, GT_THREADS, smem, s>>>(x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta, stages);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+template <int T>
+static int launch_tma_epi(int epi, const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K,
+                          long long ldw, float* y, int ldy, cudaStream_t s, int grid_cap) {
+  if (epi == PS_EPI_STORE) return launch_tma<T, PS_EPI_STORE>(x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+  if (epi == PS_EPI_ACCUM) return launch_tma<T, PS_EPI_ACCUM>(x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+  return launch_tma<T, PS_EPI_SWIGLU>(x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+}
+
+// Entry used by gemv.cu's dispatcher (tt <= 8 tokens of one launch).
+int gemv_tma_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
+                    int ldy, int epi, cudaStream_t s, int grid_cap) {
+  if (tt == 1) return launch_tma_epi<1>(epi, x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+  if (tt == 2) return launch_tma_epi<2>(epi, x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+  if (tt <= 4) return launch_tma_epi<4>(epi, x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+  return launch_tma_epi<8>(epi, x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
+}
+
+}  // namespace ps

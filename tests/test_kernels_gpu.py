@@ -32,8 +32,13 @@ def rel_err(a, b):
 
 @pytest.mark.parametrize("t", [1, 2, 3, 4, 8, 13, 32])
 @pytest.mark.parametrize("epi", [0, 1, 2])
-@pytest.mark.parametrize("N,K", [(6144, 4096), (256, 14336), (130, 512)])
-def test_gemv(t, epi, N, K):
+@pytest.mark.parametrize("N,K", [(6144, 4096), (256, 14336), (130, 512), (28672, 4096), (4096, 14336),
+                                 (1000, 1544), (2, 2056)])
+@pytest.mark.parametrize("rows", [0, 2])
+def test_gemv(t, epi, N, K, rows):
+    """rows 0 = bulk-copy kernel (gemv_tma.cu), 2 = register-burst kernel (gemv.cu).
+    Shapes cover partial K chunks (1544, 2056 = 2048 + 8), odd row counts per CTA
+    and a matrix with fewer rows than SMs."""
     lib = L()
     g = torch.Generator(device="cuda").manual_seed(t * 100 + N)
     x = torch.randn(t, K, device="cuda", generator=g)
@@ -48,7 +53,8 @@ def test_gemv(t, epi, N, K):
         if epi == 1:
             ref = ref + y
         ldy = N
-    lib.call("ps_gemv_bf16", x.data_ptr(), K, t, W.data_ptr(), N, K, K, y.data_ptr(), ldy, epi, stream())
+    lib.call("ps_gemv_bf16_cfg", x.data_ptr(), K, t, W.data_ptr(), N, K, K, y.data_ptr(), ldy, epi, stream(),
+             rows, 0, 0)
     torch.cuda.synchronize()
     assert rel_err(y, ref) < 2e-5
 

@@ -30,12 +30,12 @@ def run(M, N, K, epi, variant, reps=10):
         C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16); ldc = N
     else:
         C = torch.zeros(M, N, device="cuda"); ldc = N
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > L2
     s = torch.cuda.current_stream().cuda_stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     for i in range(reps + 3):
-        flush.zero_()
+        flush.sum()
         e0.record()
         if variant == "cublas":
             torch.matmul(A, B.T)

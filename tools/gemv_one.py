@@ -1,12 +1,20 @@
-import sys, torch
+"""One GEMV shape launched 4 times (L2 flushed between) for ncu captures:
+python tools/gemv_one.py N K [t] [rows]  (rows 0 = bulk-copy kernel, 2 = register-burst)."""
+import sys
+
+import torch
+
 sys.path.insert(0, ".")
 from paper_2604_26334_b200.runtime import lib as L
+
 N, K = int(sys.argv[1]), int(sys.argv[2])
+t = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+rows = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 W = torch.empty(N, K, dtype=torch.bfloat16, device="cuda").normal_()
-x = torch.randn(1, K, device="cuda"); y = torch.zeros(1, N, device="cuda")
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+x = torch.randn(t, K, device="cuda"); y = torch.zeros(t, N, device="cuda")
+flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > L2
 s = torch.cuda.current_stream().cuda_stream
 for i in range(4):
-    flush.zero_()
-    L.call("ps_gemv_bf16", x.data_ptr(), K, 1, W.data_ptr(), N, K, K, y.data_ptr(), N, 0, s)
+    flush.sum()
+    L.call("ps_gemv_bf16_cfg", x.data_ptr(), K, t, W.data_ptr(), N, K, K, y.data_ptr(), N, 0, s, rows, 0, 0)
 torch.cuda.synchronize()

@@ -21,5 +21,5 @@ def run(N, K, rows=0, ks=0, grid=0, reps=5):
     return best
 
 for N, K in [(1536, 2048), (8192, 4096), (16384, 4096)]:
-    for cfg in [(2, 0, 0), (2, 1, 0), (2, 8, 0), (4, 8, 0), (2, 8, 148 * 2)]:
+    for cfg in [(2, 0, 0), (2, 8, 0), (2, 8, 148 * 2), (-1, 0, 0), (-1, 0, 296)]:
         print(json.dumps({"N": N, "K": K, "cfg": cfg, "zero_copy_GBps": round(run(N, K, *cfg), 2)}), flush=True)
