@@ -159,12 +159,11 @@ def gemv_kernel_roofline(L, peaks) -> dict:
     x = torch.randn(1, K, device="cuda")
     y = torch.zeros(1, N // 2, device="cuda")
     flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > L2
-    s = L.stream_create(True)
-    e0, e1 = L.event_create(True), L.event_create(True)
+    s = torch.cuda.current_stream().cuda_stream   # the flush runs on the same stream, so the
+    e0, e1 = L.event_create(True), L.event_create(True)  # GPU is busy while the host enqueues
     times = []
     for i in range(12):
         flush.sum()                   # evict W from L2 (read-only: leaves no dirty lines to write back)
-        torch.cuda.synchronize()
         L.call("ps_event_record", e0, s)
         L.call("ps_gemv_bf16", x.data_ptr(), K, 1, W.data_ptr(), N, K, K, y.data_ptr(), N // 2, 2, s)
         L.call("ps_event_record", e1, s)
@@ -175,10 +174,16 @@ def gemv_kernel_roofline(L, peaks) -> dict:
     avg = sum(times) / len(times)
     achieved = nbytes / avg / GB
     peak = peaks.get("hbm_gbs", 6650.0)
+    traffic, tsrc = None, None
+    prof = os.path.join(REPO, "profiles", "r01_ncu_gemv_tma_235MB.jsonl")
+    if os.path.exists(prof):   # dram bytes read + written per launch, one ncu --set full capture
+        with open(prof) as fh:
+            rec = json.loads(fh.readline())
+        traffic, tsrc = int(rec["traffic_bytes"]), "profiles/r01_ncu_gemv_tma_235MB.jsonl (ncu --set full)"
     return {"kernel": "ps_gemv_bf16 (K1 bulk-copy kernel, SwiGLU epilogue) 28672x4096, t=1", "bound": "hbm",
             "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "algorithmic_bytes": nbytes,
-            "avg_launch_us": round(avg * 1e6, 2), "traffic": None,
+            "avg_launch_us": round(avg * 1e6, 2), "traffic": traffic, "traffic_source": tsrc,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
 
 
