@@ -114,6 +114,8 @@ int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, int n_kv, in
                    const int* req_slot, const void* kv_base, long long kv_req_stride,
                    long long kv_row_stride, const int* lens, int max_len, float scale, float* out,
                    int ldo, float* workspace, long long workspace_floats, void* stream);
+/* Workspace floats ps_attn_decode needs for this shape (0 when one split covers max_len). */
+int ps_attn_decode_workspace(int batch, int n_heads, int head_dim, int max_len, long long* floats);
 int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_start, const int* p0,
                     const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
                     const void* kv_base, long long kv_req_stride, long long kv_row_stride,

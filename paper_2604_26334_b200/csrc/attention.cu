@@ -17,12 +17,15 @@
 //   ldmatrix.trans.
 #include <float.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "../../include/pshard.h"
 
 namespace ps {
 
 // ------------------------------- decode -------------------------------------
+#define PS_DECODE_CHUNK 128  // positions per split (4 warps x 32)
 template <int HD, int G>
 __global__ void __launch_bounds__(128)
 attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __restrict__ kv_base,
@@ -59,26 +62,40 @@ attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __
     for (int e = 0; e < PER; ++e) acc[g][e] = 0.f;
   }
 
+  // Each warp takes 32 positions per step: lane = position for the scores, lane =
+  // PER contiguous dims for V. Every K and V load of the step is issued before
+  // any is used (16 + 32 independent loads per lane), so a step costs one
+  // memory round trip instead of one per position.
+  using VT = typename std::conditional<PER == 4, uint2, uint32_t>::type;
   for (int t0 = begin + warp * 32; t0 < end; t0 += 4 * 32) {
-    int p = t0 + lane;
-    bool valid = p < end;
+    const int p = t0 + lane;
+    const bool valid = p < end;
+    const int cnt = min(32, end - t0);
+    uint4 kk[HD / 8];
+    const uint4* krow = reinterpret_cast<const uint4*>(kcol + (long long)(valid ? p : t0) * kv_row_stride);
+#pragma unroll
+    for (int c = 0; c < HD / 8; ++c) kk[c] = valid ? __ldg(krow + c) : make_uint4(0, 0, 0, 0);
+    VT vv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const VT* vrow = reinterpret_cast<const VT*>(vcol + (long long)(t0 + (j < cnt ? j : 0)) * kv_row_stride +
+                                                   lane * PER);
+      vv[j] = __ldg(vrow);
+    }
     float s[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) s[g] = 0.f;
-    if (valid) {
-      const uint4* krow = reinterpret_cast<const uint4*>(kcol + (long long)p * kv_row_stride);
-#pragma unroll 4
-      for (int c = 0; c < HD / 8; ++c) {
-        uint4 kk = krow[c];
-        float k8[8] = {bf16_lo(kk.x), bf16_hi(kk.x), bf16_lo(kk.y), bf16_hi(kk.y),
-                       bf16_lo(kk.z), bf16_hi(kk.z), bf16_lo(kk.w), bf16_hi(kk.w)};
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float4* qq = reinterpret_cast<const float4*>(&qs[g][8 * c]);
-          float4 a = qq[0], bb = qq[1];
-          s[g] += a.x * k8[0] + a.y * k8[1] + a.z * k8[2] + a.w * k8[3] + bb.x * k8[4] + bb.y * k8[5] +
-                  bb.z * k8[6] + bb.w * k8[7];
-        }
+    for (int c = 0; c < HD / 8; ++c) {
+      const uint4 k4 = kk[c];
+      const float k8[8] = {bf16_lo(k4.x), bf16_hi(k4.x), bf16_lo(k4.y), bf16_hi(k4.y),
+                           bf16_lo(k4.z), bf16_hi(k4.z), bf16_lo(k4.w), bf16_hi(k4.w)};
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float4* qq = reinterpret_cast<const float4*>(&qs[g][8 * c]);
+        const float4 a = qq[0], bb = qq[1];
+        s[g] += a.x * k8[0] + a.y * k8[1] + a.z * k8[2] + a.w * k8[3] + bb.x * k8[4] + bb.y * k8[5] +
+                bb.z * k8[6] + bb.w * k8[7];
       }
     }
     float pr[G];
@@ -94,22 +111,21 @@ attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __
       for (int e = 0; e < PER; ++e) acc[g][e] *= corr;
       m[g] = mn;
     }
-    int cnt = min(32, end - t0);
-    for (int j = 0; j < cnt; ++j) {
-      const __nv_bfloat16* vrow = vcol + (long long)(t0 + j) * kv_row_stride + lane * PER;
-      float vv[PER];
-      if (PER == 4) {
-        uint2 w = *reinterpret_cast<const uint2*>(vrow);
-        vv[0] = bf16_lo(w.x); vv[1] = bf16_hi(w.x); vv[2 % PER] = bf16_lo(w.y); vv[3 % PER] = bf16_hi(w.y);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float v4[PER];
+      if constexpr (PER == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(&vv[j]);
+        v4[0] = bf16_lo(w.x); v4[1] = bf16_hi(w.x); v4[2] = bf16_lo(w.y); v4[3] = bf16_hi(w.y);
       } else {
-        uint32_t w = *reinterpret_cast<const uint32_t*>(vrow);
-        vv[0] = bf16_lo(w); vv[1 % PER] = bf16_hi(w);
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(&vv[j]);
+        v4[0] = bf16_lo(w); v4[1] = bf16_hi(w);
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        float pj = __shfl_sync(0xffffffffu, pr[g], j);
+        const float pj = __shfl_sync(0xffffffffu, pr[g], j);   // 0 for j >= cnt (invalid lanes)
 #pragma unroll
-        for (int e = 0; e < PER; ++e) acc[g][e] = fmaf(pj, vv[e], acc[g][e]);
+        for (int e = 0; e < PER; ++e) acc[g][e] = fmaf(pj, v4[e], acc[g][e]);
       }
     }
   }
@@ -368,6 +384,14 @@ static int decode_dispatch(int G, dim3 grid, cudaStream_t s, const float* q, int
   return PS_OK;
 }
 
+extern "C" int ps_attn_decode_workspace(int batch, int n_heads, int head_dim, int max_len, long long* floats) {
+  PS_REQUIRE(floats != nullptr, "ps_attn_decode_workspace: floats is null");
+  int n_splits = (max_len + PS_DECODE_CHUNK - 1) / PS_DECODE_CHUNK;
+  if (n_splits < 1) n_splits = 1;
+  *floats = n_splits > 1 ? (long long)batch * n_heads * n_splits * (head_dim + 2) : 0;
+  return PS_OK;
+}
+
 extern "C" int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, int n_kv, int head_dim,
                               const int* req_slot, const void* kv_base, long long kv_req_stride,
                               long long kv_row_stride, const int* lens, int max_len,
@@ -376,7 +400,7 @@ extern "C" int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, i
   PS_REQUIRE(n_heads % n_kv == 0, "ps_attn_decode: n_heads %% n_kv != 0");
   if (batch <= 0) return PS_OK;
   int G = n_heads / n_kv;
-  int chunk = 256;
+  int chunk = PS_DECODE_CHUNK;
   int n_splits = (max_len + chunk - 1) / chunk;
   if (n_splits < 1) n_splits = 1;
   long long need = (long long)batch * n_heads * n_splits * (head_dim + 2);

@@ -153,8 +153,8 @@ class Executor:
             self.xn16 = self.att16 = self.hid16 = 0
         self.xs = a.alloc_high("xs", B * d * 4)
         self.logits = a.alloc_high("logits", B * self.V * 4)
-        splits = max(1, math.ceil(self.cap / 256))
-        self.ws_floats = B * self.h * splits * (self.hd + 2) if T <= GEMV_MAX_T else 0
+        # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
+        self.ws_floats = L.attn_decode_workspace(B, self.h, self.hd, self.cap)
         self.ws = a.alloc_high("attn_ws", max(1, self.ws_floats) * 4)
         if self.moe is not None:
             E, k, eff = self.moe.n_experts, self.moe.top_k, self.moe.expert_ffn_dim

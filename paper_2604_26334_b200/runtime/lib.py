@@ -51,6 +51,7 @@ _SIGS = {
     "ps_rmsnorm": [_p, _i, _p, _i, _p, _i, _f, _p, _i, _i, _p],
     "ps_qkv_rope_append": [_p, _i, _i, _i, _i, _i, _p, _p, _p, _ll, _ll, _p, _p, _p, _f, _p],
     "ps_attn_decode": [_p, _i, _i, _i, _i, _i, _p, _p, _ll, _ll, _p, _i, _f, _p, _i, _p, _ll, _p],
+    "ps_attn_decode_workspace": [_i, _i, _i, _i, C.POINTER(_ll)],
     "ps_attn_prefill": [_p, _i, _i, _p, _p, _p, _i, _i, _i, _i, _p, _ll, _ll, _f, _p, _i, _i, _p],
     "ps_upload_small": [_p, _p, _i, _p],
     "ps_moe_route_topk": [_p, _i, _i, _i, _i, _i, _p, _p, _p],
@@ -102,7 +103,7 @@ def lib():
 KERNEL_CALLS = frozenset({
     "ps_gemv_bf16", "ps_gemm_bf16", "ps_rmsnorm", "ps_qkv_rope_append", "ps_attn_decode",
     "ps_attn_prefill", "ps_embed_gather", "ps_argmax", "ps_cast_f32_bf16", "ps_add_f32",
-    "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_gemv_bf16_cfg",
+    "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_gemv_bf16_cfg", "ps_gemm_bf16_cfg",
     "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine"})
 counters = {"kernel_calls": 0, "memcpy_calls": 0}
 
@@ -117,6 +118,13 @@ def call(name: str, *args) -> int:
         msg = lib().ps_last_error().decode(errors="replace")
         raise PshardError(f"{name} failed ({rc}): {msg}")
     return rc
+
+
+def attn_decode_workspace(batch: int, n_heads: int, head_dim: int, max_len: int) -> int:
+    """Floats of workspace ps_attn_decode needs (split-KV partials)."""
+    n = C.c_longlong(0)
+    call("ps_attn_decode_workspace", batch, n_heads, head_dim, max_len, C.byref(n))
+    return n.value
 
 
 def out_ptr() -> C.c_void_p:

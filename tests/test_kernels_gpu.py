@@ -183,7 +183,8 @@ def _attn_ref(q, K, V, qpos):
 
 @pytest.mark.parametrize("hd,h,kv,lens", [(128, 32, 8, [2304]), (128, 32, 8, [1, 17, 640, 300]),
                                           (64, 8, 8, [160, 5]), (128, 64, 8, [4224]),
-                                          (128, 32, 4, [1000])])
+                                          (128, 32, 4, [1000]), (128, 32, 32, [16384, 129]),
+                                          (128, 32, 8, [33, 128, 127, 1])])
 def test_attn_decode(hd, h, kv, lens):
     lib = L()
     B, cap = len(lens), max(lens)
@@ -192,8 +193,7 @@ def test_attn_decode(hd, h, kv, lens):
     q = torch.randn(B, h * hd, device="cuda", generator=g)
     ln = torch.tensor(lens, dtype=torch.int32, device="cuda")
     out = torch.zeros(B, h * hd, device="cuda")
-    splits = math.ceil(cap / 256)
-    ws = torch.zeros(B * h * splits * (hd + 2), device="cuda")
+    ws = torch.zeros(max(1, lib.attn_decode_workspace(B, h, hd, cap)), device="cuda")
     lib.call("ps_attn_decode", q.data_ptr(), h * hd, B, h, kv, hd, 0, cache.data_ptr(), 2 * kv * hd,
              B * 2 * kv * hd, ln.data_ptr(), cap, 1 / math.sqrt(hd), out.data_ptr(), h * hd,
              ws.data_ptr(), ws.numel(), stream())
