@@ -96,6 +96,8 @@ class Executor:
         self.Tmax = max_tokens
         self.shards = build_shards(spec, context_len, kv_slots)
         self.by_layer_kind = {(s.layer_index, s.kind): s for s in self.shards}
+        self.shard_kind = {s.id: s.kind for s in self.shards}
+        self._gapfill, self._piece_override, self._prefetched = None, {}, {}
         L.lib()
 
         s = spec
@@ -302,23 +304,24 @@ class Executor:
         L.call("ps_event_record", ev, stream)
         return ev
 
-    def _pieces(self, sid: int, names: list, even: set) -> list:
+    def _pieces(self, sid: int, names: list, even: set, chunk: int | None = None) -> list:
         """Row-aligned pieces (<= chunk bytes) covering `names` in blob order:
         [(byte_start, byte_end, [(tensor, r0, r1), ...])]; 1-row tensors
         (norm vectors) ride in the piece that follows them."""
+        chunk = chunk or self.chunk
         blob = self.w.layout.blobs[sid]
         out, items, start, end, big = [], [], None, 0, False
         for name in names:
             t = blob.tensors[name]
             row_b = t.cols * 2
-            step = max(1, self.chunk // row_b)
+            step = max(1, chunk // row_b)
             if name in even:
                 step = max(2, step // 2 * 2)
             r = 0
             while r < t.rows:
                 r1 = min(t.rows, r + step)
                 b0, b1 = t.offset + r * row_b, t.offset + r1 * row_b
-                if big and t.rows > 1 and b1 - start > self.chunk:
+                if big and t.rows > 1 and b1 - start > chunk:
                     out.append((start, end, items))
                     items, start, big = [], None, False
                 if start is None:
@@ -381,7 +384,8 @@ class Executor:
             advance_to(len(consumers))
             return
 
-        pieces = self._pieces(sid, names, {c.tensor for c in consumers if c.even_rows})
+        pieces = self._piece_override.pop(sid, None) or \
+            self._pieces(sid, names, {c.tensor for c in consumers if c.even_rows})
         host = self.w.shard_ptr(sid)
         # A piece is released once nothing enqueued later reads it: matrix rows as
         # soon as their consumer has been enqueued for them ("rows" token), small
@@ -399,9 +403,13 @@ class Executor:
                 discharge(entry, i)
 
         for b0, b1, items in pieces:
-            region, pdev, arrived = self.ring.upload(host + b0, b1 - b0, f"s{sid}@{b0}")
-            self._stat.bytes_streamed += b1 - b0
-            self._stat.copies += 1
+            pre = self._prefetched.pop((sid, b0), None)
+            if pre is not None:
+                region, pdev, arrived = pre
+            else:
+                region, pdev, arrived = self.ring.upload(host + b0, b1 - b0, f"s{sid}@{b0}")
+                self._stat.bytes_streamed += b1 - b0
+                self._stat.copies += 1
             pending = set()
             for name, _, _ in items:
                 rows_consumer = own.get(name) if blob.tensors[name].rows > 1 else None
@@ -483,6 +491,7 @@ class Executor:
             if mode == "zerocopy":
                 touched = min(E, P)
                 self._stat.zero_copy_bytes += e0.offset + touched * stride
+                self._gapfill_step()
         else:
             host = self.w.shard_ptr(sid)
             per_piece = max(1, (self.chunk - e0.offset) // stride)
@@ -503,6 +512,49 @@ class Executor:
                 first = False
                 lo = hi
         L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
+
+    # ------------------------------------------------- gap filling (MoE decode)
+    def _plan_gapfill(self, gemv: bool, R: int) -> None:
+        """Zero-copy MoE decode leaves the host link idle between layers (attention,
+        router and top-k of the next layer run while nothing crosses the link); the
+        output head is the one ring-streamed shard of such a pass and is only read
+        at its end. Cut the head into one piece per zero-copy MoE layer and upload
+        piece k right after layer k's experts finish (the copy stream waits on that
+        event), so head bytes fill the gaps instead of sharing the link with expert
+        reads. Enabled only when nothing else in the pass uses the ring."""
+        self._gapfill, self._piece_override, self._prefetched = None, {}, {}
+        if not (gemv and R and self.moe is not None and self.ring is not None):
+            return
+        head_sid = self.by_layer_kind[(self.spec.n_layers, ShardKind.OUTPUT_HEAD)].id
+        if self.residency[head_sid][0] != "stream":
+            return
+        zc = 0
+        for sid, (mode, _) in self.residency.items():
+            kind = self.shard_kind[sid]
+            if kind is ShardKind.MOE_EXPERT_GROUP:
+                zc += mode in ("zerocopy", "stream")
+            elif sid != head_sid and mode == "stream":
+                return
+        if zc == 0 or any(m == "stream" for m in self.kv_mode.values()):
+            return
+        blob = self.w.layout.blobs[head_sid]
+        names = [n for n in blob.tensors if n in ("final_norm", "lm_head")]
+        chunk = max(4 << 20, -(-blob.nbytes // zc))
+        pieces = self._pieces(head_sid, names, set(), chunk=min(chunk, self.chunk))
+        if sum((b1 - b0 + 255) // 256 * 256 for b0, b1, _ in pieces) > self.ring.capacity * 9 // 10:
+            return
+        self._piece_override[head_sid] = pieces
+        self._gapfill = (head_sid, list(pieces))
+
+    def _gapfill_step(self) -> None:
+        if not self._gapfill or not self._gapfill[1]:
+            return
+        sid, todo = self._gapfill
+        b0, b1, _ = todo.pop(0)
+        L.call("ps_stream_wait_event", self.h2d, self._record(self.cs))   # after this layer's experts
+        self._prefetched[(sid, b0)] = self.ring.upload(self.w.shard_ptr(sid) + b0, b1 - b0, f"s{sid}@{b0}")
+        self._stat.bytes_streamed += b1 - b0
+        self._stat.copies += 1
 
     def _matmul(self, T, act, W, N, K, out, ldo, epi) -> None:
         """out (epi)= act @ W[:N]^T for T tokens: GEMV on fp32 act (T <= 32)
@@ -580,6 +632,8 @@ class Executor:
 
         def norm(w_ptr):
             L.call("ps_rmsnorm", self.x, d, 0, T, w_ptr, d, eps, xn, d, 0 if gemv else 1, self.cs)
+
+        self._plan_gapfill(gemv, len(ps.sample))
 
         for layer in range(self.spec.n_layers):
             attn_sid = self.by_layer_kind[(layer, ShardKind.ATTENTION)].id
