@@ -141,8 +141,34 @@ int ps_moe_expert_gu(const void* x, int ldx, int x_bf16, const int* plan, int E,
 int ps_moe_expert_down(const float* h, const int* plan, int E, int P, const void* expert_base,
                        long long expert_stride, long long down_off, int eff, int d, float* out,
                        int e_lo, int e_hi, void* stream);
+/* Same expert kernels with an expert -> slot map: expert e is read from
+ * expert_base + slot_of_expert[e] * expert_stride (the routed-expert fetcher's VRAM slots). */
+int ps_moe_expert_gu_mapped(const void* x, int ldx, int x_bf16, const int* plan, int E, int P, int k,
+                            const void* expert_base, long long expert_stride, long long gu_off, int eff,
+                            int d, float* h, int e_lo, int e_hi, const int* slot_of_expert, void* stream);
+int ps_moe_expert_down_mapped(const float* h, const int* plan, int E, int P, const void* expert_base,
+                              long long expert_stride, long long down_off, int eff, int d, float* out,
+                              int e_lo, int e_hi, const int* slot_of_expert, void* stream);
 int ps_moe_combine(const float* out, const int* plan, int E, int P, const float* w, int T, int k,
                    int d, float* y, int ldy, void* stream);
+
+/* ---- routed-expert fetcher (copy-engine uploads of router-selected experts) --
+ * Replaces the zero-copy read of a streamed expert group in decode passes: the GPU
+ * publishes the routed expert ids (ps_moe_publish, host-mapped, seq-tagged), a host
+ * thread enqueues one cudaMemcpyAsync per routed expert into VRAM slots on its own
+ * copy stream and then copies `seq` into a device flag; ps_wait_flag holds the
+ * compute stream until the flag reaches seq (2 s timeout -> device error flag, no hang).
+ * ps_fetcher_submit must be called once per published seq, in seq order. */
+int ps_fetcher_create(int max_experts, void** out);
+int ps_fetcher_destroy(void* fetcher);
+int ps_fetcher_info(void* fetcher, void** copy_stream, void** flag_dev, long long* experts_copied,
+                    long long* bytes_copied, int* error);
+int ps_fetcher_submit(void* fetcher, unsigned seq, const void* host_base, long long expert_stride,
+                      long long expert_bytes, void* slot_base, long long slot_stride);
+int ps_moe_publish(void* fetcher, const int* ids, int P, int E, int* slot_of_expert, unsigned seq,
+                   void* stream);
+int ps_wait_flag(void* fetcher, unsigned seq, void* stream);
+int ps_fetcher_device_error(void* fetcher, unsigned* seq_out);
 
 /* ---- K6: embedding gather (zero-copy from host-mapped table), greedy -------
  * Not priced by the reference (embeddings are outside the plan,

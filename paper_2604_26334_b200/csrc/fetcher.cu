@@ -1,0 +1,275 @@
+// Routed-expert fetcher: copy-engine uploads of the experts a router picked.
+//
+// A MoE layer's experts are known only after its router runs on the GPU
+// (SURVEY.md §7 hard part 6), so a copy-engine upload cannot be enqueued
+// ahead of time the way the streamer enqueues dense pieces. Reading the
+// routed experts zero-copy works but costs ~8 % of the host link (SM reads
+// travel as 128-byte PCIe requests; the copy engine moves larger ones:
+// 51 vs 55.6 GB/s measured). The fetcher closes that gap with one host
+// thread per executor:
+//
+//   compute stream:  ... router -> top-k -> ps_moe_publish -> ps_wait_flag -> experts ...
+//   host thread:     sees the published expert list (host-mapped, seq-tagged),
+//                    enqueues one cudaMemcpyAsync per routed expert into fixed
+//                    VRAM slots on its own copy stream, then a 4-byte copy of
+//                    the sequence number into a device flag
+//   ps_wait_flag:    one thread spins (nanosleep) until the flag reaches seq
+//
+// ps_moe_publish also writes slot_of_expert[E] (rank among the routed experts,
+// -1 otherwise), which the mapped expert kernels use to find each expert's
+// slot. The wait kernel gives up after a timeout and raises a device-side
+// error flag instead of hanging the GPU if the host thread ever stalls.
+#include <stdint.h>
+#include <string.h>
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
+
+#include "common.cuh"
+#include "../../include/pshard.h"
+
+namespace ps {
+
+// publish block (host-mapped): [0] seq, [1] count, [2..] expert ids ascending
+constexpr int PUB_HEADER = 2;
+
+__global__ void moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ slot_of_expert,
+                                   volatile unsigned* __restrict__ pub, unsigned seq) {
+  extern __shared__ int mark[];  // E
+  for (int e = threadIdx.x; e < E; e += blockDim.x) mark[e] = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < P; p += blockDim.x) mark[ids[p]] = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int e = 0; e < E; ++e) {
+      if (mark[e]) {
+        slot_of_expert[e] = n;
+        pub[PUB_HEADER + n] = (unsigned)e;
+        ++n;
+      } else {
+        slot_of_expert[e] = -1;
+      }
+    }
+    pub[1] = (unsigned)n;
+    __threadfence_system();   // ids and count are visible to the host before seq
+    pub[0] = seq;
+    __threadfence_system();
+  }
+}
+
+__global__ void wait_flag_kernel(const volatile unsigned* __restrict__ flag, unsigned seq,
+                                 unsigned* __restrict__ error_flag, unsigned long long timeout_ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned v = *flag;
+    if ((int)(v - seq) >= 0) break;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicExch(error_flag, seq);
+      break;
+    }
+    __nanosleep(200);
+  }
+  __threadfence();
+}
+
+struct FetchJob {
+  unsigned seq;
+  const char* host_base;
+  long long expert_stride, expert_bytes;
+  char* slot_base;
+  long long slot_stride;
+};
+
+class ExpertFetcher {
+ public:
+  ExpertFetcher(int max_experts) : max_experts_(max_experts) {}
+
+  int init() {
+    PS_CHECK_CUDA(cudaHostAlloc(&pub_host_, (PUB_HEADER + max_experts_) * sizeof(unsigned), cudaHostAllocMapped));
+    memset((void*)pub_host_, 0, (PUB_HEADER + max_experts_) * sizeof(unsigned));
+    PS_CHECK_CUDA(cudaHostGetDevicePointer((void**)&pub_dev_, (void*)pub_host_, 0));
+    PS_CHECK_CUDA(cudaHostAlloc(&seq_src_, kSeqRing * sizeof(unsigned), cudaHostAllocDefault));
+    PS_CHECK_CUDA(cudaMalloc(&flag_dev_, 2 * sizeof(unsigned)));   // [flag, error]
+    PS_CHECK_CUDA(cudaMemset(flag_dev_, 0, 2 * sizeof(unsigned)));
+    PS_CHECK_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    PS_CHECK_CUDA(cudaGetDevice(&device_));
+    thread_ = std::thread([this] { run(); });
+    return PS_OK;
+  }
+
+  ~ExpertFetcher() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    if (thread_.joinable()) thread_.join();
+    if (stream_) {
+      cudaStreamSynchronize(stream_);
+      cudaStreamDestroy(stream_);
+    }
+    if (flag_dev_) cudaFree(flag_dev_);
+    if (seq_src_) cudaFreeHost(seq_src_);
+    if (pub_host_) cudaFreeHost((void*)pub_host_);
+  }
+
+  void submit(const FetchJob& j) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      q_.push_back(j);
+    }
+    cv_.notify_one();
+  }
+
+  unsigned* pub_dev() const { return pub_dev_; }
+  unsigned* flag_dev() const { return flag_dev_; }
+  cudaStream_t stream() const { return stream_; }
+  long long experts_copied() const { return copied_.load(); }
+  long long bytes_copied() const { return bytes_.load(); }
+  int error() const { return error_.load(); }
+
+ private:
+  static constexpr int kSeqRing = 1024;
+
+  void run() {
+    cudaSetDevice(device_);
+    while (true) {
+      FetchJob j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+        if (stop_ && q_.empty()) return;
+        j = q_.front();
+        q_.pop_front();
+      }
+      // wait for the GPU to publish this layer's routed experts
+      auto t0 = std::chrono::steady_clock::now();
+      unsigned spins = 0;
+      while ((int)(pub_host_[0] - j.seq) < 0) {
+        if (++spins > 4096) {
+          std::this_thread::yield();
+          if (stopping() || std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) {
+            error_.store(1);
+            break;
+          }
+        }
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      unsigned n = pub_host_[1];
+      if (n > (unsigned)max_experts_) n = 0, error_.store(2);
+      for (unsigned r = 0; r < n; ++r) {
+        const unsigned e = pub_host_[PUB_HEADER + r];
+        if (cudaMemcpyAsync(j.slot_base + r * j.slot_stride, j.host_base + (long long)e * j.expert_stride,
+                            j.expert_bytes, cudaMemcpyHostToDevice, stream_) != cudaSuccess)
+          error_.store(3);
+      }
+      copied_ += n;
+      bytes_ += (long long)n * j.expert_bytes;
+      unsigned* src = seq_src_ + (ring_i_++ % kSeqRing);
+      *src = j.seq;
+      if (cudaMemcpyAsync(flag_dev_, src, sizeof(unsigned), cudaMemcpyHostToDevice, stream_) != cudaSuccess)
+        error_.store(3);
+    }
+  }
+
+  bool stopping() {
+    std::lock_guard<std::mutex> g(mu_);
+    return stop_;
+  }
+
+  int max_experts_;
+  int device_ = 0;
+  volatile unsigned* pub_host_ = nullptr;
+  unsigned* pub_dev_ = nullptr;
+  unsigned* seq_src_ = nullptr;
+  unsigned* flag_dev_ = nullptr;
+  unsigned ring_i_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::thread thread_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<FetchJob> q_;
+  bool stop_ = false;
+  std::atomic<long long> copied_{0}, bytes_{0};
+  std::atomic<int> error_{0};
+};
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" {
+
+int ps_fetcher_create(int max_experts, void** out) {
+  PS_REQUIRE(out && max_experts >= 1 && max_experts <= 4096, "ps_fetcher_create: max_experts=%d", max_experts);
+  auto* f = new ExpertFetcher(max_experts);
+  int rc = f->init();
+  if (rc) {
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return PS_OK;
+}
+
+int ps_fetcher_destroy(void* f) {
+  delete static_cast<ExpertFetcher*>(f);
+  return PS_OK;
+}
+
+int ps_fetcher_info(void* f, void** copy_stream, void** flag_dev, long long* experts_copied, long long* bytes_copied,
+                    int* error) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr, "ps_fetcher_info: null fetcher");
+  if (copy_stream) *copy_stream = x->stream();
+  if (flag_dev) *flag_dev = x->flag_dev();
+  if (experts_copied) *experts_copied = x->experts_copied();
+  if (bytes_copied) *bytes_copied = x->bytes_copied();
+  if (error) *error = x->error();
+  return PS_OK;
+}
+
+int ps_fetcher_submit(void* f, unsigned seq, const void* host_base, long long expert_stride, long long expert_bytes,
+                      void* slot_base, long long slot_stride) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr, "ps_fetcher_submit: null fetcher");
+  PS_REQUIRE(expert_bytes > 0 && slot_stride >= expert_bytes, "ps_fetcher_submit: bad sizes");
+  x->submit(FetchJob{seq, static_cast<const char*>(host_base), expert_stride, expert_bytes,
+                     static_cast<char*>(slot_base), slot_stride});
+  return PS_OK;
+}
+
+int ps_moe_publish(void* f, const int* ids, int P, int E, int* slot_of_expert, unsigned seq, void* stream) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr && P >= 1 && E >= 1, "ps_moe_publish: P=%d E=%d", P, E);
+  moe_publish_kernel<<<1, 256, E * sizeof(int), (cudaStream_t)stream>>>(ids, P, E, slot_of_expert, x->pub_dev(),
+                                                                         seq);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+int ps_wait_flag(void* f, unsigned seq, void* stream) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr, "ps_wait_flag: null fetcher");
+  wait_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(x->flag_dev(), seq, x->flag_dev() + 1,
+                                                      2000000000ull /* 2 s */);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+int ps_fetcher_device_error(void* f, unsigned* seq_out) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr && seq_out, "ps_fetcher_device_error: null argument");
+  PS_CHECK_CUDA(cudaMemcpy(seq_out, x->flag_dev() + 1, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+}  // extern "C"

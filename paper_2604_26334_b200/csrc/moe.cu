@@ -188,7 +188,8 @@ template <bool XBF16>
 __global__ void __launch_bounds__(MOE_WARPS * 32)
 expert_gu_kernel(const void* __restrict__ x, int ldx, const int* __restrict__ plan, int E, int P, int k,
                  int max_items, const unsigned char* __restrict__ expert_base, long long expert_stride,
-                 long long gu_off, int eff, int d, float* __restrict__ h, int e_lo, int e_hi) {
+                 long long gu_off, int eff, int d, float* __restrict__ h, int e_lo, int e_hi,
+                 const int* __restrict__ slot_of_expert) {
   const int* first = plan + 1;
   const int* items = plan + 2 + E;
   const int* perm = items + 3 * max_items;
@@ -202,7 +203,8 @@ expert_gu_kernel(const void* __restrict__ x, int ldx, const int* __restrict__ pl
     int it = it_lo + (int)(u / tiles);
     int tile = (int)(u % tiles);
     int e = items[3 * it], start = items[3 * it + 1], n = items[3 * it + 2];
-    const __nv_bfloat16* Wg = reinterpret_cast<const __nv_bfloat16*>(expert_base + e * expert_stride + gu_off);
+    const long long slot = slot_of_expert ? slot_of_expert[e] : e;
+    const __nv_bfloat16* Wg = reinterpret_cast<const __nv_bfloat16*>(expert_base + slot * expert_stride + gu_off);
     long long xoff[MOE_TILE];
 #pragma unroll
     for (int i = 0; i < MOE_TILE; ++i) xoff[i] = (long long)(perm[start + min(i, n - 1)] / k) * ldx;
@@ -221,7 +223,8 @@ expert_gu_kernel(const void* __restrict__ x, int ldx, const int* __restrict__ pl
 __global__ void __launch_bounds__(MOE_WARPS * 32)
 expert_down_kernel(const float* __restrict__ h, const int* __restrict__ plan, int E, int max_items,
                    const unsigned char* __restrict__ expert_base, long long expert_stride, long long down_off,
-                   int eff, int d, float* __restrict__ out, int e_lo, int e_hi) {
+                   int eff, int d, float* __restrict__ out, int e_lo, int e_hi,
+                   const int* __restrict__ slot_of_expert) {
   const int* first = plan + 1;
   const int* items = plan + 2 + E;
   const int it_lo = first[e_lo], it_hi = first[e_hi];
@@ -233,7 +236,8 @@ expert_down_kernel(const float* __restrict__ h, const int* __restrict__ plan, in
     int it = it_lo + (int)(u / tiles);
     int tile = (int)(u % tiles);
     int e = items[3 * it], start = items[3 * it + 1], n = items[3 * it + 2];
-    const __nv_bfloat16* Wd = reinterpret_cast<const __nv_bfloat16*>(expert_base + e * expert_stride + down_off);
+    const long long slot = slot_of_expert ? slot_of_expert[e] : e;
+    const __nv_bfloat16* Wd = reinterpret_cast<const __nv_bfloat16*>(expert_base + slot * expert_stride + down_off);
     long long xoff[MOE_TILE];
 #pragma unroll
     for (int i = 0; i < MOE_TILE; ++i) xoff[i] = (long long)(start + min(i, n - 1)) * eff;
@@ -301,18 +305,36 @@ int ps_moe_plan(const int* ids, int P, int E, int* plan, void* stream) {
   return PS_OK;
 }
 
-int ps_moe_expert_gu(const void* x, int ldx, int x_bf16, const int* plan, int E, int P, int k,
-                     const void* expert_base, long long expert_stride, long long gu_off, int eff, int d,
-                     float* h, int e_lo, int e_hi, void* stream) {
+int ps_moe_expert_gu_mapped(const void* x, int ldx, int x_bf16, const int* plan, int E, int P, int k,
+                            const void* expert_base, long long expert_stride, long long gu_off, int eff, int d,
+                            float* h, int e_lo, int e_hi, const int* slot_of_expert, void* stream) {
   PS_REQUIRE(d % 8 == 0 && eff % 8 == 0, "ps_moe_expert_gu: d, eff must be multiples of 8");
   int max_items = P / MOE_TILE + E;
   auto base = static_cast<const unsigned char*>(expert_base);
   if (x_bf16)
     expert_gu_kernel<true><<<persistent_grid(), MOE_WARPS * 32, 0, (cudaStream_t)stream>>>(
-        x, ldx, plan, E, P, k, max_items, base, expert_stride, gu_off, eff, d, h, e_lo, e_hi);
+        x, ldx, plan, E, P, k, max_items, base, expert_stride, gu_off, eff, d, h, e_lo, e_hi, slot_of_expert);
   else
     expert_gu_kernel<false><<<persistent_grid(), MOE_WARPS * 32, 0, (cudaStream_t)stream>>>(
-        x, ldx, plan, E, P, k, max_items, base, expert_stride, gu_off, eff, d, h, e_lo, e_hi);
+        x, ldx, plan, E, P, k, max_items, base, expert_stride, gu_off, eff, d, h, e_lo, e_hi, slot_of_expert);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+int ps_moe_expert_gu(const void* x, int ldx, int x_bf16, const int* plan, int E, int P, int k,
+                     const void* expert_base, long long expert_stride, long long gu_off, int eff, int d,
+                     float* h, int e_lo, int e_hi, void* stream) {
+  return ps_moe_expert_gu_mapped(x, ldx, x_bf16, plan, E, P, k, expert_base, expert_stride, gu_off, eff, d, h,
+                                 e_lo, e_hi, nullptr, stream);
+}
+
+int ps_moe_expert_down_mapped(const float* h, const int* plan, int E, int P, const void* expert_base,
+                              long long expert_stride, long long down_off, int eff, int d, float* out, int e_lo,
+                              int e_hi, const int* slot_of_expert, void* stream) {
+  int max_items = P / MOE_TILE + E;
+  expert_down_kernel<<<persistent_grid(), MOE_WARPS * 32, 0, (cudaStream_t)stream>>>(
+      h, plan, E, max_items, static_cast<const unsigned char*>(expert_base), expert_stride, down_off, eff, d, out,
+      e_lo, e_hi, slot_of_expert);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -320,12 +342,8 @@ int ps_moe_expert_gu(const void* x, int ldx, int x_bf16, const int* plan, int E,
 int ps_moe_expert_down(const float* h, const int* plan, int E, int P, const void* expert_base,
                        long long expert_stride, long long down_off, int eff, int d, float* out, int e_lo,
                        int e_hi, void* stream) {
-  int max_items = P / MOE_TILE + E;
-  expert_down_kernel<<<persistent_grid(), MOE_WARPS * 32, 0, (cudaStream_t)stream>>>(
-      h, plan, E, max_items, static_cast<const unsigned char*>(expert_base), expert_stride, down_off, eff, d, out,
-      e_lo, e_hi);
-  PS_CHECK_LAUNCH();
-  return PS_OK;
+  return ps_moe_expert_down_mapped(h, plan, E, P, expert_base, expert_stride, down_off, eff, d, out, e_lo, e_hi,
+                                   nullptr, stream);
 }
 
 int ps_moe_combine(const float* out, const int* plan, int E, int P, const float* w, int T, int k, int d,

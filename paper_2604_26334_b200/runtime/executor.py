@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -97,6 +98,10 @@ class Executor:
         self.shards = build_shards(spec, context_len, kv_slots)
         self.by_layer_kind = {(s.layer_index, s.kind): s for s in self.shards}
         self.shard_kind = {s.id: s.kind for s in self.shards}
+        # routed-expert fetcher (copy-engine expert uploads in MoE decode); PS_MOE_FETCH=0 disables
+        self.fetcher, self.fetch_seq = None, 0
+        self.fetch_enabled = os.environ.get("PS_MOE_FETCH", "1") != "0"
+        self.expert_slots, self.expert_slot_bytes = 0, 0
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
         L.lib()
 
@@ -169,6 +174,7 @@ class Executor:
             self.m_plan = a.alloc_high("moe_plan", n_ints.value * 4)
             self.m_h = a.alloc_high("moe_h", P * eff * 4)
             self.m_out = a.alloc_high("moe_out", P * d * 4)
+            self.m_slotmap = a.alloc_high("moe_slot_of_expert", E * 4)
 
     def _carve_persistent(self) -> None:
         """Small buffers whose content outlives a pass (tokens, rope table)."""
@@ -278,6 +284,8 @@ class Executor:
         pieces, else the budget is infeasible for this executor."""
         self.arena.high = self.fixed_high
         self.arena.high_marks.pop("ring", None)
+        self.arena.high_marks.pop("expert_slots", None)
+        self._carve_expert_slots(tier)
         free = self.arena.free_bytes
         ring_bytes = max(0, min(self.ring_cap, free)) // 256 * 256
         self.chunk = min(self.chunk_cap, max(1 << 16, ring_bytes // 6 // 256 * 256))
@@ -294,6 +302,54 @@ class Executor:
         self.ring = CopyRing(self.arena.alloc_high("ring", ring_bytes), ring_bytes, self.h2d,
                              self.events)
         self.ring.tracer = self.tracer
+
+    # ------------------------------------------------- routed-expert fetcher
+    def _expert_geometry(self, sid: int, layer: int) -> tuple:
+        """(offset of expert 0, stride between experts, offset of wdown in an
+        expert, bytes of one expert) inside a MoE group's blob."""
+        blob = self.w.layout.blobs[sid]
+        e0 = blob.tensors[f"L{layer}.e0.wgu"]
+        E = self.moe.n_experts
+        stride = blob.tensors[f"L{layer}.e1.wgu"].offset - e0.offset if E > 1 else blob.nbytes - e0.offset
+        wd = blob.tensors[f"L{layer}.e0.wdown"]
+        nbytes = wd.offset + wd.rows * wd.cols * 2 - e0.offset
+        return e0.offset, stride, wd.offset - e0.offset, nbytes
+
+    def _carve_expert_slots(self, tier: int) -> None:
+        """VRAM slots for the routed experts of one MoE layer in a decode pass
+        (min(E, T*k) experts), carved before the ring so fetcher copies never
+        race the ring's reuse. Used when a decode tier streams expert groups and
+        the slots take at most a quarter of the free budget; otherwise the
+        expert kernels read the routed experts zero-copy."""
+        self.expert_slots, self.expert_slot_bytes = 0, 0
+        if self.moe is None or self.T_tier > GEMV_MAX_T or not self.fetch_enabled:
+            return
+        groups = [sid for sid, (m, _) in self.residency.items()
+                  if m == "stream" and self.shard_kind[sid] is ShardKind.MOE_EXPERT_GROUP]
+        if not groups:
+            return
+        layer = self.shards[groups[0]].layer_index
+        _, _, _, ebytes = self._expert_geometry(groups[0], layer)
+        slot = (ebytes + 255) // 256 * 256
+        n = min(self.moe.n_experts, self.T_tier * self.moe.top_k)
+        if n * slot > self.arena.free_bytes // 4:
+            return
+        self.expert_slots = self.arena.alloc_high("expert_slots", n * slot)
+        self.expert_slot_bytes = slot
+        if self.fetcher is None:
+            out = C.c_void_p()
+            L.call("ps_fetcher_create", self.moe.n_experts, C.byref(out))
+            self.fetcher = out.value
+
+    def fetcher_stats(self) -> dict:
+        if self.fetcher is None:
+            return {}
+        n, b, err = C.c_longlong(), C.c_longlong(), C.c_int()
+        L.call("ps_fetcher_info", self.fetcher, None, None, C.byref(n), C.byref(b), C.byref(err))
+        dev_err = C.c_uint()
+        L.call("ps_fetcher_device_error", self.fetcher, C.byref(dev_err))
+        return {"experts_copied": n.value, "bytes_copied": b.value, "host_error": err.value,
+                "device_timeout_seq": dev_err.value}
 
     # --------------------------------------------------------------- helpers
     def _wait(self, ev: int) -> None:
@@ -483,6 +539,33 @@ class Executor:
                    eff, d, self.m_h, lo, hi, self.cs)
             L.call("ps_moe_expert_down", self.m_h, self.m_plan, E, P, ebase, stride, down_off, eff, d,
                    self.m_out, lo, hi, self.cs)
+
+        planned = self.residency[sid][0]
+        if gemv and planned == "stream" and self.expert_slots:
+            # routed experts through the copy engine (csrc/fetcher.cu)
+            host = self.w.shard_ptr(sid)
+            _, _, _, ebytes = self._expert_geometry(sid, layer)
+            slots, sb = self.expert_slots, self.expert_slot_bytes
+            self.fetch_seq = (self.fetch_seq + 1) & 0xFFFFFFFF or 1
+            seq = self.fetch_seq
+
+            def fetched(_p, _a, _b):
+                L.call("ps_fetcher_submit", self.fetcher, seq, host + e0.offset, stride, ebytes, slots, sb)
+                L.call("ps_moe_publish", self.fetcher, self.m_ids, P, E, self.m_slotmap, seq, self.cs)
+                L.call("ps_wait_flag", self.fetcher, seq, self.cs)
+                L.call("ps_moe_expert_gu_mapped", xn, d, 0, self.m_plan, E, P, k, slots, sb, 0, eff, d,
+                       self.m_h, 0, E, self.m_slotmap, self.cs)
+                L.call("ps_moe_expert_down_mapped", self.m_h, self.m_plan, E, P, slots, sb, down_off, eff, d,
+                       self.m_out, 0, E, self.m_slotmap, self.cs)
+
+            self._traced(f"L{layer}.router+topk", route, host)
+            self._traced(f"L{layer}.experts (fetched)", fetched, 0, 0, 0)
+            self._stat.zero_copy_bytes += e0.offset
+            self._stat.bytes_streamed += min(E, P) * ebytes
+            self._stat.copies += min(E, P)
+            self._gapfill_step()
+            L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
+            return
 
         if mode in ("pinned", "zerocopy"):
             base = dev if mode == "pinned" else self.w.shard_ptr(sid)
@@ -772,6 +855,10 @@ class Executor:
             L.call("ps_stream_synchronize", s)
 
     def close(self) -> None:
+        if self.fetcher is not None:
+            self.synchronize()
+            L.call("ps_fetcher_destroy", self.fetcher)
+            self.fetcher = None
         if self.kv_host:
             self.synchronize()
             L.host_free(self.kv_host)

@@ -59,6 +59,15 @@ _SIGS = {
     "ps_moe_plan": [_p, _i, _i, _p, _p],
     "ps_moe_expert_gu": [_p, _i, _i, _p, _i, _i, _i, _p, _ll, _ll, _i, _i, _p, _i, _i, _p],
     "ps_moe_expert_down": [_p, _p, _i, _i, _p, _ll, _ll, _i, _i, _p, _i, _i, _p],
+    "ps_moe_expert_gu_mapped": [_p, _i, _i, _p, _i, _i, _i, _p, _ll, _ll, _i, _i, _p, _i, _i, _p, _p],
+    "ps_moe_expert_down_mapped": [_p, _p, _i, _i, _p, _ll, _ll, _i, _i, _p, _i, _i, _p, _p],
+    "ps_fetcher_create": [_i, _pp],
+    "ps_fetcher_destroy": [_p],
+    "ps_fetcher_info": [_p, _pp, _pp, C.POINTER(_ll), C.POINTER(_ll), C.POINTER(_i)],
+    "ps_fetcher_submit": [_p, C.c_uint, _p, _ll, _ll, _p, _ll],
+    "ps_moe_publish": [_p, _p, _i, _i, _p, C.c_uint, _p],
+    "ps_wait_flag": [_p, C.c_uint, _p],
+    "ps_fetcher_device_error": [_p, C.POINTER(C.c_uint)],
     "ps_moe_combine": [_p, _p, _i, _i, _p, _i, _i, _i, _p, _i, _p],
     "ps_embed_gather": [_p, _p, _i, _i, _p, _i, _p],
     "ps_argmax": [_p, _i, _i, _i, _p, _p],
@@ -104,7 +113,8 @@ KERNEL_CALLS = frozenset({
     "ps_gemv_bf16", "ps_gemm_bf16", "ps_rmsnorm", "ps_qkv_rope_append", "ps_attn_decode",
     "ps_attn_prefill", "ps_embed_gather", "ps_argmax", "ps_cast_f32_bf16", "ps_add_f32",
     "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_gemv_bf16_cfg", "ps_gemm_bf16_cfg",
-    "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine"})
+    "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine",
+    "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_wait_flag"})
 counters = {"kernel_calls": 0, "memcpy_calls": 0}
 
 

@@ -358,3 +358,42 @@ def test_moe_pipeline(T, zero_copy, x_bf16):
     assert rel_err(y - y0, ref) < 1e-4
     if host:
         lib.host_free(host)
+
+
+def test_expert_fetcher_publish_copy_wait():
+    """ps_moe_publish -> host thread copies the routed experts (ascending id) into
+    slots -> ps_wait_flag; mapped expert kernels see expert e at its slot."""
+    import ctypes
+    lib = L()
+    E, k, P, nbytes = 16, 4, 8, 4096
+    f = ctypes.c_void_p()
+    lib.call("ps_fetcher_create", E, ctypes.byref(f))
+    try:
+        host = lib.host_alloc(E * nbytes, mapped=True)
+        src = (np.arange(E * nbytes, dtype=np.uint32) % 251).astype(np.uint8)
+        src.reshape(E, nbytes)[:, 0] = np.arange(E)           # expert id in byte 0
+        ctypes.memmove(host, src.ctypes.data, src.nbytes)
+        slots = torch.zeros(E * nbytes, dtype=torch.uint8, device="cuda")
+        slotmap = torch.zeros(E, dtype=torch.int32, device="cuda")
+        for seq, ids in enumerate([[3, 9, 3, 1, 15, 9, 0, 1], [2, 2, 2, 2, 2, 2, 2, 2]], start=1):
+            dev_ids = torch.tensor(ids, dtype=torch.int32, device="cuda")
+            lib.call("ps_fetcher_submit", f, seq, host, nbytes, nbytes, slots.data_ptr(), nbytes)
+            lib.call("ps_moe_publish", f, dev_ids.data_ptr(), P, E, slotmap.data_ptr(), seq, stream())
+            lib.call("ps_wait_flag", f, seq, stream())
+            torch.cuda.synchronize()
+            routed = sorted(set(ids))
+            m = slotmap.cpu().numpy()
+            for e in range(E):
+                assert m[e] == (routed.index(e) if e in routed else -1)
+            got = slots.cpu().numpy().reshape(E, nbytes)
+            for r, e in enumerate(routed):
+                assert np.array_equal(got[r], src.reshape(E, nbytes)[e])
+        n, b, err = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_int()
+        lib.call("ps_fetcher_info", f, None, None, ctypes.byref(n), ctypes.byref(b), ctypes.byref(err))
+        assert (n.value, err.value) == (5 + 1, 0)
+        dev_err = ctypes.c_uint()
+        lib.call("ps_fetcher_device_error", f, ctypes.byref(dev_err))
+        assert dev_err.value == 0
+        lib.host_free(host)
+    finally:
+        lib.call("ps_fetcher_destroy", f)
