@@ -48,7 +48,17 @@ class Engine:
 
     def __init__(self, model, budget_bytes: float, context_len: int, batch: int = 1,
                  machine="b200", profile: str | None = None, seed: int = 0,
-                 max_tokens: int | None = None, chunk_bytes: int = 64 << 20):
+                 max_tokens: int | None = None, chunk_bytes: int = 64 << 20,
+                 checkpoint: str | None = None):
+        """`model`: preset name or ModelSpec (random-init weights), or None with
+        `checkpoint` = a directory holding config.json + safetensors (real weights,
+        runtime/checkpoint.py)."""
+        ckpt = None
+        if checkpoint is not None:
+            from .checkpoint import Checkpoint, spec_from_hf_config
+            ckpt = Checkpoint(checkpoint)
+            if model is None:
+                model, ck_arch = spec_from_hf_config(ckpt.config, seed=seed)
         self.spec: ModelSpec = catalog.builtin_model(model) if isinstance(model, str) else model
         self.machine: MachineSpec = (catalog.builtin_machine(machine) if isinstance(machine, str)
                                      else machine)
@@ -57,6 +67,8 @@ class Engine:
         self.context_len = int(context_len)
         self.batch = int(batch)
         self.arch = arch_for(self.spec, seed)
+        if ckpt is not None and ckpt.config:
+            self.arch = spec_from_hf_config(ckpt.config, seed=seed)[1]
         # per-tier plans; tiers the budget cannot plan are unreachable (time = inf)
         self.plans = reachable_tiers(self.spec, self.machine, self.db, self.budget,
                                      self.context_len, self.batch)
@@ -69,7 +81,10 @@ class Engine:
                                    {t: TierEntry(t, p) for t, p in self.plans.items()})
         self.weights = HostWeights(self.spec, self.arch)
         t0 = time.perf_counter()
-        self.weights.generate()
+        if ckpt is not None:
+            self.weights.load(ckpt)
+        else:
+            self.weights.generate()
         self.load_seconds = time.perf_counter() - t0
         self.max_tokens = max_tokens
         self.chunk_bytes = chunk_bytes

@@ -225,6 +225,26 @@ class HostWeights:
                                      .from_address(self.tensor_ptr(shard_id, name))))
         return buf.reshape(t.rows, t.cols)
 
+    def blob_bytes(self) -> np.ndarray:
+        """uint8 view of the whole pinned blob (no copy)."""
+        import ctypes
+        return np.ctypeslib.as_array((ctypes.c_uint8 * self.layout.total_bytes).from_address(self.base))
+
+    def embed_bytes(self) -> np.ndarray:
+        import ctypes
+        return np.ctypeslib.as_array((ctypes.c_uint8 * self.layout.embed_bytes).from_address(self.embed))
+
+    def load(self, ckpt) -> int:
+        """Fill the blob from a safetensors checkpoint (runtime/checkpoint.py)
+        instead of the random init; returns the bytes written."""
+        from .checkpoint import fill_from_checkpoint
+        return fill_from_checkpoint(self.layout, self.blob_bytes(), self.embed_bytes(), ckpt)
+
+    def export(self, out_dir: str) -> list:
+        """Write the blob as an HF-named bf16 safetensors checkpoint + config.json."""
+        from .checkpoint import export_safetensors
+        return export_safetensors(self.layout, self.blob_bytes(), self.embed_bytes(), out_dir)
+
     def embed_view(self) -> np.ndarray:
         n = self.spec.vocab_size * self.spec.d_model
         buf = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint16 * n).from_address(self.embed))

@@ -1,0 +1,191 @@
+"""Checkpoint loading (runtime/checkpoint.py): safetensors parsing, HF-name mapping
+onto the shard-contiguous layout (q/k/v concatenation, gate/up interleave, experts,
+tied heads), dtype rounding, config.json -> ModelSpec, export round trip. CPU only;
+the GPU round trip through Engine is in test_engine_gpu.py."""
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2604_26334_b200.planning import catalog
+from paper_2604_26334_b200.runtime import checkpoint as ck
+from paper_2604_26334_b200.runtime.model import WeightLayout, arch_for
+
+
+def test_bf16_rounding_matches_torch():
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(10000).astype(np.float32) * 10.0 ** rng.integers(-8, 8, 10000),
+                        np.array([0.0, -0.0, np.inf, -np.inf, 1e-40, 3.3895314e38], np.float32)])
+    want = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ck.bf16_bits(x), want)
+    h = rng.standard_normal(1000).astype(np.float16)
+    want = torch.from_numpy(h).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ck.bf16_bits(h), want)
+
+
+def _hf_tensors(spec, arch, rng, tied=False, f32_names=()):
+    """Random HF-named tensors for `spec` -> {name: (dtype, shape, array)}."""
+    d, hd, h, kv = spec.d_model, spec.head_dim, spec.n_heads, spec.n_kv_heads
+    out = {}
+
+    def add(name, shape):
+        a = rng.integers(0, 1 << 16, size=shape, dtype=np.uint16)
+        a = a & 0x7F7F   # finite bf16 patterns only
+        if name in f32_names:
+            f = (a.astype(np.uint32) << 16).view(np.float32)
+            out[name] = ("F32", shape, f)
+        else:
+            out[name] = ("BF16", shape, a)
+
+    add("model.embed_tokens.weight", (spec.vocab_size, d))
+    for i in range(spec.n_layers):
+        p = f"model.layers.{i}."
+        add(p + "input_layernorm.weight", (d,))
+        add(p + "self_attn.q_proj.weight", (h * hd, d))
+        add(p + "self_attn.k_proj.weight", (kv * hd, d))
+        add(p + "self_attn.v_proj.weight", (kv * hd, d))
+        add(p + "self_attn.o_proj.weight", (d, h * hd))
+        if arch.qk_norm:
+            add(p + "self_attn.q_norm.weight", (hd,))
+            add(p + "self_attn.k_norm.weight", (hd,))
+        add(p + "post_attention_layernorm.weight", (d,))
+        if spec.moe:
+            m = spec.moe
+            add(p + "mlp.gate.weight", (m.n_experts, d))
+            for e in range(m.n_experts):
+                add(p + f"mlp.experts.{e}.gate_proj.weight", (m.expert_ffn_dim, d))
+                add(p + f"mlp.experts.{e}.up_proj.weight", (m.expert_ffn_dim, d))
+                add(p + f"mlp.experts.{e}.down_proj.weight", (d, m.expert_ffn_dim))
+        else:
+            add(p + "mlp.gate_proj.weight", (spec.ffn_dim, d))
+            add(p + "mlp.up_proj.weight", (spec.ffn_dim, d))
+            add(p + "mlp.down_proj.weight", (d, spec.ffn_dim))
+    add("model.norm.weight", (d,))
+    if not tied:
+        add("lm_head.weight", (spec.vocab_size, d))
+    return out
+
+
+def _write(tmp, spec, arch, tensors, shards=2):
+    names = list(tensors)
+    per = -(-len(names) // shards)
+    wm = {}
+    for s in range(shards):
+        part = {n: tensors[n] for n in names[s * per:(s + 1) * per]}
+        fn = f"model-{s + 1:05d}-of-{shards:05d}.safetensors"
+        ck.write_safetensors(tmp / fn, part)
+        wm.update({n: fn for n in part})
+    (tmp / "model.safetensors.index.json").write_text(json.dumps({"weight_map": wm}))
+    (tmp / "config.json").write_text(json.dumps(ck.hf_config(spec, arch)))
+
+
+def _bits(entry):
+    dtype, shape, a = entry
+    return ck.bf16_bits(a) if dtype == "F32" else a
+
+
+@pytest.mark.parametrize("model,tied", [("tiny-llama", False), ("tiny-moe", True)])
+def test_fill_maps_every_tensor(tmp_path, model, tied):
+    spec = catalog.builtin_model(model)
+    arch = arch_for(spec)
+    rng = np.random.default_rng(1)
+    f32 = {"model.layers.0.self_attn.k_proj.weight", "model.norm.weight"}
+    tensors = _hf_tensors(spec, arch, rng, tied=tied, f32_names=f32)
+    _write(tmp_path, spec, arch, tensors)
+    lay = WeightLayout(spec, arch)
+    blob = np.zeros(lay.total_bytes, np.uint8)
+    emb = np.zeros(lay.embed_bytes, np.uint8)
+    c = ck.Checkpoint(tmp_path)
+    assert len(c.files) == 2
+    ck.fill_from_checkpoint(lay, blob, emb, c)
+
+    def view(sid, name):
+        b = lay.blobs[sid]
+        t = b.tensors[name]
+        o = b.offset + t.offset
+        return blob[o:o + t.nbytes].view(np.uint16).reshape(t.rows, t.cols)
+
+    assert np.array_equal(emb.view(np.uint16).reshape(spec.vocab_size, -1),
+                          tensors["model.embed_tokens.weight"][2])
+    for sid, b in lay.blobs.items():
+        i = b.layer
+        p = f"model.layers.{i}."
+        for name in b.tensors:
+            got = view(sid, name)
+            leaf = name.split(".", 1)[1] if name.startswith("L") else name
+            if leaf == "wqkv":
+                want = np.concatenate([_bits(tensors[p + f"self_attn.{x}_proj.weight"]) for x in "qkv"])
+            elif leaf == "wgu":
+                want = np.empty_like(got)
+                want[0::2] = _bits(tensors[p + "mlp.gate_proj.weight"])
+                want[1::2] = _bits(tensors[p + "mlp.up_proj.weight"])
+            elif leaf.endswith(".wgu"):
+                e = int(leaf.split(".")[0][1:])
+                want = np.empty_like(got)
+                want[0::2] = _bits(tensors[p + f"mlp.experts.{e}.gate_proj.weight"])
+                want[1::2] = _bits(tensors[p + f"mlp.experts.{e}.up_proj.weight"])
+            elif leaf.endswith(".wdown") and leaf.startswith("e"):
+                e = int(leaf.split(".")[0][1:])
+                want = _bits(tensors[p + f"mlp.experts.{e}.down_proj.weight"])
+            elif name == "lm_head":
+                want = _bits(tensors["model.embed_tokens.weight" if tied else "lm_head.weight"])
+            else:
+                want = _bits(tensors[ck.hf_name(b.tensors[name].init[1])]).reshape(got.shape)
+            assert np.array_equal(got, want), name
+
+
+def test_export_round_trip(tmp_path):
+    spec = catalog.builtin_model("tiny-moe")
+    arch = arch_for(spec)
+    lay = WeightLayout(spec, arch)
+    rng = np.random.default_rng(2)
+    blob = np.zeros(lay.total_bytes, np.uint8)
+    for b in lay.blobs.values():          # random bytes in every tensor, zero padding
+        for t in b.tensors.values():
+            o = b.offset + t.offset
+            blob[o:o + t.nbytes] = rng.integers(0, 256, t.nbytes, dtype=np.uint8)
+    emb = rng.integers(0, 256, lay.embed_bytes, dtype=np.uint8)
+    files = ck.export_safetensors(lay, blob, emb, tmp_path, max_shard_bytes=1 << 20)
+    assert len(files) > 1
+    c = ck.Checkpoint(tmp_path)
+    spec2, arch2 = ck.spec_from_hf_config(c.config)
+    assert (spec2.n_layers, spec2.d_model, spec2.moe, spec2.vocab_size) == \
+        (spec.n_layers, spec.d_model, spec.moe, spec.vocab_size)
+    assert (arch2.qk_norm, arch2.rms_eps, arch2.rope_theta) == (arch.qk_norm, arch.rms_eps, arch.rope_theta)
+    blob2, emb2 = np.zeros_like(blob), np.zeros_like(emb)
+    ck.fill_from_checkpoint(WeightLayout(spec2, arch2), blob2, emb2, c)
+    assert np.array_equal(blob, blob2) and np.array_equal(emb, emb2)
+
+
+LLAMA31_8B = {"architectures": ["LlamaForCausalLM"], "hidden_size": 4096, "intermediate_size": 14336,
+              "max_position_embeddings": 131072, "model_type": "llama", "num_attention_heads": 32,
+              "num_hidden_layers": 32, "num_key_value_heads": 8, "rms_norm_eps": 1e-05,
+              "rope_scaling": {"factor": 8.0, "high_freq_factor": 4.0, "low_freq_factor": 1.0,
+                               "original_max_position_embeddings": 8192, "rope_type": "llama3"},
+              "rope_theta": 500000.0, "tie_word_embeddings": False, "vocab_size": 128256}
+QWEN3_30B_A3B = {"architectures": ["Qwen3MoeForCausalLM"], "head_dim": 128, "hidden_size": 2048,
+                 "intermediate_size": 6144, "max_position_embeddings": 40960, "model_type": "qwen3_moe",
+                 "moe_intermediate_size": 768, "norm_topk_prob": True, "num_attention_heads": 32,
+                 "num_experts": 128, "num_experts_per_tok": 8, "num_hidden_layers": 48,
+                 "num_key_value_heads": 4, "rms_norm_eps": 1e-06, "rope_theta": 1000000.0,
+                 "vocab_size": 151936}
+
+
+@pytest.mark.parametrize("cfg,preset", [(LLAMA31_8B, "llama3.1-8b"), (QWEN3_30B_A3B, "qwen3-30b-a3b")])
+def test_public_configs_match_presets(cfg, preset):
+    """The public HF configs of the BASELINE models map to the same ModelSpec /
+    Arch the presets hard-code, so a real checkpoint plans exactly like the bench."""
+    spec, arch = ck.spec_from_hf_config(cfg, name=preset)
+    ref = catalog.builtin_model(preset)
+    assert spec == ref
+    assert arch == arch_for(ref)
+
+
+def test_rejects_bad_files(tmp_path):
+    (tmp_path / "x.safetensors").write_bytes(b"\x01")
+    with pytest.raises(Exception):
+        ck.Checkpoint(tmp_path / "x.safetensors")
+    with pytest.raises(Exception):
+        ck.spec_from_hf_config(dict(LLAMA31_8B, rope_scaling={"rope_type": "yarn", "factor": 4.0}))

@@ -225,3 +225,26 @@ def test_tiny_moe_fetched_experts_exact(monkeypatch):
                 assert st["experts_copied"] % moe.top_k == 0 and st["experts_copied"] > 0, st
                 used += 1
     assert used > 0, "no budget exercised the fetcher"
+
+
+@pytest.mark.parametrize("model,frac", [("tiny-llama", 0.6), ("tiny-moe", 1.0)])
+def test_checkpoint_round_trip_generates_same_tokens(tmp_path, model, frac):
+    """Random-init weights exported as an HF safetensors checkpoint and loaded
+    back (Engine(None, checkpoint=dir)) fill a byte-identical host blob and
+    generate the same tokens."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model(model)
+    budget = frac * total_model_bytes(spec)
+    prompt = _prompt(40, spec.vocab_size, seed=5)
+    eng = Engine(spec, budget_bytes=budget, context_len=160)
+    want = eng.generate([prompt], gen_len=8).tokens[0]
+    files = eng.weights.export(str(tmp_path))
+    blob = eng.weights.blob_bytes().copy()
+    eng.close()
+    assert files
+    eng2 = Engine(None, budget_bytes=budget, context_len=160, checkpoint=str(tmp_path))
+    assert eng2.spec.n_layers == spec.n_layers and eng2.spec.moe == spec.moe
+    assert np.array_equal(eng2.weights.blob_bytes(), blob)
+    got = eng2.generate([prompt], gen_len=8).tokens[0]
+    eng2.close()
+    assert np.array_equal(got, want)
