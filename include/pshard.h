@@ -39,6 +39,10 @@ const char* ps_last_error(void);
 int ps_abi_version(void);
 int ps_device_info(int device, int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem);
 int ps_set_device(int device);
+/* Load every kernel of the library now (CUDA lazy module loading would otherwise load
+ * a kernel at its first launch — stalling behind any spinning kernel, e.g. ps_wait_flag).
+ * The executor calls it once before its first pass; n_loaded may be NULL. */
+int ps_preload_kernels(int* n_loaded);
 
 /* ---- host memory and the copy engine --------------------------------------
  * Replace the simulated PCIe channels of `pkg/src/shardplan/simulator.py:156-207`

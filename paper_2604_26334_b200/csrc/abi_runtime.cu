@@ -54,7 +54,24 @@ bool is_host_ptr(const void* p) {
 }
 }  // namespace ps
 
+int ps_preload_gemv();
+int ps_preload_gemv_tma();
+int ps_preload_gemm();
+int ps_preload_attention();
+int ps_preload_elementwise();
+int ps_preload_moe();
+extern "C" int ps_preload_fetcher();
+
 extern "C" {
+
+int ps_preload_kernels(int* n_loaded) {
+  static int loaded = -1;
+  if (loaded < 0)
+    loaded = ps_preload_gemv() + ps_preload_gemv_tma() + ps_preload_gemm() + ps_preload_attention() +
+             ps_preload_elementwise() + ps_preload_moe() + ps_preload_fetcher();
+  if (n_loaded) *n_loaded = loaded;
+  return PS_OK;
+}
 
 const char* ps_last_error(void) { return g_err; }
 

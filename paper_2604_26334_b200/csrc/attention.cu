@@ -439,3 +439,14 @@ extern "C" int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
+
+int ps_preload_attention() {
+  int n = 0;
+#define PS_G(HD) \
+  touch_kernel(attn_decode_kernel<HD, 1>, n); touch_kernel(attn_decode_kernel<HD, 2>, n); \
+  touch_kernel(attn_decode_kernel<HD, 4>, n); touch_kernel(attn_decode_kernel<HD, 8>, n); \
+  touch_kernel(attn_decode_merge_kernel<HD>, n); touch_kernel(attn_prefill_kernel<HD>, n);
+  PS_G(64) PS_G(128)
+#undef PS_G
+  return n;
+}

@@ -76,3 +76,17 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 }  // namespace ps
+
+// Module preloading: touch a kernel so CUDA's lazy loader loads it now. Every TU
+// lists the kernels it launches in ps_preload_<tu>(); ps_preload_kernels() calls
+// them all. A kernel loaded for the first time while another kernel spins on the
+// device (ps_wait_flag) would stall the load until the spin ends — so the executor
+// preloads everything before its first pass.
+namespace ps {
+template <typename F>
+inline void touch_kernel(F* f, int& n) {
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(f)) == cudaSuccess) ++n;
+  else cudaGetLastError();
+}
+}  // namespace ps

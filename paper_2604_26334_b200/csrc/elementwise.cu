@@ -323,3 +323,20 @@ extern "C" int ps_upload_small(void* dst, const void* src, int nbytes, void* str
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
+
+int ps_preload_elementwise() {
+  using namespace ps;
+  int n = 0;
+  touch_kernel(init_uniform_bf16_kernel, n);
+  touch_kernel(rmsnorm_kernel<true>, n);
+  touch_kernel(rmsnorm_kernel<false>, n);
+  touch_kernel(qkv_post_kernel<64>, n);
+  touch_kernel(qkv_post_kernel<128>, n);
+  touch_kernel(embed_kernel, n);
+  touch_kernel(argmax_kernel, n);
+  touch_kernel(cast_f32_bf16_kernel, n);
+  touch_kernel(add_f32_kernel, n);
+  touch_kernel(init_interleaved_bf16_kernel, n);
+  touch_kernel(upload_small_kernel, n);
+  return n;
+}

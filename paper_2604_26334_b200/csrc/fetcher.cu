@@ -208,8 +208,19 @@ using namespace ps;
 
 extern "C" {
 
+int ps_preload_fetcher() {
+  int n = 0;
+  touch_kernel(moe_publish_kernel, n);
+  touch_kernel(wait_flag_kernel, n);
+  return n;
+}
+
+int ps_preload_kernels(int* n_loaded);
+
 int ps_fetcher_create(int max_experts, void** out) {
   PS_REQUIRE(out && max_experts >= 1 && max_experts <= 4096, "ps_fetcher_create: max_experts=%d", max_experts);
+  int loaded = 0;
+  ps_preload_kernels(&loaded);   // no lazy module load may happen while ps_wait_flag spins
   auto* f = new ExpertFetcher(max_experts);
   int rc = f->init();
   if (rc) {

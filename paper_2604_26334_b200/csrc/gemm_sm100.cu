@@ -542,3 +542,17 @@ extern "C" int ps_gemm_bf16_cfg(const void* A, int M, int K, long long lda, cons
                                 void* C, int ldc, int epilogue, void* stream, int variant) {
   return ps::gemm_checked(A, M, K, lda, B, N, ldb, C, ldc, epilogue, stream, variant);
 }
+
+int ps_preload_gemm() {
+  using namespace ps;
+  int n = 0;
+  touch_kernel(gemm_bf16_tcgen05_kernel<PS_EPI_STORE>, n);
+  touch_kernel(gemm_bf16_tcgen05_kernel<PS_EPI_ACCUM>, n);
+  touch_kernel(gemm_bf16_tcgen05_kernel<PS_EPI_STORE_BF16>, n);
+  touch_kernel(gemm_bf16_tcgen05_kernel<PS_EPI_SWIGLU>, n);
+  touch_kernel(gemm_bf16_pair_kernel<PS_EPI_STORE>, n);
+  touch_kernel(gemm_bf16_pair_kernel<PS_EPI_ACCUM>, n);
+  touch_kernel(gemm_bf16_pair_kernel<PS_EPI_STORE_BF16>, n);
+  touch_kernel(gemm_bf16_pair_kernel<PS_EPI_SWIGLU>, n);
+  return n;
+}

@@ -262,3 +262,17 @@ extern "C" int ps_gemv_bf16_cfg(const float* x, int ldx, int t, const void* W, i
                                 int grid_cap) {
   return ps::gemv_checked(x, ldx, t, W, N, K, ldw, y, ldy, epilogue, stream, rows, ksplit, grid_cap);
 }
+
+int ps_preload_gemv() {
+  using namespace ps;
+  int n = 0;
+#define PS_T4(T, R, K)                                         \
+  touch_kernel(gemv_bf16_kernel<T, R, K, PS_EPI_STORE>, n);    \
+  touch_kernel(gemv_bf16_kernel<T, R, K, PS_EPI_ACCUM>, n);    \
+  touch_kernel(gemv_bf16_kernel<T, R, K, PS_EPI_SWIGLU>, n);
+#define PS_TK(T, R) PS_T4(T, R, 1) PS_T4(T, R, 2) PS_T4(T, R, 4) PS_T4(T, R, 8)
+  PS_TK(1, 4) PS_TK(1, 2) PS_TK(2, 2) PS_TK(4, 2) PS_TK(8, 2)
+#undef PS_TK
+#undef PS_T4
+  return n;
+}

@@ -269,3 +269,15 @@ int gemv_tma_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int
 }
 
 }  // namespace ps
+
+int ps_preload_gemv_tma() {
+  using namespace ps;
+  int n = 0;
+#define PS_T(T)                                                \
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_STORE>, n);           \
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_ACCUM>, n);           \
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_SWIGLU>, n);
+  PS_T(1) PS_T(2) PS_T(4) PS_T(8)
+#undef PS_T
+  return n;
+}

@@ -356,3 +356,15 @@ int ps_moe_combine(const float* out, const int* plan, int E, int P, const float*
 }
 
 }  // extern "C"
+
+int ps_preload_moe() {
+  using namespace ps;
+  int n = 0;
+  touch_kernel(route_topk_kernel, n);
+  touch_kernel(moe_plan_kernel, n);
+  touch_kernel(expert_gu_kernel<true>, n);
+  touch_kernel(expert_gu_kernel<false>, n);
+  touch_kernel(expert_down_kernel, n);
+  touch_kernel(moe_combine_kernel, n);
+  return n;
+}

@@ -49,10 +49,11 @@ class Engine:
     def __init__(self, model, budget_bytes: float, context_len: int, batch: int = 1,
                  machine="b200", profile: str | None = None, seed: int = 0,
                  max_tokens: int | None = None, chunk_bytes: int = 64 << 20,
-                 checkpoint: str | None = None):
+                 checkpoint: str | None = None, shared_weights: str | None = None):
         """`model`: preset name or ModelSpec (random-init weights), or None with
         `checkpoint` = a directory holding config.json + safetensors (real weights,
-        runtime/checkpoint.py)."""
+        runtime/checkpoint.py). `shared_weights`: a /dev/shm segment name shared by
+        the replicas of one node (one host copy of the weights per node)."""
         ckpt = None
         if checkpoint is not None:
             from .checkpoint import Checkpoint, spec_from_hf_config
@@ -79,10 +80,15 @@ class Engine:
             self.table = TierTable(self.spec.name, self.machine.name, self.budget,
                                    self.context_len,
                                    {t: TierEntry(t, p) for t, p in self.plans.items()})
-        self.weights = HostWeights(self.spec, self.arch)
+        self.weights = HostWeights(self.spec, self.arch, shared=shared_weights)
         t0 = time.perf_counter()
         if ckpt is not None:
-            self.weights.load(ckpt)
+            if self.weights.shared is None or self.weights.shared.creator:
+                self.weights.load(ckpt)
+                if self.weights.shared is not None:
+                    self.weights.shared.mark_ready()
+            else:
+                self.weights.shared.wait_ready()
         else:
             self.weights.generate()
         self.load_seconds = time.perf_counter() - t0

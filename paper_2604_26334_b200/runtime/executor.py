@@ -97,6 +97,8 @@ class Executor:
         self.Tmax = max_tokens
         self.shards = build_shards(spec, context_len, kv_slots)
         self.by_layer_kind = {(s.layer_index, s.kind): s for s in self.shards}
+        n_loaded = C.c_int()
+        L.call("ps_preload_kernels", C.byref(n_loaded))   # no lazy module load mid-pass
         self.shard_kind = {s.id: s.kind for s in self.shards}
         # routed-expert fetcher (copy-engine expert uploads in MoE decode); PS_MOE_FETCH=0 disables
         self.fetcher, self.fetch_seq = None, 0
@@ -341,6 +343,30 @@ class Executor:
             L.call("ps_fetcher_create", self.moe.n_experts, C.byref(out))
             self.fetcher = out.value
 
+    def _fetch_debug(self, layer, seq, P, E, host, stride, ebytes, slots, sb) -> None:
+        """PS_FETCH_DEBUG=1: synchronise and check ids, slot map and slot bytes."""
+        import torch
+        L.call("ps_stream_synchronize", self.cs)
+        ids = np.zeros(P, np.int32)
+        L.call("ps_memcpy_async", ids.ctypes.data, self.m_ids, P * 4, self.cs)
+        smap = np.zeros(E, np.int32)
+        L.call("ps_memcpy_async", smap.ctypes.data, self.m_slotmap, E * 4, self.cs)
+        L.call("ps_stream_synchronize", self.cs)
+        routed = sorted(set(int(i) for i in ids))
+        bad = [i for i in ids if not 0 <= i < E]
+        ok_map = all(smap[e] == (routed.index(e) if e in routed else -1) for e in range(E)) if not bad else False
+        mism = []
+        if not bad:
+            for r, e in enumerate(routed):
+                got = np.zeros(ebytes, np.uint8)
+                L.call("ps_memcpy_async", got.ctypes.data, slots + r * sb, ebytes, self.cs)
+                L.call("ps_stream_synchronize", self.cs)
+                want = np.ctypeslib.as_array((C.c_uint8 * ebytes).from_address(host + e * stride))
+                if not np.array_equal(got, want):
+                    mism.append(e)
+        print(f"[fetch-debug] layer {layer} seq {seq} ids {ids.tolist()} bad {bad} map_ok {ok_map} "
+              f"slot_mismatch {mism} stats {self.fetcher_stats()}", flush=True)
+
     def fetcher_stats(self) -> dict:
         if self.fetcher is None:
             return {}
@@ -553,6 +579,8 @@ class Executor:
                 L.call("ps_fetcher_submit", self.fetcher, seq, host + e0.offset, stride, ebytes, slots, sb)
                 L.call("ps_moe_publish", self.fetcher, self.m_ids, P, E, self.m_slotmap, seq, self.cs)
                 L.call("ps_wait_flag", self.fetcher, seq, self.cs)
+                if os.environ.get("PS_FETCH_DEBUG"):
+                    self._fetch_debug(layer, seq, P, E, host + e0.offset, stride, ebytes, slots, sb)
                 L.call("ps_moe_expert_gu_mapped", xn, d, 0, self.m_plan, E, P, k, slots, sb, 0, eff, d,
                        self.m_h, 0, E, self.m_slotmap, self.cs)
                 L.call("ps_moe_expert_down_mapped", self.m_h, self.m_plan, E, P, slots, sb, down_off, eff, d,
@@ -606,7 +634,8 @@ class Executor:
         event), so head bytes fill the gaps instead of sharing the link with expert
         reads. Enabled only when nothing else in the pass uses the ring."""
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
-        if not (gemv and R and self.moe is not None and self.ring is not None):
+        if not (gemv and R and self.moe is not None and self.ring is not None) or \
+                os.environ.get("PS_GAPFILL", "1") == "0":
             return
         head_sid = self.by_layer_kind[(self.spec.n_layers, ShardKind.OUTPUT_HEAD)].id
         if self.residency[head_sid][0] != "stream":

@@ -24,6 +24,7 @@ _SIGS = {
     "ps_abi_version": [],
     "ps_device_info": [_i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_sz)],
     "ps_set_device": [_i],
+    "ps_preload_kernels": [C.POINTER(_i)],
     "ps_host_alloc": [_sz, _i, _pp],
     "ps_host_free": [_p],
     "ps_host_register": [_p, _sz, _i],

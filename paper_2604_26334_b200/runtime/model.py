@@ -185,22 +185,108 @@ class WeightLayout:
         return self.blobs[shard_id].tensors[name]
 
 
+class SharedHostBlob:
+    """One host buffer shared by every process of a node (data-parallel replicas):
+    a /dev/shm file, mmapped and pinned in each process with cudaHostRegister
+    (mapped, portable). The process that creates the file fills it and then
+    drops a `.ready` marker; the others map it and wait for the marker, so a
+    node holds one copy of the weights instead of one per GPU."""
+
+    def __init__(self, name: str, nbytes: int, timeout_s: float = 3600.0):
+        import ctypes
+        import mmap
+        import os
+        self.path = f"/dev/shm/{name}"
+        self.nbytes = nbytes
+        self.timeout_s = timeout_s
+        try:
+            self.fd = os.open(self.path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+            self.creator = True
+            os.ftruncate(self.fd, nbytes)
+        except FileExistsError:
+            self.creator = False
+            self.fd = os.open(self.path, os.O_RDWR)
+            t0 = __import__("time").time()
+            while os.fstat(self.fd).st_size < nbytes:
+                if __import__("time").time() - t0 > 60:
+                    raise TimeoutError(f"{self.path}: creator never sized the blob")
+                __import__("time").sleep(0.05)
+        self.mm = mmap.mmap(self.fd, nbytes)
+        self.addr = ctypes.addressof(ctypes.c_char.from_buffer(self.mm))
+        L.call("ps_host_register", self.addr, nbytes, 1)
+
+    @staticmethod
+    def fits(nbytes: int) -> bool:
+        import os
+        try:
+            st = os.statvfs("/dev/shm")
+        except OSError:
+            return False
+        return st.f_bavail * st.f_frsize > nbytes * 1.05
+
+    def mark_ready(self) -> None:
+        with open(self.path + ".ready", "w") as fh:
+            fh.write("ok")
+
+    def wait_ready(self) -> None:
+        import os
+        import time
+        t0 = time.time()
+        while not os.path.exists(self.path + ".ready"):
+            if time.time() - t0 > self.timeout_s:
+                raise TimeoutError(f"{self.path}: weights never marked ready")
+            time.sleep(0.1)
+
+    def close(self) -> None:
+        import os
+        if self.addr:
+            L.call("ps_host_unregister", self.addr)
+            self.addr = 0
+            import gc
+            gc.collect()   # drop the ctypes view before unmapping
+            try:
+                self.mm.close()
+            except BufferError:
+                pass
+            os.close(self.fd)
+            if self.creator:
+                for p in (self.path, self.path + ".ready"):
+                    try:
+                        os.unlink(p)
+                    except FileNotFoundError:
+                        pass
+
+
 class HostWeights:
     """Pinned + mapped host blob holding every shard, plus the embedding table.
 
     `generate()` fills it on the GPU (deterministic per tensor name) through
     a bounded device staging buffer and D2H copies; the staging buffer is
     released before the VRAM arena is created, so it does not count against
-    the budget.
+    the budget. With `shared=name` the blob and table live in one /dev/shm
+    segment shared by the node's replicas (SharedHostBlob): only the process
+    that created it generates, the others wait for it.
     """
 
-    def __init__(self, spec: ModelSpec, arch: Arch):
+    def __init__(self, spec: ModelSpec, arch: Arch, shared: str | None = None):
         self.spec, self.arch = spec, arch
         self.layout = WeightLayout(spec, arch)
-        self.base = L.host_alloc(self.layout.total_bytes, mapped=True)
-        self.embed = L.host_alloc(self.layout.embed_bytes, mapped=True)
+        self.shared = None
+        if shared is not None:
+            total = _align(self.layout.total_bytes) + self.layout.embed_bytes
+            self.shared = SharedHostBlob(shared, total)
+            self.base = self.shared.addr
+            self.embed = self.shared.addr + _align(self.layout.total_bytes)
+        else:
+            self.base = L.host_alloc(self.layout.total_bytes, mapped=True)
+            self.embed = L.host_alloc(self.layout.embed_bytes, mapped=True)
 
     def close(self) -> None:
+        if self.shared is not None:
+            if self.base:
+                self.base = self.embed = 0
+                self.shared.close()
+            return
         if self.base:
             L.host_free(self.base)
             L.host_free(self.embed)
@@ -251,6 +337,14 @@ class HostWeights:
         return buf.reshape(self.spec.vocab_size, self.spec.d_model)
 
     def generate(self, staging_bytes: int = 256 << 20) -> None:
+        if self.shared is not None and not self.shared.creator:
+            self.shared.wait_ready()          # another replica of this node fills it
+            return
+        self._generate(staging_bytes)
+        if self.shared is not None:
+            self.shared.mark_ready()
+
+    def _generate(self, staging_bytes: int) -> None:
         import torch
         seed = self.arch.seed
         stream = torch.cuda.current_stream().cuda_stream

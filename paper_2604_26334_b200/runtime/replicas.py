@@ -41,3 +41,17 @@ def aggregate(tokens: int, seconds: float, device: str = "cpu") -> dict:
     total, slowest = float(t.item()), float(s.item())
     return {"tokens": total, "seconds_max": slowest, "value": total / slowest,
             "world": dist.get_world_size()}
+
+
+def shared_weights_name(model: str, seed: int = 0) -> str | None:
+    """A /dev/shm segment name every replica of this job agrees on (rank 0 draws a
+    random token and broadcasts it), or None outside torch.distributed. Replicas on
+    one node then hold one host copy of the weights (model.SharedHostBlob)."""
+    import secrets
+
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return None
+    box = [secrets.token_hex(6) if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return f"pshard_{model}_{seed}_{box[0]}"

@@ -248,3 +248,49 @@ def test_checkpoint_round_trip_generates_same_tokens(tmp_path, model, frac):
     got = eng2.generate([prompt], gen_len=8).tokens[0]
     eng2.close()
     assert np.array_equal(got, want)
+
+
+def _shared_weights_worker(name, q):
+    import hashlib
+    import sys
+    import os
+    sys.path.insert(0, os.getcwd())
+    from paper_2604_26334_b200.planning import catalog as cat
+    from paper_2604_26334_b200.runtime.model import HostWeights, arch_for as af
+    spec = cat.builtin_model("tiny-llama")
+    hw = HostWeights(spec, af(spec), shared=name)
+    hw.generate()
+    digest = hashlib.sha256(hw.blob_bytes().tobytes() + hw.embed_bytes().tobytes()).hexdigest()
+    q.put((hw.shared.creator, digest))
+    import time
+    time.sleep(1.0)   # keep the mapping alive while the other replica reads
+    hw.close()
+
+
+def test_shared_host_weights_two_processes():
+    """Two replicas on one node map ONE /dev/shm copy of the weights: exactly one
+    generates, both see the bytes a private blob gets."""
+    import hashlib
+    import multiprocessing as mp
+    import secrets
+    from paper_2604_26334_b200.runtime.model import HostWeights, SharedHostBlob, arch_for
+    spec = catalog.builtin_model("tiny-llama")
+    hw = HostWeights(spec, arch_for(spec))
+    hw.generate()
+    want = hashlib.sha256(hw.blob_bytes().tobytes() + hw.embed_bytes().tobytes()).hexdigest()
+    hw.close()
+    if not SharedHostBlob.fits(64 << 20):
+        pytest.skip("/dev/shm too small on this box")
+    name = "pshard_test_" + secrets.token_hex(4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_shared_weights_worker, args=(name, q)) for _ in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in ps:
+        p.join(60)
+    assert sorted(c for c, _ in got) == [False, True]
+    assert all(d == want for _, d in got)
+    import os
+    assert not os.path.exists(f"/dev/shm/{name}")

@@ -55,3 +55,29 @@ def test_two_replicas_aggregate_over_gloo():
 def test_single_process_aggregate_is_local():
     out = aggregate(tokens=10, seconds=2.0)
     assert out == {"tokens": 10, "seconds_max": 2.0, "value": 5.0, "world": 1}
+
+
+def _shared_name_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_26334_b200.runtime.replicas import shared_weights_name
+    q.put((rank, shared_weights_name("tiny-llama")))
+    dist.destroy_process_group()
+
+
+def test_shared_weights_name_agreed_across_ranks():
+    import multiprocessing as mp
+    import random
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randint(20000, 40000)
+    ps = [ctx.Process(target=_shared_name_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(60)
+    names = dict(q.get(timeout=10) for _ in range(2))
+    assert names[0] == names[1] and names[0].startswith("pshard_tiny-llama_0_")
