@@ -304,6 +304,8 @@ def run_ours(args, rank: int, world: int) -> dict:
         "gpu_launches": None,
         "clocks": clocks.summary(),
         "ttft": {"ms": round(res.ttft_s * 1e3, 2), "migration_bytes": int(res.migration_bytes),
+                 "switches": [{"from": a, "to": b, "kv_rows": r, "moved": mv, "model_h2d": h, "model_d2h": dd}
+                              for a, b, r, mv, (h, dd) in res.switches],
                  "prefill_pass_ms": round(res.passes[0][2] * 1e3, 2) if res.passes else None},
         "model_load_s": round(eng.load_seconds, 2),
         "host_weights": "shared /dev/shm segment per node" if shared else "private pinned blob",

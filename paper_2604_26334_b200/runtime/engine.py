@@ -41,6 +41,9 @@ class GenerateResult:
     decode_time_s: float
     passes: list = field(default_factory=list)   # (tier, T, seconds, bytes streamed)
     migration_bytes: int = 0
+    # tier switches: (from tier, to tier, live KV rows, bytes the executor moved,
+    # (h2d, d2h) bytes the migration model predicts)
+    switches: list = field(default_factory=list)
 
 
 class Engine:
@@ -49,7 +52,8 @@ class Engine:
     def __init__(self, model, budget_bytes: float, context_len: int, batch: int = 1,
                  machine="b200", profile: str | None = None, seed: int = 0,
                  max_tokens: int | None = None, chunk_bytes: int = 64 << 20,
-                 checkpoint: str | None = None, shared_weights: str | None = None):
+                 checkpoint: str | None = None, shared_weights: str | None = None,
+                 migration_aware: bool = False):
         """`model`: preset name or ModelSpec (random-init weights), or None with
         `checkpoint` = a directory holding config.json + safetensors (real weights,
         runtime/checkpoint.py). `shared_weights`: a /dev/shm segment name shared by
@@ -95,6 +99,10 @@ class Engine:
         self.max_tokens = max_tokens
         self.chunk_bytes = chunk_bytes
         self.executor: Executor | None = None
+        from .migration import MigrationModel
+        self.migration = MigrationModel(self.spec, self.weights.layout, self.plans, self.context_len,
+                                        self.batch)
+        self.migration_aware = migration_aware
 
     # -- tier selection over reachable tiers (pick_tier, planner.py:451-460) --
     def pick_tier(self, n_new: int) -> int:
@@ -165,9 +173,19 @@ class Engine:
         passes = []
         migration = 0
         last_sampled = None
+        switches = []
         while any(p > 0 for p in prompt_left) or any(g > 0 for g in gen_left):
-            tier = self.pick_tier(outstanding_tokens(prompt_left, gen_left))
-            migration += ex.set_tier(tier)
+            n_out = outstanding_tokens(prompt_left, gen_left)
+            rows = max(ex.kv_len) if ex.kv_len else 0
+            if self.migration_aware:
+                tier = self.migration.pick_tier(n_out, ex.tier, rows, self.machine)
+            else:
+                tier = self.pick_tier(n_out)
+            if tier != ex.tier:
+                prev = ex.tier
+                moved = ex.set_tier(tier)
+                migration += moved
+                switches.append((prev, tier, rows, moved, self.migration.bytes(prev, tier, rows)))
             step = schedule_iteration(tier, prompt_left, gen_left)
             slots, n_new, p0, ids, sample = [], [], [], [], []
             decode_ids_from_device = True
@@ -235,7 +253,7 @@ class Engine:
         tps = decode_tokens / decode_time if decode_time > 0 else float("inf")
         return GenerateResult([np.array(o, np.int32) for o in out], ttft, tps,
                               ttft + 100.0 / tps if tps else float("inf"),
-                              decode_tokens, decode_time, pass_rows, migration)
+                              decode_tokens, decode_time, pass_rows, migration, switches)
 
     @staticmethod
     def _pending_count(pending_host, slot) -> int:

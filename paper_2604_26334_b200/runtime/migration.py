@@ -1,0 +1,99 @@
+"""Residency-migration cost model and migration-aware tier choice.
+
+SURVEY.md §8f row 3. The reference charges a tier switch nothing: its
+SetupForSched is free (`SPEC.md:430`, `pkg/src/shardplan/simulator.py:239-314`
+never prices a residency change). On a real GPU a switch moves bytes — KV
+caches that leave VRAM go home over D2H, newly pinned weights and KV caches
+come in over H2D — and the executor measures exactly those bytes
+(`Executor.set_tier`). This module predicts them from the plans alone, with
+the executor's own policy:
+
+1. every VRAM-pinned KV cache of the old tier is written home
+   (`rows * batch * row_bytes` each, rows = longest live context);
+2. the new tier's pinned set is carved bottom-up in pin order
+   (priority, layer, id), 256-byte aligned; a weight shard whose offset is
+   unchanged stays, every other pinned weight is uploaded whole;
+3. every VRAM-pinned KV cache of the new tier is uploaded (same rows).
+
+`seconds()` prices the bytes on the machine's link rates (the executor runs
+the copies back to back on one stream). `pick_tier()` is the reference's
+`pick_tier` rule (`pkg/src/shardplan/planner.py:451-460`: argmin over ascending
+tiers of ceil(n / t) * time[t], strict <) plus the migration seconds of
+switching from the current tier — an extension the engine applies only when
+asked (`Engine(..., migration_aware=True)`), so the default loop stays the
+reference's.
+"""
+
+from __future__ import annotations
+
+from ..planning.graph import ShardKind, build_shards
+from ..planning.hardware import MachineSpec
+from ..planning.placement import TIERS, Residency, SchedulePlan
+
+ALIGN = 256
+
+
+def _up(n: int) -> int:
+    return (n + ALIGN - 1) // ALIGN * ALIGN
+
+
+class MigrationModel:
+    def __init__(self, spec, layout, plans: dict, context_len: int, batch: int):
+        self.spec, self.plans = spec, plans
+        self.shards = build_shards(spec, context_len, batch)
+        self.batch = batch
+        self.row_bytes = 2 * spec.n_kv_heads * spec.head_dim * 2
+        self.kv_layer_bytes = context_len * batch * self.row_bytes
+        self.blob_bytes = {sid: b.nbytes for sid, b in layout.blobs.items()}
+
+    def _phys(self, shard) -> int:
+        if shard.kind is ShardKind.KV_CACHE:
+            return self.kv_layer_bytes
+        return self.blob_bytes[shard.id]
+
+    def pinned_offsets(self, plan: SchedulePlan) -> dict:
+        """shard id -> arena offset of every VRAM-pinned shard (executor carve order)."""
+        pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
+                        key=lambda p: (self.shards[p.shard_id].priority,
+                                       self.shards[p.shard_id].layer_index, p.shard_id))
+        out, off = {}, 0
+        for p in pinned:
+            out[p.shard_id] = off
+            off += _up(self._phys(self.shards[p.shard_id]))
+        return out
+
+    def bytes(self, from_tier: int | None, to_tier: int, kv_rows: int) -> tuple[int, int]:
+        """(h2d, d2h) bytes of switching from `from_tier` (None: nothing resident)
+        to `to_tier` with `kv_rows` live rows of KV per request."""
+        if from_tier == to_tier:
+            return 0, 0
+        rows_bytes = kv_rows * self.batch * self.row_bytes
+        old = self.pinned_offsets(self.plans[from_tier]) if from_tier is not None else {}
+        new = self.pinned_offsets(self.plans[to_tier])
+        d2h = sum(rows_bytes for sid in old if self.shards[sid].kind is ShardKind.KV_CACHE)
+        h2d = 0
+        for sid, off in new.items():
+            s = self.shards[sid]
+            if s.kind is ShardKind.KV_CACHE:
+                h2d += rows_bytes
+            elif old.get(sid) != off:
+                h2d += self._phys(s)
+        return h2d, d2h
+
+    def seconds(self, from_tier, to_tier, kv_rows: int, machine: MachineSpec) -> float:
+        h2d, d2h = self.bytes(from_tier, to_tier, kv_rows)
+        return h2d / machine.pcie_h2d_bw + d2h / machine.pcie_d2h_bw
+
+    def pick_tier(self, n_new: int, current: int | None, kv_rows: int, machine: MachineSpec) -> int:
+        """Reference pick_tier over reachable tiers, plus the switch cost."""
+        best, best_cost = None, None
+        for tier in TIERS:
+            plan = self.plans.get(tier)
+            if plan is None:
+                continue
+            cost = -(-n_new // tier) * plan.estimated_time
+            if current is not None and tier != current:
+                cost = cost + self.seconds(current, tier, kv_rows, machine)
+            if best_cost is None or cost < best_cost:
+                best, best_cost = tier, cost
+        return best

@@ -294,3 +294,26 @@ def test_shared_host_weights_two_processes():
     assert all(d == want for _, d in got)
     import os
     assert not os.path.exists(f"/dev/shm/{name}")
+
+
+@pytest.mark.parametrize("model,frac,prompt_len", [("tiny-llama", 0.5, 128), ("tiny-llama", 0.8, 100),
+                                                   ("tiny-moe", 0.9, 60)])
+def test_migration_model_predicts_executor_switch_bytes(model, frac, prompt_len):
+    """Every tier switch of a generate run moves exactly the bytes the plan-only
+    migration model predicts (runtime/migration.py vs Executor.set_tier); the
+    migration-aware loop generates the same tokens."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model(model)
+    prompt = _prompt(prompt_len, spec.vocab_size, seed=9)
+    eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160)
+    eng.prepare([prompt_len], 8)
+    res = eng.generate([prompt], gen_len=8)
+    eng.close()
+    assert res.switches, "no tier switch exercised"
+    for prev, tier, rows, moved, (h2d, d2h) in res.switches:
+        assert moved == h2d + d2h, (prev, tier, rows, moved, h2d, d2h)
+    eng2 = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, migration_aware=True)
+    eng2.prepare([prompt_len], 8)
+    res2 = eng2.generate([prompt], gen_len=8)
+    eng2.close()
+    assert np.array_equal(res.tokens[0], res2.tokens[0])
