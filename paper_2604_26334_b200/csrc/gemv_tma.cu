@@ -6,21 +6,21 @@
 //
 // Why a second GEMV: the register-burst kernel (gemv.cu) keeps its bytes in
 // flight in registers, so occupancy caps it near 65-78 % of HBM. Here one
-// producer lane per CTA keeps an 8-stage x 16 KB ring of cp.async.bulk copies
-// in flight (128 KB per SM, no register cost) and 8 consumer warps read the
+// producer lane per CTA keeps a 5-stage x 32 KB ring of cp.async.bulk copies
+// in flight (160 KB per SM, no register cost) and 8 consumer warps read the
 // weights from shared memory.
 //
 // Decomposition (persistent, one CTA per SM): CTA b owns the contiguous row
 // range [b*R, (b+1)*R) (R even, so SwiGLU gate/up pairs never straddle CTAs)
 // and walks it K-chunk-outer: for each chunk of KC <= 2048 columns every
 // consumer thread holds its 8 columns of x (x t tokens) in registers and the
-// ring streams the range's rows in blocks of RS rows (RS*KC*2 <= 16 KB, one
+// ring streams the range's rows in blocks of RS rows (RS*KC*2 = 32 KB, one
 // bulk copy per row segment). Per stage each thread forms RS x t partial dot
-// products, the 32 values are reduce-scattered across the warp with 31
-// shuffles, summed over the 8 warps through shared memory and accumulated
-// into a per-row fp32 accumulator in shared memory; the epilogue (store /
-// accumulate / SwiGLU) runs once per row after the last chunk. The summation
-// order is fixed: results are deterministic.
+// products, reduce-scattered across its warp with shuffles, and the warp adds
+// them into its own per-row fp32 accumulators in shared memory — warps never
+// synchronise with each other inside the K loop. The epilogue sums the 8
+// warps' partials (fixed order: deterministic) and stores / accumulates /
+// applies SwiGLU once per row.
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -29,15 +29,15 @@
 
 namespace ps {
 
-constexpr int GT_STAGES = 8;
-constexpr int GT_STAGE_BYTES = 16384;
+constexpr int GT_STAGES = 5;
+constexpr int GT_STAGE_BYTES = 32768;
 constexpr int GT_CONSUMERS = 8;                      // consumer warps
 constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp
 
 // Per token count: columns per consumer thread (x kept in registers: CPT * T floats)
-// and rows per stage (RS * KC * 2 = 16 KB, KC = 256 * CPT columns per chunk).
+// and rows per stage (RS * KC * 2 = 32 KB, KC = 256 * CPT columns per chunk).
 template <int T> struct GtShape {
-  static constexpr int CPT = T == 4 ? 16 : 8;
+  static constexpr int CPT = T <= 4 ? 16 : 8;
   static constexpr int KC = GT_CONSUMERS * 32 * CPT;
   static constexpr int RS = GT_STAGE_BYTES / (KC * 2);
   static constexpr int V = RS * T;  // partial sums reduced per stage
@@ -83,8 +83,9 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * GT_STAGE_BYTES);
   uint64_t* empty = full + stages;
-  float* red = reinterpret_cast<float*>(empty + stages);  // [2][GT_CONSUMERS][32]
-  float* acc = red + 2 * GT_CONSUMERS * 32;                   // [rows_per_cta][T]
+  // per-warp row accumulators [GT_CONSUMERS][rows_per_cta][T]: warps never wait for
+  // each other inside the K loop; the 8 partials are summed once, in the epilogue
+  float* acc = reinterpret_cast<float*>(empty + stages);
 
   const int r0 = blockIdx.x * rows_per_cta;
   if (r0 >= N) return;  // whole CTA, before any barrier
@@ -98,7 +99,7 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], GT_CONSUMERS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < nrows * T; i += GT_THREADS) acc[i] = 0.f;
+  for (int i = threadIdx.x; i < GT_CONSUMERS * rows_per_cta * T; i += GT_THREADS) acc[i] = 0.f;
   __syncthreads();
 
   if (warp == 0) {
@@ -133,7 +134,8 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
     for (int o = 16; o >= 1; o >>= 1)
       if (n > 1) { if (lane & o) my_idx += n / 2; n >>= 1; }
   }
-  const bool writer = (lane & ((32 / V) - 1)) == 0;
+  constexpr int PER_LANE = V > 32 ? V / 32 : 1;   // values a lane holds after the reduce-scatter
+  const bool writer = V >= 32 || (lane & ((32 / V) - 1)) == 0;
   int it = 0, s = 0;
   uint32_t ph = 0;
   for (int c = 0; c < nchunks; ++c) {
@@ -184,32 +186,35 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
       // reduce-scatter V values over the warp, then butterfly the rest: lane l ends
       // with the warp sum of value my_idx
       warp_reduce_scatter<V, 16, V>(v, lane);
-      const int buf = it & 1;
-      if (writer) red[(buf * GT_CONSUMERS + cw) * 32 + my_idx] = v[0];
-      named_sync(1, GT_CONSUMERS * 32);
-      if (j < V) {
-        const int r = j / T, t = j - (j / T) * T;
-        if (r < nr) {
-          float sum = 0.f;
+      if (writer) {
 #pragma unroll
-          for (int w = 0; w < GT_CONSUMERS; ++w) sum += red[(buf * GT_CONSUMERS + w) * 32 + j];
-          acc[(rb - r0 + r) * T + t] += sum;
+        for (int i = 0; i < PER_LANE; ++i) {
+          const int idx = my_idx + i;
+          const int r = idx / T, t = idx - (idx / T) * T;
+          if (r < nr) acc[(cw * rows_per_cta + rb - r0 + r) * T + t] += v[i];
         }
       }
     }
   }
   named_sync(1, GT_CONSUMERS * 32);
+  const int stride_w = rows_per_cta * T;
   for (int idx = j; idx < nrows * T; idx += GT_CONSUMERS * 32) {
     const int r = idx / T, t = idx - (idx / T) * T;
     if (t >= tt) continue;
     const int row = r0 + r;
+    float a = 0.f, b = 0.f;
+#pragma unroll
+    for (int w = 0; w < GT_CONSUMERS; ++w) a += acc[w * stride_w + idx];   // fixed order: deterministic
     if (EPI == PS_EPI_SWIGLU) {
-      if ((r & 1) == 0 && row + 1 < N)
-        y[(long long)t * ldy + (row >> 1)] = silu(acc[idx]) * acc[idx + T];
+      if ((r & 1) == 0 && row + 1 < N) {
+#pragma unroll
+        for (int w = 0; w < GT_CONSUMERS; ++w) b += acc[w * stride_w + idx + T];
+        y[(long long)t * ldy + (row >> 1)] = silu(a) * b;
+      }
     } else if (EPI == PS_EPI_ACCUM) {
-      y[(long long)t * ldy + row] += acc[idx];
+      y[(long long)t * ldy + row] += a;
     } else {
-      y[(long long)t * ldy + row] = acc[idx];
+      y[(long long)t * ldy + row] = a;
     }
   }
 }
@@ -236,11 +241,11 @@ static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, i
   }
   const int stages = g_tma_stages;
   // the per-row accumulators share shared memory with the ring
-  const int max_rows = ((232448 - stages * (GT_STAGE_BYTES + 16) - 2 * GT_CONSUMERS * 32 * 4) / (T * 4)) & ~1;
+  const int max_rows = ((232448 - stages * (GT_STAGE_BYTES + 16)) / (GT_CONSUMERS * T * 4)) & ~1;
   int rows_per_cta = 2 * ((pairs + grid - 1) / grid);
   if (rows_per_cta > max_rows) rows_per_cta = max_rows;
   grid = (N + rows_per_cta - 1) / rows_per_cta;
-  const size_t smem = (size_t)stages * (GT_STAGE_BYTES + 16) + 2 * GT_CONSUMERS * 32 * 4 + (size_t)rows_per_cta * T * 4;
+  const size_t smem = (size_t)stages * (GT_STAGE_BYTES + 16) + (size_t)GT_CONSUMERS * rows_per_cta * T * 4;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(os.path.dirname(_HERE), "_lib", "libpshard.so")
+LIB_PATH = os.environ.get("PSHARD_LIB") or os.path.join(os.path.dirname(_HERE), "_lib", "libpshard.so")
 
 PS_EPI_STORE, PS_EPI_ACCUM, PS_EPI_SWIGLU, PS_EPI_STORE_BF16 = 0, 1, 2, 3
 
