@@ -37,25 +37,40 @@ namespace ps {
 // publish block (host-mapped): [0] seq, [1] count, [2..] expert ids ascending
 constexpr int PUB_HEADER = 2;
 
-__global__ void moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ slot_of_expert,
-                                   volatile unsigned* __restrict__ pub, unsigned seq) {
-  extern __shared__ int mark[];  // E
+__global__ void __launch_bounds__(1024)
+moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ slot_of_expert,
+                   volatile unsigned* __restrict__ pub, unsigned seq) {
+  extern __shared__ int mark[];            // E flags, then 32 warp totals
+  int* warp_tot = mark + E;
+  __shared__ int base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int e = threadIdx.x; e < E; e += blockDim.x) mark[e] = 0;
+  if (threadIdx.x == 0) base = 0;
   __syncthreads();
   for (int p = threadIdx.x; p < P; p += blockDim.x) mark[ids[p]] = 1;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int e = 0; e < E; ++e) {
-      if (mark[e]) {
-        slot_of_expert[e] = n;
-        pub[PUB_HEADER + n] = (unsigned)e;
-        ++n;
-      } else {
-        slot_of_expert[e] = -1;
-      }
+  // ranks in ascending expert id: ballot prefix within a warp, scan of warp totals
+  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    const bool hit = e < E && mark[e];
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) warp_tot[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = base;
+      for (int w = 0; w < nwarps; ++w) { const int t = warp_tot[w]; warp_tot[w] = acc; acc += t; }
+      base = acc;
     }
-    pub[1] = (unsigned)n;
+    __syncthreads();
+    if (e < E) {
+      const int rank = warp_tot[warp] + __popc(m & ((1u << lane) - 1));
+      slot_of_expert[e] = hit ? rank : -1;
+      if (hit) pub[PUB_HEADER + rank] = (unsigned)e;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pub[1] = (unsigned)base;
     __threadfence_system();   // ids and count are visible to the host before seq
     pub[0] = seq;
     __threadfence_system();
@@ -165,11 +180,18 @@ class ExpertFetcher {
       std::atomic_thread_fence(std::memory_order_acquire);
       unsigned n = pub_host_[1];
       if (n > (unsigned)max_experts_) n = 0, error_.store(2);
-      for (unsigned r = 0; r < n; ++r) {
+      // one copy per run of consecutive expert ids when host and slot strides agree
+      // (slots are in ascending-id order, so the run is contiguous on both sides)
+      const bool coalesce = j.expert_stride == j.slot_stride;
+      for (unsigned r = 0; r < n;) {
         const unsigned e = pub_host_[PUB_HEADER + r];
-        if (cudaMemcpyAsync(j.slot_base + r * j.slot_stride, j.host_base + (long long)e * j.expert_stride,
-                            j.expert_bytes, cudaMemcpyHostToDevice, stream_) != cudaSuccess)
+        unsigned run = 1;
+        while (coalesce && r + run < n && pub_host_[PUB_HEADER + r + run] == e + run) ++run;
+        const long long bytes = (long long)(run - 1) * j.expert_stride + j.expert_bytes;
+        if (cudaMemcpyAsync(j.slot_base + r * j.slot_stride, j.host_base + (long long)e * j.expert_stride, bytes,
+                            cudaMemcpyHostToDevice, stream_) != cudaSuccess)
           error_.store(3);
+        r += run;
       }
       copied_ += n;
       bytes_ += (long long)n * j.expert_bytes;
@@ -261,8 +283,9 @@ int ps_fetcher_submit(void* f, unsigned seq, const void* host_base, long long ex
 int ps_moe_publish(void* f, const int* ids, int P, int E, int* slot_of_expert, unsigned seq, void* stream) {
   auto* x = static_cast<ExpertFetcher*>(f);
   PS_REQUIRE(x != nullptr && P >= 1 && E >= 1, "ps_moe_publish: P=%d E=%d", P, E);
-  moe_publish_kernel<<<1, 256, E * sizeof(int), (cudaStream_t)stream>>>(ids, P, E, slot_of_expert, x->pub_dev(),
-                                                                         seq);
+  const int threads = E >= 1024 ? 1024 : (E + 31) / 32 * 32;
+  moe_publish_kernel<<<1, threads, (E + 32) * sizeof(int), (cudaStream_t)stream>>>(ids, P, E, slot_of_expert,
+                                                                                   x->pub_dev(), seq);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

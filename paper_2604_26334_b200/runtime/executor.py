@@ -105,6 +105,9 @@ class Executor:
         self.fetch_enabled = os.environ.get("PS_MOE_FETCH", "1") != "0"
         self.expert_slots, self.expert_slot_bytes = 0, 0
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
+        self._prefix_queue, self._prefix_dev = [], {}
+        from collections import deque
+        self._throttle_q = deque()
         L.lib()
 
         s = spec
@@ -367,6 +370,23 @@ class Executor:
         print(f"[fetch-debug] layer {layer} seq {seq} ids {ids.tolist()} bad {bad} map_ok {ok_map} "
               f"slot_mismatch {mism} stats {self.fetcher_stats()}", flush=True)
 
+    def _throttle_host(self, window: int = 4) -> None:
+        """Keep the host at most `window` fetched MoE layers ahead of the GPU. A host
+        that runs further fills the driver's command queue and then blocks *inside* a
+        launch call, holding the context lock the fetcher thread needs for its
+        cudaMemcpyAsync — which delays the copies the GPU is spinning on. Polling an
+        event (cudaEventQuery, no lock held while sleeping) keeps the queue shallow."""
+        import time
+        q = self._throttle_q
+        ev = self.events.next()
+        L.call("ps_event_record", ev, self.cs)
+        q.append(ev)
+        while len(q) > window:
+            head = q[0]
+            while not L.event_query(head):
+                time.sleep(20e-6)
+            q.popleft()
+
     def fetcher_stats(self) -> dict:
         if self.fetcher is None:
             return {}
@@ -574,24 +594,36 @@ class Executor:
             slots, sb = self.expert_slots, self.expert_slot_bytes
             self.fetch_seq = (self.fetch_seq + 1) & 0xFFFFFFFF or 1
             seq = self.fetch_seq
+            pre = self._prefix_dev.pop(sid, None)     # ffn_norm + router staged by gap filling
+            if pre is not None:
+                region, base, arrived = pre
+                self._wait(arrived)
+            else:
+                base = host
+                self._stat.zero_copy_bytes += e0.offset
+            self._traced(f"L{layer}.router+topk", route, base)
+            if pre is not None:
+                self.ring.seal(region, [self._record(self.cs)])
 
-            def fetched(_p, _a, _b):
+            def fetch(_p, _a, _b):
                 L.call("ps_fetcher_submit", self.fetcher, seq, host + e0.offset, stride, ebytes, slots, sb)
                 L.call("ps_moe_publish", self.fetcher, self.m_ids, P, E, self.m_slotmap, seq, self.cs)
                 L.call("ps_wait_flag", self.fetcher, seq, self.cs)
                 if os.environ.get("PS_FETCH_DEBUG"):
                     self._fetch_debug(layer, seq, P, E, host + e0.offset, stride, ebytes, slots, sb)
+
+            def run(_p, _a, _b):
                 L.call("ps_moe_expert_gu_mapped", xn, d, 0, self.m_plan, E, P, k, slots, sb, 0, eff, d,
                        self.m_h, 0, E, self.m_slotmap, self.cs)
                 L.call("ps_moe_expert_down_mapped", self.m_h, self.m_plan, E, P, slots, sb, down_off, eff, d,
                        self.m_out, 0, E, self.m_slotmap, self.cs)
 
-            self._traced(f"L{layer}.router+topk", route, host)
-            self._traced(f"L{layer}.experts (fetched)", fetched, 0, 0, 0)
-            self._stat.zero_copy_bytes += e0.offset
+            self._throttle_host()
+            self._traced(f"L{layer}.experts fetch", fetch, 0, 0, 0)
+            self._gapfill_step()      # the copy stream may move the next prefix / head piece now
+            self._traced(f"L{layer}.experts", run, 0, 0, 0)
             self._stat.bytes_streamed += min(E, P) * ebytes
             self._stat.copies += min(E, P)
-            self._gapfill_step()
             L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
             return
 
@@ -626,44 +658,83 @@ class Executor:
 
     # ------------------------------------------------- gap filling (MoE decode)
     def _plan_gapfill(self, gemv: bool, R: int) -> None:
-        """Zero-copy MoE decode leaves the host link idle between layers (attention,
-        router and top-k of the next layer run while nothing crosses the link); the
-        output head is the one ring-streamed shard of such a pass and is only read
-        at its end. Cut the head into one piece per zero-copy MoE layer and upload
-        piece k right after layer k's experts finish (the copy stream waits on that
-        event), so head bytes fill the gaps instead of sharing the link with expert
-        reads. Enabled only when nothing else in the pass uses the ring."""
+        """Zero-copy / fetched MoE decode leaves the host link idle between layers
+        (expert kernels, the next layer's attention, router and top-k run while no
+        expert byte can move yet). Two kinds of bytes are known in advance and fill
+        those gaps, uploaded on the ring's copy stream gated on the cs event that
+        marks "this layer's experts are in VRAM" (fetched) or "this layer's experts
+        ran" (zero-copy):
+        * the next fetched MoE layer's prefix (ffn_norm + router, ~0.5 MB), so its
+          route runs from VRAM instead of reading the router over PCIe;
+        * one piece of the output head — the pass's one ring-streamed dense shard,
+          read only at its end — per MoE layer.
+        Enabled only when nothing else in the pass uses the ring."""
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
+        self._prefix_queue, self._prefix_dev = [], {}
         if not (gemv and R and self.moe is not None and self.ring is not None) or \
                 os.environ.get("PS_GAPFILL", "1") == "0":
             return
         head_sid = self.by_layer_kind[(self.spec.n_layers, ShardKind.OUTPUT_HEAD)].id
         if self.residency[head_sid][0] != "stream":
             return
-        zc = 0
+        moe_streamed = []
         for sid, (mode, _) in self.residency.items():
             kind = self.shard_kind[sid]
             if kind is ShardKind.MOE_EXPERT_GROUP:
-                zc += mode in ("zerocopy", "stream")
+                if mode in ("zerocopy", "stream"):
+                    moe_streamed.append(sid)
             elif sid != head_sid and mode == "stream":
                 return
+        zc = len(moe_streamed)
         if zc == 0 or any(m == "stream" for m in self.kv_mode.values()):
             return
         blob = self.w.layout.blobs[head_sid]
         names = [n for n in blob.tensors if n in ("final_norm", "lm_head")]
         chunk = max(4 << 20, -(-blob.nbytes // zc))
         pieces = self._pieces(head_sid, names, set(), chunk=min(chunk, self.chunk))
-        if sum((b1 - b0 + 255) // 256 * 256 for b0, b1, _ in pieces) > self.ring.capacity * 9 // 10:
+        if sum((b1 - b0 + 255) // 256 * 256 for b0, b1, _ in pieces) > self.ring.capacity * 8 // 10:
             return
         self._piece_override[head_sid] = pieces
         self._gapfill = (head_sid, list(pieces))
+        # router prefixes of the fetched MoE layers, in layer order; the first goes up now
+        if self.expert_slots:
+            fetched = sorted((self.shards[sid].layer_index, sid) for sid in moe_streamed
+                             if self.residency[sid][0] == "stream")
+            self._prefix_queue = [sid for _, sid in fetched]
+            self._upload_prefix()
+        # the pass opens with pinned layers and the first routing chain before any
+        # expert byte can move: two head pieces keep the link busy meanwhile
+        for _ in range(min(2, len(pieces))):
+            self._upload_head_piece()
+
+    def _upload_prefix(self) -> None:
+        if not self._prefix_queue:
+            return
+        sid = self._prefix_queue.pop(0)
+        layer = self.shards[sid].layer_index
+        e0_off = self._expert_geometry(sid, layer)[0]
+        self._prefix_dev[sid] = self.ring.upload(self.w.shard_ptr(sid), e0_off, f"moe{sid} prefix")
+        self._stat.bytes_streamed += e0_off
+        self._stat.copies += 1
 
     def _gapfill_step(self) -> None:
-        if not self._gapfill or not self._gapfill[1]:
+        """Called right after a MoE layer's experts are available (fetched: after the
+        wait kernel) or consumed (zero-copy): the copy stream uploads the next MoE
+        prefix and the next head piece once the compute stream reaches this point."""
+        if not self._gapfill:
             return
         sid, todo = self._gapfill
+        if not todo and not self._prefix_queue:
+            return
+        L.call("ps_stream_wait_event", self.h2d, self._record(self.cs))
+        self._upload_prefix()
+        self._upload_head_piece()
+
+    def _upload_head_piece(self) -> None:
+        sid, todo = self._gapfill
+        if not todo:
+            return
         b0, b1, _ = todo.pop(0)
-        L.call("ps_stream_wait_event", self.h2d, self._record(self.cs))   # after this layer's experts
         self._prefetched[(sid, b0)] = self.ring.upload(self.w.shard_ptr(sid) + b0, b1 - b0, f"s{sid}@{b0}")
         self._stat.bytes_streamed += b1 - b0
         self._stat.copies += 1
