@@ -276,10 +276,8 @@ def run_ours(args, rank: int, world: int) -> dict:
     kv_wb = sum(s.kv_writeback_bytes for s in timed_stats) / max(1, len(timed_stats))
     achieved = streamed / (t_steps / len(timed)) / GB
     plan_dec = eng.plans[eng.pick_tier(B)]
-    metric = (f"decode tokens/s at {args.budget_gb:g} GB VRAM budget ({args.model} bf16, "
-              f"batch {B}, prompt {args.prompt} + {args.gen})")
     out = {
-        "metric": metric if args.config != 2 else METRIC, "value": round(value, 4),
+        "metric": metric_name(args), "value": round(value, 4),
         "unit": "tokens/s", "n_gpus": world,
         "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(t_max / len(timed) * 1e3, 3), "higher_is_better": True,
@@ -326,6 +324,14 @@ def run_ours(args, rank: int, world: int) -> dict:
     return out
 
 
+def metric_name(args) -> str:
+    """The arm-independent metric string of the selected config (both arms print it)."""
+    if args.config == 2 and args.model == MODEL:
+        return METRIC
+    return (f"decode tokens/s at {args.budget_gb:g} GB VRAM budget ({args.model} bf16, "
+            f"batch {args.batch}, prompt {args.prompt} + {args.gen})")
+
+
 def run_reference(args, rank: int) -> dict:
     """CPU arm: the fp32 oracle port of the same model on this host's cores."""
     import numpy as np
@@ -352,12 +358,15 @@ def run_reference(args, rank: int) -> dict:
         if i >= args.warmup:
             times.append(time.perf_counter() - s)
     v = len(times) / sum(times)
-    return {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s",
+    return {"impl": "reference", "metric": metric_name(args), "value": round(v, 4), "unit": "tokens/s",
             "n_gpus": 1, "steps": len(times), "warmup": args.warmup,
             "ms_per_step": round(sum(times) / len(times) * 1e3, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "BASELINE configs[1] sample: Llama-3.1-8B decode steps at "
-                                   "context 16 on the host CPU", "model": args.model},
+            "config": {"workload": args.workload + " — CPU sample: decode steps at context 16 "
+                                   "(fp32 oracle port on the host cores)",
+                       "model": args.model, "global_batch": 1, "seq_len": args.prompt + args.gen,
+                       "prompt": args.prompt, "gen": args.gen, "budget_gb": round(args.budget_gb, 4),
+                       "parallelism": "host cpu"},
             "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": threads,
                              "kind": "port",
                              "sample": f"{len(times)} fp32 decode steps after a 16-token prefill "
