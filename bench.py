@@ -68,6 +68,11 @@ def parse():
     ap.add_argument("--batch", type=int)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
+    ap.add_argument("--stripe", action="store_true",
+                    help="N>1: one request stream striped over every GPU's host link "
+                         "(rank 0 executes, ranks 1.. pull stripes; runtime/striping.py)")
+    ap.add_argument("--stripe-same-gpu", action="store_true",
+                    help="(functional test) put every rank on GPU 0")
     args = ap.parse_args()
     model, budget, prompt, gen, batch, desc = CONFIGS[args.config]
     args.model = args.model or model
@@ -216,10 +221,31 @@ def cpu_baseline_sample(eng, steps: int) -> dict:
 def run_ours(args, rank: int, world: int) -> dict:
     import numpy as np
     import torch
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(0 if args.stripe_same_gpu else int(os.environ.get("LOCAL_RANK", 0)))
     from paper_2604_26334_b200.runtime import lib as L
     from paper_2604_26334_b200.runtime.engine import Engine
     L.lib()
+    stripe = args.stripe and world > 1
+    leader = None
+    if stripe:
+        import secrets
+
+        import torch.distributed as dist
+        from paper_2604_26334_b200.planning import catalog
+        from paper_2604_26334_b200.runtime.model import WeightLayout, arch_for
+        from paper_2604_26334_b200.runtime.striping import StripeLeader, helper_main
+        box = [secrets.token_hex(6) if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        blob_name, ctl_name = f"pshard_{args.model}_stripe_{box[0]}", f"pshard_ctl_{box[0]}"
+        spec = catalog.builtin_model(args.model)
+        lay = WeightLayout(spec, arch_for(spec))
+        blob_bytes = (lay.total_bytes + 255) // 256 * 256 + lay.embed_bytes
+        if rank != 0:       # helper: pull stripe `rank` of every piece until the leader stops
+            dist.barrier()
+            copied = helper_main(ctl_name, rank, blob_name, blob_bytes)
+            dist.barrier()
+            return {"helper": rank, "bytes": copied}
+        leader = StripeLeader(ctl_name, world - 1)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
@@ -230,7 +256,9 @@ def run_ours(args, rank: int, world: int) -> dict:
     ctx = args.prompt + args.gen
     gen = min(args.gen, args.warmup + args.steps + 1)
     shared = None
-    if world > 1:
+    if stripe:
+        shared = blob_name
+    elif world > 1:
         # one host copy of the weights per node, mapped by every replica (/dev/shm)
         from paper_2604_26334_b200.planning import catalog
         from paper_2604_26334_b200.runtime.model import SharedHostBlob, WeightLayout, arch_for
@@ -241,12 +269,16 @@ def run_ours(args, rank: int, world: int) -> dict:
         if SharedHostBlob.fits(lay.total_bytes + lay.embed_bytes + (1 << 20)):
             shared = name
     eng = Engine(args.model, budget_bytes=args.budget_gb * GB, context_len=ctx, batch=B,
-                 shared_weights=shared)
+                 shared_weights=shared, striper=leader)
     rng = np.random.default_rng(rank)
     prompts = [rng.integers(0, eng.spec.vocab_size, args.prompt).astype(np.int32) for _ in range(B)]
+    if stripe:
+        import torch.distributed as dist
+        dist.barrier()                                 # helpers may map the blob + control block
+        eng.attach_striper([args.prompt] * B, gen)     # ... and the leader's arena
     eng.prepare([args.prompt] * B, gen)    # decode tier resident before the requests arrive
     dist = None
-    if world > 1:
+    if world > 1 and not stripe:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
@@ -268,7 +300,8 @@ def run_ours(args, rank: int, world: int) -> dict:
     zero_copy = sum(p[4] for p in timed) / max(1, len(timed))
     # replicas: sum of tokens over ranks / max over ranks of device seconds (no data collective)
     from paper_2604_26334_b200.runtime.replicas import aggregate
-    agg = aggregate(B * len(timed), t_steps, device="cuda")
+    agg = (aggregate(B * len(timed), t_steps, device="cuda") if not stripe else
+           {"seconds_max": t_steps, "value": B * len(timed) / t_steps})
     t_max, value = agg["seconds_max"], agg["value"]
     # end to end through the public API: all decode passes, host wall clock, tokens read back
     e2e_decode_wall = wall - res.ttft_s
@@ -281,16 +314,19 @@ def run_ours(args, rank: int, world: int) -> dict:
         "unit": "tokens/s", "n_gpus": world,
         "steps": len(timed), "warmup": args.warmup,
         "ms_per_step": round(t_max / len(timed) * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "strong" if stripe else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
         "ttft_ms": round(res.ttft_s * 1e3, 2),
         "config": {"workload": args.workload + " (random-init weights)",
                    "model": args.model, "global_batch": world * B, "seq_len": ctx,
                    "prompt": args.prompt, "gen": args.gen, "budget_gb": round(args.budget_gb, 4),
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"stripe{world}" if stripe else f"replicas{world}") if world > 1
+                   else "single",
                    "decode_tier": eng.pick_tier(B), "decode_plan": plan_dec.kind.value,
                    "l2": f"inputs larger than L2 ({streamed / GB:.2f} GB streamed per step)"},
-        "roofline": {"bound": "h2d", "achieved": round(achieved, 2), "peak": round(h2d_peak, 2),
-                     "unit": "GB/s", "frac": round(achieved / h2d_peak, 4),
+        "roofline": {"bound": "h2d", "achieved": round(achieved, 2),
+                     "peak": round(h2d_peak * (world if stripe else 1), 2),
+                     "unit": "GB/s", "frac": round(achieved / (h2d_peak * (world if stripe else 1)), 4),
                      "traffic": None, "algorithmic_bytes_per_step": int(streamed),
                      "peak_source": "pinned cudaMemcpyAsync 1 GiB best-of-5, measured in this run",
                      "what": "copy-engine weight stream (dominant stage of every decode step)"},
@@ -321,6 +357,13 @@ def run_ours(args, rank: int, world: int) -> dict:
         except Exception as exc:  # reported, never fatal
             out["cpu_baseline"] = {"value": None, "error": repr(exc)[:300]}
     eng.close()
+    if stripe:
+        out["stripe"] = {"helpers": world - 1, "striped_pieces": leader.striped_pieces,
+                         "striped_bytes": leader.striped_bytes, "wait_timeout_seq": leader.error_seq(),
+                         "peak_note": "roofline peak = world x this GPU's measured H2D (one link per GPU)"}
+        leader.close()
+        import torch.distributed as dist
+        dist.barrier()
     return out
 
 
@@ -387,11 +430,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(0 if args.stripe_same_gpu else int(os.environ.get("LOCAL_RANK", 0)))
+        # striped mode only needs host-side control (barriers, a broadcast): gloo
+        dist.init_process_group("gloo" if args.stripe else "nccl")
     out = run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(out))
+    elif args.stripe:
+        print(json.dumps(out), file=sys.stderr)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -174,6 +174,29 @@ int ps_moe_publish(void* fetcher, const int* ids, int P, int E, int* slot_of_exp
 int ps_wait_flag(void* fetcher, unsigned seq, void* stream);
 int ps_fetcher_device_error(void* fetcher, unsigned* seq_out);
 
+/* ---- NVLink-striped streaming (runtime/striping.py) ----------------------------
+ * Every GPU of a node pulls one stripe of each leader ring piece over its own PCIe
+ * link into the leader's ring (CUDA IPC, peer writes over NVLink). The control block
+ * (ps_stripe_ctl_bytes bytes) lives in shared host memory mapped by every process and
+ * registered (ps_host_register). Leader: ps_stripe_leader_init exports the VRAM
+ * allocation holding `ring` and creates the helpers' done[] flags; per piece,
+ * ps_stripe_post (host, before) + ps_stripe_signal (its copy stream, after the
+ * region's release waits) + its own stripe; consumers wait with ps_stripe_wait
+ * (2 s timeout -> ps_stripe_error). Helper j >= 1: ps_stripe_helper_run serves
+ * until ps_stripe_stop. Replaces the single-link channel priced at
+ * `pkg/src/shardplan/machine.py:99-101` by N links. */
+int ps_stripe_ctl_bytes(long long* n);
+int ps_stripe_leader_init(void* ctl_host, int n_helpers, void* ring, void** done_dev);
+int ps_stripe_leader_free(void* done_dev);
+int ps_stripe_post(void* ctl_host, unsigned seq, long long src_off, long long dst_off, long long bytes,
+                   long long stripe);
+int ps_stripe_signal(void* ctl_dev, unsigned seq, void* stream);
+int ps_stripe_wait(void* done_dev, int n_helpers, unsigned seq, void* stream);
+int ps_stripe_error(void* done_dev, unsigned* seq_out);
+int ps_stripe_helper_run(void* ctl_host, int j, void* blob_host, long long* bytes_out);
+int ps_stripe_ready(void* ctl_host, int* n_ready);   /* helpers attached so far */
+int ps_stripe_stop(void* ctl_host);
+
 /* ---- K6: embedding gather (zero-copy from host-mapped table), greedy -------
  * Not priced by the reference (embeddings are outside the plan,
  * `pkg/src/shardplan/model_graph.py:279-297`); the head's MATMUL is

@@ -53,7 +53,7 @@ class Engine:
                  machine="b200", profile: str | None = None, seed: int = 0,
                  max_tokens: int | None = None, chunk_bytes: int = 64 << 20,
                  checkpoint: str | None = None, shared_weights: str | None = None,
-                 migration_aware: bool = False):
+                 migration_aware: bool = False, striper=None):
         """`model`: preset name or ModelSpec (random-init weights), or None with
         `checkpoint` = a directory holding config.json + safetensors (real weights,
         runtime/checkpoint.py). `shared_weights`: a /dev/shm segment name shared by
@@ -103,6 +103,7 @@ class Engine:
         self.migration = MigrationModel(self.spec, self.weights.layout, self.plans, self.context_len,
                                         self.batch)
         self.migration_aware = migration_aware
+        self.striper = striper        # runtime.striping.StripeLeader: helper GPUs pull stripes
 
     # -- tier selection over reachable tiers (pick_tier, planner.py:451-460) --
     def pick_tier(self, n_new: int) -> int:
@@ -124,9 +125,23 @@ class Engine:
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,
                                      self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes)
+            if self.striper is not None:
+                if self.weights.shared is None:
+                    raise SpecError("striped streaming needs node-shared weights (shared_weights=...)")
+                self.striper.attach(self.executor.arena.base, self.weights.base,
+                                    self.weights.shared.nbytes)
+                self.executor.striper = self.striper
+                if self.executor.ring is not None:
+                    self.executor.ring.striper = self.striper
         elif max_tokens > self.executor.Tmax:
             raise SpecError(f"pass of {max_tokens} tokens exceeds the executor's {self.executor.Tmax}")
         return self.executor
+
+    def attach_striper(self, prompt_lens: list, gen_len: int) -> None:
+        """Create the executor now and export its arena to the stripe helpers (they
+        must map it before the first striped piece); then wait for them."""
+        self._ensure_executor(self.max_pass_tokens(prompt_lens, gen_len))
+        self.striper.wait_helpers()
 
     def max_pass_tokens(self, prompt_lens: list, gen_len: int) -> int:
         """Largest T any pass of generate() will run (dry run of the loop)."""

@@ -102,6 +102,7 @@ class Executor:
         self.shard_kind = {s.id: s.kind for s in self.shards}
         # routed-expert fetcher (copy-engine expert uploads in MoE decode); PS_MOE_FETCH=0 disables
         self.fetcher, self.fetch_seq = None, 0
+        self.striper = None                           # runtime.striping.StripeLeader (set by Engine)
         self.fetch_enabled = os.environ.get("PS_MOE_FETCH", "1") != "0"
         self.expert_slots, self.expert_slot_bytes = 0, 0
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
@@ -307,6 +308,7 @@ class Executor:
         self.ring = CopyRing(self.arena.alloc_high("ring", ring_bytes), ring_bytes, self.h2d,
                              self.events)
         self.ring.tracer = self.tracer
+        self.ring.striper = self.striper
 
     # ------------------------------------------------- routed-expert fetcher
     def _expert_geometry(self, sid: int, layer: int) -> tuple:
@@ -398,7 +400,12 @@ class Executor:
                 "device_timeout_seq": dev_err.value}
 
     # --------------------------------------------------------------- helpers
-    def _wait(self, ev: int) -> None:
+    def _wait(self, ev) -> None:
+        if isinstance(ev, tuple):            # striped piece: own stripe + helpers' stripes
+            ev, seq = ev
+            L.call("ps_stream_wait_event", self.cs, ev)
+            self.ring.striper.wait(seq, self.cs)
+            return
         L.call("ps_stream_wait_event", self.cs, ev)
 
     def _record(self, stream: int) -> int:

@@ -69,6 +69,16 @@ _SIGS = {
     "ps_moe_publish": [_p, _p, _i, _i, _p, C.c_uint, _p],
     "ps_wait_flag": [_p, C.c_uint, _p],
     "ps_fetcher_device_error": [_p, C.POINTER(C.c_uint)],
+    "ps_stripe_ctl_bytes": [C.POINTER(_ll)],
+    "ps_stripe_leader_init": [_p, _i, _p, _pp],
+    "ps_stripe_leader_free": [_p],
+    "ps_stripe_post": [_p, C.c_uint, _ll, _ll, _ll, _ll],
+    "ps_stripe_signal": [_p, C.c_uint, _p],
+    "ps_stripe_wait": [_p, _i, C.c_uint, _p],
+    "ps_stripe_error": [_p, C.POINTER(C.c_uint)],
+    "ps_stripe_helper_run": [_p, _i, _p, C.POINTER(_ll)],
+    "ps_stripe_stop": [_p],
+    "ps_stripe_ready": [_p, C.POINTER(_i)],
     "ps_moe_combine": [_p, _p, _i, _i, _p, _i, _i, _i, _p, _i, _p],
     "ps_embed_gather": [_p, _p, _i, _i, _p, _i, _p],
     "ps_argmax": [_p, _i, _i, _i, _p, _p],
@@ -115,7 +125,8 @@ KERNEL_CALLS = frozenset({
     "ps_attn_prefill", "ps_embed_gather", "ps_argmax", "ps_cast_f32_bf16", "ps_add_f32",
     "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_gemv_bf16_cfg", "ps_gemm_bf16_cfg",
     "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine",
-    "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_wait_flag"})
+    "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_wait_flag",
+    "ps_stripe_signal", "ps_stripe_wait"})
 counters = {"kernel_calls": 0, "memcpy_calls": 0}
 
 

@@ -62,6 +62,7 @@ class CopyRing:
         self.bytes_copied = 0
         self.copies = 0
         self.tracer = None
+        self.striper = None        # runtime.striping.StripeLeader on a striped node
 
     def _reserve(self, nbytes: int, tag: str) -> Region:
         n = (nbytes + 255) // 256 * 256
@@ -91,19 +92,26 @@ class CopyRing:
     def upload(self, src_host: int, nbytes: int, tag: str, reserve: int = 0
                ) -> tuple[Region, int, int]:
         """Copy `nbytes` from pinned host memory into a region of
-        max(nbytes, reserve) bytes. Returns (region, device address, arrived event)."""
+        max(nbytes, reserve) bytes. Returns (region, device address, arrived): an
+        event, or (event, stripe sequence) for a piece striped across GPUs."""
         region = self._reserve(max(nbytes, reserve), tag)
         dst = self.base + region.start
         tr = self.tracer
         ev0 = tr.begin(self.stream) if tr is not None and nbytes else None
-        L.memcpy_async(dst, src_host, nbytes, self.stream)
+        seq = None
+        if self.striper is not None and self.striper.covers(src_host, nbytes):
+            # stripe 0 here, stripes 1.. by the helper GPUs (runtime/striping.py)
+            seq = self.striper.upload(dst, src_host, nbytes, self.stream)
+        else:
+            L.memcpy_async(dst, src_host, nbytes, self.stream)
         if ev0 is not None:
             tr.end(f"{tag} ({nbytes >> 20} MiB)", "h2d", ev0, self.stream)
         ev = self.events.next()
         L.call("ps_event_record", ev, self.stream)
         self.bytes_copied += nbytes
         self.copies += 1
-        return region, dst, ev
+        # "arrived" is the copy-stream event, plus the helpers' sequence when striped
+        return region, dst, (ev if seq is None else (ev, seq))
 
     def reserve_only(self, nbytes: int, tag: str) -> tuple[Region, int]:
         """Ring space without an upload (e.g. room for appended KV rows)."""

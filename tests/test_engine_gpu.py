@@ -317,3 +317,61 @@ def test_migration_model_predicts_executor_switch_bytes(model, frac, prompt_len)
     res2 = eng2.generate([prompt], gen_len=8)
     eng2.close()
     assert np.array_equal(res.tokens[0], res2.tokens[0])
+
+
+def _stripe_helper(ctl_name, j, blob_name, blob_bytes, q):
+    import os
+    import sys
+    sys.path.insert(0, os.getcwd())
+    try:
+        from paper_2604_26334_b200.runtime.striping import helper_main
+        q.put(("ok", helper_main(ctl_name, j, blob_name, blob_bytes)))
+    except Exception as e:   # pragma: no cover - reported to the parent
+        q.put(("error", repr(e)))
+
+
+@pytest.mark.parametrize("n_helpers", [1, 2])
+def test_striped_streaming_helpers_on_one_gpu(n_helpers):
+    """Leader + helper processes (all on the one GPU of this box: the functional path;
+    on a node each helper owns a GPU and a PCIe link): every streamed weight piece of
+    a GPU_ONLY plan is split into stripes that the helpers copy into the leader's ring
+    through CUDA IPC. Tokens equal the unstriped run's; helpers moved their share."""
+    import multiprocessing as mp
+    import secrets
+    from paper_2604_26334_b200.runtime.engine import Engine
+    from paper_2604_26334_b200.runtime.model import SharedHostBlob
+    from paper_2604_26334_b200.runtime.striping import StripeLeader
+    spec = catalog.builtin_model("tiny-moe")
+    budget = 0.9 * total_model_bytes(spec)        # GPU_ONLY: attention, KV, experts, head stream
+    prompt = _prompt(40, spec.vocab_size, seed=3)
+    ref = Engine(spec, budget_bytes=budget, context_len=160, chunk_bytes=256 << 10)
+    want = ref.generate([prompt], gen_len=8)
+    ref.close()
+    if not SharedHostBlob.fits(64 << 20):
+        pytest.skip("/dev/shm too small")
+    tok = secrets.token_hex(4)
+    blob_name, ctl_name = f"pshard_stripe_blob_{tok}", f"pshard_stripe_ctl_{tok}"
+    leader = StripeLeader(ctl_name, n_helpers, min_bytes=32 << 10)
+    eng = Engine(spec, budget_bytes=budget, context_len=160, chunk_bytes=256 << 10,
+                 shared_weights=blob_name, striper=leader)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_stripe_helper, args=(ctl_name, j + 1, blob_name, eng.weights.shared.nbytes, q))
+          for j in range(n_helpers)]
+    for p in ps:
+        p.start()
+    try:
+        eng.attach_striper([len(prompt)], 8)
+        got = eng.generate([prompt], gen_len=8)
+        err = leader.error_seq()
+        striped = leader.striped_pieces
+    finally:
+        eng.close()
+        leader.close()
+    res = [q.get(timeout=60) for _ in ps]
+    for p in ps:
+        p.join(30)
+    assert all(kind == "ok" for kind, _ in res), res
+    assert err == 0, f"stripe wait timed out at seq {err}"
+    assert striped > 0 and all(b > 0 for _, b in res), (striped, res)
+    assert np.array_equal(got.tokens[0], want.tokens[0])
