@@ -125,6 +125,7 @@ class Engine:
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,
                                      self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes)
+            self.migration.pins_fn = self.executor.pins_for   # include the spare pins
             if self.striper is not None:
                 if self.weights.shared is None:
                     raise SpecError("striped streaming needs node-shared weights (shared_weights=...)")

@@ -104,6 +104,11 @@ class Executor:
         self.fetcher, self.fetch_seq = None, 0
         self.striper = None                           # runtime.striping.StripeLeader (set by Engine)
         self.fetch_enabled = os.environ.get("PS_MOE_FETCH", "1") != "0"
+        # cache streamed / CPU-placed weight shards in budget the ring does not need
+        # (PS_SPARE_PIN=0 runs the plan's residency exactly)
+        self.spare_pin = os.environ.get("PS_SPARE_PIN", "1") != "0"
+        self.ring_keep_pieces = int(os.environ.get("PS_RING_KEEP_PIECES", "6"))   # ring kept for streaming
+        self.spare_pinned = []
         self.expert_slots, self.expert_slot_bytes = 0, 0
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
         self._prefix_queue, self._prefix_dev = [], {}
@@ -148,39 +153,38 @@ class Executor:
         self._prev_sample_slots = None
 
     # ------------------------------------------------------------------ layout
-    def _carve_activations(self, T: int) -> None:
-        """Activation buffers for passes of <= T tokens (re-carved per tier, so a
-        decode tier holds only what the plan's activation scratch allows)."""
-        a, B, d = self.arena, self.B, self.d
+    def _activation_spec(self, T: int) -> list:
+        """(attribute, tag, bytes) of the activation buffers for passes of <= T tokens."""
+        B, d = self.B, self.d
         t32 = min(T, GEMV_MAX_T)
-        self.x = a.alloc_high("x", T * d * 4)
-        self.qkv = a.alloc_high("qkv", T * self.qkv_rows * 4)
-        self.xn32 = a.alloc_high("xn32", t32 * d * 4)
-        self.att32 = a.alloc_high("att32", t32 * self.h * self.hd * 4)
-        self.hid32 = a.alloc_high("hid32", t32 * self.ffn * 4)
+        spec = [("x", "x", T * d * 4), ("qkv", "qkv", T * self.qkv_rows * 4),
+                ("xn32", "xn32", t32 * d * 4), ("att32", "att32", t32 * self.h * self.hd * 4),
+                ("hid32", "hid32", t32 * self.ffn * 4)]
         if T > GEMV_MAX_T:
-            self.xn16 = a.alloc_high("xn16", T * d * 2)
-            self.att16 = a.alloc_high("att16", T * self.h * self.hd * 2)
-            self.hid16 = a.alloc_high("hid16", T * self.ffn * 2)
-        else:
-            self.xn16 = self.att16 = self.hid16 = 0
-        self.xs = a.alloc_high("xs", B * d * 4)
-        self.logits = a.alloc_high("logits", B * self.V * 4)
+            spec += [("xn16", "xn16", T * d * 2), ("att16", "att16", T * self.h * self.hd * 2),
+                     ("hid16", "hid16", T * self.ffn * 2)]
+        spec += [("xs", "xs", B * d * 4), ("logits", "logits", B * self.V * 4)]
         # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
-        self.ws_floats = L.attn_decode_workspace(B, self.h, self.hd, self.cap)
-        self.ws = a.alloc_high("attn_ws", max(1, self.ws_floats) * 4)
+        ws = L.attn_decode_workspace(B, self.h, self.hd, self.cap)
+        spec.append(("ws", "attn_ws", max(1, ws) * 4))
         if self.moe is not None:
             E, k, eff = self.moe.n_experts, self.moe.top_k, self.moe.expert_ffn_dim
             P = T * k
             n_ints = C.c_longlong()
             L.call("ps_moe_plan_ints", P, E, C.byref(n_ints))
-            self.m_logits = a.alloc_high("moe_logits", T * E * 4)
-            self.m_ids = a.alloc_high("moe_ids", P * 4)
-            self.m_w = a.alloc_high("moe_w", P * 4)
-            self.m_plan = a.alloc_high("moe_plan", n_ints.value * 4)
-            self.m_h = a.alloc_high("moe_h", P * eff * 4)
-            self.m_out = a.alloc_high("moe_out", P * d * 4)
-            self.m_slotmap = a.alloc_high("moe_slot_of_expert", E * 4)
+            spec += [("m_logits", "moe_logits", T * E * 4), ("m_ids", "moe_ids", P * 4),
+                     ("m_w", "moe_w", P * 4), ("m_plan", "moe_plan", n_ints.value * 4),
+                     ("m_h", "moe_h", P * eff * 4), ("m_out", "moe_out", P * d * 4),
+                     ("m_slotmap", "moe_slot_of_expert", E * 4)]
+        return spec
+
+    def _carve_activations(self, T: int) -> None:
+        """Activation buffers for passes of <= T tokens (re-carved per tier, so a
+        decode tier holds only what the plan's activation scratch allows)."""
+        self.xn16 = self.att16 = self.hid16 = 0
+        for attr, tag, n in self._activation_spec(T):
+            setattr(self, attr, self.arena.alloc_high(tag, n))
+        self.ws_floats = L.attn_decode_workspace(self.B, self.h, self.hd, self.cap)
 
     def _carve_persistent(self) -> None:
         """Small buffers whose content outlives a pass (tokens, rope table)."""
@@ -220,6 +224,79 @@ class Executor:
         return self.kv_host + layer * self.kv_layer_bytes
 
     # --------------------------------------------------------------- residency
+    def _plan_modes(self, plan) -> tuple:
+        """(pinned placements in pin order, {shard id: 'stream' | 'zerocopy'} of the rest)."""
+        pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
+                        key=lambda p: (self.shards[p.shard_id].priority,
+                                       self.shards[p.shard_id].layer_index, p.shard_id))
+        modes = {}
+        for p in plan.placements:
+            if p.residency is Residency.VRAM_PINNED:
+                continue
+            if p.exec_backend is Backend.CPU:
+                modes[p.shard_id] = "zerocopy"
+            elif p.streaming in (Streaming.WEIGHTS_H2D, Streaming.KV_H2D, Streaming.WEIGHTS_AND_KV):
+                modes[p.shard_id] = "stream"
+            else:
+                raise SpecError(f"unsupported placement {p}")
+        return pinned, modes
+
+    def _slot_bytes(self, T: int, modes: dict, free: int) -> tuple:
+        """(slot count, slot bytes) of the routed-expert fetcher at this tier (0, 0: none)."""
+        if self.moe is None or T > GEMV_MAX_T or not self.fetch_enabled:
+            return 0, 0
+        groups = [sid for sid, m in modes.items()
+                  if m == "stream" and self.shard_kind[sid] is ShardKind.MOE_EXPERT_GROUP]
+        if not groups:
+            return 0, 0
+        _, _, _, ebytes = self._expert_geometry(groups[0], self.shards[groups[0]].layer_index)
+        slot = (ebytes + 255) // 256 * 256
+        n = min(self.moe.n_experts, T * self.moe.top_k)
+        if n * slot > free // 4:
+            return 0, 0
+        return n, slot
+
+    def pins_for(self, tier: int) -> list:
+        """Shard ids carved into VRAM at `tier`, in carve order: the plan's pinned
+        set in pin order, then the *spare pins* — streamed or CPU-placed weight
+        shards cached in budget the plan reserved as double-buffer scratch
+        (2 x the largest streamed shard, `pkg/src/shardplan/planner.py:132-159`)
+        but the piece-wise ring does not need. Pure: a function of the plan, the
+        layout and the budget, so the migration model can predict switches."""
+        plan = self.plans[tier]
+        T = min(tier, self.Tmax)
+        pinned, modes = self._plan_modes(plan)
+        out = [p.shard_id for p in pinned]
+        if not self.spare_pin:
+            return out
+        up = lambda n: (n + 255) // 256 * 256  # noqa: E731
+        high = (self.arena.capacity - self.persist_high) + sum(up(n) for _, _, n in self._activation_spec(T))
+        low = sum(up(self._phys_bytes(self.shards[sid])) for sid in out)
+        free = self.arena.capacity - high - low
+        n_slots, slot = self._slot_bytes(T, modes, free)
+        kv_streams = any(m == "stream" and self.shards[sid].kind is ShardKind.KV_CACHE
+                         for sid, m in modes.items())
+        ring_keep = min(self.ring_cap, self.ring_keep_pieces * self.chunk_cap +
+                        (self.kv_layer_bytes if kv_streams else 0))
+        spare = free - n_slots * slot - ring_keep - min(32 << 20, self.arena.capacity // 64)
+        if spare <= 0:
+            return out
+        k_frac = 1.0
+        if self.moe is not None:
+            k_frac = min(1.0, T * self.moe.top_k / self.moe.n_experts)
+
+        def value(sid):   # link bytes saved per token per VRAM byte
+            return k_frac if self.shard_kind[sid] is ShardKind.MOE_EXPERT_GROUP else 1.0
+        cands = sorted((sid for sid in modes if self.shard_kind[sid] is not ShardKind.KV_CACHE),
+                       key=lambda sid: (-value(sid), self.shards[sid].priority, self.shards[sid].layer_index,
+                                        sid))
+        for sid in cands:
+            b = up(self._phys_bytes(self.shards[sid]))
+            if b <= spare:
+                out.append(sid)
+                spare -= b
+        return out
+
     def set_tier(self, tier: int) -> int:
         """Make `tier`'s plan resident (the paper's SetupForSched); returns the
         bytes moved. The reference charges this 0; the engine
@@ -242,14 +319,15 @@ class Executor:
         self.arena.high = self.persist_high        # drop the previous tier's activations + ring
         self.arena.reset_low()                     # ... and its pinned region
         self.T_tier = min(tier, self.Tmax)
+        pins = self.pins_for(tier)                 # plan pins, then spare pins
+        _, modes = self._plan_modes(plan)
         self._carve_activations(self.T_tier)
         self.fixed_high = self.arena.high
         self.residency, self.kv_vram, self.kv_mode = {}, {}, {}
-        pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
-                        key=lambda p: (self.shards[p.shard_id].priority,
-                                       self.shards[p.shard_id].layer_index, p.shard_id))
-        for p in pinned:
-            s = self.shards[p.shard_id]
+        plan_pinned = {p.shard_id for p in plan.placements if p.residency is Residency.VRAM_PINNED}
+        self.spare_pinned = [sid for sid in pins if sid not in plan_pinned]
+        for sid in pins:
+            s = self.shards[sid]
             dev = self.arena.alloc_low(f"pin{s.id}", self._phys_bytes(s))
             if s.kind is ShardKind.KV_CACHE:
                 self.kv_vram[s.layer_index] = dev
@@ -262,27 +340,20 @@ class Executor:
                     L.memcpy_async(dev, self.w.shard_ptr(s.id), nbytes, self.cs)
                     moved += nbytes
                 self.residency[s.id] = ("pinned", dev)
-        for p in plan.placements:
-            if p.residency is Residency.VRAM_PINNED:
+        for sid, mode in modes.items():
+            if sid in self.residency:
                 continue
-            s = self.shards[p.shard_id]
-            if p.exec_backend is Backend.CPU:
-                mode = "zerocopy"
-            elif p.streaming in (Streaming.WEIGHTS_H2D, Streaming.KV_H2D,
-                                 Streaming.WEIGHTS_AND_KV):
-                mode = "stream"
-            else:
-                raise SpecError(f"unsupported placement {p}")
+            s = self.shards[sid]
             if s.kind is ShardKind.KV_CACHE:
                 self.kv_mode[s.layer_index] = mode
             else:
-                self.residency[s.id] = (mode, 0)
-        self._carve_ring(tier)
+                self.residency[sid] = (mode, 0)
+        self._carve_ring(tier, modes)
         L.call("ps_stream_synchronize", self.cs)
         self.tier = tier
         return moved
 
-    def _carve_ring(self, tier: int) -> None:
+    def _carve_ring(self, tier: int, modes: dict | None = None) -> None:
         """The staging ring takes what the tier's pinned set leaves (<= ring_cap).
 
         A tier that streams nothing (every shard pinned or zero-copy) needs no
@@ -291,7 +362,7 @@ class Executor:
         self.arena.high = self.fixed_high
         self.arena.high_marks.pop("ring", None)
         self.arena.high_marks.pop("expert_slots", None)
-        self._carve_expert_slots(tier)
+        self._carve_expert_slots(tier, modes)
         free = self.arena.free_bytes
         ring_bytes = max(0, min(self.ring_cap, free)) // 256 * 256
         self.chunk = min(self.chunk_cap, max(1 << 16, ring_bytes // 6 // 256 * 256))
@@ -322,25 +393,22 @@ class Executor:
         nbytes = wd.offset + wd.rows * wd.cols * 2 - e0.offset
         return e0.offset, stride, wd.offset - e0.offset, nbytes
 
-    def _carve_expert_slots(self, tier: int) -> None:
+    def _carve_expert_slots(self, tier: int, modes: dict | None = None) -> None:
         """VRAM slots for the routed experts of one MoE layer in a decode pass
         (min(E, T*k) experts), carved before the ring so fetcher copies never
         race the ring's reuse. Used when a decode tier streams expert groups and
-        the slots take at most a quarter of the free budget; otherwise the
-        expert kernels read the routed experts zero-copy."""
+        the slots take at most a quarter of the free budget (decided before spare
+        pinning, `_slot_bytes`); otherwise the expert kernels read the routed
+        experts zero-copy."""
         self.expert_slots, self.expert_slot_bytes = 0, 0
-        if self.moe is None or self.T_tier > GEMV_MAX_T or not self.fetch_enabled:
+        if modes is None:
+            modes = {sid: m for sid, (m, _) in self.residency.items() if m != "pinned"}
+        plan_free = self.arena.free_bytes + sum((self._phys_bytes(self.shards[sid]) + 255) // 256 * 256
+                                                for sid in getattr(self, "spare_pinned", []))
+        n, slot = self._slot_bytes(self.T_tier, modes, plan_free)
+        if not n:
             return
-        groups = [sid for sid, (m, _) in self.residency.items()
-                  if m == "stream" and self.shard_kind[sid] is ShardKind.MOE_EXPERT_GROUP]
-        if not groups:
-            return
-        layer = self.shards[groups[0]].layer_index
-        _, _, _, ebytes = self._expert_geometry(groups[0], layer)
-        slot = (ebytes + 255) // 256 * 256
-        n = min(self.moe.n_experts, self.T_tier * self.moe.top_k)
-        if n * slot > self.arena.free_bytes // 4:
-            return
+        # the spare pins were sized around these slots
         self.expert_slots = self.arena.alloc_high("expert_slots", n * slot)
         self.expert_slot_bytes = slot
         if self.fetcher is None:
@@ -682,8 +750,7 @@ class Executor:
                 os.environ.get("PS_GAPFILL", "1") == "0":
             return
         head_sid = self.by_layer_kind[(self.spec.n_layers, ShardKind.OUTPUT_HEAD)].id
-        if self.residency[head_sid][0] != "stream":
-            return
+        head_streams = self.residency[head_sid][0] == "stream"   # a spare-pinned head needs no pieces
         moe_streamed = []
         for sid, (mode, _) in self.residency.items():
             kind = self.shard_kind[sid]
@@ -695,13 +762,15 @@ class Executor:
         zc = len(moe_streamed)
         if zc == 0 or any(m == "stream" for m in self.kv_mode.values()):
             return
-        blob = self.w.layout.blobs[head_sid]
-        names = [n for n in blob.tensors if n in ("final_norm", "lm_head")]
-        chunk = max(4 << 20, -(-blob.nbytes // zc))
-        pieces = self._pieces(head_sid, names, set(), chunk=min(chunk, self.chunk))
-        if sum((b1 - b0 + 255) // 256 * 256 for b0, b1, _ in pieces) > self.ring.capacity * 8 // 10:
-            return
-        self._piece_override[head_sid] = pieces
+        pieces = []
+        if head_streams:
+            blob = self.w.layout.blobs[head_sid]
+            names = [n for n in blob.tensors if n in ("final_norm", "lm_head")]
+            chunk = max(4 << 20, -(-blob.nbytes // zc))
+            pieces = self._pieces(head_sid, names, set(), chunk=min(chunk, self.chunk))
+            if sum((b1 - b0 + 255) // 256 * 256 for b0, b1, _ in pieces) > self.ring.capacity * 8 // 10:
+                return
+            self._piece_override[head_sid] = pieces
         self._gapfill = (head_sid, list(pieces))
         # router prefixes of the fetched MoE layers, in layer order; the first goes up now
         if self.expert_slots:

@@ -11,8 +11,9 @@ the executor's own policy:
 1. every VRAM-pinned KV cache of the old tier is written home
    (`rows * batch * row_bytes` each, rows = longest live context);
 2. the new tier's pinned set is carved bottom-up in pin order
-   (priority, layer, id), 256-byte aligned; a weight shard whose offset is
-   unchanged stays, every other pinned weight is uploaded whole;
+   (priority, layer, id), 256-byte aligned, followed by the executor's spare
+   pins (`Executor.pins_for`); a weight shard whose offset is unchanged stays,
+   every other pinned weight is uploaded whole;
 3. every VRAM-pinned KV cache of the new tier is uploaded (same rows).
 
 `seconds()` prices the bytes on the machine's link rates (the executor runs
@@ -38,8 +39,10 @@ def _up(n: int) -> int:
 
 
 class MigrationModel:
-    def __init__(self, spec, layout, plans: dict, context_len: int, batch: int):
+    def __init__(self, spec, layout, plans: dict, context_len: int, batch: int, pins_fn=None):
         self.spec, self.plans = spec, plans
+        # tier -> shard ids in carve order; the executor's pins_for adds its spare pins
+        self.pins_fn = pins_fn
         self.shards = build_shards(spec, context_len, batch)
         self.batch = batch
         self.row_bytes = 2 * spec.n_kv_heads * spec.head_dim * 2
@@ -51,15 +54,21 @@ class MigrationModel:
             return self.kv_layer_bytes
         return self.blob_bytes[shard.id]
 
-    def pinned_offsets(self, plan: SchedulePlan) -> dict:
-        """shard id -> arena offset of every VRAM-pinned shard (executor carve order)."""
-        pinned = sorted((p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
-                        key=lambda p: (self.shards[p.shard_id].priority,
-                                       self.shards[p.shard_id].layer_index, p.shard_id))
+    def pinned_offsets(self, tier: int) -> dict:
+        """shard id -> arena offset of every VRAM-resident shard at `tier` (executor
+        carve order: the plan's pins in pin order, then any spare pins)."""
+        if self.pins_fn is not None:
+            sids = self.pins_fn(tier)
+        else:
+            plan = self.plans[tier]
+            sids = [p.shard_id for p in sorted(
+                (p for p in plan.placements if p.residency is Residency.VRAM_PINNED),
+                key=lambda p: (self.shards[p.shard_id].priority, self.shards[p.shard_id].layer_index,
+                               p.shard_id))]
         out, off = {}, 0
-        for p in pinned:
-            out[p.shard_id] = off
-            off += _up(self._phys(self.shards[p.shard_id]))
+        for sid in sids:
+            out[sid] = off
+            off += _up(self._phys(self.shards[sid]))
         return out
 
     def bytes(self, from_tier: int | None, to_tier: int, kv_rows: int) -> tuple[int, int]:
@@ -68,8 +77,8 @@ class MigrationModel:
         if from_tier == to_tier:
             return 0, 0
         rows_bytes = kv_rows * self.batch * self.row_bytes
-        old = self.pinned_offsets(self.plans[from_tier]) if from_tier is not None else {}
-        new = self.pinned_offsets(self.plans[to_tier])
+        old = self.pinned_offsets(from_tier) if from_tier is not None else {}
+        new = self.pinned_offsets(to_tier)
         d2h = sum(rows_bytes for sid in old if self.shards[sid].kind is ShardKind.KV_CACHE)
         h2d = 0
         for sid, off in new.items():

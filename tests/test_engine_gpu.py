@@ -375,3 +375,28 @@ def test_striped_streaming_helpers_on_one_gpu(n_helpers):
     assert err == 0, f"stripe wait timed out at seq {err}"
     assert striped > 0 and all(b > 0 for _, b in res), (striped, res)
     assert np.array_equal(got.tokens[0], want.tokens[0])
+
+
+@pytest.mark.parametrize("model,frac", [("tiny-moe", 0.9), ("tiny-moe", 1.0)])
+def test_spare_pins_same_tokens_fewer_link_bytes(monkeypatch, model, frac):
+    """Budget the plan reserves as double-buffer scratch but the piece-wise ring does
+    not need caches streamed / CPU-placed shards (Executor.pins_for): same tokens as
+    the plan's exact residency, fewer bytes over the host link, and the migration
+    model still predicts every tier switch exactly."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model(model)
+    prompt = _prompt(24, spec.vocab_size, seed=21)
+    out = {}
+    for spare in ("0", "1"):
+        monkeypatch.setenv("PS_SPARE_PIN", spare)
+        eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, chunk_bytes=64 << 10)
+        res = eng.generate([prompt], gen_len=8)
+        ex = eng.executor
+        link = sum(s.bytes_streamed + s.zero_copy_bytes for s in ex.stats if s.T == 1)
+        out[spare] = (res.tokens[0].tolist(), link, list(ex.spare_pinned))
+        for prev, tier, rows, moved, (h2d, d2h) in res.switches:
+            assert moved == h2d + d2h, (spare, prev, tier, moved, h2d, d2h)
+        eng.close()
+    assert out["1"][0] == out["0"][0]
+    assert out["1"][2], "no spare pin was made"
+    assert out["1"][1] < out["0"][1], (out["1"][1], out["0"][1])

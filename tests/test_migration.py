@@ -24,7 +24,7 @@ def _model(name, frac=None, budget=None, ctx=2304, batch=1):
 def test_fresh_executor_uploads_every_pinned_shard():
     spec, m, plans, mm = _model("llama3.1-8b", budget=4e9)
     for tier, plan in plans.items():
-        h2d, d2h = mm.bytes(None, tier, 0)
+        h2d, d2h = mm.bytes(None, tier, 0)   # plan-only model (no executor spare pins)
         assert d2h == 0
         want = sum(mm._phys(mm.shards[p.shard_id]) for p in plan.placements
                    if p.residency is Residency.VRAM_PINNED and mm.shards[p.shard_id].kind is not ShardKind.KV_CACHE)
