@@ -34,12 +34,15 @@
 
 namespace ps {
 
-// publish block (host-mapped): [0] seq, [1] count, [2..] expert ids ascending
-constexpr int PUB_HEADER = 2;
+// publish block (host-mapped, 64-bit words tagged with the sequence number in the high
+// half): [0] = seq:count, [1 + r] = seq:expert id of rank r (ascending ids). Every word
+// carries its own tag, so the host can accept the block word by word and the GPU
+// needs no system-scope fence (which would queue behind the copy engines' PCIe reads).
+constexpr int PUB_HEADER = 1;
 
 __global__ void __launch_bounds__(1024)
 moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ slot_of_expert,
-                   volatile unsigned* __restrict__ pub, unsigned seq) {
+                   volatile unsigned long long* __restrict__ pub, unsigned seq) {
   extern __shared__ int mark[];            // E flags, then 32 warp totals
   int* warp_tot = mark + E;
   __shared__ int base;
@@ -65,16 +68,11 @@ moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ 
     if (e < E) {
       const int rank = warp_tot[warp] + __popc(m & ((1u << lane) - 1));
       slot_of_expert[e] = hit ? rank : -1;
-      if (hit) pub[PUB_HEADER + rank] = (unsigned)e;
+      if (hit) pub[PUB_HEADER + rank] = ((unsigned long long)seq << 32) | (unsigned)e;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    pub[1] = (unsigned)base;
-    __threadfence_system();   // ids and count are visible to the host before seq
-    pub[0] = seq;
-    __threadfence_system();
-  }
+  if (threadIdx.x == 0) pub[0] = ((unsigned long long)seq << 32) | (unsigned)base;
 }
 
 __global__ void wait_flag_kernel(const volatile unsigned* __restrict__ flag, unsigned seq,
@@ -108,8 +106,9 @@ class ExpertFetcher {
   ExpertFetcher(int max_experts) : max_experts_(max_experts) {}
 
   int init() {
-    PS_CHECK_CUDA(cudaHostAlloc(&pub_host_, (PUB_HEADER + max_experts_) * sizeof(unsigned), cudaHostAllocMapped));
-    memset((void*)pub_host_, 0, (PUB_HEADER + max_experts_) * sizeof(unsigned));
+    PS_CHECK_CUDA(cudaHostAlloc(&pub_host_, (PUB_HEADER + max_experts_) * sizeof(unsigned long long),
+                                cudaHostAllocMapped));
+    memset((void*)pub_host_, 0, (PUB_HEADER + max_experts_) * sizeof(unsigned long long));
     PS_CHECK_CUDA(cudaHostGetDevicePointer((void**)&pub_dev_, (void*)pub_host_, 0));
     PS_CHECK_CUDA(cudaHostAlloc(&seq_src_, kSeqRing * sizeof(unsigned), cudaHostAllocDefault));
     PS_CHECK_CUDA(cudaMalloc(&flag_dev_, 2 * sizeof(unsigned)));   // [flag, error]
@@ -144,7 +143,7 @@ class ExpertFetcher {
     cv_.notify_one();
   }
 
-  unsigned* pub_dev() const { return pub_dev_; }
+  unsigned long long* pub_dev() const { return pub_dev_; }
   unsigned* flag_dev() const { return flag_dev_; }
   cudaStream_t stream() const { return stream_; }
   long long experts_copied() const { return copied_.load(); }
@@ -168,25 +167,40 @@ class ExpertFetcher {
       // wait for the GPU to publish this layer's routed experts
       auto t0 = std::chrono::steady_clock::now();
       unsigned spins = 0;
-      while ((int)(pub_host_[0] - j.seq) < 0) {
+      bool seen = true;
+      while ((unsigned)(pub_host_[0] >> 32) != j.seq) {
         if (++spins > 4096) {
           std::this_thread::yield();
           if (stopping() || std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) {
             error_.store(1);
+            seen = false;
             break;
           }
         }
       }
       std::atomic_thread_fence(std::memory_order_acquire);
-      unsigned n = pub_host_[1];
+      unsigned n = seen ? (unsigned)(pub_host_[0] & 0xffffffffu) : 0;
       if (n > (unsigned)max_experts_) n = 0, error_.store(2);
       // one copy per run of consecutive expert ids when host and slot strides agree
       // (slots are in ascending-id order, so the run is contiguous on both sides)
       const bool coalesce = j.expert_stride == j.slot_stride;
+      unsigned ids[4096];
+      for (unsigned r = 0; r < n; ++r) {      // each word carries the tag: wait for this seq's
+        unsigned long long w;
+        while ((unsigned)((w = pub_host_[PUB_HEADER + r]) >> 32) != j.seq) {
+          if (stopping()) break;
+        }
+        ids[r] = (unsigned)(w & 0xffffffffu);
+        if (ids[r] >= (unsigned)max_experts_) {   // never copy outside the group
+          error_.store(2);
+          n = r;
+          break;
+        }
+      }
       for (unsigned r = 0; r < n;) {
-        const unsigned e = pub_host_[PUB_HEADER + r];
+        const unsigned e = ids[r];
         unsigned run = 1;
-        while (coalesce && r + run < n && pub_host_[PUB_HEADER + r + run] == e + run) ++run;
+        while (coalesce && r + run < n && ids[r + run] == e + run) ++run;
         const long long bytes = (long long)(run - 1) * j.expert_stride + j.expert_bytes;
         if (cudaMemcpyAsync(j.slot_base + r * j.slot_stride, j.host_base + (long long)e * j.expert_stride, bytes,
                             cudaMemcpyHostToDevice, stream_) != cudaSuccess)
@@ -209,8 +223,8 @@ class ExpertFetcher {
 
   int max_experts_;
   int device_ = 0;
-  volatile unsigned* pub_host_ = nullptr;
-  unsigned* pub_dev_ = nullptr;
+  volatile unsigned long long* pub_host_ = nullptr;
+  unsigned long long* pub_dev_ = nullptr;
   unsigned* seq_src_ = nullptr;
   unsigned* flag_dev_ = nullptr;
   unsigned ring_i_ = 0;
