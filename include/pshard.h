@@ -125,6 +125,18 @@ int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_start, cons
                     const void* kv_base, long long kv_req_stride, long long kv_row_stride,
                     float scale, void* out, int ldo, int out_bf16, void* stream);
 
+/* Same attention on the tcgen05 tensor cores (attention_tc.cu): S and O accumulate in
+ * TMEM, K/V tiles arrive by TMA from the cache viewed as a 4-D tensor
+ * [positions kv_positions][slots][2*n_kv heads][head_dim] (so kv_req_stride must be
+ * 2*n_kv*head_dim and kv_row_stride a multiple of it). head_dim 64 or 128. */
+int ps_attn_prefill_tc(const float* q, int ldq, int batch, const int* q_start, const int* p0,
+                       const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
+                       const void* kv_base, long long kv_req_stride, long long kv_row_stride,
+                       int kv_positions, float scale, void* out, int ldo, int out_bf16, void* stream);
+/* Pipeline watchdog of ps_attn_prefill_tc: non-zero = a barrier wait gave up after 1 s
+ * ((role << 24) | (barrier << 16) | key block); reset clears it. */
+int ps_attn_tc_watchdog(unsigned* code, int reset);
+
 /* ---- K5: MoE router + routed experts ------------------------------------------
  * Replace MOE_ROUTE (t, d, E) and the expert MATMUL (t*k, d, mats*eff) of
  * `pkg/src/shardplan/model_graph.py:181-200`. Everything stays on the device:

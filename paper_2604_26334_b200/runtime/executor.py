@@ -935,9 +935,10 @@ class Executor:
                            i_slot, kv_base, self.row_elems, row_stride, i_lens, max_len, scale,
                            att, hq, self.ws, self.ws_floats, self.cs)
                 else:
-                    L.call("ps_attn_prefill", self.qkv, self.qkv_rows, nb, i_qstart, i_p0, i_slot,
+                    # tcgen05 / TMEM / TMA flash attention (attention_tc.cu)
+                    L.call("ps_attn_prefill_tc", self.qkv, self.qkv_rows, nb, i_qstart, i_p0, i_slot,
                            max_new, self.h, self.kv, self.hd, kv_base, self.row_elems, row_stride,
-                           scale, att, hq, 0 if gemv else 1, self.cs)
+                           max_len, scale, att, hq, 0 if gemv else 1, self.cs)
                 if kv_region is not None:
                     # appended rows -> the layer's host home (D2H stream), then release
                     L.call("ps_stream_wait_event", self.d2h, self._record(self.cs))

@@ -52,6 +52,8 @@ _SIGS = {
     "ps_rmsnorm": [_p, _i, _p, _i, _p, _i, _f, _p, _i, _i, _p],
     "ps_qkv_rope_append": [_p, _i, _i, _i, _i, _i, _p, _p, _p, _ll, _ll, _p, _p, _p, _f, _p],
     "ps_attn_decode": [_p, _i, _i, _i, _i, _i, _p, _p, _ll, _ll, _p, _i, _f, _p, _i, _p, _ll, _p],
+    "ps_attn_prefill_tc": [_p, _i, _i, _p, _p, _p, _i, _i, _i, _i, _p, _ll, _ll, _i, _f, _p, _i, _i, _p],
+    "ps_attn_tc_watchdog": [C.POINTER(C.c_uint), _i],
     "ps_attn_decode_workspace": [_i, _i, _i, _i, C.POINTER(_ll)],
     "ps_attn_prefill": [_p, _i, _i, _p, _p, _p, _i, _i, _i, _i, _p, _ll, _ll, _f, _p, _i, _i, _p],
     "ps_upload_small": [_p, _p, _i, _p],
@@ -126,7 +128,7 @@ KERNEL_CALLS = frozenset({
     "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_gemv_bf16_cfg", "ps_gemm_bf16_cfg",
     "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine",
     "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_wait_flag",
-    "ps_stripe_signal", "ps_stripe_wait"})
+    "ps_stripe_signal", "ps_stripe_wait", "ps_attn_prefill_tc"})
 counters = {"kernel_calls": 0, "memcpy_calls": 0}
 
 

@@ -207,8 +207,13 @@ def test_attn_decode(hd, h, kv, lens):
 
 @pytest.mark.parametrize("hd,h,kv,seqs", [(128, 32, 8, [(0, 2048)]), (64, 8, 8, [(0, 128)]),
                                           (128, 32, 8, [(0, 100), (37, 64), (500, 5)]),
-                                          (128, 32, 4, [(0, 300)])])
-def test_attn_prefill(hd, h, kv, seqs):
+                                          (128, 32, 4, [(0, 300)]), (128, 64, 8, [(3000, 200)]),
+                                          (128, 32, 8, [(0, 512)] * 4), (64, 4, 2, [(7, 129), (0, 1)])])
+@pytest.mark.parametrize("kernel", ["ps_attn_prefill", "ps_attn_prefill_tc"])
+def test_attn_prefill(hd, h, kv, seqs, kernel):
+    """kernel: the mma.sync flash attention or the tcgen05/TMEM/TMA one; varlen
+    requests with p0 > 0 (chunked prefill), GQA groups 1-8, head dims 64 / 128,
+    partial query and key blocks."""
     lib = L()
     B = len(seqs)
     cap = max(p0 + n for p0, n in seqs)
@@ -220,9 +225,14 @@ def test_attn_prefill(hd, h, kv, seqs):
     qs = torch.tensor(q_start, device="cuda")
     p0 = torch.tensor([p for p, _ in seqs], dtype=torch.int32, device="cuda")
     out = torch.zeros(T, h * hd, device="cuda", dtype=torch.bfloat16)
-    lib.call("ps_attn_prefill", q.data_ptr(), h * hd, B, qs.data_ptr(), p0.data_ptr(), 0,
-             max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd,
-             1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
+    if kernel == "ps_attn_prefill":
+        lib.call("ps_attn_prefill", q.data_ptr(), h * hd, B, qs.data_ptr(), p0.data_ptr(), 0,
+                 max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd,
+                 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
+    else:
+        lib.call("ps_attn_prefill_tc", q.data_ptr(), h * hd, B, qs.data_ptr(), p0.data_ptr(), 0,
+                 max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd, cap,
+                 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
     torch.cuda.synchronize()
     for b, (s0, n) in enumerate(seqs):
         K = cache[: s0 + n, b, 0].float()
