@@ -141,6 +141,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 2^x on the SFU (ex2.approx: ~2 ulp, exact 0 for -inf); P is rounded to bf16 anyway
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t pack2_bf16(float a, float b) {
   __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&p);
@@ -310,21 +317,27 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const float* 
         for (int e = 0; e < 32; ++e) sv[c + e] = t[e];
       }
       const int k0 = j * TC_BK;
-      float mx = -INFINITY;
+      // the causal / length mask only touches blocks that reach past this row's position
+      if (k0 + TC_BK - 1 > qpos || k0 + TC_BK > kv_end) {
 #pragma unroll
-      for (int c = 0; c < TC_BK; ++c) {
-        if (k0 + c > qpos || k0 + c >= kv_end) sv[c] = -INFINITY;
-        mx = fmaxf(mx, sv[c]);
+        for (int c = 0; c < TC_BK; ++c)
+          if (k0 + c > qpos || k0 + c >= kv_end) sv[c] = -INFINITY;
       }
-      const float m_new = fmaxf(m, mx);
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < TC_BK; c += 2) { mx0 = fmaxf(mx0, sv[c]); mx1 = fmaxf(mx1, sv[c + 1]); }
+      const float m_new = fmaxf(m, fmaxf(mx0, mx1));
       const float base = m_new == -INFINITY ? 0.f : m_new;
-      const float corr = exp2f(m - base);          // 0 when m = -inf (first block)
-      float rs = 0.f;
+      const float corr = fast_exp2(m - base);      // 0 when m = -inf (first block)
+      float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
-      for (int c = 0; c < TC_BK; ++c) {
-        sv[c] = exp2f(sv[c] - base);
-        rs += sv[c];
+      for (int c = 0; c < TC_BK; c += 2) {
+        sv[c] = fast_exp2(sv[c] - base);
+        sv[c + 1] = fast_exp2(sv[c + 1] - base);
+        rs0 += sv[c];
+        rs1 += sv[c + 1];
       }
+      const float rs = rs0 + rs1;
       l = l * corr + rs;
       if (j > 0) {
         wait_wd(o_done, (j - 1) & 1, 0x03020000u | (j & 0xffff));   // O(j-1) complete, P buffer free
