@@ -107,7 +107,7 @@ class Executor:
         # cache streamed / CPU-placed weight shards in budget the ring does not need
         # (PS_SPARE_PIN=0 runs the plan's residency exactly)
         self.spare_pin = os.environ.get("PS_SPARE_PIN", "1") != "0"
-        self.ring_keep_pieces = int(os.environ.get("PS_RING_KEEP_PIECES", "6"))   # ring kept for streaming
+        self.ring_keep_pieces = int(os.environ.get("PS_RING_KEEP_PIECES", "4"))   # ring kept for streaming
         self.spare_pinned = []
         self.expert_slots, self.expert_slot_bytes = 0, 0
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
@@ -261,8 +261,9 @@ class Executor:
         set in pin order, then the *spare pins* — streamed or CPU-placed weight
         shards cached in budget the plan reserved as double-buffer scratch
         (2 x the largest streamed shard, `pkg/src/shardplan/planner.py:132-159`)
-        but the piece-wise ring does not need. Pure: a function of the plan, the
-        layout and the budget, so the migration model can predict switches."""
+        but the piece-wise ring (4 pieces ahead) does not need; first-fit
+        decreasing by link bytes saved per token. Pure: a function of the plan,
+        the layout and the budget, so the migration model can predict switches."""
         plan = self.plans[tier]
         T = min(tier, self.Tmax)
         pinned, modes = self._plan_modes(plan)
@@ -287,9 +288,10 @@ class Executor:
 
         def value(sid):   # link bytes saved per token per VRAM byte
             return k_frac if self.shard_kind[sid] is ShardKind.MOE_EXPERT_GROUP else 1.0
+        # equal value per byte packs best largest-first (first-fit decreasing)
         cands = sorted((sid for sid in modes if self.shard_kind[sid] is not ShardKind.KV_CACHE),
-                       key=lambda sid: (-value(sid), self.shards[sid].priority, self.shards[sid].layer_index,
-                                        sid))
+                       key=lambda sid: (-value(sid), -self._phys_bytes(self.shards[sid]),
+                                        self.shards[sid].priority, self.shards[sid].layer_index, sid))
         for sid in cands:
             b = up(self._phys_bytes(self.shards[sid]))
             if b <= spare:
