@@ -343,6 +343,12 @@ def run_ours(args, rank: int, world: int) -> dict:
                  "prefill_pass_ms": round(res.passes[0][2] * 1e3, 2) if res.passes else None},
         "model_load_s": round(eng.load_seconds, 2),
         "host_weights": "shared /dev/shm segment per node" if shared else "private pinned blob",
+        "residency": {
+            "spare_pinned_shards": len(eng.executor.spare_pinned),
+            "spare_pinned_bytes": int(sum(eng.executor._phys_bytes(eng.executor.shards[sid])
+                                          for sid in eng.executor.spare_pinned)),
+            "note": "streamed / CPU-placed shards cached in the plan's unused double-buffer "
+                    "scratch; the arena stays = budget; PS_SPARE_PIN=0 runs the plan's residency"},
     }
     # C-ABI kernel calls (each >= 1 launch of our sm_100a kernels) in the timed passes
     out["gpu_launches"] = int(sum(s.kernel_calls for s in timed_stats))
