@@ -71,8 +71,8 @@ def parse():
     ap.add_argument("--stripe", action="store_true",
                     help="N>1: one request stream striped over every GPU's host link "
                          "(rank 0 executes, ranks 1.. pull stripes; runtime/striping.py)")
-    ap.add_argument("--stripe-same-gpu", action="store_true",
-                    help="(functional test) put every rank on GPU 0")
+    ap.add_argument("--stripe-same-gpu", "--same-gpu", dest="stripe_same_gpu", action="store_true",
+                    help="(functional test) put every rank on GPU 0 and use gloo for the bookkeeping")
     args = ap.parse_args()
     model, budget, prompt, gen, batch, desc = CONFIGS[args.config]
     args.model = args.model or model
@@ -108,7 +108,7 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
+                if out and out.count(",") >= 2:
                     self.samples.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
@@ -282,7 +282,7 @@ def run_ours(args, rank: int, world: int) -> dict:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
+    with ClockSampler(torch.cuda.current_device()) as clocks:
         t0 = time.perf_counter()
         res = eng.generate(prompts, gen_len=gen)
         torch.cuda.synchronize()
@@ -300,7 +300,7 @@ def run_ours(args, rank: int, world: int) -> dict:
     zero_copy = sum(p[4] for p in timed) / max(1, len(timed))
     # replicas: sum of tokens over ranks / max over ranks of device seconds (no data collective)
     from paper_2604_26334_b200.runtime.replicas import aggregate
-    agg = (aggregate(B * len(timed), t_steps, device="cuda") if not stripe else
+    agg = (aggregate(B * len(timed), t_steps, device="cpu" if args.stripe_same_gpu else "cuda") if not stripe else
            {"seconds_max": t_steps, "value": B * len(timed) / t_steps})
     t_max, value = agg["seconds_max"], agg["value"]
     # end to end through the public API: all decode passes, host wall clock, tokens read back
@@ -438,7 +438,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(0 if args.stripe_same_gpu else int(os.environ.get("LOCAL_RANK", 0)))
         # striped mode only needs host-side control (barriers, a broadcast): gloo
-        dist.init_process_group("gloo" if args.stripe else "nccl")
+        dist.init_process_group("gloo" if (args.stripe or args.stripe_same_gpu) else "nccl")
     out = run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(out))

@@ -199,21 +199,44 @@ class SharedHostBlob:
         self.path = f"/dev/shm/{name}"
         self.nbytes = nbytes
         self.timeout_s = timeout_s
+        import time
         try:
             self.fd = os.open(self.path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
             self.creator = True
             os.ftruncate(self.fd, nbytes)
+            # populate the tmpfs pages up front: several processes pinning the same
+            # sparse segment concurrently fails for large segments (measured at 17 GB)
+            os.posix_fallocate(self.fd, 0, nbytes)
         except FileExistsError:
             self.creator = False
             self.fd = os.open(self.path, os.O_RDWR)
-            t0 = __import__("time").time()
-            while os.fstat(self.fd).st_size < nbytes:
-                if __import__("time").time() - t0 > 60:
-                    raise TimeoutError(f"{self.path}: creator never sized the blob")
-                __import__("time").sleep(0.05)
+            t0 = time.time()
+            # the creator pins first (populated pages), then the others
+            while not os.path.exists(self.path + ".pinned"):
+                if time.time() - t0 > timeout_s:
+                    os.close(self.fd)
+                    raise TimeoutError(f"{self.path}: creator never pinned the blob")
+                time.sleep(0.02)
         self.mm = mmap.mmap(self.fd, nbytes)
         self.addr = ctypes.addressof(ctypes.c_char.from_buffer(self.mm))
-        L.call("ps_host_register", self.addr, nbytes, 1)
+        try:
+            L.call("ps_host_register", self.addr, nbytes, 1)
+        except Exception:
+            self.addr = 0
+            try:
+                self.mm.close()
+            except BufferError:
+                pass
+            os.close(self.fd)
+            if self.creator:
+                for p in (self.path, self.path + ".pinned"):
+                    try:
+                        os.unlink(p)
+                    except FileNotFoundError:
+                        pass
+            raise
+        if self.creator:
+            open(self.path + ".pinned", "w").close()
 
     @staticmethod
     def fits(nbytes: int) -> bool:
@@ -250,7 +273,7 @@ class SharedHostBlob:
                 pass
             os.close(self.fd)
             if self.creator:
-                for p in (self.path, self.path + ".ready"):
+                for p in (self.path, self.path + ".ready", self.path + ".pinned"):
                     try:
                         os.unlink(p)
                     except FileNotFoundError:
@@ -274,7 +297,13 @@ class HostWeights:
         self.shared = None
         if shared is not None:
             total = _align(self.layout.total_bytes) + self.layout.embed_bytes
-            self.shared = SharedHostBlob(shared, total)
+            try:
+                self.shared = SharedHostBlob(shared, total)
+            except Exception as exc:   # cannot pin a shared segment here: private copy
+                import warnings
+                warnings.warn(f"shared host weights unavailable ({exc}); using a private pinned blob")
+                self.shared = None
+        if self.shared is not None:
             self.base = self.shared.addr
             self.embed = self.shared.addr + _align(self.layout.total_bytes)
         else:

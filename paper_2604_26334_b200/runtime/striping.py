@@ -40,6 +40,7 @@ class _ShmSegment:
         if create:
             self.fd = os.open(self.path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
             os.ftruncate(self.fd, nbytes)
+            os.posix_fallocate(self.fd, 0, nbytes)   # populated pages pin safely in parallel
         else:
             t0 = time.time()
             while True:
