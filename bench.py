@@ -281,6 +281,9 @@ def run_ours(args, rank: int, world: int) -> dict:
     if world > 1 and not stripe:
         import torch.distributed as dist
         dist.barrier()
+        sh = eng.weights.shared
+        if sh is not None and sh.creator:
+            sh.unlink()    # every replica has it mapped: a crashed job leaks no /dev/shm
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clocks:
         t0 = time.perf_counter()
@@ -306,6 +309,9 @@ def run_ours(args, rank: int, world: int) -> dict:
     # end to end through the public API: all decode passes, host wall clock, tokens read back
     e2e_decode_wall = wall - res.ttft_s
     e2e = B * (gen - 1) / e2e_decode_wall
+    if world > 1 and not stripe:   # whole job: tokens of every replica / slowest replica's wall
+        e2e = aggregate(B * (gen - 1), e2e_decode_wall,
+                        device="cpu" if args.stripe_same_gpu else "cuda")["value"]
     kv_wb = sum(s.kv_writeback_bytes for s in timed_stats) / max(1, len(timed_stats))
     achieved = streamed / (t_steps / len(timed)) / GB
     plan_dec = eng.plans[eng.pick_tier(B)]

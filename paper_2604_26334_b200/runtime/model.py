@@ -203,19 +203,28 @@ class SharedHostBlob:
         try:
             self.fd = os.open(self.path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
             self.creator = True
-            os.ftruncate(self.fd, nbytes)
-            # populate the tmpfs pages up front: several processes pinning the same
-            # sparse segment concurrently fails for large segments (measured at 17 GB)
-            os.posix_fallocate(self.fd, 0, nbytes)
+            try:
+                os.ftruncate(self.fd, nbytes)
+                # populate the tmpfs pages up front: several processes pinning the same
+                # sparse segment concurrently fails for large segments (measured at
+                # 17 GB), and a full /dev/shm fails here instead of SIGBUS later
+                os.posix_fallocate(self.fd, 0, nbytes)
+            except OSError:
+                os.close(self.fd)
+                os.unlink(self.path)
+                raise
         except FileExistsError:
             self.creator = False
             self.fd = os.open(self.path, os.O_RDWR)
             t0 = time.time()
-            # the creator pins first (populated pages), then the others
+            # the creator pins first (populated pages), then the others; a creator
+            # that failed unlinks the file, which ends the wait
             while not os.path.exists(self.path + ".pinned"):
-                if time.time() - t0 > timeout_s:
+                gone = not os.path.exists(self.path)
+                if gone or time.time() - t0 > timeout_s:
                     os.close(self.fd)
-                    raise TimeoutError(f"{self.path}: creator never pinned the blob")
+                    raise (FileNotFoundError if gone else TimeoutError)(
+                        f"{self.path}: creator never pinned the blob")
                 time.sleep(0.02)
         self.mm = mmap.mmap(self.fd, nbytes)
         self.addr = ctypes.addressof(ctypes.c_char.from_buffer(self.mm))
@@ -256,9 +265,21 @@ class SharedHostBlob:
         import time
         t0 = time.time()
         while not os.path.exists(self.path + ".ready"):
+            if not os.path.exists(self.path):
+                raise FileNotFoundError(f"{self.path}: creator left before the weights were ready")
             if time.time() - t0 > self.timeout_s:
                 raise TimeoutError(f"{self.path}: weights never marked ready")
             time.sleep(0.1)
+
+    def unlink(self) -> None:
+        """Remove the name once every process that needs it has mapped the segment;
+        the memory lives until the last mapping goes."""
+        import os
+        for p in (self.path, self.path + ".ready", self.path + ".pinned"):
+            try:
+                os.unlink(p)
+            except FileNotFoundError:
+                pass
 
     def close(self) -> None:
         import os
@@ -273,11 +294,7 @@ class SharedHostBlob:
                 pass
             os.close(self.fd)
             if self.creator:
-                for p in (self.path, self.path + ".ready", self.path + ".pinned"):
-                    try:
-                        os.unlink(p)
-                    except FileNotFoundError:
-                        pass
+                self.unlink()
 
 
 class HostWeights:

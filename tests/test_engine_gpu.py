@@ -258,10 +258,15 @@ def _shared_weights_worker(name, q):
     from paper_2604_26334_b200.planning import catalog as cat
     from paper_2604_26334_b200.runtime.model import HostWeights, arch_for as af
     spec = cat.builtin_model("tiny-llama")
-    hw = HostWeights(spec, af(spec), shared=name)
-    hw.generate()
-    digest = hashlib.sha256(hw.blob_bytes().tobytes() + hw.embed_bytes().tobytes()).hexdigest()
-    q.put((hw.shared.creator, digest))
+    try:
+        hw = HostWeights(spec, af(spec), shared=name)
+        hw.generate()
+        digest = hashlib.sha256(hw.blob_bytes().tobytes() + hw.embed_bytes().tobytes()).hexdigest()
+        q.put((hw.shared.creator if hw.shared else None, digest))
+    except BaseException as exc:   # report instead of leaving the parent waiting
+        import traceback
+        q.put((None, "".join(traceback.format_exception(exc))))
+        raise
     import time
     time.sleep(1.0)   # keep the mapping alive while the other replica reads
     hw.close()
@@ -290,7 +295,7 @@ def test_shared_host_weights_two_processes():
     got = [q.get(timeout=120) for _ in range(2)]
     for p in ps:
         p.join(60)
-    assert sorted(c for c, _ in got) == [False, True]
+    assert sorted(c for c, _ in got if c is not None) == [False, True], got
     assert all(d == want for _, d in got)
     import os
     assert not os.path.exists(f"/dev/shm/{name}")
