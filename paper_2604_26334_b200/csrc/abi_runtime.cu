@@ -60,6 +60,7 @@ int ps_preload_gemm();
 int ps_preload_attention();
 int ps_preload_elementwise();
 int ps_preload_moe();
+int ps_preload_moe_decode();
 extern "C" int ps_preload_fetcher();
 int ps_preload_striper();
 int ps_preload_attention_tc();
@@ -70,7 +71,7 @@ int ps_preload_kernels(int* n_loaded) {
   static int loaded = -1;
   if (loaded < 0)
     loaded = ps_preload_gemv() + ps_preload_gemv_tma() + ps_preload_gemm() + ps_preload_attention() +
-             ps_preload_elementwise() + ps_preload_moe() + ps_preload_fetcher() + ps_preload_striper() +
+             ps_preload_elementwise() + ps_preload_moe() + ps_preload_moe_decode() + ps_preload_fetcher() + ps_preload_striper() +
              ps_preload_attention_tc();
   if (n_loaded) *n_loaded = loaded;
   return PS_OK;

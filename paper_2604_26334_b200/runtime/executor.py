@@ -44,6 +44,7 @@ from .model import Arch, HostWeights, rope_table
 from .streamer import CopyRing, EventPool
 
 GEMV_MAX_T = 32
+PS_MOE_DECODE_TICKETS = 1024   # include/pshard.h
 
 
 @dataclass
@@ -201,6 +202,10 @@ class Executor:
         self.rope = a.alloc_high("rope", rope.nbytes)
         self.host_stage = L.host_alloc(max(1 << 20, rope.nbytes, T * 4 + 4096), mapped=False)
         self._h2d_sync(self.rope, rope)
+        self.m_tickets = 0
+        if self.moe is not None:   # ps_moe_decode_experts' row-block tickets (self-resetting)
+            self.m_tickets = a.alloc_high("moe_tickets", 4 * PS_MOE_DECODE_TICKETS)
+            self._h2d_sync(self.m_tickets, np.zeros(PS_MOE_DECODE_TICKETS, np.uint32))
         self.host_tok = L.host_alloc(4 * B * 4096, mapped=False)
         self.host_tok_i = 0
 
@@ -651,11 +656,23 @@ class Executor:
         elif mode == "stream" and gemv:
             mode = "zerocopy"
 
+        # one token: the k routed experts as row groups of two bulk-copy launches,
+        # combine fused, no plan (csrc/moe_decode.cu)
+        planned = self.residency[sid][0]
+        fetched = gemv and planned == "stream" and bool(self.expert_slots)
+        t1 = (gemv and T == 1 and d <= 2048 and eff <= 2048 and (fetched or mode == "pinned") and
+              os.environ.get("PS_MOE_DECODE", "1") != "0")
+
         def route(base):
             norm(base + t_norm.offset)
             self._matmul(T, xn, base + t_router.offset, E, d, self.m_logits, E, L.PS_EPI_STORE)
             L.call("ps_moe_route_topk", self.m_logits, E, T, E, k, 1, self.m_ids, self.m_w, self.cs)
-            L.call("ps_moe_plan", self.m_ids, P, E, self.m_plan, self.cs)
+            if not t1:
+                L.call("ps_moe_plan", self.m_ids, P, E, self.m_plan, self.cs)
+
+        def decode_t1(ebase, slot_map):
+            L.call("ps_moe_decode_experts", xn, self.m_ids, k, slot_map, ebase, stride if not slot_map else sb,
+                   0, down_off, eff, d, self.m_h, self.m_out, self.m_w, self.x, self.m_tickets, self.cs)
 
         def experts(ebase, lo, hi):
             L.call("ps_moe_expert_gu", xn, d, 0 if gemv else 1, self.m_plan, E, P, k, ebase, stride, 0,
@@ -663,8 +680,7 @@ class Executor:
             L.call("ps_moe_expert_down", self.m_h, self.m_plan, E, P, ebase, stride, down_off, eff, d,
                    self.m_out, lo, hi, self.cs)
 
-        planned = self.residency[sid][0]
-        if gemv and planned == "stream" and self.expert_slots:
+        if fetched:
             # routed experts through the copy engine (csrc/fetcher.cu)
             host = self.w.shard_ptr(sid)
             _, _, _, ebytes = self._expert_geometry(sid, layer)
@@ -690,6 +706,9 @@ class Executor:
                     self._fetch_debug(layer, seq, P, E, host + e0.offset, stride, ebytes, slots, sb)
 
             def run(_p, _a, _b):
+                if t1:
+                    decode_t1(slots, self.m_slotmap)
+                    return
                 L.call("ps_moe_expert_gu_mapped", xn, d, 0, self.m_plan, E, P, k, slots, sb, 0, eff, d,
                        self.m_h, 0, E, self.m_slotmap, self.cs)
                 L.call("ps_moe_expert_down_mapped", self.m_h, self.m_plan, E, P, slots, sb, down_off, eff, d,
@@ -701,9 +720,14 @@ class Executor:
             self._traced(f"L{layer}.experts", run, 0, 0, 0)
             self._stat.bytes_streamed += min(E, P) * ebytes
             self._stat.copies += min(E, P)
-            L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
+            if not t1:
+                L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
             return
 
+        if mode == "pinned" and t1:
+            self._traced(f"L{layer}.router+topk", route, dev)
+            self._traced(f"L{layer}.experts", lambda *_: decode_t1(dev + e0.offset, None), 0, 0, 0)
+            return
         if mode in ("pinned", "zerocopy"):
             base = dev if mode == "pinned" else self.w.shard_ptr(sid)
             self._traced(f"L{layer}.router+topk", route, base)

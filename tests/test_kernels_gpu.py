@@ -370,6 +370,55 @@ def test_moe_pipeline(T, zero_copy, x_bf16):
         lib.host_free(host)
 
 
+@pytest.mark.parametrize("E,k,d,eff,mapped", [(16, 4, 256, 128, False), (32, 8, 2048, 768, True),
+                                              (8, 2, 512, 1536, False), (128, 8, 2048, 768, False)])
+def test_moe_decode_experts_one_token(E, k, d, eff, mapped):
+    """ps_moe_decode_experts (t = 1, no plan, combine fused) against the fp32 MoE
+    block, with and without a fetcher slot map; twice in a row (self-resetting
+    tickets) and bit-identical across runs (fixed-order combine)."""
+    import ctypes
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(E + d)
+    x = torch.randn(1, d, device="cuda", generator=g)
+    router = (torch.randn(E, d, device="cuda", generator=g) / 8).to(torch.bfloat16)
+    Wgu = (torch.randn(E, 2 * eff, d, device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    Wd = (torch.randn(E, d, eff, device="cuda", generator=g) / eff ** 0.5).to(torch.bfloat16)
+    blob = torch.cat([torch.cat([Wgu[e].reshape(-1), Wd[e].reshape(-1)]) for e in range(E)]).contiguous()
+    stride = (2 * eff * d + d * eff) * 2
+    s = stream()
+    logits = x @ router.float().T
+    ids = torch.zeros(k, dtype=torch.int32, device="cuda")
+    w = torch.zeros(k, device="cuda")
+    lib.call("ps_moe_route_topk", logits.data_ptr(), E, 1, E, k, 1, ids.data_ptr(), w.data_ptr(), s)
+    torch.cuda.synchronize()
+    base, slot_map = blob.data_ptr(), None
+    if mapped:   # routed experts copied into k slots in reverse order, as a fetcher could
+        slots = torch.zeros(k * stride // 2, dtype=torch.bfloat16, device="cuda")
+        smap = torch.full((E,), -1, dtype=torch.int32, device="cuda")
+        for j, e in enumerate(ids.tolist()):
+            sl = k - 1 - j
+            slots[sl * stride // 2:(sl + 1) * stride // 2] = blob[e * stride // 2:(e + 1) * stride // 2]
+            smap[e] = sl
+        base, slot_map = slots.data_ptr(), smap
+    h = torch.zeros(k, eff, device="cuda")
+    out = torch.zeros(k, d, device="cuda")
+    tickets = torch.zeros(1024, dtype=torch.int32, device="cuda")
+    y0 = torch.randn(1, d, device="cuda", generator=g)
+    ys = []
+    for _ in range(2):
+        y = y0.clone()
+        lib.call("ps_moe_decode_experts", x.data_ptr(), ids.data_ptr(), k,
+                 slot_map.data_ptr() if slot_map is not None else None, base, stride, 0, 2 * eff * d * 2,
+                 eff, d, h.data_ptr(), out.data_ptr(), w.data_ptr(), y.data_ptr(), tickets.data_ptr(), s)
+        torch.cuda.synchronize()
+        ys.append(y)
+    assert int(tickets.abs().sum()) == 0
+    assert torch.equal(ys[0], ys[1])
+    ref, rid, rw = _moe_ref(x, router.float(), Wgu.float(), Wd.float(), k)
+    assert torch.equal(ids.view(1, k).long(), rid)
+    assert rel_err(ys[0] - y0, ref) < 1e-4
+
+
 def test_expert_fetcher_publish_copy_wait():
     """ps_moe_publish -> host thread copies the routed experts (ascending id) into
     slots -> ps_wait_flag; mapped expert kernels see expert e at its slot."""
