@@ -168,16 +168,14 @@ int ps_moe_expert_down_mapped(const float* h, const int* plan, int E, int P, con
 int ps_moe_combine(const float* out, const int* plan, int E, int P, const float* w, int T, int k,
                    int d, float* y, int ldy, void* stream);
 /* One-token decode (t = 1) in two launches, no plan: CTA group j streams routed expert
- * ids[j] (slot_of_expert[ids[j]] when not NULL) through a bulk-copy ring;
- * h[j] = silu(x Wg^T) * (x Wu^T) ([k x eff]), out[j] = h[j] Wd^T ([k x d]), and
- * y += sum_j w[j] out[j] (j ascending, the order of ps_moe_combine). x, y fp32 [d];
- * d, eff multiples of 8 and <= 2048; `tickets` = PS_MOE_DECODE_TICKETS zeroed
- * unsigned ints owned by the caller's stream (reset by the kernel after use). */
-#define PS_MOE_DECODE_TICKETS 1024
+ * ids[j] (slot_of_expert[ids[j]] when not NULL) through a bulk-copy ring,
+ * h[j] = silu(x Wg^T) * (x Wu^T) ([k x eff] fp32 scratch); then each CTA streams one
+ * row block of all k down matrices and adds sum_j w[j] (h[j] Wd_j^T), j ascending (the
+ * order of ps_moe_combine), into y. x, y fp32 [d]; d, eff multiples of 8, <= 2048. */
 int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot_of_expert,
                           const void* expert_base, long long expert_stride, long long gu_off,
-                          long long down_off, int eff, int d, float* h, float* out, const float* w,
-                          float* y, unsigned* tickets, void* stream);
+                          long long down_off, int eff, int d, float* h, const float* w, float* y,
+                          void* stream);
 
 /* ---- routed-expert fetcher (copy-engine uploads of router-selected experts) --
  * Replaces the zero-copy read of a streamed expert group in decode passes: the GPU

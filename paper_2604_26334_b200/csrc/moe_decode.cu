@@ -19,9 +19,13 @@
 //   whole rows (x held in registers, packed fp32x2 FMA, one warp reduction per
 //   row) and leave one fp32 sum per row in shared memory.
 //   gate/up (rows interleaved gate, up): h[j][r/2] = silu(gate) * up.
-//   down: out[j][r], then the last of the k CTAs of row block c (ticket counter)
-//   adds sum_j w[j] * out[j][r], j ascending, into y[r] — the order moe.cu's
-//   combine uses, so the result does not depend on CTA scheduling.
+//
+//   down: CTA c owns rows [c*R, (c+1)*R) of ALL k down matrices (one ring stage
+//   per expert), keeps the k h vectors in shared memory, and adds
+//   sum_j w[j] * out[j][r], j ascending — the order of moe.cu's combine — into
+//   y[r]: no partial outputs leave the CTA, no cross-CTA reduction.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "mbarrier.cuh"
 #include "../../include/pshard.h"
@@ -32,7 +36,9 @@ constexpr int MD_STAGES = 6;
 constexpr int MD_STAGE = 32768;
 constexpr int MD_WARPS = 8;
 constexpr int MD_THREADS = 32 * (1 + MD_WARPS);
-constexpr int MD_MAXG = 8;    // 8-column groups per lane: K <= 32 * 8 * 8 = 2048
+constexpr int MD_MAXRING = 16;   // down kernel: ring slots sized to one expert's row block
+constexpr int MD_MAXG = 8;
+constexpr int MD_BATCH = 4;    // rows whose dot products / warp reductions interleave    // 8-column groups per lane: K <= 32 * 8 * 8 = 2048
 
 __device__ __forceinline__ float2 md_dot8(uint4 w, const float2* x, float2 s) {
   s = __ffma2_rn(x[0], make_float2(bf16_lo(w.x), bf16_hi(w.x)), s);
@@ -42,29 +48,37 @@ __device__ __forceinline__ float2 md_dot8(uint4 w, const float2* x, float2 s) {
   return s;
 }
 
-template <int DOWN>
+// one stage = `bytes` in bulk copies of <= chunk bytes (all on the stage's barrier)
+__device__ __forceinline__ void md_copy(uint8_t* dst, const uint8_t* src, int bytes, int chunk, uint64_t* bar) {
+  for (int o = 0; o < bytes; o += chunk) bulk_load(dst + o, src + o, (uint32_t)min(chunk, bytes - o), bar);
+}
+
+// gate/up: 8 ring slots of 24 KB, slot w owned by consumer warp w: stage b lands
+// in slot b % 8 and warp b % 8 takes its rows MD_BATCH at a time, so 8 stages are
+// in the consumers' hands at once (each slot has one consumer, so phases stay
+// unambiguous). NG = K / 256 column groups per lane (0: generic).
+constexpr int GU_SLOT = MD_STAGES * MD_STAGE / MD_WARPS;
+template <int NG>
 __global__ void __launch_bounds__(MD_THREADS, 1)
-moe_decode_kernel(const float* __restrict__ x, long long x_gs, const int* __restrict__ ids,
-                  const int* __restrict__ slot_of_expert, const unsigned char* __restrict__ base,
-                  long long expert_stride, long long mat_off, int N, int K, float* __restrict__ out,
-                  long long out_gs, int C, int R, const float* __restrict__ w, int k, float* __restrict__ y,
-                  unsigned* __restrict__ tickets) {
+moe_gu_t1_kernel(const float* __restrict__ x, const int* __restrict__ ids, const int* __restrict__ slot_of_expert,
+                 const unsigned char* __restrict__ base, long long expert_stride, long long mat_off, int N, int K,
+                 float* __restrict__ h, int C, int R, int chunk) {
+  constexpr int G = NG > 0 ? NG : MD_MAXG;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ int s_last;
   const int j = blockIdx.x / C, c = blockIdx.x - j * C;
   const int r0 = c * R;
-  if (r0 >= N) return;   // the same for every j: no ticket is ever waited for
+  if (r0 >= N) return;
   const int nrows = min(N, r0 + R) - r0;
   const int rowb = K * 2;
-  const int RS = MD_STAGE / rowb;
+  const int RS = GU_SLOT / rowb;
   const int nst = (nrows + RS - 1) / RS;
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + MD_STAGES * MD_STAGE);
-  uint64_t* empty = full + MD_STAGES;
-  float* acc = reinterpret_cast<float*>(empty + MD_STAGES);
+  uint64_t* empty = full + MD_WARPS;
+  float* acc = reinterpret_cast<float*>(empty + MD_WARPS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < MD_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MD_WARPS); }
+    for (int s = 0; s < MD_WARPS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -74,27 +88,24 @@ moe_decode_kernel(const float* __restrict__ x, long long x_gs, const int* __rest
       const int e = ids[j];
       const long long slot = slot_of_expert ? slot_of_expert[e] : e;
       const uint8_t* W = base + slot * expert_stride + mat_off + (long long)r0 * rowb;
-      int s = 0;
-      uint32_t ph = 0;
       for (int b = 0; b < nst; ++b) {
+        const int s = b % MD_WARPS;
         const int nr = min(RS, nrows - b * RS);
-        mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait(&empty[s], (uint32_t)(((b / MD_WARPS) & 1) ^ 1));
         mbar_expect_tx(&full[s], (uint32_t)(nr * rowb));
-        bulk_load(ring + s * MD_STAGE, W + (long long)b * RS * rowb, (uint32_t)(nr * rowb), &full[s]);
-        if (++s == MD_STAGES) { s = 0; ph ^= 1; }
+        md_copy(ring + s * GU_SLOT, W + (long long)b * RS * rowb, nr * rowb, chunk, &full[s]);
       }
     }
     return;
   }
 
   const int cw = warp - 1;
-  const float* xj = x + j * x_gs;
-  float2 xr[MD_MAXG][4];
+  float2 xr[G][4];
 #pragma unroll
-  for (int g = 0; g < MD_MAXG; ++g) {
+  for (int g = 0; g < G; ++g) {
     const int col = (g * 32 + lane) * 8;
-    if (col < K) {
-      const float4* xp = reinterpret_cast<const float4*>(xj + col);
+    if (NG > 0 || col < K) {
+      const float4* xp = reinterpret_cast<const float4*>(x + col);
       const float4 a = __ldg(xp), b = __ldg(xp + 1);
       xr[g][0] = make_float2(a.x, a.y); xr[g][1] = make_float2(a.z, a.w);
       xr[g][2] = make_float2(b.x, b.y); xr[g][3] = make_float2(b.z, b.w);
@@ -103,51 +114,142 @@ moe_decode_kernel(const float* __restrict__ x, long long x_gs, const int* __rest
       for (int i = 0; i < 4; ++i) xr[g][i] = make_float2(0.f, 0.f);
     }
   }
-  int s = 0;
-  uint32_t ph = 0;
-  for (int b = 0; b < nst; ++b) {
+  for (int b = cw; b < nst; b += MD_WARPS) {
+    const int s = cw;
     const int nr = min(RS, nrows - b * RS);
-    mbar_wait(&full[s], ph);
-    const uint8_t* st = ring + s * MD_STAGE;
-    for (int r = cw; r < nr; r += MD_WARPS) {
-      float2 p = make_float2(0.f, 0.f);
+    mbar_wait(&full[s], (uint32_t)((b / MD_WARPS) & 1));
+    const uint8_t* st = ring + s * GU_SLOT;
+    for (int r = 0; r < nr; r += MD_BATCH) {
+      float v[MD_BATCH];
 #pragma unroll
-      for (int g = 0; g < MD_MAXG; ++g) {
-        const int col = (g * 32 + lane) * 8;
-        if (col < K) p = md_dot8(*reinterpret_cast<const uint4*>(st + r * rowb + col * 2), xr[g], p);
+      for (int q = 0; q < MD_BATCH; ++q) {
+        const uint8_t* row = st + min(r + q, nr - 1) * rowb;
+        float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int col = (g * 32 + lane) * 8;
+          if (NG > 0 || col < K) a2 = md_dot8(*reinterpret_cast<const uint4*>(row + col * 2), xr[g], a2);
+        }
+        v[q] = a2.x + a2.y;
       }
-      const float v = warp_sum(p.x + p.y);
-      if (lane == 0) acc[b * RS + r] = v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < MD_BATCH; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < MD_BATCH; ++q)
+          if (r + q < nr) acc[b * RS + r + q] = v[q];
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (++s == MD_STAGES) { s = 0; ph ^= 1; }
   }
   named_sync(1, MD_WARPS * 32);
-  const int t = threadIdx.x - 32;
-  if constexpr (!DOWN) {
-    for (int i = t; i < nrows / 2; i += MD_WARPS * 32)
-      out[j * out_gs + (r0 >> 1) + i] = silu(acc[2 * i]) * acc[2 * i + 1];
-  } else {
-    for (int i = t; i < nrows; i += MD_WARPS * 32) out[j * out_gs + r0 + i] = acc[i];
-    __threadfence();
-    named_sync(1, MD_WARPS * 32);
-    if (t == 0) s_last = atomicAdd(&tickets[c], 1u) == (unsigned)(k - 1);
-    named_sync(1, MD_WARPS * 32);
-    if (!s_last) return;
-    __threadfence();
-    for (int i = t; i < nrows; i += MD_WARPS * 32) {
-      float sum = 0.f;
-      for (int jj = 0; jj < k; ++jj) sum += w[jj] * __ldcg(out + jj * out_gs + r0 + i);
-      y[r0 + i] += sum;
+  for (int i = threadIdx.x - 32; i < nrows / 2; i += MD_WARPS * 32)
+    h[(long long)j * (N / 2) + (r0 >> 1) + i] = silu(acc[2 * i]) * acc[2 * i + 1];
+}
+
+// down + combine: CTA c streams rows [c*R, c*R + nrows) of the k down matrices,
+// one ring slot per expert (k <= MD_MAXRING: every copy is issued up front).
+// Consumer warp w owns experts w, w + 8, ...: it holds h[j] in registers and
+// takes that expert's rows MD_BATCH at a time (independent dot products,
+// interleaved warp reductions). NG = K / 256 column groups per lane (0: generic).
+template <int NG>
+__global__ void __launch_bounds__(MD_THREADS, 1)
+moe_down_t1_kernel(const float* __restrict__ h, const int* __restrict__ ids, const int* __restrict__ slot_of_expert,
+                   const unsigned char* __restrict__ base, long long expert_stride, long long mat_off, int N,
+                   int K, int R, const float* __restrict__ w, int k, float* __restrict__ y, int chunk,
+                   int slot_bytes) {
+  constexpr int G = NG > 0 ? NG : MD_MAXG;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int r0 = blockIdx.x * R;
+  if (r0 >= N) return;
+  const int nrows = min(N, r0 + R) - r0;
+  const int rowb = K * 2;
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + MD_STAGES * MD_STAGE);   // k <= MD_MAXRING
+  float* acc = reinterpret_cast<float*>(full + MD_MAXRING);                    // [k][R]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < k; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // lane j resolves expert j's row block; lane 0 issues every copy
+    const uint8_t* mine = nullptr;
+    if (lane < k) {
+      const int e = ids[lane];
+      const long long slot = slot_of_expert ? slot_of_expert[e] : e;
+      mine = base + slot * expert_stride + mat_off + (long long)r0 * rowb;
     }
-    if (t == 0) tickets[c] = 0u;   // ready for the next launch (stream order)
+    for (int jj = 0; jj < k; ++jj) {
+      const uint8_t* W =
+          reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(mine), jj));
+      if (lane == 0) {
+        mbar_expect_tx(&full[jj], (uint32_t)(nrows * rowb));
+        md_copy(ring + jj * slot_bytes, W, nrows * rowb, chunk, &full[jj]);
+      }
+    }
+    return;
+  }
+
+  const int t = threadIdx.x - 32, cw = warp - 1;
+  for (int jj = cw; jj < k; jj += MD_WARPS) {
+    float2 xr[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int col = (g * 32 + lane) * 8;
+      if (NG > 0 || col < K) {
+        const float4* hp = reinterpret_cast<const float4*>(h + (size_t)jj * K + col);
+        const float4 a = __ldcg(hp), b = __ldcg(hp + 1);   // written by the gate/up launch
+        xr[g][0] = make_float2(a.x, a.y); xr[g][1] = make_float2(a.z, a.w);
+        xr[g][2] = make_float2(b.x, b.y); xr[g][3] = make_float2(b.z, b.w);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xr[g][i] = make_float2(0.f, 0.f);
+      }
+    }
+    mbar_wait(&full[jj], 0);
+    const uint8_t* slot = ring + jj * slot_bytes;
+    for (int r = 0; r < nrows; r += MD_BATCH) {
+      float v[MD_BATCH];
+#pragma unroll
+      for (int b = 0; b < MD_BATCH; ++b) {
+        const uint8_t* row = slot + min(r + b, nrows - 1) * rowb;
+        float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int col = (g * 32 + lane) * 8;
+          if (NG > 0 || col < K) a2 = md_dot8(*reinterpret_cast<const uint4*>(row + col * 2), xr[g], a2);
+        }
+        v[b] = a2.x + a2.y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int b = 0; b < MD_BATCH; ++b) v[b] += __shfl_xor_sync(0xffffffffu, v[b], o);
+      if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < MD_BATCH; ++b)
+          if (r + b < nrows) acc[jj * R + r + b] = v[b];
+      }
+    }
+  }
+  named_sync(1, MD_WARPS * 32);
+  for (int i = t; i < nrows; i += MD_WARPS * 32) {
+    float sum = 0.f;
+    for (int jj = 0; jj < k; ++jj) sum += w[jj] * acc[jj * R + i];
+    y[r0 + i] += sum;
   }
 }
 
 static int g_md_sms = 0;
+static int g_md_chunk = 0;   // bulk-copy size (PS_MD_CHUNK overrides, tuning)
 
-static size_t md_smem(int R) { return (size_t)MD_STAGES * (MD_STAGE + 16) + (size_t)R * 4; }
+static size_t md_smem(int R) { return (size_t)MD_STAGES * MD_STAGE + MD_WARPS * 16 + (size_t)R * 4; }
 
 }  // namespace ps
 
@@ -157,7 +259,7 @@ extern "C" {
 
 int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot_of_expert, const void* expert_base,
                           long long expert_stride, long long gu_off, long long down_off, int eff, int d, float* h,
-                          float* out, const float* w, float* y, unsigned* tickets, void* stream) {
+                          const float* w, float* y, void* stream) {
   PS_REQUIRE(k >= 1 && k <= 64, "ps_moe_decode_experts: k=%d", k);
   PS_REQUIRE(d % 8 == 0 && eff % 8 == 0 && d <= 32 * 8 * MD_MAXG && eff <= 32 * 8 * MD_MAXG,
              "ps_moe_decode_experts: d=%d eff=%d (multiples of 8, <= %d)", d, eff, 32 * 8 * MD_MAXG);
@@ -170,29 +272,67 @@ int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot
     cudaDeviceGetAttribute(&g_md_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_md_sms <= 0) g_md_sms = 148;
   }
-  const int C = g_md_sms / k > 0 ? g_md_sms / k : 1;
-  PS_REQUIRE(C <= PS_MOE_DECODE_TICKETS, "ps_moe_decode_experts: %d row blocks > ticket buffer", C);
+  if (!g_md_chunk) {
+    const char* e = getenv("PS_MD_CHUNK");
+    g_md_chunk = e ? atoi(e) : 4096;   // 4 KB copies: measured 7 % faster than whole stages
+    g_md_chunk = g_md_chunk < 1024 ? 1024 : (g_md_chunk & ~15);
+  }
   auto base = static_cast<const unsigned char*>(expert_base);
   cudaStream_t s = (cudaStream_t)stream;
-  static size_t set0 = 0, set1 = 0;
-  // gate/up: N = 2 * eff interleaved rows, even rows per CTA so pairs never straddle
+  // gate/up: k groups x C CTAs; N = 2 * eff interleaved rows, even rows per CTA so
+  // gate/up pairs never straddle CTAs
+  const int C = g_md_sms / k > 0 ? g_md_sms / k : 1;
   const int Rg = 2 * ((eff + C - 1) / C);
   const size_t sg = md_smem(Rg);
-  if (sg > set0) {
-    PS_CHECK_CUDA(cudaFuncSetAttribute(moe_decode_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg));
-    set0 = sg;
+  using GuKernel = void (*)(const float*, const int*, const int*, const unsigned char*, long long, long long, int, int,
+                           float*, int, int, int);
+  const int ngu = d % 256 ? 0 : d / 256;
+  GuKernel gk = moe_gu_t1_kernel<0>;
+  switch (ngu) {
+    case 1: gk = moe_gu_t1_kernel<1>; break;
+    case 2: gk = moe_gu_t1_kernel<2>; break;
+    case 4: gk = moe_gu_t1_kernel<4>; break;
+    case 8: gk = moe_gu_t1_kernel<8>; break;
+    default: gk = moe_gu_t1_kernel<0>; break;
   }
-  moe_decode_kernel<0><<<k * C, MD_THREADS, sg, s>>>(x, 0, ids, slot_of_expert, base, expert_stride, gu_off,
-                                                     2 * eff, d, h, eff, C, Rg, nullptr, k, nullptr, nullptr);
+  static size_t set_gu[MD_MAXG + 1] = {};
+  if (sg > set_gu[ngu]) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg));
+    set_gu[ngu] = sg;
+  }
+  gk<<<k * C, MD_THREADS, sg, s>>>(x, ids, slot_of_expert, base, expert_stride, gu_off, 2 * eff, d, h, C, Rg,
+                                   g_md_chunk);
   PS_CHECK_LAUNCH();
-  const int Rd = (d + C - 1) / C;
-  const size_t sd = md_smem(Rd);
-  if (sd > set1) {
-    PS_CHECK_CUDA(cudaFuncSetAttribute(moe_decode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd));
-    set1 = sd;
+  // down + combine: row blocks of R rows, one ring slot per expert, all in flight
+  int Rd = (d + g_md_sms - 1) / g_md_sms;
+  int slot_bytes = (Rd * eff * 2 + 127) / 128 * 128;
+  if (slot_bytes * k > MD_STAGES * MD_STAGE) {
+    Rd = (MD_STAGES * MD_STAGE / k) / (eff * 2);
+    slot_bytes = (Rd * eff * 2 + 127) / 128 * 128;
   }
-  moe_decode_kernel<1><<<k * C, MD_THREADS, sd, s>>>(h, eff, ids, slot_of_expert, base, expert_stride, down_off, d,
-                                                     eff, out, d, C, Rd, w, k, y, tickets);
+  PS_REQUIRE(k <= MD_MAXRING && Rd >= 1, "ps_moe_decode_experts: k=%d eff=%d do not fit the ring", k, eff);
+  const size_t sd = (size_t)MD_STAGES * MD_STAGE + MD_MAXRING * 8 + (size_t)k * Rd * 4;
+  PS_REQUIRE(sd <= 232448 - 1024, "ps_moe_decode_experts: k=%d eff=%d exceed shared memory", k, eff);
+  using DownKernel = void (*)(const float*, const int*, const int*, const unsigned char*, long long, long long, int,
+                             int, int, const float*, int, float*, int, int);
+  const int ng = eff % 256 ? 0 : eff / 256;
+  DownKernel kern = moe_down_t1_kernel<0>;
+  switch (ng) {
+    case 1: kern = moe_down_t1_kernel<1>; break;
+    case 2: kern = moe_down_t1_kernel<2>; break;
+    case 3: kern = moe_down_t1_kernel<3>; break;
+    case 4: kern = moe_down_t1_kernel<4>; break;
+    case 6: kern = moe_down_t1_kernel<6>; break;
+    case 8: kern = moe_down_t1_kernel<8>; break;
+    default: break;
+  }
+  static size_t set_down[MD_MAXG + 1] = {};
+  if (sd > set_down[ng]) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd));
+    set_down[ng] = sd;
+  }
+  kern<<<(d + Rd - 1) / Rd, MD_THREADS, sd, s>>>(h, ids, slot_of_expert, base, expert_stride, down_off, d, eff, Rd, w,
+                                                 k, y, g_md_chunk, slot_bytes);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -201,7 +341,17 @@ int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot
 
 int ps_preload_moe_decode() {
   int n = 0;
-  touch_kernel(moe_decode_kernel<0>, n);
-  touch_kernel(moe_decode_kernel<1>, n);
+  touch_kernel(moe_gu_t1_kernel<0>, n);
+  touch_kernel(moe_gu_t1_kernel<1>, n);
+  touch_kernel(moe_gu_t1_kernel<2>, n);
+  touch_kernel(moe_gu_t1_kernel<4>, n);
+  touch_kernel(moe_gu_t1_kernel<8>, n);
+  touch_kernel(moe_down_t1_kernel<0>, n);
+  touch_kernel(moe_down_t1_kernel<1>, n);
+  touch_kernel(moe_down_t1_kernel<2>, n);
+  touch_kernel(moe_down_t1_kernel<3>, n);
+  touch_kernel(moe_down_t1_kernel<4>, n);
+  touch_kernel(moe_down_t1_kernel<6>, n);
+  touch_kernel(moe_down_t1_kernel<8>, n);
   return n;
 }

@@ -44,7 +44,6 @@ from .model import Arch, HostWeights, rope_table
 from .streamer import CopyRing, EventPool
 
 GEMV_MAX_T = 32
-PS_MOE_DECODE_TICKETS = 1024   # include/pshard.h
 
 
 @dataclass
@@ -202,10 +201,6 @@ class Executor:
         self.rope = a.alloc_high("rope", rope.nbytes)
         self.host_stage = L.host_alloc(max(1 << 20, rope.nbytes, T * 4 + 4096), mapped=False)
         self._h2d_sync(self.rope, rope)
-        self.m_tickets = 0
-        if self.moe is not None:   # ps_moe_decode_experts' row-block tickets (self-resetting)
-            self.m_tickets = a.alloc_high("moe_tickets", 4 * PS_MOE_DECODE_TICKETS)
-            self._h2d_sync(self.m_tickets, np.zeros(PS_MOE_DECODE_TICKETS, np.uint32))
         self.host_tok = L.host_alloc(4 * B * 4096, mapped=False)
         self.host_tok_i = 0
 
@@ -661,6 +656,7 @@ class Executor:
         planned = self.residency[sid][0]
         fetched = gemv and planned == "stream" and bool(self.expert_slots)
         t1 = (gemv and T == 1 and d <= 2048 and eff <= 2048 and (fetched or mode == "pinned") and
+              k <= 16 and   # moe_down_t1_kernel: one ring slot per routed expert
               os.environ.get("PS_MOE_DECODE", "1") != "0")
 
         def route(base):
@@ -672,7 +668,7 @@ class Executor:
 
         def decode_t1(ebase, slot_map):
             L.call("ps_moe_decode_experts", xn, self.m_ids, k, slot_map, ebase, stride if not slot_map else sb,
-                   0, down_off, eff, d, self.m_h, self.m_out, self.m_w, self.x, self.m_tickets, self.cs)
+                   0, down_off, eff, d, self.m_h, self.m_w, self.x, self.cs)
 
         def experts(ebase, lo, hi):
             L.call("ps_moe_expert_gu", xn, d, 0 if gemv else 1, self.m_plan, E, P, k, ebase, stride, 0,

@@ -374,8 +374,8 @@ def test_moe_pipeline(T, zero_copy, x_bf16):
                                               (8, 2, 512, 1536, False), (128, 8, 2048, 768, False)])
 def test_moe_decode_experts_one_token(E, k, d, eff, mapped):
     """ps_moe_decode_experts (t = 1, no plan, combine fused) against the fp32 MoE
-    block, with and without a fetcher slot map; twice in a row (self-resetting
-    tickets) and bit-identical across runs (fixed-order combine)."""
+    block, with and without a fetcher slot map; bit-identical across runs
+    (fixed-order combine)."""
     import ctypes
     lib = L()
     g = torch.Generator(device="cuda").manual_seed(E + d)
@@ -401,18 +401,15 @@ def test_moe_decode_experts_one_token(E, k, d, eff, mapped):
             smap[e] = sl
         base, slot_map = slots.data_ptr(), smap
     h = torch.zeros(k, eff, device="cuda")
-    out = torch.zeros(k, d, device="cuda")
-    tickets = torch.zeros(1024, dtype=torch.int32, device="cuda")
     y0 = torch.randn(1, d, device="cuda", generator=g)
     ys = []
     for _ in range(2):
         y = y0.clone()
         lib.call("ps_moe_decode_experts", x.data_ptr(), ids.data_ptr(), k,
                  slot_map.data_ptr() if slot_map is not None else None, base, stride, 0, 2 * eff * d * 2,
-                 eff, d, h.data_ptr(), out.data_ptr(), w.data_ptr(), y.data_ptr(), tickets.data_ptr(), s)
+                 eff, d, h.data_ptr(), w.data_ptr(), y.data_ptr(), s)
         torch.cuda.synchronize()
         ys.append(y)
-    assert int(tickets.abs().sum()) == 0
     assert torch.equal(ys[0], ys[1])
     ref, rid, rw = _moe_ref(x, router.float(), Wgu.float(), Wd.float(), k)
     assert torch.equal(ids.view(1, k).long(), rid)
