@@ -25,6 +25,10 @@ ap.add_argument("--skip", type=int, default=3)
 ap.add_argument("--out", default="gpurun_out/cupti.json")
 a = ap.parse_args()
 model, budget, prompt, gen, batch, desc = bench.CONFIGS[a.config]
+if budget is None:   # config 1: 50 % of the plan's weight bytes (bench.py)
+    from paper_2604_26334_b200.planning import catalog
+    from paper_2604_26334_b200.planning.graph import total_model_bytes
+    budget = 0.5 * total_model_bytes(catalog.builtin_model(model))
 eng = Engine(model, budget_bytes=budget, context_len=prompt + gen, batch=batch)
 prompts = [np.random.default_rng(i).integers(0, eng.spec.vocab_size, prompt).astype(np.int32)
            for i in range(batch)]
