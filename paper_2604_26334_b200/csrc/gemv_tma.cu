@@ -41,6 +41,8 @@ template <int T> struct GtShape {
   static constexpr int KC = GT_CONSUMERS * 32 * CPT;
   static constexpr int RS = GT_STAGE_BYTES / (KC * 2);
   static constexpr int V = RS * T;  // partial sums reduced per stage
+  // warp_reduce_scatter halves V each step: a non-power-of-two V would drop values
+  static_assert(RS >= 1 && (V & (V - 1)) == 0, "rows x tokens per stage must be a power of two");
 };
 
 // 8 bf16 weights x 8 fp32 activations, packed fp32x2 FMA (two partial sums).
