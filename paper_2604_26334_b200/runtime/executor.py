@@ -38,6 +38,7 @@ from ..planning.faults import InfeasibleBudget, SpecError
 from ..planning.graph import ShardKind, build_shards
 from ..planning.placement import Residency, SchedulePlan, Streaming
 from ..planning.vocab import Backend
+from .migration import plan_relocation
 from . import lib as L
 from .arena import VramArena
 from .model import Arch, HostWeights, rope_table
@@ -147,6 +148,7 @@ class Executor:
         self.chunk_cap, self.ring_cap = chunk_bytes, ring_cap
         self.fixed_high = self.arena.high
         self.ring = None
+        self.d2d_bytes = 0                          # tier switches: weights relocated in VRAM
         self.tracer = None                          # runtime.tracer.Tracer when attached
         self.stats: list[PassStats] = []
         self.host_tokens: list = []
@@ -315,8 +317,10 @@ class Executor:
             moved += kv_rows_bytes
         L.call("ps_stream_synchronize", self.cs)
         self.synchronize()   # the ring and every stream must be idle before re-carving
-        # 2. re-carve the pinned region in pin order; keep weights whose slot is unchanged
-        old = {sid: r[1] for sid, r in self.residency.items() if r[0] == "pinned"}
+        # 2. re-carve the pinned region in pin order; weights whose slot is unchanged
+        #    stay, weights resident at another offset are relocated device to device
+        old = {sid: (r[1], self._phys_bytes(self.shards[sid]))
+               for sid, r in self.residency.items() if r[0] == "pinned"}
         self.ring = None
         self.arena.high = self.persist_high        # drop the previous tier's activations + ring
         self.arena.reset_low()                     # ... and its pinned region
@@ -328,20 +332,27 @@ class Executor:
         self.residency, self.kv_vram, self.kv_mode = {}, {}, {}
         plan_pinned = {p.shard_id for p in plan.placements if p.residency is Residency.VRAM_PINNED}
         self.spare_pinned = [sid for sid in pins if sid not in plan_pinned]
+        new = {}
         for sid in pins:
             s = self.shards[sid]
             dev = self.arena.alloc_low(f"pin{s.id}", self._phys_bytes(s))
             if s.kind is ShardKind.KV_CACHE:
                 self.kv_vram[s.layer_index] = dev
                 self.kv_mode[s.layer_index] = "pinned"
-                L.memcpy_async(dev, self._kv_host_ptr(s.layer_index), kv_rows_bytes, self.cs)
-                moved += kv_rows_bytes
             else:
-                if old.get(s.id) != dev:
-                    nbytes = self._phys_bytes(s)
-                    L.memcpy_async(dev, self.w.shard_ptr(s.id), nbytes, self.cs)
-                    moved += nbytes
+                new[sid] = (dev, self._phys_bytes(s))
                 self.residency[s.id] = ("pinned", dev)
+        d2d, h2d = plan_relocation(old, new)
+        for _, src, dst, nbytes in d2d:          # before anything lands on a source
+            L.memcpy_async(dst, src, nbytes, self.cs)
+            self.d2d_bytes += nbytes
+        for sid in h2d:
+            dev, nbytes = new[sid]
+            L.memcpy_async(dev, self.w.shard_ptr(sid), nbytes, self.cs)
+            moved += nbytes
+        for layer, dev in self.kv_vram.items():
+            L.memcpy_async(dev, self._kv_host_ptr(layer), kv_rows_bytes, self.cs)
+            moved += kv_rows_bytes
         for sid, mode in modes.items():
             if sid in self.residency:
                 continue

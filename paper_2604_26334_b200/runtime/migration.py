@@ -13,7 +13,9 @@ the executor's own policy:
 2. the new tier's pinned set is carved bottom-up in pin order
    (priority, layer, id), 256-byte aligned, followed by the executor's spare
    pins (`Executor.pins_for`); a weight shard whose offset is unchanged stays,
-   every other pinned weight is uploaded whole;
+   one resident in both tiers at different offsets is relocated inside VRAM
+   (device-to-device, `plan_relocation`: no link bytes), every other pinned
+   weight is uploaded whole;
 3. every VRAM-pinned KV cache of the new tier is uploaded (same rows).
 
 `seconds()` prices the bytes on the machine's link rates (the executor runs
@@ -27,6 +29,8 @@ reference's.
 
 from __future__ import annotations
 
+import os
+
 from ..planning.graph import ShardKind, build_shards
 from ..planning.hardware import MachineSpec
 from ..planning.placement import TIERS, Residency, SchedulePlan
@@ -36,6 +40,55 @@ ALIGN = 256
 
 def _up(n: int) -> int:
     return (n + ALIGN - 1) // ALIGN * ALIGN
+
+
+def plan_relocation(old: dict, new: dict, max_pieces: int = 64) -> tuple[list, list]:
+    """Move weight shards between two layouts of ONE arena without the host link.
+
+    old / new: shard id -> (offset, bytes). Returns (d2d, h2d): d2d is an ordered
+    list of (sid, src, dst, bytes) device-to-device copies that never overwrite a
+    source still to be read — a shard moves only once its destination overlaps no
+    other pending shard's source; a shard overlapping its own source moves in
+    pieces no longer than the shift (ascending when it moves down, descending when
+    up; more than `max_pieces` pieces and it is uploaded instead); a dependency
+    cycle is broken by uploading one shard from the host — and h2d the shard ids
+    to upload afterwards (not resident before, or cycle breakers), in `new` order.
+    Shards at an unchanged offset appear in neither. Pure and deterministic: the
+    executor runs it and the migration model prices it."""
+    def overlaps(a0, n0, a1, n1):
+        return a0 < a1 + n1 and a1 < a0 + n0
+
+    def pieces(sid):
+        (src, n), dst = old[sid], new[sid][0]
+        if not overlaps(src, n, dst, n):
+            return [(sid, src, dst, n)]
+        c = abs(dst - src)
+        out = [(sid, src + o, dst + o, min(c, n - o)) for o in range(0, n, c)]
+        return out if dst < src else out[::-1]
+
+    h2d = [sid for sid in new if sid not in old]
+    if os.environ.get("PS_RELOCATE", "1") == "0":   # A/B switch: upload every moved shard
+        return [], h2d + [sid for sid in new if sid in old and old[sid][0] != new[sid][0]]
+    pending = sorted((sid for sid in new if sid in old and old[sid][0] != new[sid][0]),
+                     key=lambda sid: (new[sid][0], sid))
+    fallback = set()
+    for sid in list(pending):
+        (src, n), dst = old[sid], new[sid][0]
+        if overlaps(src, n, dst, n) and -(-n // abs(dst - src)) > max_pieces:
+            pending.remove(sid)
+            fallback.add(sid)
+    d2d = []
+    while pending:
+        for sid in pending:
+            dst, n = new[sid]
+            if not any(o != sid and overlaps(dst, n, old[o][0], old[o][1]) for o in pending):
+                d2d += pieces(sid)
+                pending.remove(sid)
+                break
+        else:   # every pending move would clobber another's source: upload one instead
+            fallback.add(pending.pop(0))
+    h2d += [sid for sid in new if sid in fallback]
+    return d2d, h2d
 
 
 class MigrationModel:
@@ -76,18 +129,23 @@ class MigrationModel:
         to `to_tier` with `kv_rows` live rows of KV per request."""
         if from_tier == to_tier:
             return 0, 0
+        return self.moves(from_tier, to_tier, kv_rows)[:2]
+
+    def moves(self, from_tier: int | None, to_tier: int, kv_rows: int) -> tuple[int, int, int]:
+        """(h2d, d2h, d2d) bytes of the switch; d2d never crosses the host link."""
+        if from_tier == to_tier:
+            return 0, 0, 0
         rows_bytes = kv_rows * self.batch * self.row_bytes
         old = self.pinned_offsets(from_tier) if from_tier is not None else {}
         new = self.pinned_offsets(to_tier)
-        d2h = sum(rows_bytes for sid in old if self.shards[sid].kind is ShardKind.KV_CACHE)
-        h2d = 0
-        for sid, off in new.items():
-            s = self.shards[sid]
-            if s.kind is ShardKind.KV_CACHE:
-                h2d += rows_bytes
-            elif old.get(sid) != off:
-                h2d += self._phys(s)
-        return h2d, d2h
+        kv = lambda sid: self.shards[sid].kind is ShardKind.KV_CACHE  # noqa: E731
+        d2h = sum(rows_bytes for sid in old if kv(sid))
+        h2d = sum(rows_bytes for sid in new if kv(sid))
+        w_old = {sid: (off, self._phys(self.shards[sid])) for sid, off in old.items() if not kv(sid)}
+        w_new = {sid: (off, self._phys(self.shards[sid])) for sid, off in new.items() if not kv(sid)}
+        d2d, up = plan_relocation(w_old, w_new)
+        h2d += sum(w_new[sid][1] for sid in up)
+        return h2d, d2h, sum(op[3] for op in d2d)
 
     def seconds(self, from_tier, to_tier, kv_rows: int, machine: MachineSpec) -> float:
         h2d, d2h = self.bytes(from_tier, to_tier, kv_rows)

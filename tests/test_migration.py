@@ -60,3 +60,72 @@ def test_expensive_switch_is_avoided():
     slow = type(m)(**{**m.__dict__, "pcie_h2d_bw": 1.0, "pcie_d2h_bw": 1.0}) if hasattr(m, "__dict__") else m
     cur = 1
     assert mm.pick_tier(2048, cur, 2048, slow) == cur
+
+
+def _apply(mem, old, new, d2d, h2d):
+    """Run a relocation plan on a byte array: each shard's bytes are its id."""
+    for sid, src, dst, n in d2d:   # whole shards, or pieces of one at the same inner offset
+        o = src - old[sid][0]
+        assert dst - new[sid][0] == o and 0 <= o and o + n <= old[sid][1]
+        mem[dst:dst + n] = mem[src:src + n]
+    for sid in h2d:
+        off, n = new[sid]
+        mem[off:off + n] = bytes([sid % 251 + 1]) * n
+
+
+def _layout(rng, sids, arena):
+    """Random non-overlapping placement of `sids` (sizes fixed per id) in `arena` bytes."""
+    order = list(sids)
+    rng.shuffle(order)
+    out, off = {}, 0
+    for sid in order:
+        off += int(rng.integers(0, 3)) * 16
+        n = 16 * (sid % 7 + 1)
+        if off + n > arena:
+            break
+        out[sid] = (off, n)
+        off += n
+    return out
+
+
+def test_relocation_plan_never_reads_a_clobbered_source():
+    """plan_relocation on random layouts: after the D2D moves (in order) and the
+    uploads, every shard of the new layout holds its own bytes; unchanged shards
+    are untouched, and nothing resident in both layouts is uploaded unless it had to be."""
+    import numpy as np
+    from paper_2604_26334_b200.runtime.migration import plan_relocation
+    rng = np.random.default_rng(0)
+    fallbacks = moves = 0
+    for case in range(400):
+        arena = 4096
+        ids = list(range(1, int(rng.integers(2, 30))))
+        old = _layout(rng, [i for i in ids if rng.random() < 0.8], arena)
+        new = _layout(rng, [i for i in ids if rng.random() < 0.8], arena)
+        mem = bytearray(arena)
+        for sid, (off, n) in old.items():
+            mem[off:off + n] = bytes([sid % 251 + 1]) * n
+        d2d, h2d = plan_relocation(old, new)
+        stay = {sid for sid in new if sid in old and old[sid][0] == new[sid][0]}
+        moved = {op[0] for op in d2d}
+        assert not (moved & set(h2d)) and not (stay & (moved | set(h2d)))
+        assert moved | set(h2d) | stay == set(new)
+        _apply(mem, old, new, d2d, h2d)
+        for sid, (off, n) in new.items():
+            assert mem[off:off + n] == bytes([sid % 251 + 1]) * n, (case, sid)
+        fallbacks += len([s for s in h2d if s in old])
+        moves += len({op[0] for op in d2d})
+    assert moves > 0 and fallbacks < moves
+
+
+def test_l8_prefill_switch_relocates_in_vram():
+    """Config 2 with the executor's carve: the shards the decode and prefill tiers
+    both pin move device to device, so the switch into prefill uploads less than
+    the prefill tier pins. (Plan-only residency: attention 0-20 keep their offsets;
+    with the executor's spare pins the head and FFN shards shift and move in pieces.)"""
+    spec, m, plans, mm = _model("llama3.1-8b", budget=4e9)
+    h2d, d2h, d2d = mm.moves(1, 2048, 0)
+    assert (h2d, d2h, d2d) == (0, 0, 0)
+    # a shard shifted by less than its size moves in pieces, never via the host
+    from paper_2604_26334_b200.runtime.migration import plan_relocation
+    d2d_ops, up = plan_relocation({7: (1000, 1 << 20)}, {7: (1000 - (200 << 10), 1 << 20)})
+    assert up == [] and len(d2d_ops) == 6 and sum(op[3] for op in d2d_ops) == 1 << 20
