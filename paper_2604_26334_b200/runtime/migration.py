@@ -51,7 +51,7 @@ def plan_relocation(old: dict, new: dict, max_pieces: int = 64) -> tuple[list, l
     other pending shard's source; a shard overlapping its own source moves in
     pieces no longer than the shift (ascending when it moves down, descending when
     up; more than `max_pieces` pieces and it is uploaded instead); a dependency
-    cycle is broken by uploading one shard from the host — and h2d the shard ids
+    cycle is broken by uploading its smallest shard from the host — and h2d the shard ids
     to upload afterwards (not resident before, or cycle breakers), in `new` order.
     Shards at an unchanged offset appear in neither. Pure and deterministic: the
     executor runs it and the migration model prices it."""
@@ -85,8 +85,10 @@ def plan_relocation(old: dict, new: dict, max_pieces: int = 64) -> tuple[list, l
                 d2d += pieces(sid)
                 pending.remove(sid)
                 break
-        else:   # every pending move would clobber another's source: upload one instead
-            fallback.add(pending.pop(0))
+        else:   # every pending move would clobber another's source: upload the smallest
+            victim = min(pending, key=lambda sid: (new[sid][1], new[sid][0], sid))
+            pending.remove(victim)
+            fallback.add(victim)
     h2d += [sid for sid in new if sid in fallback]
     return d2d, h2d
 
