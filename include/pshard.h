@@ -137,6 +137,14 @@ int ps_attn_prefill_tc(const float* q, int ldq, int batch, const int* q_start, c
  * ((role << 24) | (barrier << 16) | key block); reset clears it. */
 int ps_attn_tc_watchdog(unsigned* code, int reset);
 
+/* Programmatic dependent launch for the decode-pass kernels (rmsnorm, qkv/RoPE,
+ * decode attention + merge, GEMVs, embed, argmax, add, small uploads): while on,
+ * each is launched with cudaLaunchAttributeProgrammaticStreamSerialization and
+ * waits (griddepcontrol.wait) for the previous kernel inside, so launch gaps
+ * overlap. Only valid while no copy or other stream produces a kernel's inputs
+ * (the executor enables it for passes over fully resident weights). Default off. */
+int ps_set_pdl(int on);
+
 /* ---- K5: MoE router + routed experts ------------------------------------------
  * Replace MOE_ROUTE (t, d, E) and the expert MATMUL (t*k, d, mats*eff) of
  * `pkg/src/shardplan/model_graph.py:181-200`. Everything stays on the device:

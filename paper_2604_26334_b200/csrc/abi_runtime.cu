@@ -65,6 +65,8 @@ extern "C" int ps_preload_fetcher();
 int ps_preload_striper();
 int ps_preload_attention_tc();
 
+namespace ps { int g_pdl = 0; }
+
 extern "C" {
 
 int ps_preload_kernels(int* n_loaded) {
@@ -164,6 +166,11 @@ int ps_stream_create(int high_priority, void** out) {
 
 int ps_stream_destroy(void* stream) {
   if (stream) PS_CHECK_CUDA(cudaStreamDestroy((cudaStream_t)stream));
+  return PS_OK;
+}
+
+int ps_set_pdl(int on) {
+  ps::g_pdl = on ? 1 : 0;
   return PS_OK;
 }
 

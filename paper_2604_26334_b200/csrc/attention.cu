@@ -32,6 +32,8 @@ attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __
                    long long kv_req_stride, long long kv_row_stride, const int* __restrict__ req_slot, const int* __restrict__ lens, int n_kv, int chunk, float scale,
                    float* __restrict__ out, int ldo, float* __restrict__ ws_o, float* __restrict__ ws_ml,
                    int n_splits) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int PER = HD / 32;
   __shared__ __align__(16) float qs[G][HD];
   __shared__ float red_ml[4][G][2];
@@ -168,6 +170,8 @@ attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __
 template <int HD>
 __global__ void attn_decode_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_ml,
                                          int n_heads, int n_splits, float* __restrict__ out, int ldo) {
+  pdl_trigger();
+  pdl_wait();
   int b = blockIdx.y, h = blockIdx.x, d = threadIdx.x;
   long long base = ((long long)b * n_heads + h) * n_splits;
   float M = -INFINITY;
@@ -370,8 +374,8 @@ static int decode_dispatch(int G, dim3 grid, cudaStream_t s, const float* q, int
                            long long req_stride, long long stride, const int* req_slot, const int* lens, int n_kv, int chunk, float scale, float* out, int ldo,
                            float* ws_o, float* ws_ml, int n_splits) {
 #define PS_DEC(GG)                                                                                       \
-  attn_decode_kernel<HD, GG><<<grid, 128, 0, s>>>(q, ldq, base, req_stride, stride, req_slot, lens, n_kv, chunk, scale, out, ldo, \
-                                                  ws_o, ws_ml, n_splits)
+  launch_k(attn_decode_kernel<HD, GG>, grid, 128, 0, s, q, ldq, base, req_stride, stride, req_slot, lens, n_kv, chunk, \
+           scale, out, ldo, ws_o, ws_ml, n_splits)
   switch (G) {
     case 1: PS_DEC(1); break;
     case 2: PS_DEC(2); break;
@@ -415,8 +419,10 @@ extern "C" int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, i
   else if (head_dim == 64) rc = decode_dispatch<64>(G, grid, s, q, ldq, base, kv_req_stride, kv_row_stride, req_slot, lens, n_kv, chunk, scale, out, ldo, ws_o, ws_ml, n_splits);
   else { ps_set_error("ps_attn_decode: head_dim %d unsupported", head_dim); return PS_ERR_UNSUPPORTED; }
   if (rc || n_splits == 1) return rc;
-  if (head_dim == 128) attn_decode_merge_kernel<128><<<dim3(n_heads, batch), 128, 0, s>>>(ws_o, ws_ml, n_heads, n_splits, out, ldo);
-  else attn_decode_merge_kernel<64><<<dim3(n_heads, batch), 64, 0, s>>>(ws_o, ws_ml, n_heads, n_splits, out, ldo);
+  if (head_dim == 128)
+    launch_k(attn_decode_merge_kernel<128>, dim3(n_heads, batch), 128, 0, s, ws_o, ws_ml, n_heads, n_splits, out, ldo);
+  else
+    launch_k(attn_decode_merge_kernel<64>, dim3(n_heads, batch), 64, 0, s, ws_o, ws_ml, n_heads, n_splits, out, ldo);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

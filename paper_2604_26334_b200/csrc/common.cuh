@@ -83,6 +83,35 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // device (ps_wait_flag) would stall the load until the spin ends — so the executor
 // preloads everything before its first pass.
 namespace ps {
+// ---- programmatic dependent launch (PDL) ---------------------------------------
+// Passes whose weights are all VRAM-resident (no ring copies, no fetcher) are
+// chains of small dependent kernels; with PDL the next kernel is launched while
+// the previous one runs and blocks in griddepcontrol.wait until it completed, so
+// the ~2 us launch gap between them disappears (the bulk-copy GEMV additionally
+// starts streaming its weights before the wait). Kernels launched through
+// launch_k() call pdl_trigger() first and pdl_wait() before touching any buffer
+// an earlier kernel writes or reads; both are no-ops for a normal launch.
+extern int g_pdl;   // ps_set_pdl(): launch_k() adds the PDL attribute while set
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <typename F>
 inline void touch_kernel(F* f, int& n) {
   cudaFuncAttributes a;

@@ -36,6 +36,8 @@ template <bool OUT_BF16>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ rows,
                                const __nv_bfloat16* __restrict__ w, int d, float eps,
                                void* __restrict__ out, int ldo) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   int r = blockIdx.x;
   int src = rows ? rows[r] : r;
@@ -62,6 +64,8 @@ __global__ void qkv_post_kernel(float* __restrict__ qkv, int ldq, int n_heads, i
                                 const float2* __restrict__ rope,  // [ctx][HD/2] (cos, sin)
                                 const __nv_bfloat16* __restrict__ q_norm,
                                 const __nv_bfloat16* __restrict__ k_norm, float eps) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int PER = HD / 32;
   constexpr int HALF = HD / 2;
   int tok = blockIdx.x;
@@ -113,6 +117,8 @@ __global__ void qkv_post_kernel(float* __restrict__ qkv, int ldq, int n_heads, i
 // ---- embedding gather (table may be host-mapped: zero-copy) ----
 __global__ void embed_kernel(const __nv_bfloat16* __restrict__ table, const int* __restrict__ ids,
                              int d, float* __restrict__ out, int ldo) {
+  pdl_trigger();
+  pdl_wait();
   int r = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + (long long)ids[r] * d);
   float* o = out + (long long)r * ldo;
@@ -127,6 +133,8 @@ __global__ void embed_kernel(const __nv_bfloat16* __restrict__ table, const int*
 
 // ---- greedy argmax per row; ties -> lowest index (torch.argmax semantics) ----
 __global__ void argmax_kernel(const float* __restrict__ logits, int V, int ldl, int* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sv[32];
   __shared__ int si[32];
   const float* row = logits + (long long)blockIdx.x * ldl;
@@ -165,6 +173,8 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ src, int lds, __n
 }
 
 __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, long long n) {
+  pdl_trigger();
+  pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     dst[i] += src[i];
@@ -192,11 +202,11 @@ int ps_rmsnorm(const float* x, int ldx, const int* rows, int n_rows, const void*
   if (n_rows <= 0) return PS_OK;
   int threads = d >= 1024 ? 1024 : ((d + 31) / 32) * 32;
   if (out_bf16)
-    rmsnorm_kernel<true><<<n_rows, threads, 0, (cudaStream_t)stream>>>(
-        x, ldx, rows, static_cast<const __nv_bfloat16*>(w), d, eps, out, ldo);
+    launch_k(rmsnorm_kernel<true>, n_rows, threads, 0, (cudaStream_t)stream,
+             x, ldx, rows, static_cast<const __nv_bfloat16*>(w), d, eps, out, ldo);
   else
-    rmsnorm_kernel<false><<<n_rows, threads, 0, (cudaStream_t)stream>>>(
-        x, ldx, rows, static_cast<const __nv_bfloat16*>(w), d, eps, out, ldo);
+    launch_k(rmsnorm_kernel<false>, n_rows, threads, 0, (cudaStream_t)stream,
+             x, ldx, rows, static_cast<const __nv_bfloat16*>(w), d, eps, out, ldo);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -216,12 +226,12 @@ int ps_qkv_rope_append(float* qkv, int ldq, int t, int n_heads, int n_kv, int he
   cudaStream_t s = (cudaStream_t)stream;
   switch (head_dim) {
     case 64:
-      qkv_post_kernel<64><<<grid, warps * 32, 0, s>>>(qkv, ldq, n_heads, n_kv, pos, req, base,
-                                                      kv_req_stride, kv_row_stride, cs, qn, kn, eps);
+      launch_k(qkv_post_kernel<64>, grid, warps * 32, 0, s, qkv, ldq, n_heads, n_kv, pos, req, base,
+               kv_req_stride, kv_row_stride, cs, qn, kn, eps);
       break;
     case 128:
-      qkv_post_kernel<128><<<grid, warps * 32, 0, s>>>(qkv, ldq, n_heads, n_kv, pos, req, base,
-                                                       kv_req_stride, kv_row_stride, cs, qn, kn, eps);
+      launch_k(qkv_post_kernel<128>, grid, warps * 32, 0, s, qkv, ldq, n_heads, n_kv, pos, req, base,
+               kv_req_stride, kv_row_stride, cs, qn, kn, eps);
       break;
     default:
       ps_set_error("ps_qkv_rope_append: head_dim %d unsupported (64, 128)", head_dim);
@@ -235,15 +245,15 @@ int ps_embed_gather(const void* table, const int* ids, int n, int d, float* out,
                     void* stream) {
   PS_REQUIRE(d % 8 == 0, "ps_embed_gather: d must be a multiple of 8");
   if (n <= 0) return PS_OK;
-  embed_kernel<<<n, 128, 0, (cudaStream_t)stream>>>(static_cast<const __nv_bfloat16*>(table),
-                                                    ids, d, out, ldo);
+  launch_k(embed_kernel, n, 128, 0, (cudaStream_t)stream, static_cast<const __nv_bfloat16*>(table), ids, d,
+           out, ldo);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
 
 int ps_argmax(const float* logits, int rows, int V, int ldl, int* out, void* stream) {
   if (rows <= 0) return PS_OK;
-  argmax_kernel<<<rows, 1024, 0, (cudaStream_t)stream>>>(logits, V, ldl, out);
+  launch_k(argmax_kernel, rows, 1024, 0, (cudaStream_t)stream, logits, V, ldl, out);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -264,7 +274,7 @@ int ps_add_f32(float* dst, const float* src, long long n, void* stream) {
   if (n <= 0) return PS_OK;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  add_f32_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(dst, src, n);
+  launch_k(add_f32_kernel, blocks, 256, 0, (cudaStream_t)stream, dst, src, n);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -307,6 +317,8 @@ extern "C" int ps_init_interleaved_bf16(void* dst, long long rows_each, long lon
 namespace ps {
 struct SmallBlob { unsigned char b[4000]; };
 __global__ void upload_small_kernel(unsigned char* dst, SmallBlob blob, int n) {
+  pdl_trigger();
+  pdl_wait();
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = blob.b[i];
 }
 }  // namespace ps
@@ -319,7 +331,8 @@ extern "C" int ps_upload_small(void* dst, const void* src, int nbytes, void* str
   if (nbytes == 0) return PS_OK;
   ps::SmallBlob blob;
   memcpy(blob.b, src, nbytes);
-  ps::upload_small_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(static_cast<unsigned char*>(dst), blob, nbytes);
+  ps::launch_k(ps::upload_small_kernel, 1, 256, 0, (cudaStream_t)stream, static_cast<unsigned char*>(dst), blob,
+               nbytes);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

@@ -28,6 +28,8 @@ template <int T, int ROWS, int KSPLIT, int EPI>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
 gemv_bf16_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W,
                  int N, int K, long long ldw, int kpart, float* __restrict__ y, int ldy) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int GROUPS = GEMV_WARPS / KSPLIT;
   constexpr int UNROLL = (T == 1) ? 8 : (T <= 4 ? 4 : 2);   // 16-byte loads in flight per row
   constexpr int STEP = 256;  // 32 lanes x 8 bf16
@@ -163,7 +165,8 @@ static void launch4(int n_tiles, int grid_cap, cudaStream_t s, const float* x, i
   }
   int cap = grid_cap > 0 ? grid_cap : per_sm * sm_count();
   dim3 grid(n_tiles < cap ? n_tiles : cap);
-  gemv_bf16_kernel<T, ROWS, KSPLIT, EPI><<<grid, GEMV_WARPS * 32, 0, s>>>(x, ldx, tt, W, N, K, ldw, kpart, y, ldy);
+  launch_k(gemv_bf16_kernel<T, ROWS, KSPLIT, EPI>, grid, GEMV_WARPS * 32, 0, s, x, ldx, tt, W, N, K, ldw, kpart, y,
+           ldy);
 }
 
 template <int T, int ROWS, int KSPLIT>

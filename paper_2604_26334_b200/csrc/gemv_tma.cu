@@ -89,6 +89,7 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
   // each other inside the K loop; the 8 partials are summed once, in the epilogue
   float* acc = reinterpret_cast<float*>(empty + stages);
 
+  pdl_trigger();
   const int r0 = blockIdx.x * rows_per_cta;
   if (r0 >= N) return;  // whole CTA, before any barrier
   const int r1 = min(N, r0 + rows_per_cta);
@@ -126,6 +127,9 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
     return;
   }
 
+  // weights are never written inside a pass (the producer may stream them before
+  // the previous kernel finished); x and y are: consumers wait for it (PDL)
+  pdl_wait();
   const int j = threadIdx.x - 32;  // consumer thread 0..255
   const int cw = warp - 1;
   // value index this lane holds after the reduce-scatter, and whether it writes it
@@ -253,7 +257,7 @@ static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, i
     PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  gemv_tma_kernel<T, EPI><<<grid, GT_THREADS, smem, s>>>(x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta, stages);
+  launch_k(gemv_tma_kernel<T, EPI>, grid, GT_THREADS, smem, s, x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta, stages);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

@@ -866,7 +866,27 @@ class Executor:
             self._h2d_sync(dst, arr)
 
     # ----------------------------------------------------------------- the pass
+    def _pdl_ok(self, T: int) -> bool:
+        """Programmatic dependent launch for this pass (csrc/common.cuh): only when every
+        weight it reads is VRAM-resident or host-mapped (no ring copies, no fetched
+        experts, no stripes), so the only producers of a kernel's inputs are earlier
+        kernels on the compute stream."""
+        return (T <= GEMV_MAX_T and os.environ.get("PS_PDL", "1") != "0" and self.striper is None and
+                not self.expert_slots and
+                all(m != "stream" for m, _ in self.residency.values()) and
+                all(m != "stream" for m in self.kv_mode.values()))
+
     def run_pass(self, ps: PassSpec) -> PassStats:
+        pdl = self._pdl_ok(ps.T)
+        if pdl:
+            L.call("ps_set_pdl", 1)
+        try:
+            return self._run_pass(ps)
+        finally:
+            if pdl:
+                L.call("ps_set_pdl", 0)
+
+    def _run_pass(self, ps: PassSpec) -> PassStats:
         T = ps.T
         if T > self.T_tier:
             raise SpecError(f"pass of {T} tokens exceeds the tier's {self.T_tier}-token buffers")

@@ -82,6 +82,7 @@ _SIGS = {
     "ps_stripe_stop": [_p],
     "ps_stripe_ready": [_p, C.POINTER(_i)],
     "ps_moe_combine": [_p, _p, _i, _i, _p, _i, _i, _i, _p, _i, _p],
+    "ps_set_pdl": [_i],
     "ps_moe_decode_experts": [_p, _p, _i, _p, _p, _ll, _ll, _ll, _i, _i, _p, _p, _p, _p],
     "ps_embed_gather": [_p, _p, _i, _i, _p, _i, _p],
     "ps_argmax": [_p, _i, _i, _i, _p, _p],

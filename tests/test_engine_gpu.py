@@ -64,6 +64,28 @@ def test_tiny_gemv_path_greedy_exact(tiny, oracle, frac):
     assert np.array_equal(res.tokens[0], want), (frac, kinds, res.tokens[0], want)
 
 
+@pytest.mark.parametrize("frac", [0.5, 1.5])
+def test_pdl_passes_bit_identical(tiny, monkeypatch, frac):
+    """Decode passes over resident weights run with programmatic dependent launch
+    (csrc/common.cuh launch_k); the tokens and the last pass's logits are
+    bit-identical to plain stream-ordered launches (PS_PDL=0)."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    prompt = _prompt(20, tiny.vocab_size, seed=11)
+    out = {}
+    for pdl in ("1", "0"):
+        monkeypatch.setenv("PS_PDL", pdl)
+        eng = Engine(tiny, budget_bytes=frac * total_model_bytes(tiny), context_len=160)
+        res = eng.generate([prompt], gen_len=24)
+        ex = eng.executor
+        used = ex._pdl_ok(1)
+        logits = ex.logits_host(1).copy()
+        eng.close()
+        out[pdl] = (res.tokens[0], logits, used)
+    assert out["1"][2] and not out["0"][2]
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+
+
 @pytest.mark.parametrize("frac", [0.5, 0.25, 1.5])
 def test_tiny_config1_teacher_forced(tiny, oracle, frac):
     """BASELINE config 1 (prompt 128 + 32): the prompt pass runs the tcgen05
