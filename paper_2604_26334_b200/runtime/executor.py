@@ -871,8 +871,11 @@ class Executor:
         weight it reads is VRAM-resident or host-mapped (no ring copies, no fetched
         experts, no stripes), so the only producers of a kernel's inputs are earlier
         kernels on the compute stream."""
-        return (T <= GEMV_MAX_T and os.environ.get("PS_PDL", "1") != "0" and self.striper is None and
-                not self.expert_slots and
+        if T > GEMV_MAX_T or os.environ.get("PS_PDL", "1") == "0" or self.striper is not None:
+            return False
+        if os.environ.get("PS_PDL_STREAMED", "0") == "1":   # experiment: ring + fetcher passes too
+            return True
+        return (not self.expert_slots and
                 all(m != "stream" for m, _ in self.residency.values()) and
                 all(m != "stream" for m in self.kv_mode.values()))
 
