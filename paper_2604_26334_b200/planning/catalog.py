@@ -18,7 +18,7 @@ from __future__ import annotations
 from .graph import ModelSpec, model_from_dict
 from .hardware import MachineSpec, machine_from_dict
 
-__all__ = ["list_presets", "list_b200_presets", "builtin_model", "builtin_machine",
+__all__ = ["list_presets", "list_b200_presets", "builtin_model", "builtin_machine", "striped_machine",
            "builtin_vision", "model_doc", "machine_doc"]
 
 _KINDS = ("models", "machines", "vision")
@@ -136,6 +136,23 @@ def builtin_model(name: str) -> ModelSpec:
 
 def builtin_machine(name: str) -> MachineSpec:
     return machine_from_dict(machine_doc(name))
+
+
+def striped_machine(machine: MachineSpec, links: int) -> MachineSpec:
+    """The link model of NVLink-striped streaming: `links`
+    GPUs each pull 1/links of every streamed piece over their own PCIe link into
+    the executing GPU, so host -> device bytes move at `links` x the per-GPU rate
+    (`pkg/src/shardplan/machine.py:99-101` prices one link). Device -> host (KV
+    write-back) stays on the executing GPU's link. links = 1 returns `machine`
+    itself, so unstriped plans are the reference's bit for bit. The copy keeps the
+    MachineSpec schema (no new field), so save/load round trips are unchanged."""
+    if links < 1:
+        raise ValueError(f"links must be >= 1, got {links}")
+    if links == 1:
+        return machine
+    import dataclasses
+    return dataclasses.replace(machine, name=f"{machine.name}-x{links}",
+                               pcie_h2d_bw=machine.pcie_h2d_bw * links)
 
 
 def builtin_vision(name: str):

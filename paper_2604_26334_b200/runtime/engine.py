@@ -68,6 +68,8 @@ class Engine:
         self.machine: MachineSpec = (catalog.builtin_machine(machine) if isinstance(machine, str)
                                      else machine)
         self.db: ProfileDb = load_profile(profile) if profile else synth_profile(self.machine)
+        if striper is not None:   # N links feed this GPU: plan with the striped link model
+            self.machine = catalog.striped_machine(self.machine, striper.n_helpers + 1)
         self.budget = float(budget_bytes)
         self.context_len = int(context_len)
         self.batch = int(batch)

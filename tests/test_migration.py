@@ -129,3 +129,26 @@ def test_l8_prefill_switch_relocates_in_vram():
     from paper_2604_26334_b200.runtime.migration import plan_relocation
     d2d_ops, up = plan_relocation({7: (1000, 1 << 20)}, {7: (1000 - (200 << 10), 1 << 20)})
     assert up == [] and len(d2d_ops) == 6 and sum(op[3] for op in d2d_ops) == 1 << 20
+
+
+def test_striped_link_model():
+    """SURVEY §8f row 1's link model: N striping GPUs multiply the host -> device
+    rate; one link is the reference machine itself (plans bit-identical), more
+    links keep the placements (budget-driven) and shrink the link-bound estimates."""
+    from paper_2604_26334_b200.planning.costdb import synth_profile
+    from paper_2604_26334_b200.planning.hardware import machine_to_dict
+    spec = catalog.builtin_model("llama3.1-8b")
+    m = catalog.builtin_machine("b200")
+    assert catalog.striped_machine(m, 1) is m
+    m4 = catalog.striped_machine(m, 4)
+    assert m4.pcie_h2d_bw == 4 * m.pcie_h2d_bw and m4.pcie_d2h_bw == m.pcie_d2h_bw
+    assert set(machine_to_dict(m4)) == set(machine_to_dict(m))      # schema unchanged
+    db = synth_profile(m)
+    p1 = reachable_tiers(spec, m, db, 4e9, 2304, 1)
+    p4 = reachable_tiers(spec, m4, db, 4e9, 2304, 1)
+    for t in (1, 2048):
+        key = lambda p: [(x.shard_id, x.residency, x.streaming) for x in p.placements]  # noqa: E731
+        assert key(p1[t]) == key(p4[t])
+        assert p4[t].estimated_time < 0.35 * p1[t].estimated_time   # prefill adds compute + D2H
+    with pytest.raises(ValueError):
+        catalog.striped_machine(m, 0)
