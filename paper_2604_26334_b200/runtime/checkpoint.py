@@ -121,6 +121,14 @@ class Checkpoint:
         return bf16_bits(src).reshape(shape)
 
 
+def open_checkpoint(path: str | os.PathLike):
+    """A `.gguf` file (runtime/gguf.py) or a safetensors directory / file."""
+    if str(path).endswith(".gguf"):
+        from .gguf import GgufCheckpoint
+        return GgufCheckpoint(path)
+    return Checkpoint(path)
+
+
 # -- config.json -> (ModelSpec, Arch) -----------------------------------------------
 
 def spec_from_hf_config(cfg: dict, name: str | None = None, max_context: int | None = None,

@@ -55,13 +55,13 @@ class Engine:
                  checkpoint: str | None = None, shared_weights: str | None = None,
                  migration_aware: bool = False, striper=None):
         """`model`: preset name or ModelSpec (random-init weights), or None with
-        `checkpoint` = a directory holding config.json + safetensors (real weights,
-        runtime/checkpoint.py). `shared_weights`: a /dev/shm segment name shared by
+        `checkpoint` = a directory holding config.json + safetensors, or a .gguf file
+        (real weights, runtime/checkpoint.py, runtime/gguf.py). `shared_weights`: a /dev/shm segment name shared by
         the replicas of one node (one host copy of the weights per node)."""
         ckpt = None
         if checkpoint is not None:
-            from .checkpoint import Checkpoint, spec_from_hf_config
-            ckpt = Checkpoint(checkpoint)
+            from .checkpoint import open_checkpoint, spec_from_hf_config
+            ckpt = open_checkpoint(checkpoint)
             if model is None:
                 model, ck_arch = spec_from_hf_config(ckpt.config, seed=seed)
         self.spec: ModelSpec = catalog.builtin_model(model) if isinstance(model, str) else model

@@ -377,6 +377,11 @@ class HostWeights:
         from .checkpoint import export_safetensors
         return export_safetensors(self.layout, self.blob_bytes(), self.embed_bytes(), out_dir)
 
+    def export_gguf(self, path: str) -> int:
+        """Write the blob as a GGUF v3 file (llama.cpp conventions, runtime/gguf.py)."""
+        from .gguf import write_gguf
+        return write_gguf(path, self.layout, self.blob_bytes(), self.embed_bytes(), self.arch)
+
     def embed_view(self) -> np.ndarray:
         n = self.spec.vocab_size * self.spec.d_model
         buf = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint16 * n).from_address(self.embed))

@@ -189,3 +189,72 @@ def test_rejects_bad_files(tmp_path):
         ck.Checkpoint(tmp_path / "x.safetensors")
     with pytest.raises(Exception):
         ck.spec_from_hf_config(dict(LLAMA31_8B, rope_scaling={"rope_type": "yarn", "factor": 4.0}))
+
+
+# -- GGUF (runtime/gguf.py) ---------------------------------------------------------
+
+def test_gguf_rope_permutation_is_llama_cpp_order():
+    """llama.cpp stores each llama q/k head with rotary pairs adjacent: HF rows
+    (0, 1, 2, 3) of a 4-dim head are stored as (0, 2, 1, 3); unpermute inverts it."""
+    from paper_2604_26334_b200.runtime import gguf
+    w = np.arange(8, dtype=np.uint16).reshape(8, 1)          # 2 heads x hd 4
+    p = gguf.permute_rope_rows(w, 2)
+    assert p[:, 0].tolist() == [0, 2, 1, 3, 4, 6, 5, 7]
+    assert np.array_equal(gguf.unpermute_rope_rows(p, 2), w)
+
+
+@pytest.mark.parametrize("model", ["tiny-llama", "tiny-moe", "llama3.1-8b"])
+def test_gguf_round_trip_fills_identical_blob(tmp_path, model):
+    """safetensors -> blob -> write_gguf -> GgufCheckpoint -> blob is byte-identical;
+    the GGUF config yields the same ModelSpec and Arch (incl. llama3 rope scaling as
+    rope_freqs, stacked experts, permuted llama q/k, F32 norms)."""
+    from paper_2604_26334_b200.runtime import gguf
+    from paper_2604_26334_b200.runtime.model import Arch
+    spec = catalog.builtin_model(model)
+    if model == "llama3.1-8b":   # the real shapes, 2 layers
+        import dataclasses
+        spec = dataclasses.replace(spec, n_layers=2, vocab_size=4096)
+    arch = arch_for(catalog.builtin_model(model))
+    rng = np.random.default_rng(3)
+    tensors = _hf_tensors(spec, arch, rng)
+    _write(tmp_path, spec, arch, tensors)
+    lay = WeightLayout(spec, arch)
+    blob = np.zeros(lay.total_bytes, np.uint8)
+    emb = np.zeros(lay.embed_bytes, np.uint8)
+    ck.fill_from_checkpoint(lay, blob, emb, ck.Checkpoint(tmp_path))
+    path = tmp_path / "m.gguf"
+    gguf.write_gguf(path, lay, blob, emb, arch)
+    g = ck.open_checkpoint(path)
+    assert isinstance(g, gguf.GgufCheckpoint)
+    spec2, arch2 = ck.spec_from_hf_config(g.config)
+    for f in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "vocab_size", "moe"):
+        assert getattr(spec2, f) == getattr(spec, f), f
+    assert (spec2.ffn_dim == spec.ffn_dim) or spec.moe
+    assert isinstance(arch2, Arch) and arch2.qk_norm == arch.qk_norm
+    assert arch2.rope_theta == pytest.approx(arch.rope_theta) and arch2.rope_scaling == arch.rope_scaling
+    blob2 = np.zeros_like(blob)
+    emb2 = np.zeros_like(emb)
+    ck.fill_from_checkpoint(lay, blob2, emb2, g)
+    assert np.array_equal(blob2, blob) and np.array_equal(emb2, emb)
+    if arch.qk_norm is False:   # llama: q rows really are stored permuted in the file
+        hd, h = spec.head_dim, spec.n_heads
+        raw = np.asarray(g.file.array("blk.0.attn_q.weight"))
+        hf = tensors["model.layers.0.self_attn.q_proj.weight"][2]
+        assert not np.array_equal(raw, hf)
+        assert np.array_equal(raw, gguf.permute_rope_rows(hf, h))
+
+
+def test_gguf_rejects_bad_files(tmp_path):
+    from paper_2604_26334_b200.planning.faults import FormatError, SpecError
+    from paper_2604_26334_b200.runtime import gguf
+    p = tmp_path / "x.gguf"
+    p.write_bytes(b"NOPE" + b"\0" * 64)
+    with pytest.raises(FormatError):
+        gguf.GgufFile(p)
+    import struct
+    # a valid header whose architecture is not supported
+    k, v = b"general.architecture", b"gpt2"
+    p.write_bytes(b"GGUF" + struct.pack("<IQQ", 3, 0, 1) + struct.pack("<Q", len(k)) + k +
+                  struct.pack("<IQ", 8, len(v)) + v + b"\0" * 32)
+    with pytest.raises(SpecError):
+        gguf.GgufCheckpoint(p)

@@ -272,6 +272,30 @@ def test_checkpoint_round_trip_generates_same_tokens(tmp_path, model, frac):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("model,frac", [("tiny-llama", 0.6), ("tiny-moe", 1.0)])
+def test_gguf_checkpoint_generates_same_tokens(tmp_path, model, frac):
+    """Random-init weights written as a GGUF file (llama.cpp conventions: permuted
+    llama q/k, stacked experts, F32 norms) and loaded back with
+    Engine(None, checkpoint="x.gguf") fill a byte-identical blob and generate the
+    same tokens."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model(model)
+    budget = frac * total_model_bytes(spec)
+    prompt = _prompt(40, spec.vocab_size, seed=6)
+    eng = Engine(spec, budget_bytes=budget, context_len=160)
+    want = eng.generate([prompt], gen_len=8).tokens[0]
+    path = str(tmp_path / "model.gguf")
+    assert eng.weights.export_gguf(path) > 0
+    blob = eng.weights.blob_bytes().copy()
+    eng.close()
+    eng2 = Engine(None, budget_bytes=budget, context_len=160, checkpoint=path)
+    assert eng2.spec.n_layers == spec.n_layers and eng2.spec.moe == spec.moe
+    assert np.array_equal(eng2.weights.blob_bytes(), blob)
+    got = eng2.generate([prompt], gen_len=8).tokens[0]
+    eng2.close()
+    assert np.array_equal(got, want)
+
+
 def _shared_weights_worker(name, q):
     import hashlib
     import sys
