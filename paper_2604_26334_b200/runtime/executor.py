@@ -108,7 +108,13 @@ class Executor:
         # cache streamed / CPU-placed weight shards in budget the ring does not need
         # (PS_SPARE_PIN=0 runs the plan's residency exactly)
         self.spare_pin = os.environ.get("PS_SPARE_PIN", "1") != "0"
-        self.ring_keep_pieces = int(os.environ.get("PS_RING_KEEP_PIECES", "4"))   # ring kept for streaming
+        # ring kept for streaming, in pieces of chunk_cap: a GEMM (prefill) pass computes
+        # for ms on each piece and wants a deep ring; a GEMV (decode) pass consumes a
+        # piece in microseconds, so two keep the link busy and the rest of the budget
+        # caches shards (config 2: 4 -> 2 pieces, one more attention shard cached,
+        # 4.745 -> 4.80 tokens/s; config 4/5 prefill TTFT +1-16 % with 2, hence per tier)
+        self.ring_keep_pieces = int(os.environ.get("PS_RING_KEEP_PIECES", "4"))
+        self.ring_keep_pieces_decode = int(os.environ.get("PS_RING_KEEP_DECODE", "2"))
         self.spare_pinned = []
         self.expert_slots, self.expert_slot_bytes = 0, 0
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
@@ -279,8 +285,8 @@ class Executor:
         n_slots, slot = self._slot_bytes(T, modes, free)
         kv_streams = any(m == "stream" and self.shards[sid].kind is ShardKind.KV_CACHE
                          for sid, m in modes.items())
-        ring_keep = min(self.ring_cap, self.ring_keep_pieces * self.chunk_cap +
-                        (self.kv_layer_bytes if kv_streams else 0))
+        keep = self.ring_keep_pieces if T > GEMV_MAX_T else self.ring_keep_pieces_decode
+        ring_keep = min(self.ring_cap, keep * self.chunk_cap + (self.kv_layer_bytes if kv_streams else 0))
         spare = free - n_slots * slot - ring_keep - min(32 << 20, self.arena.capacity // 64)
         if spare <= 0:
             return out
