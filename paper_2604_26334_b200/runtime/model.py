@@ -188,27 +188,34 @@ class WeightLayout:
 class SharedHostBlob:
     """One host buffer shared by every process of a node (data-parallel replicas):
     a /dev/shm file, mmapped and pinned in each process with cudaHostRegister
-    (mapped, portable). The process that creates the file fills it and then
-    drops a `.ready` marker; the others map it and wait for the marker, so a
-    node holds one copy of the weights instead of one per GPU."""
+    (mapped, portable), so a node holds one copy of the weights instead of one per
+    GPU. The process that creates the file pins it first, fills it and then sets a
+    ready flag; the others wait for the pinned flag, pin, and wait for the ready
+    flag. Both flags live in a header page behind the weights, inside the shared
+    memory itself, so a replica that is slow to arrive still sees them after the
+    creator has finished and removed the name (the mapping outlives the name)."""
+
+    HEADER = 4096
+    PINNED, READY = b"PSPINNED", b"PS_READY"
 
     def __init__(self, name: str, nbytes: int, timeout_s: float = 3600.0):
         import ctypes
         import mmap
         import os
+        import time
         self.path = f"/dev/shm/{name}"
         self.nbytes = nbytes
         self.timeout_s = timeout_s
-        import time
+        total = nbytes + self.HEADER
         try:
             self.fd = os.open(self.path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
             self.creator = True
             try:
-                os.ftruncate(self.fd, nbytes)
+                os.ftruncate(self.fd, total)
                 # populate the tmpfs pages up front: several processes pinning the same
                 # sparse segment concurrently fails for large segments (measured at
                 # 17 GB), and a full /dev/shm fails here instead of SIGBUS later
-                os.posix_fallocate(self.fd, 0, nbytes)
+                os.posix_fallocate(self.fd, 0, total)
             except OSError:
                 os.close(self.fd)
                 os.unlink(self.path)
@@ -216,20 +223,14 @@ class SharedHostBlob:
         except FileExistsError:
             self.creator = False
             self.fd = os.open(self.path, os.O_RDWR)
-            t0 = time.time()
-            # the creator pins first (populated pages), then the others; a creator
-            # that failed unlinks the file, which ends the wait
-            while not os.path.exists(self.path + ".pinned"):
-                gone = not os.path.exists(self.path)
-                if gone or time.time() - t0 > timeout_s:
-                    os.close(self.fd)
-                    raise (FileNotFoundError if gone else TimeoutError)(
-                        f"{self.path}: creator never pinned the blob")
-                time.sleep(0.02)
-        self.mm = mmap.mmap(self.fd, nbytes)
+            self._wait(lambda: os.fstat(self.fd).st_size >= total, "sized the blob")
+        self.mm = mmap.mmap(self.fd, total)
+        if not self.creator:
+            # the creator pins first (populated pages), then the others
+            self._wait(lambda: self._flag(0) == self.PINNED, "pinned the blob")
         self.addr = ctypes.addressof(ctypes.c_char.from_buffer(self.mm))
         try:
-            L.call("ps_host_register", self.addr, nbytes, 1)
+            L.call("ps_host_register", self.addr, total, 1)
         except Exception:
             self.addr = 0
             try:
@@ -238,14 +239,26 @@ class SharedHostBlob:
                 pass
             os.close(self.fd)
             if self.creator:
-                for p in (self.path, self.path + ".pinned"):
-                    try:
-                        os.unlink(p)
-                    except FileNotFoundError:
-                        pass
+                self.unlink()
             raise
         if self.creator:
-            open(self.path + ".pinned", "w").close()
+            self.mm[nbytes:nbytes + 8] = self.PINNED
+
+    def _flag(self, slot: int) -> bytes:
+        o = self.nbytes + 8 * slot
+        return bytes(self.mm[o:o + 8])
+
+    def _wait(self, cond, what: str) -> None:
+        """Poll `cond`; a creator that failed removes the name, which ends the wait."""
+        import os
+        import time
+        t0 = time.time()
+        while not cond():
+            if not os.path.exists(self.path) and not cond():
+                raise FileNotFoundError(f"{self.path}: creator left before it {what}")
+            if time.time() - t0 > self.timeout_s:
+                raise TimeoutError(f"{self.path}: creator never {what}")
+            time.sleep(0.02)
 
     @staticmethod
     def fits(nbytes: int) -> bool:
@@ -257,29 +270,20 @@ class SharedHostBlob:
         return st.f_bavail * st.f_frsize > nbytes * 1.05
 
     def mark_ready(self) -> None:
-        with open(self.path + ".ready", "w") as fh:
-            fh.write("ok")
+        o = self.nbytes + 8
+        self.mm[o:o + 8] = self.READY
 
     def wait_ready(self) -> None:
-        import os
-        import time
-        t0 = time.time()
-        while not os.path.exists(self.path + ".ready"):
-            if not os.path.exists(self.path):
-                raise FileNotFoundError(f"{self.path}: creator left before the weights were ready")
-            if time.time() - t0 > self.timeout_s:
-                raise TimeoutError(f"{self.path}: weights never marked ready")
-            time.sleep(0.1)
+        self._wait(lambda: self._flag(1) == self.READY, "filled the weights")
 
     def unlink(self) -> None:
         """Remove the name once every process that needs it has mapped the segment;
         the memory lives until the last mapping goes."""
         import os
-        for p in (self.path, self.path + ".ready", self.path + ".pinned"):
-            try:
-                os.unlink(p)
-            except FileNotFoundError:
-                pass
+        try:
+            os.unlink(self.path)
+        except FileNotFoundError:
+            pass
 
     def close(self) -> None:
         import os
