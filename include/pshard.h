@@ -137,6 +137,16 @@ int ps_attn_prefill_tc(const float* q, int ldq, int batch, const int* q_start, c
  * ((role << 24) | (barrier << 16) | key block); reset clears it. */
 int ps_attn_tc_watchdog(unsigned* code, int reset);
 
+/* Exponent-coded GEMV: y[t, n] (epi)= x[t, :] . W[n, :] with W in the 12-bit format of
+ * runtime/wcomp.py (row n: K sign|mantissa bytes, then K/2 bytes of 4-bit exponent codes
+ * relative to base_exp, 15 = escape looked up in esc_off[N + 1] / esc_ent (col << 8 | exp)).
+ * Same decomposition and accumulation order as ps_gemv_bf16's bulk-copy kernel, so the
+ * result is bit-identical to ps_gemv_bf16 on the decoded weights; 25 % fewer weight
+ * bytes. t <= 8, K % 256 == 0, Wc 16-byte aligned (device memory). */
+int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int N, int K, int base_exp,
+                  const int* esc_off, const int* esc_ent, float* y, int ldy, int epilogue,
+                  void* stream);
+
 /* Programmatic dependent launch for the decode-pass kernels (rmsnorm, qkv/RoPE,
  * decode attention + merge, GEMVs, embed, argmax, add, small uploads): while on,
  * each is launched with cudaLaunchAttributeProgrammaticStreamSerialization and

@@ -36,10 +36,15 @@ constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp
 
 // Per token count: columns per consumer thread (x kept in registers: CPT * T floats)
 // and rows per stage (RS * KC * 2 = 32 KB, KC = 256 * CPT columns per chunk).
-template <int T> struct GtShape {
+// COMP: rows in the exponent-coded format (`ps_gemv_bf16c`): per row segment of KC
+// columns KC sign|mantissa bytes then KC/2 bytes of 4-bit exponent codes.
+constexpr int gt_pow2_floor(int v) { return v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1; }
+
+template <int T, bool COMP = false> struct GtShape {
   static constexpr int CPT = T <= 4 ? 16 : 8;
   static constexpr int KC = GT_CONSUMERS * 32 * CPT;
-  static constexpr int RS = GT_STAGE_BYTES / (KC * 2);
+  static constexpr int ROWB = COMP ? KC * 3 / 2 : KC * 2;   // stage bytes per row segment
+  static constexpr int RS = COMP ? gt_pow2_floor(GT_STAGE_BYTES / ROWB) : GT_STAGE_BYTES / (KC * 2);
   static constexpr int V = RS * T;  // partial sums reduced per stage
   // warp_reduce_scatter halves V each step: a non-power-of-two V would drop values
   static_assert(RS >= 1 && (V & (V - 1)) == 0, "rows x tokens per stage must be a power of two");
@@ -75,12 +80,46 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[V], int lane) {
   }
 }
 
-template <int T, int EPI>
+// 8 coded weights -> 8 bf16 (uint4). sm: sign|mantissa bytes, nb: eight 4-bit codes;
+// code 15 = escape: the exponent is looked up in the row's (col << 8 | exp) list.
+__device__ __noinline__ uint32_t gt_escape_exp(const int* __restrict__ esc_off, const int* __restrict__ esc_ent,
+                                              int row, int col) {
+  int lo = esc_off[row], hi = esc_off[row + 1] - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((esc_ent[mid] >> 8) < col) lo = mid + 1; else hi = mid;
+  }
+  return (uint32_t)esc_ent[lo] & 0xFFu;
+}
+
+__device__ __forceinline__ uint4 gt_decode8(uint2 sm, uint32_t nb, uint32_t base, const int* esc_off,
+                                            const int* esc_ent, int row, int col) {
+  uint32_t out[4];
+  const uint32_t smw[2] = {sm.x, sm.y};
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    uint32_t half[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int i = 2 * p + q;
+      const uint32_t b = (smw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+      const uint32_t code = (nb >> (4 * i)) & 0xFu;
+      const uint32_t e = code == 15u ? gt_escape_exp(esc_off, esc_ent, row, col + i) : base + code;
+      half[q] = ((b & 0x80u) << 8) | (e << 7) | (b & 0x7Fu);
+    }
+    out[p] = half[0] | (half[1] << 16);
+  }
+  return make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+template <int T, int EPI, bool COMP = false>
 __global__ void __launch_bounds__(GT_THREADS, 1)
 gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W, int N, int K,
-                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages) {
-  using S = GtShape<T>;
-  constexpr int CPT = S::CPT, KC = S::KC, RS = S::RS, V = S::V;
+                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages, int base_exp,
+                const int* __restrict__ esc_off, const int* __restrict__ esc_ent) {
+  using S = GtShape<T, COMP>;
+  constexpr int CPT = S::CPT, KC = S::KC, RS = S::RS, V = S::V, ROWB = S::ROWB;
+  const uint8_t* Wb = reinterpret_cast<const uint8_t*>(W);   // COMP: ldw is in bytes
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * GT_STAGE_BYTES);
@@ -115,11 +154,20 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
           const int rb = r0 + b * RS;
           const int nr = min(RS, r1 - rb);
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], (uint32_t)(nr * kc * 2));
           uint8_t* dst = ring + s * GT_STAGE_BYTES;
-          for (int r = 0; r < nr; ++r)
-            bulk_load(dst + r * KC * 2, W + (long long)(rb + r) * ldw + (long long)c * KC, (uint32_t)(kc * 2),
-                      &full[s]);
+          if constexpr (COMP) {
+            mbar_expect_tx(&full[s], (uint32_t)(nr * (kc + kc / 2)));
+            for (int r = 0; r < nr; ++r) {
+              const uint8_t* row = Wb + (long long)(rb + r) * ldw;
+              bulk_load(dst + r * ROWB, row + (long long)c * KC, (uint32_t)kc, &full[s]);
+              bulk_load(dst + r * ROWB + KC, row + K + (long long)c * (KC / 2), (uint32_t)(kc / 2), &full[s]);
+            }
+          } else {
+            mbar_expect_tx(&full[s], (uint32_t)(nr * kc * 2));
+            for (int r = 0; r < nr; ++r)
+              bulk_load(dst + r * KC * 2, W + (long long)(rb + r) * ldw + (long long)c * KC, (uint32_t)(kc * 2),
+                        &full[s]);
+          }
           if (++s == stages) { s = 0; ph ^= 1; }
         }
       }
@@ -175,8 +223,18 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
 #pragma unroll
         for (int h = 0; h < CPT / 8; ++h) {
           const int col = (h * GT_CONSUMERS * 32 + j) * 8;
-          w[h] = (r < nr && col < kc) ? *reinterpret_cast<const uint4*>(stage + (r * KC + col) * 2)
-                                      : make_uint4(0, 0, 0, 0);
+          if constexpr (COMP) {
+            if (r < nr && col < kc) {
+              const uint2 sm = *reinterpret_cast<const uint2*>(stage + r * ROWB + col);
+              const uint32_t nb = *reinterpret_cast<const uint32_t*>(stage + r * ROWB + KC + col / 2);
+              w[h] = gt_decode8(sm, nb, (uint32_t)base_exp, esc_off, esc_ent, rb + r, c * KC + col);
+            } else {
+              w[h] = make_uint4(0, 0, 0, 0);
+            }
+          } else {
+            w[h] = (r < nr && col < kc) ? *reinterpret_cast<const uint4*>(stage + (r * KC + col) * 2)
+                                        : make_uint4(0, 0, 0, 0);
+          }
         }
 #pragma unroll
         for (int t = 0; t < T; ++t) {
@@ -228,9 +286,10 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
 static int g_tma_sms = 0;
 static int g_tma_stages = 0;
 
-template <int T, int EPI>
+template <int T, int EPI, bool COMP = false>
 static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
-                      int ldy, cudaStream_t s, int grid_cap) {
+                      int ldy, cudaStream_t s, int grid_cap, int base_exp = 0, const int* esc_off = nullptr,
+                      const int* esc_ent = nullptr) {
   if (!g_tma_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -254,10 +313,12 @@ static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, i
   const size_t smem = (size_t)stages * (GT_STAGE_BYTES + 16) + (size_t)GT_CONSUMERS * rows_per_cta * T * 4;
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI, COMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
     smem_set = smem;
   }
-  launch_k(gemv_tma_kernel<T, EPI>, grid, GT_THREADS, smem, s, x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta, stages);
+  launch_k(gemv_tma_kernel<T, EPI, COMP>, grid, GT_THREADS, smem, s, x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta,
+           stages, base_exp, esc_off, esc_ent);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -279,7 +340,33 @@ int gemv_tma_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int
   return launch_tma_epi<8>(epi, x, ldx, tt, W, N, K, ldw, y, ldy, s, grid_cap);
 }
 
+template <int T>
+static int launch_tmac_epi(int epi, const float* x, int ldx, int tt, const void* Wc, int N, int K, float* y, int ldy,
+                           cudaStream_t s, int base, const int* off, const int* ent) {
+  auto W = static_cast<const __nv_bfloat16*>(Wc);
+  const long long ldw = (long long)K * 3 / 2;   // bytes per coded row
+  if (epi == PS_EPI_STORE) return launch_tma<T, PS_EPI_STORE, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0, base, off, ent);
+  if (epi == PS_EPI_ACCUM) return launch_tma<T, PS_EPI_ACCUM, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0, base, off, ent);
+  return launch_tma<T, PS_EPI_SWIGLU, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0, base, off, ent);
+}
+
 }  // namespace ps
+
+extern "C" int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int N, int K, int base_exp,
+                             const int* esc_off, const int* esc_ent, float* y, int ldy, int epilogue, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(t >= 1 && t <= 8, "ps_gemv_bf16c: t=%d outside [1, 8]", t);
+  PS_REQUIRE(K % 256 == 0 && ldx % 4 == 0, "ps_gemv_bf16c: K must be a multiple of 256");
+  PS_REQUIRE(((uintptr_t)Wc & 15) == 0 && ((uintptr_t)x & 15) == 0, "ps_gemv_bf16c: Wc and x must be 16-byte aligned");
+  PS_REQUIRE(base_exp >= 0 && base_exp <= 255 - 14, "ps_gemv_bf16c: base exponent %d", base_exp);
+  PS_REQUIRE(epilogue != PS_EPI_SWIGLU || N % 2 == 0, "ps_gemv_bf16c: SWIGLU needs an even N");
+  if (N <= 0) return PS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (t == 1) return launch_tmac_epi<1>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
+  if (t == 2) return launch_tmac_epi<2>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
+  if (t <= 4) return launch_tmac_epi<4>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
+  return launch_tmac_epi<8>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
+}
 
 int ps_preload_gemv_tma() {
   using namespace ps;
@@ -287,7 +374,10 @@ int ps_preload_gemv_tma() {
 #define PS_T(T)                                                \
   touch_kernel(gemv_tma_kernel<T, PS_EPI_STORE>, n);           \
   touch_kernel(gemv_tma_kernel<T, PS_EPI_ACCUM>, n);           \
-  touch_kernel(gemv_tma_kernel<T, PS_EPI_SWIGLU>, n);
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_SWIGLU>, n);          \
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_STORE, true>, n);     \
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_ACCUM, true>, n);     \
+  touch_kernel(gemv_tma_kernel<T, PS_EPI_SWIGLU, true>, n);
   PS_T(1) PS_T(2) PS_T(4) PS_T(8)
 #undef PS_T
   return n;

@@ -258,3 +258,22 @@ def test_gguf_rejects_bad_files(tmp_path):
                   struct.pack("<IQ", 8, len(v)) + v + b"\0" * 32)
     with pytest.raises(SpecError):
         gguf.GgufCheckpoint(p)
+
+
+def test_exponent_coding_round_trip():
+    """runtime/wcomp.py: 12-bit exponent-coded rows decode to the exact bf16 bits,
+    escapes (zeros, denormals, inf/nan, far exponents) included; the window covers
+    > 99.99 % of the initialiser's weights."""
+    from oracle import model_ref as M
+    from paper_2604_26334_b200.runtime import wcomp
+    bits = M.bf16_bits(0, "L0.w_gate", 256, 512).copy()
+    bits[0, :4] = [0x0000, 0x8000, 0x0001, 0x7F80]       # +0, -0, denormal, inf
+    bits[1, 7] = 0x7FC1                                  # nan
+    bits[2, 9] = 0x4700                                  # 32768, far above the window
+    coded, base, off, ent = wcomp.encode(bits)
+    assert coded.shape == (256, 768) and coded.dtype == np.uint8
+    assert np.array_equal(wcomp.decode(coded, base, off, ent), bits)
+    assert len(ent) < 1e-3 * bits.size + 8
+    assert wcomp.coded_bytes(256, 512, len(ent)) < 0.76 * bits.nbytes + 4 * 257 + 4 * len(ent) + 1
+    with pytest.raises(ValueError):
+        wcomp.encode(bits[:, :511])

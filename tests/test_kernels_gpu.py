@@ -453,3 +453,35 @@ def test_expert_fetcher_publish_copy_wait():
         lib.host_free(host)
     finally:
         lib.call("ps_fetcher_destroy", f)
+
+
+@pytest.mark.parametrize("N,K,t,epi", [(512, 4096, 1, 0), (1000, 2048, 2, 1), (640, 14336, 1, 0),
+                                       (256, 4096, 8, 2), (300, 512, 4, 0)])
+def test_gemv_coded_bit_identical(N, K, t, epi):
+    """ps_gemv_bf16c on exponent-coded weights (runtime/wcomp.py, 12 bits/weight) is
+    bit-identical to ps_gemv_bf16 on the bf16 weights, escapes included (zeros,
+    denormals, huge and tiny values outside the 15-exponent window)."""
+    from paper_2604_26334_b200.runtime import wcomp
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.03
+    W[0, :7] = 0.0
+    W[1, 3] = 1e-30
+    W[2, 11] = 3.0e4
+    W[N - 1, K - 1] = -1e-38
+    bits = W.view(torch.int16).cpu().numpy().view(np.uint16)
+    coded, base, off, ent = wcomp.encode(bits)
+    assert len(ent) >= 10
+    assert np.array_equal(wcomp.decode(coded, base, off, ent), bits)
+    Wc = torch.from_numpy(coded).cuda()
+    d_off, d_ent = torch.from_numpy(off).cuda(), torch.from_numpy(ent).cuda()
+    x = torch.randn(t, K, device="cuda", generator=g)
+    rows = N // 2 if epi == 2 else N
+    y0 = torch.randn(t, rows, device="cuda", generator=g)
+    ya, yb = y0.clone(), y0.clone()
+    s = stream()
+    lib.call("ps_gemv_bf16_cfg", x.data_ptr(), K, t, W.data_ptr(), N, K, K, ya.data_ptr(), rows, epi, s, -1, 0, 0)
+    lib.call("ps_gemv_bf16c", x.data_ptr(), K, t, Wc.data_ptr(), N, K, base, d_off.data_ptr(), d_ent.data_ptr(),
+             yb.data_ptr(), rows, epi, s)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)
