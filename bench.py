@@ -349,6 +349,9 @@ def run_ours(args, rank: int, world: int) -> dict:
                               for a, b, r, mv, (h, dd) in res.switches],
                  "prefill_pass_ms": round(res.passes[0][2] * 1e3, 2) if res.passes else None},
         "model_load_s": round(eng.load_seconds, 2),
+        "link_format": ("exponent-coded dense shards in decode passes (12 bits/weight, lossless; "
+                        f"encoded in {getattr(eng, 'coded_seconds', 0.0):.1f}s at load)"
+                        if getattr(eng.weights, "coded", None) is not None else "bf16"),
         "host_weights": "shared /dev/shm segment per node" if shared else "private pinned blob",
         "residency": {
             "spare_pinned_shards": len(eng.executor.spare_pinned),

@@ -14,6 +14,7 @@ a real GPU pass of `Executor.run_pass` instead of `simulate_schedule`.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -22,7 +23,7 @@ import numpy as np
 from ..planning import catalog
 from ..planning.costdb import ProfileDb, load_profile, synth_profile
 from ..planning.faults import InfeasibleBudget, SpecError
-from ..planning.graph import ModelSpec
+from ..planning.graph import ModelSpec, ShardKind
 from ..planning.hardware import MachineSpec
 from ..planning.placement import TIERS, TierTable, TierEntry, reachable_tiers
 from ..planning.pipeline_model import outstanding_tokens, schedule_iteration
@@ -121,9 +122,41 @@ class Engine:
                 best, best_cost = tier, cost
         return best
 
+    def _build_coded(self) -> None:
+        """Exponent-coded copies of the dense shards (runtime/wcomp.py) that decode
+        passes stream instead of bf16 (25 % fewer link bytes, bit-identical results),
+        when host memory holds them: about 0.75 x the dense weight bytes, pinned.
+        Anything else (no room, allocation failure) keeps bf16 streaming."""
+        from .wcomp import CodedShards
+        need = sum(b.nbytes for b in self.weights.layout.blobs.values()
+                   if b.kind in (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD)) * 3 // 4
+        avail = 0
+        try:
+            with open("/proc/meminfo") as fh:
+                for line in fh:
+                    if line.startswith("MemAvailable:"):
+                        avail = int(line.split()[1]) * 1024
+        except OSError:
+            pass
+        if avail and need > 0.5 * avail:
+            return
+        t0 = time.perf_counter()
+        try:
+            self.weights.coded = CodedShards(self.weights, (ShardKind.ATTENTION, ShardKind.FFN,
+                                                            ShardKind.OUTPUT_HEAD))
+        except Exception as exc:   # e.g. pinned host memory exhausted: stream bf16
+            import warnings
+            warnings.warn(f"exponent-coded weights unavailable ({exc}); streaming bf16")
+            self.weights.coded = None
+            return
+        self.coded_seconds = time.perf_counter() - t0
+
     def _ensure_executor(self, max_tokens: int) -> Executor:
         if self.executor is None:
             tiers_used = self.plans
+            if (os.environ.get("PS_CODED", "1") == "1" and self.spec.moe is None and
+                    getattr(self.weights, "coded", None) is None):
+                self._build_coded()
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,
                                      self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes)
@@ -290,4 +323,8 @@ class Engine:
         if self.executor is not None:
             self.executor.close()
             self.executor = None
+        coded = getattr(self.weights, "coded", None)
+        if coded is not None:
+            coded.close()
+            self.weights.coded = None
         self.weights.close()

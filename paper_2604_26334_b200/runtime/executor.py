@@ -147,6 +147,13 @@ class Executor:
 
         self.arena = VramArena(budget_bytes)
         self._carve_persistent()
+        # exponent-coded dense shards (runtime/wcomp.py) for GEMV passes that stream
+        # them; their escape tables are host-mapped (read only for escaped weights)
+        self.coded = getattr(weights, "coded", None)
+        self._coded_call = None
+        self.d_esc_off = self.d_esc_ent = 0
+        if self.coded is not None:
+            self.d_esc_off, self.d_esc_ent = self.coded.esc_off_ptr, self.coded.esc_ent_ptr
         self.persist_high = self.arena.high       # activations + ring are carved below, per tier
         self.residency: dict[int, tuple] = {}
         self.tier = None
@@ -530,6 +537,35 @@ class Executor:
             out.append((start, end, items))
         return out
 
+    def _pieces_coded(self, sid: int, names: list, even: set, chunk: int | None = None) -> list:
+        """`_pieces` over the shard's exponent-coded layout (row bytes 1.5 x cols)."""
+        chunk = chunk or self.chunk
+        blob = self.w.layout.blobs[sid]
+        meta = self.coded.tensors[sid]
+        out, items, start, end, big = [], [], None, 0, False
+        for name in names:
+            t = blob.tensors[name]
+            off, row_b = meta[name][0], meta[name][1]
+            step = max(1, chunk // row_b)
+            if name in even:
+                step = max(2, step // 2 * 2)
+            r = 0
+            while r < t.rows:
+                r1 = min(t.rows, r + step)
+                b0, b1 = off + r * row_b, off + r1 * row_b
+                if big and t.rows > 1 and b1 - start > chunk:
+                    out.append((start, end, items))
+                    items, start, big = [], None, False
+                if start is None:
+                    start = b0
+                items.append((name, r, r1))
+                big = big or t.rows > 1
+                end = b1
+                r = r1
+        if items:
+            out.append((start, end, items))
+        return out
+
     def _shard(self, sid: int, consumers: list, T: int) -> None:
         """Make a weight shard's tensors addressable and run its consumers in order.
 
@@ -580,9 +616,16 @@ class Executor:
             advance_to(len(consumers))
             return
 
-        pieces = self._piece_override.pop(sid, None) or \
-            self._pieces(sid, names, {c.tensor for c in consumers if c.even_rows})
-        host = self.w.shard_ptr(sid)
+        coded = (self.coded is not None and T <= GEMV_MAX_T and sid in self.coded.tensors and
+                 self.striper is None and sid not in self._piece_override)
+        evens = {c.tensor for c in consumers if c.even_rows}
+        if coded:
+            meta = self.coded.tensors[sid]
+            pieces = self._pieces_coded(sid, names, evens)
+            host = self.coded.shard_ptr(sid)
+        else:
+            pieces = self._piece_override.pop(sid, None) or self._pieces(sid, names, evens)
+            host = self.w.shard_ptr(sid)
         # A piece is released once nothing enqueued later reads it: matrix rows as
         # soon as their consumer has been enqueued for them ("rows" token), small
         # tensors (norms, q/k norms) when every consumer that reads them is done.
@@ -617,12 +660,21 @@ class Executor:
             self._wait(arrived)
             for name, r0, r1 in items:
                 t = blob.tensors[name]
-                ptr = pdev + (t.offset + r0 * t.cols * 2 - b0)
+                if coded:
+                    m = meta[name]
+                    ptr = pdev + (m[0] + r0 * m[1] - b0)
+                else:
+                    ptr = pdev + (t.offset + r0 * t.cols * 2 - b0)
                 if r0 == 0:
                     self.ptrs[name] = ptr
                 if name in own:
                     advance_to(own[name])
-                    self._traced(name, consumers[ci].fn, ptr, r0, r1)
+                    if coded and m[2] >= 0:   # the consumer's GEMV reads coded rows
+                        self._coded_call = (m[2], self.d_esc_off + (m[3] + r0) * 4, self.d_esc_ent)
+                    try:
+                        self._traced(name, consumers[ci].fn, ptr, r0, r1)
+                    finally:
+                        self._coded_call = None
                     if t.rows > 1:
                         discharge(entry, ("rows", name))
                     if r1 == t.rows:
@@ -857,7 +909,12 @@ class Executor:
     def _matmul(self, T, act, W, N, K, out, ldo, epi) -> None:
         """out (epi)= act @ W[:N]^T for T tokens: GEMV on fp32 act (T <= 32)
         or the tcgen05 GEMM on bf16 act."""
-        if T <= GEMV_MAX_T:
+        if self._coded_call is not None:
+            base, esc_off, esc_ent = self._coded_call
+            for t0 in range(0, T, 8):
+                L.call("ps_gemv_bf16c", act + t0 * K * 4, K, min(8, T - t0), W, N, K, base, esc_off, esc_ent,
+                       out + t0 * ldo * 4, ldo, epi, self.cs)
+        elif T <= GEMV_MAX_T:
             L.call("ps_gemv_bf16", act, K, T, W, N, K, K, out, ldo, epi, self.cs)
         else:
             L.call("ps_gemm_bf16", act, T, K, K, W, N, K, out, ldo, epi, self.cs)
@@ -1046,6 +1103,9 @@ class Executor:
                 L.call("ps_rmsnorm", self.x, d, self.i_rows, R, p, d, eps, self.xs, d, 0, self.cs)
 
             def lm(p, r0, r1):
+                if self._coded_call is not None:
+                    self._matmul(R, self.xs, p, r1 - r0, d, self.logits + r0 * 4, self.V, L.PS_EPI_STORE)
+                    return
                 L.call("ps_gemv_bf16", self.xs, d, R, p, r1 - r0, d, d, self.logits + r0 * 4,
                        self.V, L.PS_EPI_STORE, self.cs)
 

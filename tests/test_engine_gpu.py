@@ -86,6 +86,29 @@ def test_pdl_passes_bit_identical(tiny, monkeypatch, frac):
     assert np.array_equal(out["1"][1], out["0"][1])
 
 
+@pytest.mark.parametrize("frac", [0.25, 0.3])
+def test_coded_streaming_same_tokens_fewer_bytes(tiny, monkeypatch, frac):
+    """PS_CODED=1: decode passes stream the exponent-coded copies of dense shards
+    (runtime/wcomp.py, ps_gemv_bf16c) — the same tokens and last logits as bf16
+    streaming (the coded GEMV is bit-identical), with fewer bytes on the link."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    prompt = _prompt(20, tiny.vocab_size, seed=12)
+    out = {}
+    for coded in ("0", "1"):
+        monkeypatch.setenv("PS_CODED", coded)
+        eng = Engine(tiny, budget_bytes=frac * total_model_bytes(tiny), context_len=160, chunk_bytes=1 << 20)
+        res = eng.generate([prompt], gen_len=16)
+        ex = eng.executor
+        dec = [s for s in ex.stats if s.T == 1]
+        streamed = sum(s.bytes_streamed for s in dec)
+        logits = ex.logits_host(1).copy()
+        eng.close()
+        out[coded] = (res.tokens[0], logits, streamed)
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert out["0"][2] > 0 and out["1"][2] < 0.8 * out["0"][2], (out["0"][2], out["1"][2])
+
+
 @pytest.mark.parametrize("frac", [0.5, 0.25, 1.5])
 def test_tiny_config1_teacher_forced(tiny, oracle, frac):
     """BASELINE config 1 (prompt 128 + 32): the prompt pass runs the tcgen05
