@@ -26,15 +26,16 @@ ESCAPE = 15
 
 def choose_base(bits: np.ndarray) -> int:
     """Start of the 15-exponent window that covers the most weights (ties: lowest)."""
-    exp = ((bits >> 7) & 0xFF).astype(np.int64).reshape(-1)
+    exp = (bits.reshape(-1) >> 7).astype(np.uint8)          # the uint8 cast drops the sign bit
     hist = np.bincount(exp, minlength=256)
     cover = np.convolve(hist, np.ones(15, np.int64), mode="valid")   # cover[b] = sum hist[b:b+15]
     return int(np.argmax(cover))
 
 
-def encode(bits: np.ndarray, base: int | None = None):
+def encode(bits: np.ndarray, base: int | None = None, out: np.ndarray | None = None):
     """bf16 bit patterns (uint16 [N, K], K % 2 == 0) -> (coded uint8 [N, 1.5 K], base,
-    esc_off int32 [N + 1], esc_ent int32 [n_escapes])."""
+    esc_off int32 [N + 1], esc_ent int32 [n_escapes]). `out`: optional destination
+    (uint8, N * 1.5 K bytes) written in place."""
     bits = np.ascontiguousarray(bits, dtype=np.uint16)
     n, k = bits.shape
     if k % 2:
@@ -43,18 +44,19 @@ def encode(bits: np.ndarray, base: int | None = None):
         base = choose_base(bits)
     if not 0 <= base <= 255 - 14:
         raise ValueError(f"base exponent {base} outside [0, 241]")
-    b32 = bits.astype(np.uint32)
-    sm = (((b32 >> 8) & 0x80) | (b32 & 0x7F)).astype(np.uint8)
-    exp = ((b32 >> 7) & 0xFF).astype(np.int64)
-    code = exp - base
-    esc = (code < 0) | (code > 14)
-    code = np.where(esc, ESCAPE, code).astype(np.uint8)
-    nib = (code[:, 0::2] | (code[:, 1::2] << 4)).astype(np.uint8)
-    coded = np.concatenate([sm, nib], axis=1)
-    rows, cols = np.nonzero(esc)                       # row-major: sorted by row, then column
-    esc_off = np.zeros(n + 1, np.int32)
+    coded = np.empty((n, k * 3 // 2), np.uint8) if out is None else out.reshape(n, k * 3 // 2)
+    hi = (bits >> 8).astype(np.uint8)                       # sign | exponent[7:1]
+    lo = bits.astype(np.uint8)                              # exponent[0] | mantissa
+    np.bitwise_or(hi & 0x80, lo & 0x7F, out=coded[:, :k])
+    exp = ((hi & 0x7F) << 1) | (lo >> 7)                    # uint8 exponent
+    code = exp - np.uint8(base)                             # wraps for exponents below base
+    esc = code > 14
+    code[esc] = 15
+    np.bitwise_or(code[:, 0::2], code[:, 1::2] << 4, out=coded[:, k:])
+    rows, cols = np.nonzero(esc)                            # row-major: by row, then column
+    esc_off = np.zeros(n + 1, np.int64)
     np.add.at(esc_off, rows + 1, 1)
-    esc_off = np.cumsum(esc_off, dtype=np.int64).astype(np.int32)
+    esc_off = np.cumsum(esc_off).astype(np.int32)
     esc_ent = ((cols.astype(np.int64) << 8) | exp[rows, cols]).astype(np.int32)
     return coded, base, esc_off, esc_ent
 
@@ -122,8 +124,8 @@ class CodedShards:
             sid, name = job
             bits = weights.host_view(sid, name)
             o = self.shard_off[sid] + self.tensors[sid][name][0]
-            coded, base, e_off, e_ent = encode(bits)
-            buf[o:o + coded.nbytes] = coded.reshape(-1)
+            n_b = bits.shape[0] * bits.shape[1] * 3 // 2
+            _, base, e_off, e_ent = encode(bits, out=buf[o:o + n_b])
             return base, e_off, e_ent
 
         with ThreadPoolExecutor(max_workers=threads) as pool:
