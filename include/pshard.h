@@ -137,6 +137,13 @@ int ps_attn_prefill_tc(const float* q, int ldq, int batch, const int* q_start, c
  * ((role << 24) | (barrier << 16) | key block); reset clears it. */
 int ps_attn_tc_watchdog(unsigned* code, int reset);
 
+/* Device-side faults of every spin-wait with a timeout, in host-mapped memory (a plain
+ * host load, no CUDA call, no synchronisation): words[0] = expert-fetch sequence the
+ * wait gave up on, [1] = stripe sequence, [2] = tcgen05 attention barrier code,
+ * [3] = host-side fetcher timeout (sequence never published). All zero = healthy;
+ * reset clears them. The executor raises on any non-zero word after every pass. */
+int ps_fault_status(unsigned* words /* [4] */, int reset);
+
 /* Exponent-coded GEMV: y[t, n] (epi)= x[t, :] . W[n, :] with W in the 12-bit format of
  * runtime/wcomp.py (row n: K sign|mantissa bytes, then K/2 bytes of 4-bit exponent codes
  * relative to base_exp, 15 = escape looked up in esc_off[N + 1] / esc_ent (col << 8 | exp)).

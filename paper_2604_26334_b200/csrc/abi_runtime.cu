@@ -65,9 +65,50 @@ extern "C" int ps_preload_fetcher();
 int ps_preload_striper();
 int ps_preload_attention_tc();
 
-namespace ps { int g_pdl = 0; }
+namespace ps {
+int g_pdl = 0;
+
+namespace {
+std::once_flag g_fault_once;
+unsigned* g_fault_h = nullptr;
+unsigned* g_fault_d = nullptr;
+void fault_init() {
+  if (cudaHostAlloc(reinterpret_cast<void**>(&g_fault_h), 64, cudaHostAllocMapped | cudaHostAllocPortable) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    g_fault_h = nullptr;
+    return;
+  }
+  memset(g_fault_h, 0, 64);
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_fault_d), g_fault_h, 0) != cudaSuccess) {
+    cudaGetLastError();
+    g_fault_d = nullptr;
+  }
+}
+}  // namespace
+
+unsigned* fault_host() {
+  std::call_once(g_fault_once, fault_init);
+  return g_fault_h;
+}
+unsigned* fault_dev() {
+  std::call_once(g_fault_once, fault_init);
+  return g_fault_d;
+}
+}  // namespace ps
 
 extern "C" {
+
+int ps_fault_status(unsigned* words, int reset) {
+  volatile unsigned* h = ps::fault_host();
+  PS_REQUIRE(h != nullptr && ps::fault_dev() != nullptr, "ps_fault_status: no mapped fault words");
+  PS_REQUIRE(words != nullptr, "ps_fault_status: null argument");
+  for (int i = 0; i < ps::FAULT_WORDS; ++i) {
+    words[i] = h[i];
+    if (reset) h[i] = 0;
+  }
+  return PS_OK;
+}
 
 int ps_preload_kernels(int* n_loaded) {
   static int loaded = -1;

@@ -33,8 +33,11 @@ constexpr int TC_BQ = 128, TC_BK = 128;
 
 // Watchdog for the pipeline barriers: a wait that spins for more than 1 s records
 // where it was stuck (role, barrier, block) and lets the kernel finish (wrong
-// output, never a hung GPU). Read with ps_attn_tc_watchdog().
+// output, never a hung GPU) and raises FAULT_ATTN in the host-mapped fault words
+// (common.cuh), which the executor checks after every pass. Read with
+// ps_attn_tc_watchdog() / ps_fault_status().
 __device__ unsigned g_attn_tc_stuck = 0;
+__device__ unsigned* g_attn_tc_fault = nullptr;
 
 __device__ __forceinline__ void wait_wd(uint64_t* bar, uint32_t parity, unsigned code) {
   uint32_t done = 0;
@@ -51,6 +54,7 @@ __device__ __forceinline__ void wait_wd(uint64_t* bar, uint32_t parity, unsigned
     if (it == 0) t0 = t;
     else if (t - t0 > 1000000000ull) {
       atomicCAS(&g_attn_tc_stuck, 0u, code);
+      if (g_attn_tc_fault) raise_fault(g_attn_tc_fault, FAULT_ATTN, code);
       return;
     }
   }
@@ -432,6 +436,8 @@ int ps_preload_attention_tc() {
   int n = 0;
   touch_kernel(attn_prefill_tc_kernel<64>, n);
   touch_kernel(attn_prefill_tc_kernel<128>, n);
+  unsigned* f = fault_dev();
+  if (cudaMemcpyToSymbol(g_attn_tc_fault, &f, sizeof(f)) != cudaSuccess) cudaGetLastError();
   return n;
 }
 

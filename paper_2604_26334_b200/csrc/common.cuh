@@ -93,6 +93,21 @@ namespace ps {
 // an earlier kernel writes or reads; both are no-ops for a normal launch.
 extern int g_pdl;   // ps_set_pdl(): launch_k() adds the PDL attribute while set
 
+// ---- device-side faults ----------------------------------------------------------
+// Spin-waits that give up (fetcher flag, stripe flags, tcgen05 attention barriers)
+// record a code in ONE host-mapped word array instead of hanging the GPU; the host
+// reads it with a plain load after every pass (ps_fault_status) and raises, so a
+// timed-out wait can never return wrong tokens silently. Slots: FAULT_FETCH (the
+// sequence number the expert wait gave up on), FAULT_STRIPE (stripe seq),
+// FAULT_ATTN (role/barrier code of tcgen05 attention), FAULT_HOST (host-side code).
+enum { FAULT_FETCH = 0, FAULT_STRIPE = 1, FAULT_ATTN = 2, FAULT_HOST = 3, FAULT_WORDS = 4 };
+unsigned* fault_host();     // host address of the words (mapped, zero-initialised)
+unsigned* fault_dev();      // device alias of the same words
+__device__ __forceinline__ void raise_fault(unsigned* words, int slot, unsigned code) {
+  atomicCAS_system(words + slot, 0u, code ? code : 1u);
+  __threadfence_system();
+}
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 

@@ -76,7 +76,8 @@ moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ 
 }
 
 __global__ void wait_flag_kernel(const volatile unsigned* __restrict__ flag, unsigned seq,
-                                 unsigned* __restrict__ error_flag, unsigned long long timeout_ns) {
+                                 unsigned* __restrict__ error_flag, unsigned* fault,
+                                 unsigned long long timeout_ns) {
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   while (true) {
@@ -86,6 +87,7 @@ __global__ void wait_flag_kernel(const volatile unsigned* __restrict__ flag, uns
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > timeout_ns) {
       atomicExch(error_flag, seq);
+      if (fault) raise_fault(fault, FAULT_FETCH, seq);
       break;
     }
     __nanosleep(200);
@@ -179,7 +181,15 @@ class ExpertFetcher {
         }
       }
       std::atomic_thread_fence(std::memory_order_acquire);
-      unsigned n = seen ? (unsigned)(pub_host_[0] & 0xffffffffu) : 0;
+      if (!seen) {
+        // the GPU never published this layer: copy nothing and do NOT raise the
+        // sequence flag, so the wait kernel times out and faults instead of letting
+        // the expert kernels read whatever the slots hold
+        volatile unsigned* fw = fault_host();
+        if (fw && fw[FAULT_HOST] == 0) fw[FAULT_HOST] = j.seq ? j.seq : 1;
+        continue;
+      }
+      unsigned n = (unsigned)(pub_host_[0] & 0xffffffffu);
       if (n > (unsigned)max_experts_) n = 0, error_.store(2);
       // one copy per run of consecutive expert ids when host and slot strides agree
       // (slots are in ascending-id order, so the run is contiguous on both sides)
@@ -307,7 +317,7 @@ int ps_moe_publish(void* f, const int* ids, int P, int E, int* slot_of_expert, u
 int ps_wait_flag(void* f, unsigned seq, void* stream) {
   auto* x = static_cast<ExpertFetcher*>(f);
   PS_REQUIRE(x != nullptr, "ps_wait_flag: null fetcher");
-  wait_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(x->flag_dev(), seq, x->flag_dev() + 1,
+  wait_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(x->flag_dev(), seq, x->flag_dev() + 1, fault_dev(),
                                                       2000000000ull /* 2 s */);
   PS_CHECK_LAUNCH();
   return PS_OK;

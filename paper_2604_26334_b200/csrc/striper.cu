@@ -70,7 +70,7 @@ __global__ void stripe_signal_kernel(volatile uint32_t* go, uint32_t seq) {
 }
 
 __global__ void stripe_wait_kernel(const volatile uint32_t* done, int n, uint32_t seq, uint32_t* err,
-                                   unsigned long long timeout_ns) {
+                                   unsigned* fault, unsigned long long timeout_ns) {
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int j = 0; j < n; ++j) {
@@ -79,6 +79,7 @@ __global__ void stripe_wait_kernel(const volatile uint32_t* done, int n, uint32_
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > timeout_ns) {
         atomicExch(err, seq);
+        if (fault) raise_fault(fault, FAULT_STRIPE, seq);
         return;
       }
       __nanosleep(200);
@@ -170,7 +171,8 @@ int ps_stripe_signal(void* ctl_dev, unsigned seq, void* stream) {
 // Leader GPU, on its compute stream before a striped piece's first consumer.
 int ps_stripe_wait(void* done_dev, int n_helpers, unsigned seq, void* stream) {
   auto* done = static_cast<uint32_t*>(done_dev);
-  stripe_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(done, n_helpers, seq, done + 64, 2000000000ull);
+  stripe_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(done, n_helpers, seq, done + 64, fault_dev(),
+                                                        2000000000ull);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

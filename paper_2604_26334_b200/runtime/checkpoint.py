@@ -131,11 +131,30 @@ def open_checkpoint(path: str | os.PathLike):
 
 # -- config.json -> (ModelSpec, Arch) -----------------------------------------------
 
+SUPPORTED_ARCHS = frozenset({"LlamaForCausalLM", "Qwen3ForCausalLM", "Qwen3MoeForCausalLM"})
+SUPPORTED_MODEL_TYPES = frozenset({"llama", "qwen3", "qwen3_moe"})
+
 def spec_from_hf_config(cfg: dict, name: str | None = None, max_context: int | None = None,
                         seed: int = 0) -> tuple[ModelSpec, Arch]:
     """Llama / Qwen3 / Qwen3-MoE config.json -> the planner's ModelSpec (bf16
     everywhere) and the numerics the spec does not carry."""
     arch_name = (cfg.get("architectures") or [""])[0]
+    model_type = cfg.get("model_type", "")
+    if arch_name not in SUPPORTED_ARCHS and model_type not in SUPPORTED_MODEL_TYPES:
+        raise SpecError(f"unsupported architecture {arch_name or '?'} / model_type {model_type or '?'}: "
+                        f"this build executes {sorted(SUPPORTED_ARCHS)}")
+    for key, bad in (("attention_bias", True), ("mlp_bias", True)):
+        if cfg.get(key) == bad:
+            raise SpecError(f"config sets {key}={bad}: biased projections are not implemented")
+    act = cfg.get("hidden_act", "silu")
+    if act != "silu":
+        raise SpecError(f"hidden_act {act!r} is not implemented (SwiGLU with silu only)")
+    if cfg.get("use_sliding_window"):
+        raise SpecError("sliding-window attention is not implemented")
+    if cfg.get("mlp_only_layers"):
+        raise SpecError("mlp_only_layers (dense layers inside a MoE model) are not implemented")
+    if cfg.get("num_experts") and cfg.get("decoder_sparse_step", 1) != 1:
+        raise SpecError("decoder_sparse_step != 1 (dense layers inside a MoE model) is not implemented")
     d = cfg["hidden_size"]
     heads = cfg["num_attention_heads"]
     moe = None
@@ -229,6 +248,16 @@ def fill_from_checkpoint(layout: WeightLayout, blob: np.ndarray, embed: np.ndarr
             full[parity::2] = src
         return rows * cols * 2
 
+    consumed = {hf_name(j[0], tied) for j in jobs} | {"model.embed_tokens.weight"}
+    names = getattr(ckpt, "where", None)
+    if names is not None:
+        # every weight the checkpoint carries must be one the layout executes: a tensor
+        # left over (biases, extra norms, another architecture's blocks) would be
+        # silently ignored and the outputs would be wrong
+        extra = sorted(n for n in names if n not in consumed and not n.endswith("rotary_emb.inv_freq"))
+        if extra:
+            raise FormatError(f"checkpoint tensors this layout does not consume: {extra[:8]}"
+                              f"{' ...' if len(extra) > 8 else ''} ({len(extra)} total)")
     with ThreadPoolExecutor(max_workers=threads) as pool:
         total = sum(pool.map(run, jobs))
     e = ckpt.bf16("model.embed_tokens.weight", (spec.vocab_size, spec.d_model))

@@ -47,6 +47,24 @@ class GenerateResult:
     switches: list = field(default_factory=list)
 
 
+@dataclass
+class _Session:
+    """Loop state of one request batch (the counters of `simulate_inference`)."""
+    prompts: list
+    prompt_left: list
+    gen_left: list
+    fed: list                          # prompt tokens fed so far, per request
+    out: list                          # tokens read back so far, per request
+    pending_host: list = field(default_factory=list)   # sampling passes not read yet
+    last_sampled: list | None = None
+    last_rows: int = 1
+    passes: list = field(default_factory=list)
+    switches: list = field(default_factory=list)
+    migration: int = 0
+    ttft: float | None = None
+    t_start: float = field(default_factory=time.perf_counter)
+
+
 class Engine:
     """Plan + weights + executor for one model under one VRAM budget."""
 
@@ -107,6 +125,7 @@ class Engine:
                                         self.batch)
         self.migration_aware = migration_aware
         self.striper = striper        # runtime.striping.StripeLeader: helper GPUs pull stripes
+        self._sess: _Session | None = None
 
     # -- tier selection over reachable tiers (pick_tier, planner.py:451-460) --
     def pick_tier(self, n_new: int) -> int:
@@ -196,97 +215,167 @@ class Engine:
         ex = self._ensure_executor(self.max_pass_tokens(prompt_lens, gen_len))
         return ex.set_tier(self.pick_tier(len(prompt_lens)))
 
-    # ------------------------------------------------------------------ generate
-    def generate(self, prompts: list, gen_len: int, timing: bool = True,
-                 on_pass=None) -> GenerateResult:
-        """Greedy generation for a batch of prompts, following the reference
-        loop: each iteration picks the tier for the outstanding new tokens,
-        feeds prompt chunks (a finished prompt emits its first token) or one
-        decode token per request."""
+    # ------------------------------------------------- one iteration at a time
+    def submit(self, prompts: list, gen_len: int) -> None:
+        """Start a request batch: `prompts` (one int array per request slot) each
+        to be followed by `gen_len` greedy tokens. No GPU work; the batch then
+        advances one reference iteration per `prefill()` / `decode()` call
+        (`pkg/src/shardplan/simulator.py:273-297`), or all at once in `generate()`."""
         if not prompts:
             raise SpecError("generate needs at least one request")
         if len(prompts) > self.batch:
             raise SpecError(f"{len(prompts)} requests exceed the planned batch of {self.batch}")
+        if gen_len < 1:
+            raise SpecError(f"gen_len must be >= 1, got {gen_len}")
         prompts = [np.asarray(p, np.int32) for p in prompts]
-        n = len(prompts)
+        if min(len(p) for p in prompts) < 1:
+            raise SpecError("every prompt needs at least one token")
         if max(len(p) for p in prompts) + gen_len > self.context_len:
             raise SpecError("prompt + gen exceeds the planned context length")
-        ex = self._ensure_executor(self.max_pass_tokens([len(p) for p in prompts], gen_len))
-        prompt_left = [len(p) for p in prompts]
-        gen_left = [gen_len] * n
-        fed = [0] * n                      # prompt tokens fed so far
-        out = [[] for _ in range(n)]
-        pending_host = []                  # passes whose tokens we have not read yet
-        t_start = time.perf_counter()
-        ttft = None
-        decode_time = 0.0
-        decode_tokens = 0
-        passes = []
-        migration = 0
-        last_sampled = None
-        switches = []
-        while any(p > 0 for p in prompt_left) or any(g > 0 for g in gen_left):
-            n_out = outstanding_tokens(prompt_left, gen_left)
-            rows = max(ex.kv_len) if ex.kv_len else 0
-            if self.migration_aware:
-                tier = self.migration.pick_tier(n_out, ex.tier, rows, self.machine)
-            else:
-                tier = self.pick_tier(n_out)
-            if tier != ex.tier:
-                prev = ex.tier
-                moved = ex.set_tier(tier)
-                migration += moved
-                switches.append((prev, tier, rows, moved, self.migration.bytes(prev, tier, rows)))
-            step = schedule_iteration(tier, prompt_left, gen_left)
-            slots, n_new, p0, ids, sample = [], [], [], [], []
-            decode_ids_from_device = True
-            for i in range(n):
-                if step.prompt_take[i]:
-                    k = step.prompt_take[i]
-                    slots.append(i); n_new.append(k); p0.append(fed[i])
-                    ids.append(prompts[i][fed[i]:fed[i] + k])
-                    fed[i] += k
-                    decode_ids_from_device = False
-                elif step.decode[i]:
-                    slots.append(i); n_new.append(1); p0.append(len(prompts[i]) + len(out[i]) - 1 +
-                                                              self._pending_count(pending_host, i))
-                    ids.append(None)
-                if step.emits[i]:
-                    sample.append(len(slots) - 1)
-            if decode_ids_from_device and last_sampled == slots:
-                ids_arr = None
-            else:
-                self._drain(ex, pending_host, out)
-                ids_arr = np.concatenate([a if a is not None else
-                                          np.array([out[slots[j]][-1]], np.int32)
-                                          for j, a in enumerate(ids)]).astype(np.int32)
-                # decode positions are exact once drained
-                for j, a in enumerate(ids):
-                    if a is None:
-                        p0[j] = len(prompts[slots[j]]) + len(out[slots[j]]) - 1
-            ev0 = L.event_create(True) if timing else 0
-            if timing:
-                L.call("ps_event_record", ev0, ex.cs)
-            if on_pass is not None:
-                on_pass(len(passes), tier, ex)       # e.g. attach / detach a tracer
-            stats = ex.run_pass(PassSpec(slots, n_new, p0, ids_arr, sample))
-            if sample:
-                pending_host.append([slots[j] for j in sample])
-                last_sampled = [slots[j] for j in sample]
-            ev1 = 0
-            if timing:
-                ev1 = L.event_create(True)
-                L.call("ps_event_record", ev1, ex.cs)
-            passes.append([tier, stats.T, ev0, ev1, stats.bytes_streamed,
-                           step.context_consumed == 0 and step.decoded > 0, stats.zero_copy_bytes])
-            if step.first_prompt_done and ttft is None:
-                self._drain(ex, pending_host, out)   # first token is on the host
-                ttft = time.perf_counter() - t_start
-        self._drain(ex, pending_host, out)
+        self._ensure_executor(self.max_pass_tokens([len(p) for p in prompts], gen_len))
+        n = len(prompts)
+        self._sess = _Session(prompts, [len(p) for p in prompts], [gen_len] * n, [0] * n,
+                              [[] for _ in range(n)])
+
+    @property
+    def outstanding(self) -> int:
+        """New tokens the next iteration would be planned for (0: batch finished)."""
+        s = self._sess
+        return 0 if s is None else outstanding_tokens(s.prompt_left, s.gen_left)
+
+    def prefill(self, prompts: list | None = None, gen_len: int | None = None) -> dict:
+        """One iteration that consumes prompt tokens (a chunk of every unfinished
+        prompt that fits the picked tier, plus one decode token of each request
+        already past its prompt — the reference's mixed iteration). With
+        `prompts`, starts a new batch first (`gen_len` defaults to 1). Returns
+        {request slot: token id} of the requests whose final prompt chunk ran."""
+        if prompts is not None:
+            self.submit(prompts, 1 if gen_len is None else gen_len)
+        s = self._need_session()
+        if not any(p > 0 for p in s.prompt_left):
+            raise SpecError("prefill(): no prompt tokens outstanding (call decode())")
+        return self._finish_step(self._iterate())
+
+    def decode(self) -> dict:
+        """One decode-only iteration: one new token for every request that still
+        has tokens to generate. Returns {request slot: token id}."""
+        s = self._need_session()
+        if any(p > 0 for p in s.prompt_left):
+            raise SpecError("decode(): prompt tokens outstanding (call prefill())")
+        if not any(g > 0 for g in s.gen_left):
+            raise SpecError("decode(): every request has generated its tokens")
+        return self._finish_step(self._iterate())
+
+    def logits(self) -> np.ndarray:
+        """fp32 logits [rows, V] of the last iteration's emitting requests, in slot order."""
+        return self._need_executor().logits_host(self._sess.last_rows if self._sess else 1)
+
+    def tokens(self) -> list:
+        """Tokens generated so far, per request slot."""
+        s = self._need_session()
+        self._drain(self.executor, s.pending_host, s.out)
+        return [np.array(o, np.int32) for o in s.out]
+
+    def _need_session(self) -> "_Session":
+        if getattr(self, "_sess", None) is None:
+            raise SpecError("no request batch: call submit() or prefill(prompts)")
+        return self._sess
+
+    def _need_executor(self) -> Executor:
+        if self.executor is None:
+            raise SpecError("no pass has run yet")
+        return self.executor
+
+    def _finish_step(self, emitted: list) -> dict:
+        s = self._sess
+        self._drain(self.executor, s.pending_host, s.out)
+        return {slot: int(s.out[slot][-1]) for slot in emitted}
+
+    def _iterate(self, timing: bool = False, on_pass=None) -> list:
+        """The loop body of `simulate_inference` (`simulator.py:273-297`) as one GPU
+        pass: pick the tier for the outstanding new tokens (switching residency if it
+        changes), feed prompt chunks / one decode token per request in request order,
+        run the pass. Token ids are read back lazily; returns the emitting slots."""
+        s, ex = self._sess, self.executor
+        n = len(s.prompts)
+        n_out = outstanding_tokens(s.prompt_left, s.gen_left)
+        rows = max(ex.kv_len) if ex.kv_len else 0
+        if self.migration_aware:
+            tier = self.migration.pick_tier(n_out, ex.tier, rows, self.machine)
+        else:
+            tier = self.pick_tier(n_out)
+        if tier != ex.tier:
+            prev = ex.tier
+            moved = ex.set_tier(tier)
+            s.migration += moved
+            s.switches.append((prev, tier, rows, moved, self.migration.bytes(prev, tier, rows)))
+        step = schedule_iteration(tier, s.prompt_left, s.gen_left)
+        slots, n_new, p0, ids, sample = [], [], [], [], []
+        decode_ids_from_device = True
+        for i in range(n):
+            if step.prompt_take[i]:
+                k = step.prompt_take[i]
+                slots.append(i); n_new.append(k); p0.append(s.fed[i])
+                ids.append(s.prompts[i][s.fed[i]:s.fed[i] + k])
+                s.fed[i] += k
+                decode_ids_from_device = False
+            elif step.decode[i]:
+                slots.append(i); n_new.append(1)
+                p0.append(len(s.prompts[i]) + len(s.out[i]) - 1 + self._pending_count(s.pending_host, i))
+                ids.append(None)
+            if step.emits[i]:
+                sample.append(len(slots) - 1)
+        if decode_ids_from_device and s.last_sampled == slots:
+            ids_arr = None
+        else:
+            self._drain(ex, s.pending_host, s.out)
+            ids_arr = np.concatenate([a if a is not None else
+                                      np.array([s.out[slots[j]][-1]], np.int32)
+                                      for j, a in enumerate(ids)]).astype(np.int32)
+            for j, a in enumerate(ids):      # decode positions are exact once drained
+                if a is None:
+                    p0[j] = len(s.prompts[slots[j]]) + len(s.out[slots[j]]) - 1
+        ev0 = L.event_create(True) if timing else 0
+        if timing:
+            L.call("ps_event_record", ev0, ex.cs)
+        if on_pass is not None:
+            on_pass(len(s.passes), tier, ex)       # e.g. attach / detach a tracer
+        stats = ex.run_pass(PassSpec(slots, n_new, p0, ids_arr, sample))
+        emitted = [slots[j] for j in sample]
+        if sample:
+            s.pending_host.append(emitted)
+            s.last_sampled = emitted
+            s.last_rows = len(sample)
+        ev1 = 0
+        if timing:
+            ev1 = L.event_create(True)
+            L.call("ps_event_record", ev1, ex.cs)
+        s.passes.append([tier, stats.T, ev0, ev1, stats.bytes_streamed,
+                         step.context_consumed == 0 and step.decoded > 0, stats.zero_copy_bytes])
+        if step.first_prompt_done and s.ttft is None:
+            self._drain(ex, s.pending_host, s.out)   # first token is on the host
+            s.ttft = time.perf_counter() - s.t_start
+        ex.check_errors()
+        return emitted
+
+    # ------------------------------------------------------------------ generate
+    def generate(self, prompts: list, gen_len: int, timing: bool = True,
+                 on_pass=None) -> GenerateResult:
+        """Greedy generation for a batch of prompts: `submit` then the reference
+        loop (`simulator.py:273-297`) of `prefill()` / `decode()` iterations until
+        every request has its `gen_len` tokens, with tokens read back lazily."""
+        self.submit(prompts, gen_len)
+        s, ex = self._sess, self.executor
+        s.t_start = time.perf_counter()
+        while outstanding_tokens(s.prompt_left, s.gen_left):
+            self._iterate(timing, on_pass)
+        self._drain(ex, s.pending_host, s.out)
         ex.synchronize()
-        total = time.perf_counter() - t_start
+        ex.check_errors()
+        total = time.perf_counter() - s.t_start
+        decode_time, decode_tokens = 0.0, 0
         pass_rows = []
-        for tier, T, e0, e1, nbytes, is_decode, zc in passes:
+        for tier, T, e0, e1, nbytes, is_decode, zc in s.passes:
             secs = L.event_elapsed_ms(e0, e1) / 1e3 if timing else float("nan")
             # (tier, tokens, seconds, bytes via the copy engine, bytes read zero-copy)
             pass_rows.append((tier, T, secs, nbytes, zc))
@@ -296,15 +385,11 @@ class Engine:
             if timing:
                 L.call("ps_event_destroy", e0)
                 L.call("ps_event_destroy", e1)
-        if ttft is None:
-            ttft = total
-        # decode throughput: device time from the end of the last context pass to the
-        # end of the last decode pass (passes overlap their copies, so per-pass
-        # compute-stream intervals undercount the pipelined wall time)
+        ttft = total if s.ttft is None else s.ttft
         tps = decode_tokens / decode_time if decode_time > 0 else float("inf")
-        return GenerateResult([np.array(o, np.int32) for o in out], ttft, tps,
+        return GenerateResult([np.array(o, np.int32) for o in s.out], ttft, tps,
                               ttft + 100.0 / tps if tps else float("inf"),
-                              decode_tokens, decode_time, pass_rows, migration, switches)
+                              decode_tokens, decode_time, pass_rows, s.migration, s.switches)
 
     @staticmethod
     def _pending_count(pending_host, slot) -> int:

@@ -1149,6 +1149,19 @@ class Executor:
         t = self.arena.tensor(self.logits, rows * self.V * 4).view(torch.float32)
         return t.reshape(rows, self.V).cpu().numpy()
 
+    def check_errors(self) -> None:
+        """Raise if any device-side wait gave up or the fetcher failed: a timed-out
+        wait lets its kernel finish on stale ring / slot bytes, so the pass's tokens
+        are invalid. Host-mapped fault words (a plain load, no synchronisation), plus
+        the fetcher's host-side error code."""
+        L.raise_on_fault()
+        if self.fetcher is not None:
+            err = C.c_int()
+            L.call("ps_fetcher_info", self.fetcher, None, None, None, None, C.byref(err))
+            if err.value:
+                raise L.DeviceFault(f"expert fetcher host error {err.value} "
+                                    "(1: routing never published, 2: bad expert id, 3: copy failed)")
+
     def synchronize(self) -> None:
         for s in (self.cs, self.h2d, self.d2h):
             L.call("ps_stream_synchronize", s)

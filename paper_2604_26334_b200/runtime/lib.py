@@ -54,6 +54,7 @@ _SIGS = {
     "ps_attn_decode": [_p, _i, _i, _i, _i, _i, _p, _p, _ll, _ll, _p, _i, _f, _p, _i, _p, _ll, _p],
     "ps_attn_prefill_tc": [_p, _i, _i, _p, _p, _p, _i, _i, _i, _i, _p, _ll, _ll, _i, _f, _p, _i, _i, _p],
     "ps_attn_tc_watchdog": [C.POINTER(C.c_uint), _i],
+    "ps_fault_status": [C.POINTER(C.c_uint), _i],
     "ps_attn_decode_workspace": [_i, _i, _i, _i, C.POINTER(_ll)],
     "ps_attn_prefill": [_p, _i, _i, _p, _p, _p, _i, _i, _i, _i, _p, _ll, _ll, _f, _p, _i, _i, _p],
     "ps_upload_small": [_p, _p, _i, _p],
@@ -145,6 +146,29 @@ def call(name: str, *args) -> int:
         msg = lib().ps_last_error().decode(errors="replace")
         raise PshardError(f"{name} failed ({rc}): {msg}")
     return rc
+
+
+class DeviceFault(PshardError):
+    """A device-side spin-wait gave up (expert fetch, stripe, tcgen05 attention
+    barrier) or the fetcher's host thread timed out: the pass's results are invalid."""
+
+
+FAULT_NAMES = ("expert-fetch wait timed out at sequence", "stripe wait timed out at sequence",
+               "tcgen05 attention barrier watchdog code", "fetcher host thread never saw sequence")
+
+
+def fault_status(reset: bool = False) -> tuple:
+    """The four host-mapped fault words (csrc/common.cuh); a plain host read."""
+    w = (C.c_uint * 4)()
+    call("ps_fault_status", w, 1 if reset else 0)
+    return tuple(int(x) for x in w)
+
+
+def raise_on_fault() -> None:
+    w = fault_status()
+    if any(w):
+        fault_status(reset=True)
+        raise DeviceFault("; ".join(f"{n} {v:#x}" for n, v in zip(FAULT_NAMES, w) if v))
 
 
 def attn_decode_workspace(batch: int, n_heads: int, head_dim: int, max_len: int) -> int:

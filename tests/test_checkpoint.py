@@ -191,6 +191,36 @@ def test_rejects_bad_files(tmp_path):
         ck.spec_from_hf_config(dict(LLAMA31_8B, rope_scaling={"rope_type": "yarn", "factor": 4.0}))
 
 
+@pytest.mark.parametrize("change", [
+    {"architectures": ["Qwen2ForCausalLM"], "model_type": "qwen2"},
+    {"attention_bias": True}, {"mlp_bias": True}, {"hidden_act": "gelu"},
+    {"use_sliding_window": True, "sliding_window": 4096}])
+def test_rejects_configs_it_cannot_execute(change):
+    """Configs whose numerics this build does not implement are refused instead of
+    loading as plain Llama (biases, other activations, sliding windows, other archs)."""
+    from paper_2604_26334_b200.planning.faults import SpecError
+    with pytest.raises(SpecError):
+        ck.spec_from_hf_config(dict(LLAMA31_8B, **change))
+    with pytest.raises(SpecError):
+        ck.spec_from_hf_config(dict(QWEN3_30B_A3B, mlp_only_layers=[0]))
+
+
+def test_rejects_checkpoint_with_unconsumed_tensors(tmp_path):
+    """A q_proj.bias (a Qwen2-style checkpoint) is a tensor the layout does not consume:
+    loading fails loudly instead of dropping it."""
+    from paper_2604_26334_b200.planning.faults import FormatError
+    spec = catalog.builtin_model("tiny-llama")
+    arch = arch_for(spec)
+    tensors = _hf_tensors(spec, arch, np.random.default_rng(2), tied=False, f32_names=set())
+    tensors["model.layers.0.self_attn.q_proj.bias"] = ("BF16", (spec.n_heads * spec.head_dim,),
+                                                       np.zeros(spec.n_heads * spec.head_dim, np.uint16))
+    _write(tmp_path, spec, arch, tensors, shards=1)
+    lay = WeightLayout(spec, arch)
+    with pytest.raises(FormatError, match="q_proj.bias"):
+        ck.fill_from_checkpoint(lay, np.zeros(lay.total_bytes, np.uint8), np.zeros(lay.embed_bytes, np.uint8),
+                                ck.Checkpoint(tmp_path))
+
+
 # -- GGUF (runtime/gguf.py) ---------------------------------------------------------
 
 def test_gguf_rope_permutation_is_llama_cpp_order():

@@ -474,3 +474,44 @@ def test_spare_pins_same_tokens_fewer_link_bytes(monkeypatch, model, frac):
     assert out["1"][0] == out["0"][0]
     assert out["1"][2], "no spare pin was made"
     assert out["1"][1] < out["0"][1], (out["1"][1], out["0"][1])
+
+
+@pytest.mark.parametrize("model,frac,lens", [("tiny-llama", 0.5, [128]), ("tiny-llama", 0.5, [100, 60, 128]),
+                                             ("tiny-moe", 0.9, [40])])
+def test_prefill_decode_api_equals_generate(model, frac, lens):
+    """The public one-iteration calls: `prefill()` / `decode()` are single iterations of
+    the reference loop (`pkg/src/shardplan/simulator.py:273-297`) and `generate()` is
+    built on them, so stepping by hand gives the same tokens and the same logits."""
+    from paper_2604_26334_b200.planning.faults import SpecError
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model(model)
+    prompts = [_prompt(n, spec.vocab_size, seed=40 + i) for i, n in enumerate(lens)]
+    gen = 6
+    eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=len(lens))
+    want = eng.generate(prompts, gen_len=gen)
+    want_logits = eng.logits().copy()
+    eng.close()
+    eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=len(lens))
+    with pytest.raises(SpecError):
+        eng.decode()                        # no batch submitted
+    eng.submit(prompts, gen)
+    with pytest.raises(SpecError):
+        eng.decode()                        # prompts outstanding
+    first = {}
+    while any(p > 0 for p in eng._sess.prompt_left):
+        first.update(eng.prefill())
+    assert sorted(first) == list(range(len(lens)))
+    steps = 0
+    while eng.outstanding:
+        emitted = eng.decode()
+        assert sorted(emitted) == list(range(len(lens)))
+        steps += 1
+    with pytest.raises(SpecError):
+        eng.decode()                        # every request finished
+    got = eng.tokens()
+    got_logits = eng.logits()
+    eng.close()
+    assert steps == gen - 1
+    for a, b in zip(got, want.tokens):
+        assert np.array_equal(a, b)
+    assert np.array_equal(got_logits, want_logits)
