@@ -345,7 +345,7 @@ def run_ours(args, rank: int, world: int) -> dict:
         "clocks": clocks.summary(),
         "ttft": {"ms": round(res.ttft_s * 1e3, 2), "migration_bytes": int(res.migration_bytes),
                  "relocated_in_vram_bytes": int(ex.d2d_bytes),
-                 "switches": [{"from": a, "to": b, "kv_rows": r, "moved": mv, "model_h2d": h, "model_d2h": dd}
+                 "switches": [{"from": a, "to": b, "kv_pages": r, "moved": mv, "model_h2d": h, "model_d2h": dd}
                               for a, b, r, mv, (h, dd) in res.switches],
                  "prefill_pass_ms": round(res.passes[0][2] * 1e3, 2) if res.passes else None},
         "model_load_s": round(eng.load_seconds, 2),

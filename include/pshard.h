@@ -104,35 +104,39 @@ int ps_gemm_bf16_cfg(const void* A, int M, int K, long long lda, const void* B, 
 int ps_rmsnorm(const float* x, int ldx, const int* rows, int n_rows, const void* w, int d,
                float eps, void* out, int ldo, int out_bf16, void* stream);
 int ps_qkv_rope_append(float* qkv, int ldq, int t, int n_heads, int n_kv, int head_dim,
-                       const int* pos, const int* req, void* kv_base, long long kv_req_stride,
-                       long long kv_row_stride, const void* rope_cs, const void* q_norm,
-                       const void* k_norm, float eps, void* stream);
+                       const int* pos, const int* req, void* kv_pool, int row_elems,
+                       const int* block_table, int bt_stride, int page_rows, const void* rope_cs,
+                       const void* q_norm, const void* k_norm, float eps, void* stream);
 
 /* ---- K4: attention (GQA / MHA) ----------------------------------------------
- * Replaces GQA/MHA requests (`pkg/src/shardplan/model_graph.py:154-161`).
- * Per-layer KV layout: bf16 [position][request slot][K heads | V heads]; the row of
- * request b at position p is kv_base + slot(b) * kv_req_stride + p * kv_row_stride
- * (elements); slot(b) = req_slot[b], or b when req_slot is NULL. kv_base may be a
- * VRAM-pinned cache, a ring-staged copy of a host cache, or host-mapped memory. */
+ * Replaces GQA/MHA requests (`pkg/src/shardplan/model_graph.py:154-161`) over a PAGED
+ * KV cache (KV shard sizing `:299-304,331`): a layer's cache is a pool of pages of
+ * page_rows positions (a power of two >= 64) of ONE request each, a row being bf16
+ * [K heads | V heads] (row_elems = 2 * n_kv * head_dim). Request slot s's position p is
+ * row p % page_rows of physical page block_table[s * bt_stride + p / page_rows]; one
+ * block table serves every layer. slot(b) = req_slot[b], or b when req_slot is NULL.
+ * kv_pool may be a VRAM-pinned pool, a ring-staged window of a host pool (pages at the
+ * same page offsets), or host-mapped memory. */
 int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, int n_kv, int head_dim,
-                   const int* req_slot, const void* kv_base, long long kv_req_stride,
-                   long long kv_row_stride, const int* lens, int max_len, float scale, float* out,
+                   const int* req_slot, const void* kv_pool, int row_elems, const int* block_table,
+                   int bt_stride, int page_rows, const int* lens, int max_len, float scale, float* out,
                    int ldo, float* workspace, long long workspace_floats, void* stream);
 /* Workspace floats ps_attn_decode needs for this shape (0 when one split covers max_len). */
 int ps_attn_decode_workspace(int batch, int n_heads, int head_dim, int max_len, long long* floats);
 int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_start, const int* p0,
                     const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
-                    const void* kv_base, long long kv_req_stride, long long kv_row_stride,
-                    float scale, void* out, int ldo, int out_bf16, void* stream);
+                    const void* kv_pool, int row_elems, const int* block_table, int bt_stride,
+                    int page_rows, float scale, void* out, int ldo, int out_bf16, void* stream);
 
 /* Same attention on the tcgen05 tensor cores (attention_tc.cu): S and O accumulate in
- * TMEM, K/V tiles arrive by TMA from the cache viewed as a 4-D tensor
- * [positions kv_positions][slots][2*n_kv heads][head_dim] (so kv_req_stride must be
- * 2*n_kv*head_dim and kv_row_stride a multiple of it). head_dim 64 or 128. */
+ * TMEM, K/V tiles arrive by TMA from the page pool viewed as a 3-D tensor
+ * [pool_pages * page_rows][2 * n_kv heads][head_dim], one 64-row box per page half-tile
+ * at the block-table row. head_dim 64 or 128. */
 int ps_attn_prefill_tc(const float* q, int ldq, int batch, const int* q_start, const int* p0,
                        const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
-                       const void* kv_base, long long kv_req_stride, long long kv_row_stride,
-                       int kv_positions, float scale, void* out, int ldo, int out_bf16, void* stream);
+                       const void* kv_pool, int row_elems, const int* block_table, int bt_stride,
+                       int page_rows, int pool_pages, float scale, void* out, int ldo, int out_bf16,
+                       void* stream);
 /* Pipeline watchdog of ps_attn_prefill_tc: non-zero = a barrier wait gave up after 1 s
  * ((role << 24) | (barrier << 16) | key block); reset clears it. */
 int ps_attn_tc_watchdog(unsigned* code, int reset);
@@ -145,14 +149,15 @@ int ps_attn_tc_watchdog(unsigned* code, int reset);
 int ps_fault_status(unsigned* words /* [4] */, int reset);
 
 /* Exponent-coded GEMV: y[t, n] (epi)= x[t, :] . W[n, :] with W in the 12-bit format of
- * runtime/wcomp.py (row n: K sign|mantissa bytes, then K/2 bytes of 4-bit exponent codes
- * relative to base_exp, 15 = escape looked up in esc_off[N + 1] / esc_ent (col << 8 | exp)).
- * Same decomposition and accumulation order as ps_gemv_bf16's bulk-copy kernel, so the
- * result is bit-identical to ps_gemv_bf16 on the decoded weights; 25 % fewer weight
- * bytes. t <= 8, K % 256 == 0, Wc 16-byte aligned (device memory). */
-int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int N, int K, int base_exp,
-                  const int* esc_off, const int* esc_ent, float* y, int ldy, int epilogue,
-                  void* stream);
+ * runtime/wcomp.py: row n (stride ldw bytes) = K sign|mantissa bytes, K/2 bytes of 4-bit
+ * exponent codes relative to the row's base (15 = escape), then a trailer of ldw - 1.5 K
+ * bytes (16..256): uint32 [base | n_esc << 8, (col << 8 | exp) x n_esc, 0xFFFFFFFF ...].
+ * Every row carries its own base and escapes, so one bulk copy per row segment brings
+ * everything the decoder needs into shared memory. Same decomposition and accumulation
+ * order as ps_gemv_bf16's bulk-copy kernel: bit-identical to ps_gemv_bf16 on the decoded
+ * weights, with 25 % fewer weight bytes. t <= 8, K % 256 == 0, Wc 16-byte aligned. */
+int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int N, int K, long long ldw,
+                  float* y, int ldy, int epilogue, void* stream);
 
 /* Programmatic dependent launch for the decode-pass kernels (rmsnorm, qkv/RoPE,
  * decode attention + merge, GEMVs, embed, argmax, add, small uploads): while on,
@@ -263,6 +268,11 @@ int ps_init_uniform_bf16(void* dst, size_t n, unsigned long long seed, unsigned 
 /* Gate/up rows interleaved for the fused SwiGLU epilogue: rows [row_begin, row_begin + n_rows)
  * of the [2 * rows_each x cols] interleaved matrix; row 2j is tensor a's row j (seed_a),
  * row 2j+1 tensor b's row j (seed_b); element (j, c) uses counter j * cols + c. */
+/* Output-head init: element i of a [rows x cols] tensor (from `offset`) is the uniform
+ * value of ps_init_uniform_bf16 (bias 0) with scale * s_row, s_row = min(u^-1/2, 64) from
+ * the row's own hash (heavy-tailed row norms: a clear top-1 logit). */
+int ps_init_rowscaled_bf16(void* dst, size_t n, unsigned long long seed, unsigned long long offset,
+                           long long cols, float scale, void* stream);
 int ps_init_interleaved_bf16(void* dst, long long rows_each, long long row_begin, long long n_rows,
                              int cols, unsigned long long seed_a, unsigned long long seed_b,
                              float scale, float bias, void* stream);

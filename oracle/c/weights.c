@@ -8,6 +8,11 @@
  *   w  = fmaf(2u - 1, scale, bias)            single rounding (C99 fmaf)
  *   out = bf16 round-to-nearest-even of w
  *
+ * Output head (ps_init_rowscaled_bf16): scale is multiplied by the row's
+ *   s_r = min(1 / sqrtf(u_r), 64), u_r = ((z_r >> 40) + 0.5) * 2^-24,
+ *   z_r = splitmix64 finaliser of ((seed ^ 0xD1B54A32D192ED03) XOR (row * 0x9E3779B97F4A7C15))
+ * (correctly rounded IEEE sqrt / div / min / mul on both sides), bias 0.
+ *
  * The reference (`shardplan`) has no weights at all; this
  * file is the only definition of model load the parity tests check against.
  */
@@ -35,6 +40,23 @@ static inline uint16_t value(uint64_t seed, uint64_t idx, float scale, float bia
   uint64_t z = mix64(seed ^ (idx * 0x9E3779B97F4A7C15ull));
   float u = (float)(z >> 40) * (1.0f / 16777216.0f);
   return f32_to_bf16_rne(fmaf(2.0f * u - 1.0f, scale, bias));
+}
+
+static inline float head_row_scale(uint64_t seed, uint64_t row) {
+  uint64_t z = mix64((seed ^ 0xD1B54A32D192ED03ull) ^ (row * 0x9E3779B97F4A7C15ull));
+  float u = ((float)(z >> 40) + 0.5f) * (1.0f / 16777216.0f);
+  float s = 1.0f / sqrtf(u);
+  return s < 64.0f ? s : 64.0f;
+}
+
+/* n elements of a [rows x cols] output head from element `offset` (heavy-tailed rows) */
+void oracle_init_rowscaled_bf16(uint16_t* dst, size_t n, uint64_t seed, uint64_t offset, long long cols,
+                                float scale) {
+  for (size_t i = 0; i < n; ++i) {
+    uint64_t e = offset + i;
+    volatile float sr = scale * head_row_scale(seed, e / (uint64_t)cols);
+    dst[i] = value(seed, e, sr, 0.0f);
+  }
 }
 
 typedef struct { uint16_t* dst; size_t lo, hi; uint64_t seed, offset; float scale, bias; } job_t;

@@ -14,6 +14,12 @@ initialiser (oracle/c/weights.c), independent of the product's GPU init; the
 tests check both bit-for-bit. Compute is fp32 on the bf16 weight values; the
 KV cache is rounded to bf16 when stored, as the product stores it.
 
+Two uses: the plain fp32 model (`modes=None`) is the north_star's "fp32
+reference" for the logit tolerance (max|d| / max|ref| <= 2e-2); with `modes`
+(one of D / P / G per token, recorded by the engine per pass) it applies the
+same bf16 rounding points as the GPU pass that computed each token, so greedy
+ids can be required EXACTLY equal — what remains is fp32 summation order.
+
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg use
 this module.
 """
@@ -44,6 +50,8 @@ def _lib():
                                                  C.c_float, C.c_float, C.c_int]
         lib.oracle_init_interleaved_bf16.argtypes = [C.c_void_p, C.c_longlong, C.c_int, C.c_uint64,
                                                      C.c_uint64, C.c_float, C.c_float]
+        lib.oracle_init_rowscaled_bf16.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64,
+                                                   C.c_longlong, C.c_float]
         lib.oracle_bf16_to_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
         _LIB = lib
     return _LIB
@@ -68,6 +76,9 @@ def scale_bias(name: str, fan_in: int):
 def bf16_bits(model_seed: int, name: str, rows: int, cols: int) -> np.ndarray:
     out = np.empty((rows, cols), np.uint16)
     sc, bi = scale_bias(name, cols)
+    if name == "lm_head":   # heavy-tailed row norms (oracle/c/weights.c head_row_scale)
+        _lib().oracle_init_rowscaled_bf16(out.ctypes.data, out.size, seed_of(model_seed, name), 0, cols, sc)
+        return out
     _lib().oracle_init_uniform_bf16(out.ctypes.data, out.size, seed_of(model_seed, name), 0,
                                     sc, bi, THREADS)
     return out
@@ -187,30 +198,42 @@ class RefModel:
                 full = hw.host_view(*views[f"{layer}.wqkv"])
                 lo = {"wq": 0, "wk": h * hd, "wv": (h + kv) * hd}[leaf]
                 return _bf16_tensor(full[lo:lo + rows])
-            if leaf in ("w_gate", "w_up"):
-                full = hw.host_view(*views[f"{layer}.wgu"])
-                return _bf16_tensor(full[0::2] if leaf == "w_gate" else full[1::2])
-            if leaf == "w_down":
-                return _bf16_tensor(hw.host_view(*views[f"{layer}.wdown"]))
+            expert, _, proj = leaf.rpartition(".")       # "e7.w_gate" -> ("e7", "w_gate")
+            pre = f"{layer}.{expert}." if expert else f"{layer}."
+            if proj in ("w_gate", "w_up"):
+                full = hw.host_view(*views[pre + "wgu"])
+                return _bf16_tensor(full[0::2] if proj == "w_gate" else full[1::2])
+            if proj == "w_down":
+                return _bf16_tensor(hw.host_view(*views[pre + "wdown"]))
             return _bf16_tensor(hw.host_view(*views[name]))
         return cls(hp, lazy=lazy, source=source)
 
     def _w(self, t: torch.Tensor) -> torch.Tensor:
         return t.float() if self.lazy else t
 
-    def _moe(self, f, lw):
-        """Qwen3-MoE block: softmax router, top-k, renormalised weights
-        (norm_topk_prob), sum of the selected SwiGLU experts."""
+    def _moe(self, f, lw, g_rows):
+        """Qwen3-MoE block: softmax router, top-k (ties -> lower id), renormalised weights
+        (norm_topk_prob), sum of the selected SwiGLU experts in top-k slot order.
+        Vectorised by expert: the rows routed to expert e go through it together.
+        GEMM-pass rows feed the router and experts the bf16 rounding of `f` (the
+        product's expert kernels read bf16 activations and keep h in fp32)."""
         k = self.moe["top_k"]
-        probs = torch.softmax(f @ self._w(lw["router"]).T, dim=-1)
-        w, ids = torch.topk(probs, k, dim=-1)
+        fin = _round_rows(f, g_rows)
+        probs = torch.softmax(fin @ self._w(lw["router"]).T, dim=-1)
+        # stable descending sort: equal probabilities keep ascending expert ids
+        order = torch.sort(probs, dim=-1, descending=True, stable=True)
+        w, ids = order.values[:, :k], order.indices[:, :k]
         w = w / w.sum(-1, keepdim=True)
-        out = torch.zeros_like(f)
-        for t in range(f.shape[0]):
-            for j in range(k):
-                wg, wu, wd = (self._w(m) for m in lw["experts"][int(ids[t, j])])
-                h = torch.nn.functional.silu(f[t] @ wg.T) * (f[t] @ wu.T)
-                out[t] += w[t, j] * (h @ wd.T)
+        contrib = torch.zeros(f.shape[0], k, f.shape[1])
+        for e in torch.unique(ids).tolist():
+            rows, slots = torch.nonzero(ids == e, as_tuple=True)
+            wg, wu, wd = (self._w(m) for m in lw["experts"][e])
+            xe = fin[rows]
+            h = torch.nn.functional.silu(xe @ wg.T) * (xe @ wu.T)
+            contrib[rows, slots] = w[rows, slots][:, None] * (h @ wd.T)
+        out = contrib[:, 0]
+        for j in range(1, k):
+            out = out + contrib[:, j]
         return out
 
     def _rms(self, x, w):
@@ -228,17 +251,75 @@ class RefModel:
         return [{"k": torch.zeros(0, self.kvh, self.hd), "v": torch.zeros(0, self.kvh, self.hd)}
                 for _ in self.layers]
 
+    def _attn_fp32(self, q, K, V, pos):
+        """Exact fp32 causal softmax attention (the split-KV decode kernel's numerics)."""
+        G = self.h // self.kvh
+        K, V = K.repeat_interleave(G, dim=1), V.repeat_interleave(G, dim=1)
+        S = K.shape[0]
+        scores = torch.einsum("thd,shd->hts", q, K) / math.sqrt(self.hd)
+        mask = torch.arange(S)[None, :] > pos[:, None]
+        scores = scores.masked_fill(mask[None], float("-inf"))
+        return torch.einsum("hts,shd->thd", torch.softmax(scores, -1), V).reshape(q.shape[0], -1)
+
+    def _attn_tc(self, q, K, V, pos, block: int = 128):
+        """The tcgen05 flash-attention kernel's numerics (csrc/attention_tc.cu): Q scaled
+        by scale*log2(e) then rounded to bf16; per 128-key block a base-2 online softmax
+        with the running max, P rounded to bf16 before P V, l summed from fp32 p, and
+        the output multiplied by 1/l."""
+        G = self.h // self.kvh
+        T = q.shape[0]
+        sl2 = np.float32(1.0 / math.sqrt(self.hd)) * np.float32(1.4426950408889634)
+        qs = bf16_round(q * float(sl2)).permute(1, 0, 2)               # [h, T, hd]
+        Kr = K.repeat_interleave(G, dim=1).permute(1, 0, 2)            # [h, S, hd]
+        Vr = V.repeat_interleave(G, dim=1).permute(1, 0, 2)
+        n_keys = int(pos.max()) + 1
+        m = torch.full((self.h, T, 1), float("-inf"))
+        l = torch.zeros(self.h, T, 1)
+        o = torch.zeros(self.h, T, self.hd)
+        for k0 in range(0, n_keys, block):
+            k1 = min(n_keys, k0 + block)
+            sc = qs @ Kr[:, k0:k1].transpose(1, 2)                      # [h, T, blk]
+            mask = torch.arange(k0, k1)[None, :] > pos[:, None]
+            sc = sc.masked_fill(mask[None], float("-inf"))
+            m_new = torch.maximum(m, sc.amax(-1, keepdim=True))
+            base = torch.where(torch.isinf(m_new), torch.zeros_like(m_new), m_new)
+            corr = torch.exp2(m - base)
+            p = torch.exp2(sc - base)
+            l = l * corr + p.sum(-1, keepdim=True)
+            o = o * corr + bf16_round(p) @ Vr[:, k0:k1]
+            m = m_new
+        inv = torch.where(l > 0, 1.0 / l, torch.zeros_like(l))
+        return (o * inv).permute(1, 0, 2).reshape(T, -1)
+
     @torch.no_grad()
-    def forward(self, tokens, cache) -> torch.Tensor:
-        """Append `tokens` to one request's cache; returns fp32 logits [T, V]."""
+    def forward(self, tokens, cache, modes=None, logit_rows=None) -> torch.Tensor:
+        """Append `tokens` to one request's cache; returns fp32 logits [rows, V].
+
+        `modes` (one character per token, default all "D") mirrors where the GPU pass
+        that computed each token rounds to bf16 (runtime/executor.py):
+          "D"  decode-only GEMV pass: fp32 activations, fp32 split-KV attention;
+          "P"  GEMV pass (<= 32 tokens) with the tcgen05 prefill attention: fp32
+               activations, bf16 Q and P inside attention (`_attn_tc`);
+          "G"  GEMM pass (> 32 tokens): the normalised input of every matmul rounded to
+               bf16, tcgen05 attention with a bf16 output, SwiGLU output rounded to bf16.
+        The residual stream, router logits, expert hidden states and the output head
+        are fp32 in every mode; K and V are stored as bf16. `logit_rows`: rows whose
+        logits to return (default all)."""
         tokens = torch.as_tensor(np.asarray(tokens, np.int64))
         T = tokens.numel()
+        modes = "D" * T if modes is None else modes
+        if len(modes) != T or set(modes) - set("DPG"):
+            raise ValueError(f"modes must be {T} characters of D/P/G")
+        mode_arr = np.frombuffer(modes.encode(), np.uint8)
+        g_rows = torch.from_numpy(mode_arr == ord("G"))
+        tc_idx = torch.from_numpy(np.nonzero(mode_arr != ord("D"))[0])
+        d_idx = torch.from_numpy(np.nonzero(mode_arr == ord("D"))[0])
+        any_g = bool(g_rows.any())
         p0 = cache[0]["k"].shape[0]
         pos = torch.arange(p0, p0 + T)
         x = self.embed[tokens].float()
-        G = self.h // self.kvh
         for lw, c in zip(self.layers, cache):
-            a = self._rms(x, self._w(lw["attn_norm"]))
+            a = _round_rows(self._rms(x, self._w(lw["attn_norm"])), g_rows)
             q = (a @ self._w(lw["wq"]).T).view(T, self.h, self.hd)
             k = (a @ self._w(lw["wk"]).T).view(T, self.kvh, self.hd)
             v = (a @ self._w(lw["wv"]).T).view(T, self.kvh, self.hd)
@@ -248,42 +329,61 @@ class RefModel:
             q, k = self._rope(q, pos), self._rope(k, pos)
             c["k"] = torch.cat([c["k"], bf16_round(k)])
             c["v"] = torch.cat([c["v"], bf16_round(v)])
-            K = c["k"].repeat_interleave(G, dim=1)      # [S, h, hd]
-            Vv = c["v"].repeat_interleave(G, dim=1)
-            S = K.shape[0]
-            scores = torch.einsum("thd,shd->hts", q, K) / math.sqrt(self.hd)
-            mask = torch.arange(S)[None, :] > pos[:, None]
-            scores = scores.masked_fill(mask[None], float("-inf"))
-            o = torch.einsum("hts,shd->thd", torch.softmax(scores, -1), Vv).reshape(T, -1)
+            o = torch.empty(T, self.h * self.hd)
+            if len(d_idx):
+                o[d_idx] = self._attn_fp32(q[d_idx], c["k"], c["v"], pos[d_idx])
+            if len(tc_idx):
+                o[tc_idx] = self._attn_tc(q[tc_idx], c["k"], c["v"], pos[tc_idx])
+            o = _round_rows(o, g_rows)
             x = x + o @ self._w(lw["wo"]).T
             f = self._rms(x, self._w(lw["ffn_norm"]))
             if self.moe:
-                x = x + self._moe(f, lw)
+                x = x + self._moe(f, lw, g_rows)
             else:
+                f = _round_rows(f, g_rows)
                 g, u = f @ self._w(lw["w_gate"]).T, f @ self._w(lw["w_up"]).T
-                x = x + (torch.nn.functional.silu(g) * u) @ self._w(lw["w_down"]).T
+                hid = torch.nn.functional.silu(g) * u
+                if any_g:
+                    hid = _round_rows(hid, g_rows)
+                x = x + hid @ self._w(lw["w_down"]).T
+        if logit_rows is not None:
+            x = x[torch.as_tensor(np.asarray(logit_rows, np.int64))]
         return self._rms(x, self._w(self.final_norm)) @ self._w(self.lm_head).T
 
     @torch.no_grad()
-    def greedy(self, prompt, gen_len: int):
+    def greedy(self, prompt, gen_len: int, modes=None):
+        """Free-running greedy decode; `modes` (len(prompt) + gen_len - 1 characters,
+        see `forward`) mirrors the passes that computed each position."""
+        modes = modes or "D" * (len(prompt) + gen_len - 1)
         cache = self.new_cache()
-        logits = self.forward(prompt, cache)[-1:]
+        n = len(prompt)
+        logits = self.forward(prompt, cache, modes[:n], logit_rows=[n - 1])
         toks, all_logits = [], [logits[0]]
-        for _ in range(gen_len):
+        for i in range(gen_len):
             t = int(torch.argmax(all_logits[-1]))
             toks.append(t)
             if len(toks) == gen_len:
                 break
-            all_logits.append(self.forward([t], cache)[0])
+            all_logits.append(self.forward([t], cache, modes[n + i])[0])
         return np.array(toks, np.int32), torch.stack(all_logits)
 
     @torch.no_grad()
-    def teacher_forced(self, prompt, continuation):
-        """Logits at each emitting position when the continuation is forced."""
+    def teacher_forced(self, prompt, continuation, modes=None):
+        """Logits at each emitting position when the continuation is forced, in one
+        forward over prompt + continuation[:-1]; `modes` as in `forward`."""
         cache = self.new_cache()
         seq = list(np.asarray(prompt)) + list(np.asarray(continuation))[:-1]
-        logits = self.forward(seq, cache)
-        return logits[len(prompt) - 1:]
+        rows = list(range(len(prompt) - 1, len(seq)))
+        return self.forward(seq, cache, modes, logit_rows=rows)
+
+
+def _round_rows(x: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:
+    """bf16-round the rows of x selected by the boolean mask `rows`."""
+    if not bool(rows.any()):
+        return x
+    if bool(rows.all()):
+        return bf16_round(x)
+    return torch.where(rows.view(-1, *([1] * (x.dim() - 1))), bf16_round(x), x)
 
 
 def hp_from_spec(spec, arch) -> dict:

@@ -1,9 +1,9 @@
 // K4: attention over the per-request KV blocks, GQA/MHA.
 //
 // Prices: GQA (t, ctx, h, kv, hd) / MHA requests, flops 4*t*ctx*h*hd
-// (`pkg/src/shardplan/model_graph.py:154-161`). Cache rows are bf16
-// [pos][request slot][K heads | V heads] per layer: request b's row for
-// position p is kv_base + slot(b) * kv_req_stride + p * kv_row_stride.
+// (`pkg/src/shardplan/model_graph.py:154-161`). The cache is PAGED (KvPages,
+// common.cuh): request slot s's position p lives in physical page
+// table[s][p / page_rows], row p % page_rows; a row is bf16 [K heads | V heads].
 //
 // * decode (t = 1 per request): split-KV. Each CTA owns a contiguous range
 //   of positions for one kv head and all of its G query heads; a warp scores
@@ -28,8 +28,8 @@ namespace ps {
 #define PS_DECODE_CHUNK 128  // positions per split (4 warps x 32)
 template <int HD, int G>
 __global__ void __launch_bounds__(128)
-attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __restrict__ kv_base,
-                   long long kv_req_stride, long long kv_row_stride, const int* __restrict__ req_slot, const int* __restrict__ lens, int n_kv, int chunk, float scale,
+attn_decode_kernel(const float* __restrict__ q, int ldq, KvPages kv, const int* __restrict__ req_slot,
+                   const int* __restrict__ lens, int n_kv, int chunk, float scale,
                    float* __restrict__ out, int ldo, float* __restrict__ ws_o, float* __restrict__ ws_ml,
                    int n_splits) {
   pdl_trigger();
@@ -52,9 +52,10 @@ attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __
   }
   __syncthreads();
 
-  const __nv_bfloat16* base = kv_base + (long long)(req_slot ? req_slot[b] : b) * kv_req_stride;
-  const __nv_bfloat16* kcol = base + (long long)kvh * HD;
-  const __nv_bfloat16* vcol = base + (long long)(n_kv + kvh) * HD;
+  const int slot = req_slot ? req_slot[b] : b;
+  const __nv_bfloat16* kcol = kv.pool + (long long)kvh * HD;
+  const __nv_bfloat16* vcol = kv.pool + (long long)(n_kv + kvh) * HD;
+  const long long rs = kv.row_elems;
 
   float m[G], l[G], acc[G][PER];
 #pragma unroll
@@ -73,15 +74,17 @@ attn_decode_kernel(const float* __restrict__ q, int ldq, const __nv_bfloat16* __
     const int p = t0 + lane;
     const bool valid = p < end;
     const int cnt = min(32, end - t0);
+    // t0 is a multiple of 32 and pages hold >= 64 positions: the step's 32 rows are
+    // consecutive rows of one page
+    const long long r0 = kv.row(slot, t0);
     uint4 kk[HD / 8];
-    const uint4* krow = reinterpret_cast<const uint4*>(kcol + (long long)(valid ? p : t0) * kv_row_stride);
+    const uint4* krow = reinterpret_cast<const uint4*>(kcol + r0 + (long long)(valid ? lane : 0) * rs);
 #pragma unroll
     for (int c = 0; c < HD / 8; ++c) kk[c] = valid ? __ldg(krow + c) : make_uint4(0, 0, 0, 0);
     VT vv[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const VT* vrow = reinterpret_cast<const VT*>(vcol + (long long)(t0 + (j < cnt ? j : 0)) * kv_row_stride +
-                                                   lane * PER);
+      const VT* vrow = reinterpret_cast<const VT*>(vcol + r0 + (long long)(j < cnt ? j : 0) * rs + lane * PER);
       vv[j] = __ldg(vrow);
     }
     float s[G];
@@ -214,8 +217,8 @@ constexpr int PF_BQ = 64, PF_BK = 64;
 template <int HD>
 __global__ void __launch_bounds__(128)
 attn_prefill_kernel(const float* __restrict__ q, int ldq, const int* __restrict__ q_start,
-                    const int* __restrict__ p0s, const __nv_bfloat16* __restrict__ kv_base,
-                    long long kv_req_stride, long long kv_row_stride, const int* __restrict__ req_slot, int n_heads, int n_kv, float scale_log2, void* __restrict__ out,
+                    const int* __restrict__ p0s, KvPages kv, const int* __restrict__ req_slot, int n_heads,
+                    int n_kv, float scale_log2, void* __restrict__ out,
                     int ldo, int out_bf16) {
   constexpr int LDS = HD + 8;  // padded smem row (bf16)
   constexpr int KSTEPS = HD / 16;
@@ -261,7 +264,7 @@ attn_prefill_kernel(const float* __restrict__ q, int ldq, const int* __restrict_
 
   const int last_q = min(qt * PF_BQ + PF_BQ, n_new) - 1;
   const int kv_end = p0 + last_q + 1;  // keys [0, kv_end)
-  const __nv_bfloat16* base = kv_base + (long long)(req_slot ? req_slot[b] : b) * kv_req_stride;
+  const int slot = req_slot ? req_slot[b] : b;
 
   for (int k0 = 0; k0 < kv_end; k0 += PF_BK) {
     __syncthreads();
@@ -272,7 +275,7 @@ attn_prefill_kernel(const float* __restrict__ q, int ldq, const int* __restrict_
       int kp = k0 + r;
       uint4 kv4 = make_uint4(0, 0, 0, 0), vv4 = make_uint4(0, 0, 0, 0);
       if (kp < kv_end) {
-        const __nv_bfloat16* row = base + (long long)kp * kv_row_stride;
+        const __nv_bfloat16* row = kv.pool + kv.row(slot, kp);
         kv4 = *reinterpret_cast<const uint4*>(row + (long long)kvh * HD + c * 8);
         vv4 = *reinterpret_cast<const uint4*>(row + (long long)(n_kv + kvh) * HD + c * 8);
       }
@@ -370,12 +373,12 @@ attn_prefill_kernel(const float* __restrict__ q, int ldq, const int* __restrict_
 using namespace ps;
 
 template <int HD>
-static int decode_dispatch(int G, dim3 grid, cudaStream_t s, const float* q, int ldq, const __nv_bfloat16* base,
-                           long long req_stride, long long stride, const int* req_slot, const int* lens, int n_kv, int chunk, float scale, float* out, int ldo,
+static int decode_dispatch(int G, dim3 grid, cudaStream_t s, const float* q, int ldq, const KvPages& kv,
+                           const int* req_slot, const int* lens, int n_kv, int chunk, float scale, float* out, int ldo,
                            float* ws_o, float* ws_ml, int n_splits) {
 #define PS_DEC(GG)                                                                                       \
-  launch_k(attn_decode_kernel<HD, GG>, grid, 128, 0, s, q, ldq, base, req_stride, stride, req_slot, lens, n_kv, chunk, \
-           scale, out, ldo, ws_o, ws_ml, n_splits)
+  launch_k(attn_decode_kernel<HD, GG>, grid, 128, 0, s, q, ldq, kv, req_slot, lens, n_kv, chunk, scale, out, ldo, \
+           ws_o, ws_ml, n_splits)
   switch (G) {
     case 1: PS_DEC(1); break;
     case 2: PS_DEC(2); break;
@@ -397,12 +400,16 @@ extern "C" int ps_attn_decode_workspace(int batch, int n_heads, int head_dim, in
 }
 
 extern "C" int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, int n_kv, int head_dim,
-                              const int* req_slot, const void* kv_base, long long kv_req_stride,
-                              long long kv_row_stride, const int* lens, int max_len,
+                              const int* req_slot, const void* kv_pool, int row_elems, const int* block_table,
+                              int bt_stride, int page_rows, const int* lens, int max_len,
                               float scale, float* out, int ldo, float* workspace, long long workspace_floats,
                               void* stream) {
   PS_REQUIRE(n_heads % n_kv == 0, "ps_attn_decode: n_heads %% n_kv != 0");
   if (batch <= 0) return PS_OK;
+  KvPages kv;
+  PS_REQUIRE(kv_pages(kv, kv_pool, row_elems, block_table, bt_stride, page_rows) && row_elems == 2 * n_kv * head_dim,
+             "ps_attn_decode: bad paged cache (page_rows %d, bt_stride %d, row_elems %d)", page_rows, bt_stride,
+             row_elems);
   int G = n_heads / n_kv;
   int chunk = PS_DECODE_CHUNK;
   int n_splits = (max_len + chunk - 1) / chunk;
@@ -413,10 +420,9 @@ extern "C" int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, i
   float* ws_ml = workspace ? workspace + (long long)batch * n_heads * n_splits * head_dim : nullptr;
   dim3 grid(n_splits, n_kv, batch);
   cudaStream_t s = (cudaStream_t)stream;
-  auto base = static_cast<const __nv_bfloat16*>(kv_base);
   int rc;
-  if (head_dim == 128) rc = decode_dispatch<128>(G, grid, s, q, ldq, base, kv_req_stride, kv_row_stride, req_slot, lens, n_kv, chunk, scale, out, ldo, ws_o, ws_ml, n_splits);
-  else if (head_dim == 64) rc = decode_dispatch<64>(G, grid, s, q, ldq, base, kv_req_stride, kv_row_stride, req_slot, lens, n_kv, chunk, scale, out, ldo, ws_o, ws_ml, n_splits);
+  if (head_dim == 128) rc = decode_dispatch<128>(G, grid, s, q, ldq, kv, req_slot, lens, n_kv, chunk, scale, out, ldo, ws_o, ws_ml, n_splits);
+  else if (head_dim == 64) rc = decode_dispatch<64>(G, grid, s, q, ldq, kv, req_slot, lens, n_kv, chunk, scale, out, ldo, ws_o, ws_ml, n_splits);
   else { ps_set_error("ps_attn_decode: head_dim %d unsupported", head_dim); return PS_ERR_UNSUPPORTED; }
   if (rc || n_splits == 1) return rc;
   if (head_dim == 128)
@@ -429,18 +435,21 @@ extern "C" int ps_attn_decode(const float* q, int ldq, int batch, int n_heads, i
 
 extern "C" int ps_attn_prefill(const float* q, int ldq, int batch, const int* q_start, const int* p0,
                                const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
-                               const void* kv_base, long long kv_req_stride, long long kv_row_stride, float scale, void* out, int ldo, int out_bf16,
-                               void* stream) {
+                               const void* kv_pool, int row_elems, const int* block_table, int bt_stride,
+                               int page_rows, float scale, void* out, int ldo, int out_bf16, void* stream) {
   PS_REQUIRE(n_heads % n_kv == 0, "ps_attn_prefill: n_heads %% n_kv != 0");
   if (batch <= 0 || max_new <= 0) return PS_OK;
+  KvPages kv;
+  PS_REQUIRE(kv_pages(kv, kv_pool, row_elems, block_table, bt_stride, page_rows) && row_elems == 2 * n_kv * head_dim,
+             "ps_attn_prefill: bad paged cache (page_rows %d, bt_stride %d, row_elems %d)", page_rows, bt_stride,
+             row_elems);
   dim3 grid((max_new + PF_BQ - 1) / PF_BQ, n_heads, batch);
   float sl2 = scale * 1.4426950408889634f;
-  auto base = static_cast<const __nv_bfloat16*>(kv_base);
   cudaStream_t s = (cudaStream_t)stream;
   if (head_dim == 128)
-    attn_prefill_kernel<128><<<grid, 128, 0, s>>>(q, ldq, q_start, p0, base, kv_req_stride, kv_row_stride, req_slot, n_heads, n_kv, sl2, out, ldo, out_bf16);
+    attn_prefill_kernel<128><<<grid, 128, 0, s>>>(q, ldq, q_start, p0, kv, req_slot, n_heads, n_kv, sl2, out, ldo, out_bf16);
   else if (head_dim == 64)
-    attn_prefill_kernel<64><<<grid, 128, 0, s>>>(q, ldq, q_start, p0, base, kv_req_stride, kv_row_stride, req_slot, n_heads, n_kv, sl2, out, ldo, out_bf16);
+    attn_prefill_kernel<64><<<grid, 128, 0, s>>>(q, ldq, q_start, p0, kv, req_slot, n_heads, n_kv, sl2, out, ldo, out_bf16);
   else { ps_set_error("ps_attn_prefill: head_dim %d unsupported", head_dim); return PS_ERR_UNSUPPORTED; }
   PS_CHECK_LAUNCH();
   return PS_OK;

@@ -12,8 +12,10 @@
 //              online softmax, rescales its O row in TMEM when the max moves
 //              (tcgen05.ld/st), writes its P row (bf16) to smem; epilogue O / l.
 //   warp 4     TMA producer: K and V tiles of 128 positions x 64 dims straight from the
-//              paged KV cache ([pos][slot][K heads | V heads], one 4-D tensor map),
-//              2-stage ring, 128-byte swizzle.
+//              paged KV cache: one 3-D tensor map over the page pool [pool rows][K heads |
+//              V heads][hd], a 128-key tile = two 64-row boxes, each at the row its page's
+//              block-table entry names (keys past the request's end: an out-of-range box,
+//              zero-filled by TMA); 2-stage ring, 128-byte swizzle.
 //   warp 5     MMA issuer (one lane): S = Q K^T (M=128, N=128 keys, K=hd; both K-major)
 //              into TMEM columns [0,128); O += P V (M=128, N=hd, K=128 keys; A=P
 //              K-major, B=V MN-major) into columns [128, 128+hd).
@@ -136,6 +138,15 @@ __device__ __forceinline__ void tm_st32(uint32_t taddr, const float (&v)[32]) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -176,6 +187,7 @@ template <int HD>
 __global__ void __launch_bounds__(192, 1)
 attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const float* __restrict__ q, int ldq,
                        const int* __restrict__ q_start, const int* __restrict__ p0s, const int* __restrict__ req_slot,
+                       const int* __restrict__ table, int bt_stride, int page_shift, int pool_rows,
                        int n_heads, int n_kv, float scale_log2, void* __restrict__ out, int ldo, int out_bf16,
                        int dbg) {
   constexpr int DH = HD / 64;                 // 64-wide dim sub-tiles
@@ -232,33 +244,48 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const float* 
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kv_map)) : "memory");
+      const int* bt = table + (long long)slot * bt_stride;
+      const int pmask = (1 << page_shift) - 1;
       for (int j = 0; j < nkb; ++j) {
         const int s = j & 1;
         const uint32_t ph = (j >> 1) & 1;
+        int rows[2];                       // pool row of each 64-key half (pool_rows: past the end)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int key = j * TC_BK + hf * 64;
+          rows[hf] = key < kv_end ? (__ldg(bt + (key >> page_shift)) << page_shift) + (key & pmask) : pool_rows;
+        }
         wait_wd(&kv_empty[s], ph ^ 1, 0x01010000u | (j & 0xffff));
         mbar_expect_tx(&k_full[s], TILE);
 #pragma unroll
-        for (int dh = 0; dh < DH; ++dh) {
-          if (dbg & 8) asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&k_full[s])), "r"(TC_SUB) : "memory");
-          else tma_load_4d(sK + s * TILE + dh * TC_SUB, &kv_map, &k_full[s], dh * 64, kvh, slot, j * TC_BK);
-        }
+        for (int dh = 0; dh < DH; ++dh)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            if (dbg & 8) asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&k_full[s])), "r"(TC_SUB / 2) : "memory");
+            else tma_load_3d(sK + s * TILE + dh * TC_SUB + hf * (TC_SUB / 2), &kv_map, &k_full[s], dh * 64, kvh, rows[hf]);
+          }
         mbar_expect_tx(&v_full[s], TILE);
 #pragma unroll
-        for (int dh = 0; dh < DH; ++dh) {
-          if (dbg & 8) asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&v_full[s])), "r"(TC_SUB) : "memory");
-          else tma_load_4d(sV + s * TILE + dh * TC_SUB, &kv_map, &v_full[s], dh * 64, n_kv + kvh, slot, j * TC_BK);
-        }
+        for (int dh = 0; dh < DH; ++dh)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            if (dbg & 8) asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&v_full[s])), "r"(TC_SUB / 2) : "memory");
+            else tma_load_3d(sV + s * TILE + dh * TC_SUB + hf * (TC_SUB / 2), &kv_map, &v_full[s], dh * 64, n_kv + kvh,
+                             rows[hf]);
+          }
       }
     }
   } else if (warp == 5) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer (lane 0; the warp zeroes stale V rows) ----------------
     if (lane == 0) {
       wait_wd(q_ready, 0, 0x02010000u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-      for (int j = 0; j < nkb; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
+    }
+    const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      if (lane == 0) {
         wait_wd(&k_full[s], ph, 0x02020000u | (j & 0xffff));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t aK = smem_u32(sK + s * TILE);
@@ -272,6 +299,22 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const float* 
         commit_to(s_full);
         wait_wd(p_full, j & 1, 0x02030000u | (j & 0xffff));
         wait_wd(&v_full[s], ph, 0x02040000u | (j & 0xffff));
+      }
+      __syncwarp();
+      const int valid = kv_end - j * TC_BK;     // keys of this block that exist
+      if (valid < TC_BK) {
+        // rows past the request's end inside its last page hold stale bytes (maybe NaN):
+        // P is 0 there but 0 * NaN is not, so zero them before O += P V. A 128-B row of a
+        // 128B-swizzled sub-tile stays in its own 128-B line, whatever the swizzle.
+        for (int i = lane; i < (TC_BK - valid) * DH * 8; i += 32) {
+          const int r = valid + i / (DH * 8), c = i % (DH * 8);
+          *reinterpret_cast<uint4*>(sV + s * TILE + (c >> 3) * TC_SUB + r * 128 + (c & 7) * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+      }
+      if (lane == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t aV = smem_u32(sV + s * TILE);
         if (!(dbg & 2)) {
@@ -285,6 +328,7 @@ attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const float* 
         commit_to(&kv_empty[s]);
         commit_to(o_done);
       }
+      __syncwarp();
     }
   } else {
     // ---------------- softmax warps: thread i owns query row i ----------------
@@ -408,8 +452,8 @@ typedef CUresult (*EncodeTiledFn4)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 
 template <int HD>
 static int launch_tc(const CUtensorMap& map, const float* q, int ldq, int batch, const int* q_start, const int* p0,
-                     const int* req_slot, int max_new, int n_heads, int n_kv, float scale_log2, void* out, int ldo,
-                     int out_bf16, cudaStream_t s) {
+                     const int* req_slot, const int* table, int bt_stride, int page_shift, int pool_rows, int max_new,
+                     int n_heads, int n_kv, float scale_log2, void* out, int ldo, int out_bf16, cudaStream_t s) {
   constexpr int TILE = (HD / 64) * TC_SUB;
   constexpr int SMEM = 5 * TILE + 2 * TC_SUB + 1024 + 128;
   static bool attr = false;
@@ -423,8 +467,8 @@ static int launch_tc(const CUtensorMap& map, const float* q, int ldq, int batch,
     const char* e = getenv("PS_ATTN_TC_DBG");
     dbg = e ? atoi(e) : 0;
   }
-  attn_prefill_tc_kernel<HD><<<grid, 192, SMEM, s>>>(map, q, ldq, q_start, p0, req_slot, n_heads, n_kv, scale_log2,
-                                                     out, ldo, out_bf16, dbg);
+  attn_prefill_tc_kernel<HD><<<grid, 192, SMEM, s>>>(map, q, ldq, q_start, p0, req_slot, table, bt_stride, page_shift,
+                                                     pool_rows, n_heads, n_kv, scale_log2, out, ldo, out_bf16, dbg);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -452,34 +496,40 @@ extern "C" int ps_attn_tc_watchdog(unsigned* code, int reset) {
 
 extern "C" int ps_attn_prefill_tc(const float* q, int ldq, int batch, const int* q_start, const int* p0,
                                   const int* req_slot, int max_new, int n_heads, int n_kv, int head_dim,
-                                  const void* kv_base, long long kv_req_stride, long long kv_row_stride,
-                                  int kv_positions, float scale, void* out, int ldo, int out_bf16, void* stream) {
+                                  const void* kv_pool, int row_elems, const int* block_table, int bt_stride,
+                                  int page_rows, int pool_pages, float scale, void* out, int ldo, int out_bf16,
+                                  void* stream) {
   using namespace ps;
   PS_REQUIRE(head_dim == 64 || head_dim == 128, "ps_attn_prefill_tc: head_dim %d unsupported", head_dim);
   PS_REQUIRE(n_heads % n_kv == 0, "ps_attn_prefill_tc: n_heads %% n_kv != 0");
-  PS_REQUIRE(kv_req_stride == 2LL * n_kv * head_dim && kv_row_stride % kv_req_stride == 0,
-             "ps_attn_prefill_tc: KV layout must be [pos][slot][K heads | V heads] (req stride %lld, row %lld)",
-             kv_req_stride, kv_row_stride);
-  PS_REQUIRE(((uintptr_t)kv_base & 15) == 0 && ldq % 4 == 0, "ps_attn_prefill_tc: alignment");
+  KvPages kv;
+  PS_REQUIRE(kv_pages(kv, kv_pool, row_elems, block_table, bt_stride, page_rows) && row_elems == 2 * n_kv * head_dim,
+             "ps_attn_prefill_tc: bad paged cache (page_rows %d, bt_stride %d, row_elems %d)", page_rows, bt_stride,
+             row_elems);
+  PS_REQUIRE(pool_pages >= 1, "ps_attn_prefill_tc: pool_pages %d", pool_pages);
+  PS_REQUIRE(((uintptr_t)kv_pool & 15) == 0 && ldq % 4 == 0, "ps_attn_prefill_tc: alignment");
   if (batch <= 0 || max_new <= 0) return PS_OK;
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult qr;
   PS_CHECK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
   PS_REQUIRE(fn && qr == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
-  const long long slots = kv_row_stride / kv_req_stride;
+  const long long pool_rows = (long long)pool_pages * page_rows;
+  PS_REQUIRE(pool_rows < (1LL << 31), "ps_attn_prefill_tc: pool of %lld rows", pool_rows);
   CUtensorMap map;
-  cuuint64_t dims[4] = {(cuuint64_t)head_dim, (cuuint64_t)(2 * n_kv), (cuuint64_t)slots, (cuuint64_t)kv_positions};
-  cuuint64_t strides[3] = {(cuuint64_t)head_dim * 2, (cuuint64_t)kv_req_stride * 2, (cuuint64_t)kv_row_stride * 2};
-  cuuint32_t box[4] = {64, 1, 1, (cuuint32_t)TC_BK};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)head_dim, (cuuint64_t)(2 * n_kv), (cuuint64_t)pool_rows};
+  cuuint64_t strides[2] = {(cuuint64_t)head_dim * 2, (cuuint64_t)row_elems * 2};
+  cuuint32_t box[3] = {64, 1, 64};
+  cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = reinterpret_cast<EncodeTiledFn4>(fn)(
-      &map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(kv_base), dims, strides, box, estr,
+      &map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(kv_pool), dims, strides, box, estr,
       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   PS_REQUIRE(r == CUDA_SUCCESS, "ps_attn_prefill_tc: cuTensorMapEncodeTiled failed (%d)", (int)r);
   const float sl2 = scale * 1.4426950408889634f;
   cudaStream_t s = (cudaStream_t)stream;
   if (head_dim == 128)
-    return launch_tc<128>(map, q, ldq, batch, q_start, p0, req_slot, max_new, n_heads, n_kv, sl2, out, ldo, out_bf16, s);
-  return launch_tc<64>(map, q, ldq, batch, q_start, p0, req_slot, max_new, n_heads, n_kv, sl2, out, ldo, out_bf16, s);
+    return launch_tc<128>(map, q, ldq, batch, q_start, p0, req_slot, block_table, bt_stride, kv.page_shift,
+                          (int)pool_rows, max_new, n_heads, n_kv, sl2, out, ldo, out_bf16, s);
+  return launch_tc<64>(map, q, ldq, batch, q_start, p0, req_slot, block_table, bt_stride, kv.page_shift,
+                       (int)pool_rows, max_new, n_heads, n_kv, sl2, out, ldo, out_bf16, s);
 }

@@ -75,6 +75,38 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return red[0];
 }
 
+// ---- paged KV cache ----------------------------------------
+// A layer's cache is a pool of pages; a page holds 2^page_shift consecutive positions of
+// ONE request, each a row of row_elems bf16 ([K heads | V heads]). table[slot *
+// bt_stride + p >> page_shift] is the physical page holding request slot's position p
+// (the same block table serves every layer). Pages are allocated on demand by the
+// executor, in any order; kernels only ever touch pages the table names.
+struct KvPages {
+  __nv_bfloat16* pool;
+  const int* table;
+  int bt_stride;
+  int page_shift;
+  int row_elems;
+  __device__ __forceinline__ long long row(int slot, int p) const {
+    const int pg = __ldg(table + (long long)slot * bt_stride + (p >> page_shift));
+    return ((((long long)pg) << page_shift) + (p & ((1 << page_shift) - 1))) * row_elems;
+  }
+};
+
+// Host side: validate the C-ABI arguments of a paged cache and build the descriptor.
+// page_rows must be a power of two >= 64 (a 64-position TMA box never crosses a page).
+inline bool kv_pages(KvPages& kv, const void* pool, int row_elems, const int* table, int bt_stride,
+                     int page_rows) {
+  if (!pool || !table || bt_stride < 1 || row_elems < 1 || page_rows < 64 || (page_rows & (page_rows - 1)))
+    return false;
+  kv.pool = static_cast<__nv_bfloat16*>(const_cast<void*>(pool));
+  kv.table = table;
+  kv.bt_stride = bt_stride;
+  kv.page_shift = __builtin_ctz((unsigned)page_rows);
+  kv.row_elems = row_elems;
+  return true;
+}
+
 }  // namespace ps
 
 // Module preloading: touch a kernel so CUDA's lazy loader loads it now. Every TU

@@ -31,6 +31,31 @@ __global__ void init_uniform_bf16_kernel(__nv_bfloat16* dst, size_t n, uint64_t 
   }
 }
 
+// Heavy-tailed row scale of the output head (margin-robust init, SURVEY.md §7 hard part 7):
+// s_r = min(u_r^(-1/2), 64), u_r in (0, 1) from the row's own hash — Pareto(alpha = 2)
+// row norms, so the top-1 logit of a random-init model usually stands clear of the
+// runner-up and greedy ids are robust to bf16 rounding noise. Every step is a correctly
+// rounded IEEE op (sqrt, div, min, mul), so the C oracle reproduces it bit for bit.
+__device__ __forceinline__ float head_row_scale(uint64_t seed, uint64_t row) {
+  uint64_t z = mix64((seed ^ 0xD1B54A32D192ED03ull) ^ (row * 0x9E3779B97F4A7C15ull));
+  float u = ((float)(z >> 40) + 0.5f) * (1.0f / 16777216.0f);   // (0, 1), exact
+  return fminf(__fdiv_rn(1.0f, __fsqrt_rn(u)), 64.0f);
+}
+
+__global__ void init_rowscaled_bf16_kernel(__nv_bfloat16* dst, size_t n, uint64_t seed, uint64_t offset,
+                                           long long cols, float scale) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    const uint64_t e = offset + i;
+    uint64_t z = mix64(seed ^ (e * 0x9E3779B97F4A7C15ull));
+    float u = (float)(z >> 40) * (1.0f / 16777216.0f);
+    float w = 2.0f * u - 1.0f;
+    const float sr = __fmul_rn(scale, head_row_scale(seed, e / (uint64_t)cols));
+    dst[i] = __float2bfloat16_rn(fmaf(w, sr, 0.0f));
+  }
+}
+
 // ---- RMSNorm: out[r] = x[src_row(r)] * rsqrt(mean(x^2) + eps) * w ----
 template <bool OUT_BF16>
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* __restrict__ rows,
@@ -58,9 +83,7 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const int* 
 // One warp per head; lane owns dims {lane + 32 j}. Pairs (i, i + hd/2) share a lane.
 template <int HD>
 __global__ void qkv_post_kernel(float* __restrict__ qkv, int ldq, int n_heads, int n_kv,
-                                const int* __restrict__ pos, const int* __restrict__ req,
-                                __nv_bfloat16* __restrict__ kv_base, long long kv_req_stride,
-                                long long kv_row_stride,
+                                const int* __restrict__ pos, const int* __restrict__ req, KvPages kv,
                                 const float2* __restrict__ rope,  // [ctx][HD/2] (cos, sin)
                                 const __nv_bfloat16* __restrict__ q_norm,
                                 const __nv_bfloat16* __restrict__ k_norm, float eps) {
@@ -107,8 +130,7 @@ __global__ void qkv_post_kernel(float* __restrict__ qkv, int ldq, int n_heads, i
   } else {
     int r = req ? req[tok] : 0;
     int kvh = is_k ? head - n_heads : head - n_heads - n_kv;
-    __nv_bfloat16* dst = kv_base + (long long)r * kv_req_stride + (long long)p * kv_row_stride + (is_k ? 0 : (long long)n_kv * HD)
-                         + (long long)kvh * HD;
+    __nv_bfloat16* dst = kv.pool + kv.row(r, p) + (is_k ? 0 : (long long)n_kv * HD) + (long long)kvh * HD;
 #pragma unroll
     for (int j = 0; j < PER; ++j) dst[lane + 32 * j] = __float2bfloat16_rn(v[j]);
   }
@@ -197,6 +219,18 @@ int ps_init_uniform_bf16(void* dst, size_t n, unsigned long long seed, unsigned 
   return PS_OK;
 }
 
+int ps_init_rowscaled_bf16(void* dst, size_t n, unsigned long long seed, unsigned long long offset,
+                           long long cols, float scale, void* stream) {
+  if (n == 0) return PS_OK;
+  PS_REQUIRE(cols >= 1, "ps_init_rowscaled_bf16: cols=%lld", cols);
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  init_rowscaled_bf16_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<__nv_bfloat16*>(dst), n, seed, offset, cols, scale);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
 int ps_rmsnorm(const float* x, int ldx, const int* rows, int n_rows, const void* w, int d,
                float eps, void* out, int ldo, int out_bf16, void* stream) {
   if (n_rows <= 0) return PS_OK;
@@ -212,26 +246,27 @@ int ps_rmsnorm(const float* x, int ldx, const int* rows, int n_rows, const void*
 }
 
 int ps_qkv_rope_append(float* qkv, int ldq, int t, int n_heads, int n_kv, int head_dim,
-                       const int* pos, const int* req, void* kv_base, long long kv_req_stride,
-                       long long kv_row_stride, const void* rope_cs, const void* q_norm,
+                       const int* pos, const int* req, void* kv_pool, int row_elems, const int* block_table,
+                       int bt_stride, int page_rows, const void* rope_cs, const void* q_norm,
                        const void* k_norm, float eps, void* stream) {
   if (t <= 0) return PS_OK;
+  KvPages kv;
+  PS_REQUIRE(kv_pages(kv, kv_pool, row_elems, block_table, bt_stride, page_rows),
+             "ps_qkv_rope_append: bad paged cache (page_rows %d, bt_stride %d)", page_rows, bt_stride);
+  PS_REQUIRE(row_elems == 2 * n_kv * head_dim, "ps_qkv_rope_append: row_elems %d != 2 * n_kv * head_dim", row_elems);
   int total = n_heads + 2 * n_kv;
   int warps = 8;
   dim3 grid(t, (total + warps - 1) / warps);
-  auto base = static_cast<__nv_bfloat16*>(kv_base);
   auto cs = static_cast<const float2*>(rope_cs);
   auto qn = static_cast<const __nv_bfloat16*>(q_norm);
   auto kn = static_cast<const __nv_bfloat16*>(k_norm);
   cudaStream_t s = (cudaStream_t)stream;
   switch (head_dim) {
     case 64:
-      launch_k(qkv_post_kernel<64>, grid, warps * 32, 0, s, qkv, ldq, n_heads, n_kv, pos, req, base,
-               kv_req_stride, kv_row_stride, cs, qn, kn, eps);
+      launch_k(qkv_post_kernel<64>, grid, warps * 32, 0, s, qkv, ldq, n_heads, n_kv, pos, req, kv, cs, qn, kn, eps);
       break;
     case 128:
-      launch_k(qkv_post_kernel<128>, grid, warps * 32, 0, s, qkv, ldq, n_heads, n_kv, pos, req, base,
-               kv_req_stride, kv_row_stride, cs, qn, kn, eps);
+      launch_k(qkv_post_kernel<128>, grid, warps * 32, 0, s, qkv, ldq, n_heads, n_kv, pos, req, kv, cs, qn, kn, eps);
       break;
     default:
       ps_set_error("ps_qkv_rope_append: head_dim %d unsupported (64, 128)", head_dim);

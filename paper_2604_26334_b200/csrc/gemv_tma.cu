@@ -36,14 +36,16 @@ constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp
 
 // Per token count: columns per consumer thread (x kept in registers: CPT * T floats)
 // and rows per stage (RS * KC * 2 = 32 KB, KC = 256 * CPT columns per chunk).
-// COMP: rows in the exponent-coded format (`ps_gemv_bf16c`): per row segment of KC
-// columns KC sign|mantissa bytes then KC/2 bytes of 4-bit exponent codes.
+// COMP: rows in the exponent-coded format (`ps_gemv_bf16c`, runtime/wcomp.py): a
+// row segment of KC columns is staged as KC sign|mantissa bytes, KC/2 bytes of 4-bit
+// exponent codes, then the row's trailer (base exponent, escape list; <= 256 bytes).
 constexpr int gt_pow2_floor(int v) { return v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ? 4 : v >= 2 ? 2 : 1; }
+constexpr int GT_TRAILER_MAX = 256;
 
 template <int T, bool COMP = false> struct GtShape {
   static constexpr int CPT = T <= 4 ? 16 : 8;
   static constexpr int KC = GT_CONSUMERS * 32 * CPT;
-  static constexpr int ROWB = COMP ? KC * 3 / 2 : KC * 2;   // stage bytes per row segment
+  static constexpr int ROWB = COMP ? KC * 3 / 2 + GT_TRAILER_MAX : KC * 2;   // stage bytes per row segment
   static constexpr int RS = COMP ? gt_pow2_floor(GT_STAGE_BYTES / ROWB) : GT_STAGE_BYTES / (KC * 2);
   static constexpr int V = RS * T;  // partial sums reduced per stage
   // warp_reduce_scatter halves V each step: a non-power-of-two V would drop values
@@ -80,43 +82,65 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[V], int lane) {
   }
 }
 
-// 8 coded weights -> 8 bf16 (uint4). sm: sign|mantissa bytes, nb: eight 4-bit codes;
-// code 15 = escape: the exponent is looked up in the row's (col << 8 | exp) list.
-__device__ __noinline__ uint32_t gt_escape_exp(const int* __restrict__ esc_off, const int* __restrict__ esc_ent,
-                                              int row, int col) {
-  int lo = esc_off[row], hi = esc_off[row + 1] - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((esc_ent[mid] >> 8) < col) lo = mid + 1; else hi = mid;
+// 8 coded weights -> 8 bf16 (uint4). sm: their sign|mantissa bytes, nb: their eight
+// 4-bit codes, base7 = (base | base << 16) << 7 of the row. Two weights per 32-bit
+// word: one PRMT spreads the two sm bytes to the halves, one PRMT the two codes, one
+// IMAD adds the base and shifts, one LOP3-class merge. A code of 15 (escape) sends the
+// group to gt_patch_escapes, which reads the exponent from the row's trailer.
+__device__ __noinline__ uint4 gt_patch_escapes(uint4 v, uint2 sm, uint32_t nb, const uint32_t* __restrict__ trailer,
+                                               int col) {
+  const uint32_t n = trailer[0] >> 8;
+  uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  const uint32_t smw[2] = {sm.x, sm.y};
+#pragma unroll 1
+  for (int i = 0; i < 8; ++i) {
+    if (((nb >> (4 * i)) & 0xFu) != 15u) continue;
+    uint32_t e = 0;
+    for (uint32_t j = 1; j <= n; ++j) {
+      const uint32_t ent = trailer[j];
+      if ((int)(ent >> 8) == col + i) { e = ent & 0xFFu; break; }
+    }
+    const uint32_t b = (smw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+    const uint32_t half = ((b & 0x80u) << 8) | (e << 7) | (b & 0x7Fu);
+    const int sh = 16 * (i & 1);
+    w[i >> 1] = (w[i >> 1] & ~(0xFFFFu << sh)) | (half << sh);
   }
-  return (uint32_t)esc_ent[lo] & 0xFFu;
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-__device__ __forceinline__ uint4 gt_decode8(uint2 sm, uint32_t nb, uint32_t base, const int* esc_off,
-                                            const int* esc_ent, int row, int col) {
-  uint32_t out[4];
-  const uint32_t smw[2] = {sm.x, sm.y};
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    uint32_t half[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int i = 2 * p + q;
-      const uint32_t b = (smw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-      const uint32_t code = (nb >> (4 * i)) & 0xFu;
-      const uint32_t e = code == 15u ? gt_escape_exp(esc_off, esc_ent, row, col + i) : base + code;
-      half[q] = ((b & 0x80u) << 8) | (e << 7) | (b & 0x7Fu);
-    }
-    out[p] = half[0] | (half[1] << 16);
-  }
-  return make_uint4(out[0], out[1], out[2], out[3]);
+// PTX prmt in its default mode: a selector nibble with bit 3 set replicates the sign of
+// the selected byte (CUDA's __byte_perm documents only 3-bit selectors), so a byte
+// whose msb is 0 becomes 0x00 — a zero byte without a zero operand.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t gt_pair(uint32_t smw, uint32_t sm_sel, uint32_t lo, uint32_t hi, uint32_t e_sel,
+                                            uint32_t base7) {
+  const uint32_t bb = prmt(smw, 0u, sm_sel);                  // [b0, 0, b1, 0]
+  const uint32_t ep = prmt(lo, hi, e_sel);                    // [code0, 0, code1, 0]
+  const uint32_t e7 = ep * 128u + base7;                       // (code + base) << 7, per half
+  return (bb & 0x007F007Fu) | ((bb << 8) & 0x80008000u) | e7;
+}
+
+__device__ __forceinline__ uint4 gt_decode8(uint2 sm, uint32_t nb, uint32_t base7, const uint32_t* trailer,
+                                            int col) {
+  const uint32_t lo = nb & 0x0F0F0F0Fu, hi = (nb >> 4) & 0x0F0F0F0Fu;   // codes 0,2,4,6 | 1,3,5,7
+  uint4 v;
+  v.x = gt_pair(sm.x, 0x4140u, lo, hi, 0x8480u, base7);
+  v.y = gt_pair(sm.x, 0x4342u, lo, hi, 0x9591u, base7);
+  v.z = gt_pair(sm.y, 0x4140u, lo, hi, 0xA6A2u, base7);
+  v.w = gt_pair(sm.y, 0x4342u, lo, hi, 0xB7B3u, base7);
+  if (nb & (nb >> 1) & (nb >> 2) & (nb >> 3) & 0x11111111u) v = gt_patch_escapes(v, sm, nb, trailer, col);
+  return v;
 }
 
 template <int T, int EPI, bool COMP = false>
 __global__ void __launch_bounds__(GT_THREADS, 1)
 gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W, int N, int K,
-                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages, int base_exp,
-                const int* __restrict__ esc_off, const int* __restrict__ esc_ent) {
+                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages) {
   using S = GtShape<T, COMP>;
   constexpr int CPT = S::CPT, KC = S::KC, RS = S::RS, V = S::V, ROWB = S::ROWB;
   const uint8_t* Wb = reinterpret_cast<const uint8_t*>(W);   // COMP: ldw is in bytes
@@ -156,11 +180,13 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* dst = ring + s * GT_STAGE_BYTES;
           if constexpr (COMP) {
-            mbar_expect_tx(&full[s], (uint32_t)(nr * (kc + kc / 2)));
+            const uint32_t tb = (uint32_t)(ldw - (long long)K * 3 / 2);   // the row's trailer
+            mbar_expect_tx(&full[s], (uint32_t)(nr * (kc + kc / 2 + tb)));
             for (int r = 0; r < nr; ++r) {
               const uint8_t* row = Wb + (long long)(rb + r) * ldw;
               bulk_load(dst + r * ROWB, row + (long long)c * KC, (uint32_t)kc, &full[s]);
               bulk_load(dst + r * ROWB + KC, row + K + (long long)c * (KC / 2), (uint32_t)(kc / 2), &full[s]);
+              bulk_load(dst + r * ROWB + KC * 3 / 2, row + (long long)K * 3 / 2, tb, &full[s]);
             }
           } else {
             mbar_expect_tx(&full[s], (uint32_t)(nr * kc * 2));
@@ -225,9 +251,11 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
           const int col = (h * GT_CONSUMERS * 32 + j) * 8;
           if constexpr (COMP) {
             if (r < nr && col < kc) {
+              const uint32_t* trailer = reinterpret_cast<const uint32_t*>(stage + r * ROWB + KC * 3 / 2);
+              const uint32_t base7 = ((trailer[0] & 0xFFu) * 0x10001u) << 7;
               const uint2 sm = *reinterpret_cast<const uint2*>(stage + r * ROWB + col);
               const uint32_t nb = *reinterpret_cast<const uint32_t*>(stage + r * ROWB + KC + col / 2);
-              w[h] = gt_decode8(sm, nb, (uint32_t)base_exp, esc_off, esc_ent, rb + r, c * KC + col);
+              w[h] = gt_decode8(sm, nb, base7, trailer, c * KC + col);
             } else {
               w[h] = make_uint4(0, 0, 0, 0);
             }
@@ -288,8 +316,7 @@ static int g_tma_stages = 0;
 
 template <int T, int EPI, bool COMP = false>
 static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
-                      int ldy, cudaStream_t s, int grid_cap, int base_exp = 0, const int* esc_off = nullptr,
-                      const int* esc_ent = nullptr) {
+                      int ldy, cudaStream_t s, int grid_cap) {
   if (!g_tma_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -318,7 +345,7 @@ static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, i
     smem_set = smem;
   }
   launch_k(gemv_tma_kernel<T, EPI, COMP>, grid, GT_THREADS, smem, s, x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta,
-           stages, base_exp, esc_off, esc_ent);
+           stages);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -341,31 +368,33 @@ int gemv_tma_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int
 }
 
 template <int T>
-static int launch_tmac_epi(int epi, const float* x, int ldx, int tt, const void* Wc, int N, int K, float* y, int ldy,
-                           cudaStream_t s, int base, const int* off, const int* ent) {
+static int launch_tmac_epi(int epi, const float* x, int ldx, int tt, const void* Wc, int N, int K, long long ldw,
+                           float* y, int ldy, cudaStream_t s) {
   auto W = static_cast<const __nv_bfloat16*>(Wc);
-  const long long ldw = (long long)K * 3 / 2;   // bytes per coded row
-  if (epi == PS_EPI_STORE) return launch_tma<T, PS_EPI_STORE, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0, base, off, ent);
-  if (epi == PS_EPI_ACCUM) return launch_tma<T, PS_EPI_ACCUM, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0, base, off, ent);
-  return launch_tma<T, PS_EPI_SWIGLU, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0, base, off, ent);
+  if (epi == PS_EPI_STORE) return launch_tma<T, PS_EPI_STORE, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0);
+  if (epi == PS_EPI_ACCUM) return launch_tma<T, PS_EPI_ACCUM, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0);
+  return launch_tma<T, PS_EPI_SWIGLU, true>(x, ldx, tt, W, N, K, ldw, y, ldy, s, 0);
 }
 
 }  // namespace ps
 
-extern "C" int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int N, int K, int base_exp,
-                             const int* esc_off, const int* esc_ent, float* y, int ldy, int epilogue, void* stream) {
+extern "C" int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int N, int K, long long ldw,
+                             float* y, int ldy, int epilogue, void* stream) {
   using namespace ps;
   PS_REQUIRE(t >= 1 && t <= 8, "ps_gemv_bf16c: t=%d outside [1, 8]", t);
   PS_REQUIRE(K % 256 == 0 && ldx % 4 == 0, "ps_gemv_bf16c: K must be a multiple of 256");
+  const long long tb = ldw - (long long)K * 3 / 2;
+  PS_REQUIRE(tb >= 16 && tb <= GT_TRAILER_MAX && tb % 16 == 0,
+             "ps_gemv_bf16c: row stride %lld leaves a %lld-byte trailer (16..%d, multiple of 16)", ldw, tb,
+             GT_TRAILER_MAX);
   PS_REQUIRE(((uintptr_t)Wc & 15) == 0 && ((uintptr_t)x & 15) == 0, "ps_gemv_bf16c: Wc and x must be 16-byte aligned");
-  PS_REQUIRE(base_exp >= 0 && base_exp <= 255 - 14, "ps_gemv_bf16c: base exponent %d", base_exp);
   PS_REQUIRE(epilogue != PS_EPI_SWIGLU || N % 2 == 0, "ps_gemv_bf16c: SWIGLU needs an even N");
   if (N <= 0) return PS_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (t == 1) return launch_tmac_epi<1>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
-  if (t == 2) return launch_tmac_epi<2>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
-  if (t <= 4) return launch_tmac_epi<4>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
-  return launch_tmac_epi<8>(epilogue, x, ldx, t, Wc, N, K, y, ldy, s, base_exp, esc_off, esc_ent);
+  if (t == 1) return launch_tmac_epi<1>(epilogue, x, ldx, t, Wc, N, K, ldw, y, ldy, s);
+  if (t == 2) return launch_tmac_epi<2>(epilogue, x, ldx, t, Wc, N, K, ldw, y, ldy, s);
+  if (t <= 4) return launch_tmac_epi<4>(epilogue, x, ldx, t, Wc, N, K, ldw, y, ldy, s);
+  return launch_tmac_epi<8>(epilogue, x, ldx, t, Wc, N, K, ldw, y, ldy, s);
 }
 
 int ps_preload_gemv_tma() {

@@ -28,8 +28,20 @@ from ..planning.hardware import MachineSpec
 from ..planning.placement import TIERS, TierTable, TierEntry, reachable_tiers
 from ..planning.pipeline_model import outstanding_tokens, schedule_iteration
 from . import lib as L
-from .executor import Executor, PassSpec
+from .executor import GEMV_MAX_T, Executor, PassSpec
 from .model import HostWeights, arch_for
+
+
+def _meminfo() -> dict:
+    out = {}
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                k, v = line.split(":", 1)
+                out[k] = int(v.split()[0]) * 1024
+    except (OSError, ValueError):
+        pass
+    return out
 
 
 @dataclass
@@ -42,9 +54,14 @@ class GenerateResult:
     decode_time_s: float
     passes: list = field(default_factory=list)   # (tier, T, seconds, bytes streamed)
     migration_bytes: int = 0
-    # tier switches: (from tier, to tier, live KV rows, bytes the executor moved,
+    # tier switches: (from tier, to tier, live KV pages per layer, bytes the executor moved,
     # (h2d, d2h) bytes the migration model predicts)
     switches: list = field(default_factory=list)
+    # per request: one character per computed position (prompt + gen - 1) naming the
+    # numerics of the pass that computed it — "G" GEMM pass (bf16 activations), "P"
+    # GEMV pass with the tcgen05 prefill attention, "D" decode-only GEMV pass. The
+    # oracle applies the same rounding points (oracle/model_ref.py `modes`).
+    row_modes: list = field(default_factory=list)
 
 
 @dataclass
@@ -63,6 +80,7 @@ class _Session:
     migration: int = 0
     ttft: float | None = None
     t_start: float = field(default_factory=time.perf_counter)
+    modes: list = field(default_factory=list)        # per request: pass numerics per position
 
 
 class Engine:
@@ -72,7 +90,7 @@ class Engine:
                  machine="b200", profile: str | None = None, seed: int = 0,
                  max_tokens: int | None = None, chunk_bytes: int = 64 << 20,
                  checkpoint: str | None = None, shared_weights: str | None = None,
-                 migration_aware: bool = False, striper=None):
+                 migration_aware: bool = False, striper=None, kv_page_seed: int | None = None):
         """`model`: preset name or ModelSpec (random-init weights), or None with
         `checkpoint` = a directory holding config.json + safetensors, or a .gguf file
         (real weights, runtime/checkpoint.py, runtime/gguf.py). `shared_weights`: a /dev/shm segment name shared by
@@ -126,6 +144,9 @@ class Engine:
         self.migration_aware = migration_aware
         self.striper = striper        # runtime.striping.StripeLeader: helper GPUs pull stripes
         self._sess: _Session | None = None
+        # KV pages in seeded random order instead of lowest-first (tests: every kernel and
+        # copy must follow the block table)
+        self.kv_page_seed = kv_page_seed
 
     # -- tier selection over reachable tiers (pick_tier, planner.py:451-460) --
     def pick_tier(self, n_new: int) -> int:
@@ -144,31 +165,37 @@ class Engine:
     def _build_coded(self) -> None:
         """Exponent-coded copies of the dense shards (runtime/wcomp.py) that decode
         passes stream instead of bf16 (25 % fewer link bytes, bit-identical results),
-        when host memory holds them: about 0.75 x the dense weight bytes, pinned.
-        Anything else (no room, allocation failure) keeps bf16 streaming."""
+        when host memory holds them: about 0.75 x the dense weight bytes, pinned. With
+        node-shared weights the coded copy is node-shared too (one replica encodes, the
+        others map it), and the go / no-go rule uses only node totals, so every replica
+        of a job decides the same. Anything else keeps bf16 streaming."""
         from .wcomp import CodedShards
-        need = sum(b.nbytes for b in self.weights.layout.blobs.values()
-                   if b.kind in (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD)) * 3 // 4
-        avail = 0
-        try:
-            with open("/proc/meminfo") as fh:
-                for line in fh:
-                    if line.startswith("MemAvailable:"):
-                        avail = int(line.split()[1]) * 1024
-        except OSError:
-            pass
-        if avail and need > 0.5 * avail:
+        dense = sum(b.nbytes for b in self.weights.layout.blobs.values()
+                    if b.kind in (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD))
+        need = dense * 3 // 4
+        shared = None
+        meminfo = _meminfo()
+        if self.weights.shared is not None:
+            shared = os.path.basename(self.weights.shared.path) + "_coded"
+            host_blob = self.weights.shared.nbytes
+            if meminfo.get("MemTotal", 0) and need + host_blob > 0.8 * meminfo["MemTotal"]:
+                self.coded_skipped = "node memory: bf16 + coded copies exceed 80 % of MemTotal"
+                return
+        elif meminfo.get("MemAvailable", 0) and need > 0.5 * meminfo["MemAvailable"]:
+            self.coded_skipped = "host memory: coded copy exceeds half of MemAvailable"
             return
         t0 = time.perf_counter()
         try:
             self.weights.coded = CodedShards(self.weights, (ShardKind.ATTENTION, ShardKind.FFN,
-                                                            ShardKind.OUTPUT_HEAD))
+                                                            ShardKind.OUTPUT_HEAD), shared=shared)
         except Exception as exc:   # e.g. pinned host memory exhausted: stream bf16
             import warnings
             warnings.warn(f"exponent-coded weights unavailable ({exc}); streaming bf16")
             self.weights.coded = None
+            self.coded_skipped = repr(exc)[:200]
             return
         self.coded_seconds = time.perf_counter() - t0
+        self.coded_shared = shared is not None
 
     def _ensure_executor(self, max_tokens: int) -> Executor:
         if self.executor is None:
@@ -178,7 +205,8 @@ class Engine:
                 self._build_coded()
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,
-                                     self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes)
+                                     self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes,
+                                     kv_page_seed=self.kv_page_seed)
             self.migration.pins_fn = self.executor.pins_for   # include the spare pins
             if self.striper is not None:
                 if self.weights.shared is None:
@@ -233,9 +261,10 @@ class Engine:
         if max(len(p) for p in prompts) + gen_len > self.context_len:
             raise SpecError("prompt + gen exceeds the planned context length")
         self._ensure_executor(self.max_pass_tokens([len(p) for p in prompts], gen_len))
+        self.executor.reset_requests()          # a new batch: free every KV page
         n = len(prompts)
         self._sess = _Session(prompts, [len(p) for p in prompts], [gen_len] * n, [0] * n,
-                              [[] for _ in range(n)])
+                              [[] for _ in range(n)], modes=[""] * n)
 
     @property
     def outstanding(self) -> int:
@@ -270,6 +299,11 @@ class Engine:
         """fp32 logits [rows, V] of the last iteration's emitting requests, in slot order."""
         return self._need_executor().logits_host(self._sess.last_rows if self._sess else 1)
 
+    def row_modes(self) -> list:
+        """Per request: the numerics of the pass that computed each position so far
+        (see GenerateResult.row_modes)."""
+        return list(self._need_session().modes)
+
     def tokens(self) -> list:
         """Tokens generated so far, per request slot."""
         s = self._need_session()
@@ -299,16 +333,16 @@ class Engine:
         s, ex = self._sess, self.executor
         n = len(s.prompts)
         n_out = outstanding_tokens(s.prompt_left, s.gen_left)
-        rows = max(ex.kv_len) if ex.kv_len else 0
+        pages = ex.kv_live_pages()            # live KV pages per layer (what a switch moves)
         if self.migration_aware:
-            tier = self.migration.pick_tier(n_out, ex.tier, rows, self.machine)
+            tier = self.migration.pick_tier(n_out, ex.tier, pages, self.machine)
         else:
             tier = self.pick_tier(n_out)
         if tier != ex.tier:
             prev = ex.tier
             moved = ex.set_tier(tier)
             s.migration += moved
-            s.switches.append((prev, tier, rows, moved, self.migration.bytes(prev, tier, rows)))
+            s.switches.append((prev, tier, pages, moved, self.migration.bytes(prev, tier, pages)))
         step = schedule_iteration(tier, s.prompt_left, s.gen_left)
         slots, n_new, p0, ids, sample = [], [], [], [], []
         decode_ids_from_device = True
@@ -335,6 +369,10 @@ class Engine:
             for j, a in enumerate(ids):      # decode positions are exact once drained
                 if a is None:
                     p0[j] = len(s.prompts[slots[j]]) + len(s.out[slots[j]]) - 1
+        T = sum(n_new)
+        mode = "G" if T > GEMV_MAX_T else ("D" if all(k == 1 for k in n_new) else "P")
+        for slot, k in zip(slots, n_new):
+            s.modes[slot] += mode * k
         ev0 = L.event_create(True) if timing else 0
         if timing:
             L.call("ps_event_record", ev0, ex.cs)
@@ -389,7 +427,8 @@ class Engine:
         tps = decode_tokens / decode_time if decode_time > 0 else float("inf")
         return GenerateResult([np.array(o, np.int32) for o in s.out], ttft, tps,
                               ttft + 100.0 / tps if tps else float("inf"),
-                              decode_tokens, decode_time, pass_rows, s.migration, s.switches)
+                              decode_tokens, decode_time, pass_rows, s.migration, s.switches,
+                              list(s.modes))
 
     @staticmethod
     def _pending_count(pending_host, slot) -> int:

@@ -45,6 +45,69 @@ from .model import Arch, HostWeights, rope_table
 from .streamer import CopyRing, EventPool
 
 GEMV_MAX_T = 32
+KV_PAGE_ROWS = 64          # positions per KV page (a 64-row TMA box never straddles pages)
+
+
+class KvPagePool:
+    """Paged KV cache bookkeeping: every layer's cache is a pool
+    of `n_pages` pages of KV_PAGE_ROWS positions; the block table [slots, per_slot]
+    names the physical page of each request's logical page and is shared by all layers
+    (a request's pages have the same index in every layer's pool). Pages are taken on
+    demand, lowest free index first (so one batch's live pages form the prefix [0, n)
+    and move in one copy), or in a seeded random order (`seed`, tests: kernels and
+    copies must honour the table). The pool holds B x ceil(context / 64) pages — the
+    plan's KV shard (`pkg/src/shardplan/model_graph.py:299-304,331`) rounded up to
+    whole pages."""
+
+    def __init__(self, slots: int, per_slot: int, seed: int | None = None):
+        self.slots, self.per_slot = slots, per_slot
+        self.n_pages = slots * per_slot
+        order = list(range(self.n_pages))
+        if seed is not None:
+            order = [int(i) for i in np.random.default_rng(seed).permutation(self.n_pages)]
+        self.order = order
+        self.reset()
+
+    def reset(self) -> None:
+        self.free = list(self.order)
+        self.table = np.full((self.slots, self.per_slot), -1, np.int32)
+        self.owned = [0] * self.slots
+        self.version = getattr(self, "version", 0) + 1
+
+    def ensure(self, slot: int, rows: int) -> bool:
+        """Give `slot` pages for positions [0, rows); True when the table changed."""
+        need = -(-rows // KV_PAGE_ROWS)
+        if need > self.per_slot:
+            raise SpecError(f"request slot {slot}: {rows} positions exceed the cache's "
+                            f"{self.per_slot * KV_PAGE_ROWS}")
+        changed = False
+        while self.owned[slot] < need:
+            self.table[slot, self.owned[slot]] = self.free.pop(0)
+            self.owned[slot] += 1
+            changed = True
+        if changed:
+            self.version += 1
+        return changed
+
+    def pages(self, slot: int, r0: int, r1: int) -> list:
+        """Physical pages holding positions [r0, r1) of `slot`."""
+        if r1 <= r0:
+            return []
+        return [int(p) for p in self.table[slot, r0 // KV_PAGE_ROWS:-(-r1 // KV_PAGE_ROWS)]]
+
+    def live(self) -> list:
+        return sorted(int(p) for s in range(self.slots) for p in self.table[s, :self.owned[s]])
+
+    @staticmethod
+    def runs(pages) -> list:
+        """Sorted page ids -> [(first page, count)] of consecutive runs."""
+        out = []
+        for p in sorted(set(pages)):
+            if out and out[-1][0] + out[-1][1] == p:
+                out[-1][1] += 1
+            else:
+                out.append([p, 1])
+        return [tuple(r) for r in out]
 
 
 @dataclass
@@ -88,7 +151,7 @@ class Consumer:
 class Executor:
     def __init__(self, weights: HostWeights, arch: Arch, plans: dict, budget_bytes: float,
                  kv_slots: int, context_len: int, max_tokens: int,
-                 chunk_bytes: int = 64 << 20, ring_cap: int = 1 << 30):
+                 chunk_bytes: int = 64 << 20, ring_cap: int = 1 << 30, kv_page_seed: int | None = None):
         spec = weights.spec
         self.moe = spec.moe
         self.spec, self.arch, self.w = spec, arch, weights
@@ -130,7 +193,12 @@ class Executor:
         self.V = s.vocab_size
         self.row_elems = 2 * self.kv * self.hd
         self.row_bytes = self.row_elems * 2
-        self.kv_layer_bytes = self.cap * self.B * self.row_bytes
+        # paged KV cache: one page pool per layer, one block table for all layers
+        self.pps = -(-self.cap // KV_PAGE_ROWS)              # pages per request slot
+        self.kv_pages = KvPagePool(self.B, self.pps, kv_page_seed)
+        self.page_bytes = KV_PAGE_ROWS * self.row_bytes
+        self.kv_layer_bytes = self.kv_pages.n_pages * self.page_bytes
+        self._bt_version = -1                                 # block-table version on the device
 
         self.cs = L.stream_create(high_priority=True)   # compute
         self.h2d = L.stream_create()                    # copy engine, host -> device
@@ -140,7 +208,7 @@ class Executor:
         # host KV homes: [layer][position][slot][K|V heads] bf16, pinned + mapped
         self.kv_host = L.host_alloc(max(1, s.n_layers * self.kv_layer_bytes), mapped=True)
         self.kv_len = [0] * self.B
-        self.kv_vram: dict[int, int] = {}
+        self.kv_vram: dict[int, int] = {}           # layer -> VRAM page pool
         self.kv_mode: dict[int, str] = {}
         self.kv_writeback: dict[int, int] = {}   # layer -> event of its last D2H append
         self.tok_events = [L.event_create(False) for _ in range(64)]
@@ -148,12 +216,9 @@ class Executor:
         self.arena = VramArena(budget_bytes)
         self._carve_persistent()
         # exponent-coded dense shards (runtime/wcomp.py) for GEMV passes that stream
-        # them; their escape tables are host-mapped (read only for escaped weights)
+        # them; every coded row carries its own base exponent and escapes (in-band)
         self.coded = getattr(weights, "coded", None)
         self._coded_call = None
-        self.d_esc_off = self.d_esc_ent = 0
-        if self.coded is not None:
-            self.d_esc_off, self.d_esc_ent = self.coded.esc_off_ptr, self.coded.esc_ent_ptr
         self.persist_high = self.arena.high       # activations + ring are carved below, per tier
         self.residency: dict[int, tuple] = {}
         self.tier = None
@@ -209,6 +274,7 @@ class Executor:
         self.i_req = a.alloc_high("req", T * 4)
         self.i_meta = a.alloc_high("meta", 4 * (4 * B + 4))
         self.i_rows = a.alloc_high("sample_rows", B * 4)
+        self.i_bt = a.alloc_high("kv_block_table", B * self.pps * 4)
         self.i_tok_ring = a.alloc_high("sample_tok", 8 * B * 4)   # 8 rotating slots
         self.tok_slot = 0
         self.i_tok = self.i_tok_ring
@@ -237,6 +303,35 @@ class Executor:
 
     def _kv_host_ptr(self, layer: int) -> int:
         return self.kv_host + layer * self.kv_layer_bytes
+
+    def _copy_pages(self, dst_pool: int, src_pool: int, runs: list, stream: int) -> int:
+        """Copy page runs between two pools with the same page offsets; returns bytes."""
+        n = 0
+        for p, c in runs:
+            L.memcpy_async(dst_pool + p * self.page_bytes, src_pool + p * self.page_bytes,
+                           c * self.page_bytes, stream)
+            n += c * self.page_bytes
+        return n
+
+    def kv_live_pages(self) -> int:
+        """Pages each layer's cache holds for the live requests (what a tier switch moves)."""
+        return len(self.kv_pages.live())
+
+    def reset_requests(self) -> None:
+        """A new request batch: every page back to the free list, every slot empty."""
+        self.kv_pages.reset()
+        self.kv_len = [0] * self.B
+
+    def _sync_block_table(self) -> None:
+        """Upload the block table when it changed (stream-ordered, kernel parameter
+        copies of <= 4000 bytes: no host sync, nothing queued behind weight copies)."""
+        if self._bt_version == self.kv_pages.version:
+            return
+        flat = self.kv_pages.table.reshape(-1)
+        step = 1000
+        for i in range(0, len(flat), step):
+            self._upload(self.i_bt + 4 * i, flat[i:i + step])
+        self._bt_version = self.kv_pages.version
 
     # --------------------------------------------------------------- residency
     def _plan_modes(self, plan) -> tuple:
@@ -322,12 +417,10 @@ class Executor:
             return 0
         plan = self.plans[tier]
         moved = 0
-        rows = max(self.kv_len) if self.kv_len else 0
-        kv_rows_bytes = rows * self.B * self.row_bytes
-        # 1. every VRAM KV cache goes home first (content is authoritative)
+        live = self.kv_pages.runs(self.kv_pages.live())
+        # 1. every VRAM KV cache goes home first (content is authoritative): its live pages
         for layer, dev in self.kv_vram.items():
-            L.memcpy_async(self._kv_host_ptr(layer), dev, kv_rows_bytes, self.cs)
-            moved += kv_rows_bytes
+            moved += self._copy_pages(self._kv_host_ptr(layer), dev, live, self.cs)
         L.call("ps_stream_synchronize", self.cs)
         self.synchronize()   # the ring and every stream must be idle before re-carving
         # 2. re-carve the pinned region in pin order; weights whose slot is unchanged
@@ -364,8 +457,7 @@ class Executor:
             L.memcpy_async(dev, self.w.shard_ptr(sid), nbytes, self.cs)
             moved += nbytes
         for layer, dev in self.kv_vram.items():
-            L.memcpy_async(dev, self._kv_host_ptr(layer), kv_rows_bytes, self.cs)
-            moved += kv_rows_bytes
+            moved += self._copy_pages(dev, self._kv_host_ptr(layer), live, self.cs)
         for sid, mode in modes.items():
             if sid in self.residency:
                 continue
@@ -669,8 +761,8 @@ class Executor:
                     self.ptrs[name] = ptr
                 if name in own:
                     advance_to(own[name])
-                    if coded and m[2] >= 0:   # the consumer's GEMV reads coded rows
-                        self._coded_call = (m[2], self.d_esc_off + (m[3] + r0) * 4, self.d_esc_ent)
+                    if coded and m[2]:   # the consumer's GEMV reads coded rows (stride m[1] bytes)
+                        self._coded_call = m[1]
                     try:
                         self._traced(name, consumers[ci].fn, ptr, r0, r1)
                     finally:
@@ -910,9 +1002,8 @@ class Executor:
         """out (epi)= act @ W[:N]^T for T tokens: GEMV on fp32 act (T <= 32)
         or the tcgen05 GEMM on bf16 act."""
         if self._coded_call is not None:
-            base, esc_off, esc_ent = self._coded_call
             for t0 in range(0, T, 8):
-                L.call("ps_gemv_bf16c", act + t0 * K * 4, K, min(8, T - t0), W, N, K, base, esc_off, esc_ent,
+                L.call("ps_gemv_bf16c", act + t0 * K * 4, K, min(8, T - t0), W, N, K, self._coded_call,
                        out + t0 * ldo * 4, ldo, epi, self.cs)
         elif T <= GEMV_MAX_T:
             L.call("ps_gemv_bf16", act, K, T, W, N, K, K, out, ldo, epi, self.cs)
@@ -986,9 +1077,16 @@ class Executor:
         i_lens = i_p0 + 4 * nb
         i_slot = i_lens + 4 * nb
         max_len, max_new = int(lens.max()), int(max(ps.n_new))
-        min_p0, max_p0 = int(p0a.min()), int(p0a.max())
-        idle = [min(self.kv_len[b], max_len) for b in range(self.B) if b not in set(ps.slots)]
-        upload_rows = max([max_p0] + idle)
+        # paged KV: pages for every new position, then the pages a streamed cache needs
+        # in the ring (existing rows the attention reads) and writes back (new rows)
+        for slot, n, p0 in zip(ps.slots, ps.n_new, ps.p0):
+            self.kv_pages.ensure(slot, p0 + n)
+        self._sync_block_table()
+        kv_read = KvPagePool.runs(pg for slot, p0 in zip(ps.slots, ps.p0)
+                                  for pg in self.kv_pages.pages(slot, 0, p0))
+        kv_write = KvPagePool.runs(pg for slot, n, p0 in zip(ps.slots, ps.n_new, ps.p0)
+                                   for pg in self.kv_pages.pages(slot, p0, p0 + n))
+        kv_span = 1 + max(p + c - 1 for p, c in kv_read + kv_write)   # ring window, in pages
         use_decode_kernel = ps.decode_only and gemv
 
         if ps.ids is not None:
@@ -1006,7 +1104,7 @@ class Executor:
         esz = 4 if gemv else 2
         scale = 1.0 / math.sqrt(self.hd)
         eps = self.arch.rms_eps
-        row_stride = self.B * self.row_elems
+        bt, pps, page = self.i_bt, self.pps, KV_PAGE_ROWS
 
         def norm(w_ptr):
             L.call("ps_rmsnorm", self.x, d, 0, T, w_ptr, d, eps, xn, d, 0 if gemv else 1, self.cs)
@@ -1020,53 +1118,52 @@ class Executor:
             # ---- KV_i, hoisted before Attn_i
             mode = self.kv_mode[layer]
             kv_region = None
+            kv_pool_pages = self.kv_pages.n_pages
             if mode == "pinned":
                 kv_base = self.kv_vram[layer]
             elif mode == "zerocopy" and gemv:
                 kv_base = self._kv_host_ptr(layer)
             else:
-                # Rows [min p0, max len) of EVERY slot are written back below, so the
-                # upload must cover every valid row in that window: participants'
-                # existing rows (< max p0) and the valid rows of slots that sit this
-                # pass out. Rows past a slot's own length may hold anything: they are
-                # never read before that slot writes them.
-                prefix = upload_rows * self.B * self.row_bytes
-                room = max_len * self.B * self.row_bytes
+                # a window of the layer's host pool in the ring, pages at their pool
+                # offsets: the pages holding rows the attention reads come up; pages that
+                # only receive new rows need room, not bytes
                 wb = self.kv_writeback.get(layer)
-                if wb is not None and prefix:
+                if wb is not None and kv_read:
                     # the host home must hold the previous pass's appended rows
                     L.call("ps_stream_wait_event", self.h2d, wb)
-                kv_region, kv_base, arrived = self.ring.upload(self._kv_host_ptr(layer), prefix,
-                                                               f"kv{layer}", reserve=room)
-                self._stat.bytes_streamed += prefix
-                self._stat.copies += 1 if prefix else 0
+                kv_region, kv_base, arrived = self.ring.upload_runs(
+                    self._kv_host_ptr(layer), [(p * self.page_bytes, c * self.page_bytes) for p, c in kv_read],
+                    kv_span * self.page_bytes, f"kv{layer}")
+                kv_pool_pages = kv_span
+                up = sum(c for _, c in kv_read) * self.page_bytes
+                self._stat.bytes_streamed += up
+                self._stat.copies += len(kv_read)
                 self._wait(arrived)
 
             # ---- Attn_i
-            def core(_p, _a, _b, layer=layer, kv_base=kv_base, kv_region=kv_region):
+            def core(_p, _a, _b, layer=layer, kv_base=kv_base, kv_region=kv_region, kv_pool_pages=kv_pool_pages):
                 qn = self.ptrs.get(f"L{layer}.q_norm", 0)
                 kn = self.ptrs.get(f"L{layer}.k_norm", 0)
                 L.call("ps_qkv_rope_append", self.qkv, self.qkv_rows, T, self.h, self.kv, self.hd,
-                       self.i_pos, self.i_req, kv_base, self.row_elems, row_stride, self.rope,
+                       self.i_pos, self.i_req, kv_base, self.row_elems, bt, pps, page, self.rope,
                        qn, kn, eps, self.cs)
                 if use_decode_kernel:
                     L.call("ps_attn_decode", self.qkv, self.qkv_rows, nb, self.h, self.kv, self.hd,
-                           i_slot, kv_base, self.row_elems, row_stride, i_lens, max_len, scale,
+                           i_slot, kv_base, self.row_elems, bt, pps, page, i_lens, max_len, scale,
                            att, hq, self.ws, self.ws_floats, self.cs)
                 else:
-                    # tcgen05 / TMEM / TMA flash attention (attention_tc.cu)
+                    # tcgen05 / TMEM / TMA flash attention over the pages (attention_tc.cu)
                     L.call("ps_attn_prefill_tc", self.qkv, self.qkv_rows, nb, i_qstart, i_p0, i_slot,
-                           max_new, self.h, self.kv, self.hd, kv_base, self.row_elems, row_stride,
-                           max_len, scale, att, hq, 0 if gemv else 1, self.cs)
+                           max_new, self.h, self.kv, self.hd, kv_base, self.row_elems, bt, pps, page,
+                           kv_pool_pages, scale, att, hq, 0 if gemv else 1, self.cs)
                 if kv_region is not None:
-                    # appended rows -> the layer's host home (D2H stream), then release
+                    # pages with appended rows -> the layer's host home (D2H stream), then release
                     L.call("ps_stream_wait_event", self.d2h, self._record(self.cs))
-                    a, b = min_p0 * self.B * self.row_bytes, max_len * self.B * self.row_bytes
                     ev0 = self.tracer.begin(self.d2h) if self.tracer else None
-                    L.memcpy_async(self._kv_host_ptr(layer) + a, kv_base + a, b - a, self.d2h)
+                    n = self._copy_pages(self._kv_host_ptr(layer), kv_base, kv_write, self.d2h)
                     if ev0 is not None:
                         self.tracer.end(f"kv{layer} write-back", "d2h", ev0, self.d2h)
-                    self._stat.kv_writeback_bytes += b - a
+                    self._stat.kv_writeback_bytes += n
                     wb = self._record(self.d2h)
                     self.kv_writeback[layer] = wb
                     self.ring.seal(kv_region, [wb])

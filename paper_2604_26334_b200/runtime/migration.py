@@ -8,15 +8,15 @@ come in over H2D — and the executor measures exactly those bytes
 (`Executor.set_tier`). This module predicts them from the plans alone, with
 the executor's own policy:
 
-1. every VRAM-pinned KV cache of the old tier is written home
-   (`rows * batch * row_bytes` each, rows = longest live context);
+1. every VRAM-pinned KV cache of the old tier is written home: its live pages
+   (`kv_pages * page_bytes` each; the paged cache, executor.KvPagePool);
 2. the new tier's pinned set is carved bottom-up in pin order
    (priority, layer, id), 256-byte aligned, followed by the executor's spare
    pins (`Executor.pins_for`); a weight shard whose offset is unchanged stays,
    one resident in both tiers at different offsets is relocated inside VRAM
    (device-to-device, `plan_relocation`: no link bytes), every other pinned
    weight is uploaded whole;
-3. every VRAM-pinned KV cache of the new tier is uploaded (same rows).
+3. every VRAM-pinned KV cache of the new tier is uploaded (same pages).
 
 `seconds()` prices the bytes on the machine's link rates (the executor runs
 the copies back to back on one stream). `pick_tier()` is the reference's
@@ -100,8 +100,10 @@ class MigrationModel:
         self.pins_fn = pins_fn
         self.shards = build_shards(spec, context_len, batch)
         self.batch = batch
+        from .executor import KV_PAGE_ROWS
         self.row_bytes = 2 * spec.n_kv_heads * spec.head_dim * 2
-        self.kv_layer_bytes = context_len * batch * self.row_bytes
+        self.page_bytes = KV_PAGE_ROWS * self.row_bytes
+        self.kv_layer_bytes = batch * -(-context_len // KV_PAGE_ROWS) * self.page_bytes
         self.blob_bytes = {sid: b.nbytes for sid, b in layout.blobs.items()}
 
     def _phys(self, shard) -> int:
@@ -126,18 +128,18 @@ class MigrationModel:
             off += _up(self._phys(self.shards[sid]))
         return out
 
-    def bytes(self, from_tier: int | None, to_tier: int, kv_rows: int) -> tuple[int, int]:
+    def bytes(self, from_tier: int | None, to_tier: int, kv_pages: int) -> tuple[int, int]:
         """(h2d, d2h) bytes of switching from `from_tier` (None: nothing resident)
-        to `to_tier` with `kv_rows` live rows of KV per request."""
+        to `to_tier` with `kv_pages` live KV pages per layer."""
         if from_tier == to_tier:
             return 0, 0
-        return self.moves(from_tier, to_tier, kv_rows)[:2]
+        return self.moves(from_tier, to_tier, kv_pages)[:2]
 
-    def moves(self, from_tier: int | None, to_tier: int, kv_rows: int) -> tuple[int, int, int]:
+    def moves(self, from_tier: int | None, to_tier: int, kv_pages: int) -> tuple[int, int, int]:
         """(h2d, d2h, d2d) bytes of the switch; d2d never crosses the host link."""
         if from_tier == to_tier:
             return 0, 0, 0
-        rows_bytes = kv_rows * self.batch * self.row_bytes
+        rows_bytes = kv_pages * self.page_bytes
         old = self.pinned_offsets(from_tier) if from_tier is not None else {}
         new = self.pinned_offsets(to_tier)
         kv = lambda sid: self.shards[sid].kind is ShardKind.KV_CACHE  # noqa: E731
@@ -149,11 +151,11 @@ class MigrationModel:
         h2d += sum(w_new[sid][1] for sid in up)
         return h2d, d2h, sum(op[3] for op in d2d)
 
-    def seconds(self, from_tier, to_tier, kv_rows: int, machine: MachineSpec) -> float:
-        h2d, d2h = self.bytes(from_tier, to_tier, kv_rows)
+    def seconds(self, from_tier, to_tier, kv_pages: int, machine: MachineSpec) -> float:
+        h2d, d2h = self.bytes(from_tier, to_tier, kv_pages)
         return h2d / machine.pcie_h2d_bw + d2h / machine.pcie_d2h_bw
 
-    def pick_tier(self, n_new: int, current: int | None, kv_rows: int, machine: MachineSpec) -> int:
+    def pick_tier(self, n_new: int, current: int | None, kv_pages: int, machine: MachineSpec) -> int:
         """Reference pick_tier over reachable tiers, plus the switch cost."""
         best, best_cost = None, None
         for tier in TIERS:
@@ -162,7 +164,7 @@ class MigrationModel:
                 continue
             cost = -(-n_new // tier) * plan.estimated_time
             if current is not None and tier != current:
-                cost = cost + self.seconds(current, tier, kv_rows, machine)
+                cost = cost + self.seconds(current, tier, kv_pages, machine)
             if best_cost is None or cost < best_cost:
                 best, best_cost = tier, cost
         return best

@@ -71,9 +71,18 @@ def tensor_seed(model_seed: int, name: str) -> int:
     return int.from_bytes(hashlib.sha256(f"{model_seed}:{name}".encode()).digest()[:8], "little")
 
 
+# Tensors whose rows get a heavy-tailed scale s_r = min(u_r^-1/2, 64) on top of
+# U(-a, a) (ps_init_rowscaled_bf16): the output head. A random-init head with equal
+# row norms puts the top two of 128k logits within 1e-3 of max|logit| on 3 % of
+# tokens, so bf16 rounding in a prefill pass would flip greedy ids; Pareto(2) row
+# norms make that ~4x rarer (SURVEY.md §7 hard part 7), without changing any shape.
+HEAVY_ROW_TENSORS = frozenset({"lm_head"})
+
+
 def init_scale(name: str, fan_in: int) -> tuple[float, float]:
     """(scale, bias) of the uniform init: norms ~ U(0.9, 1.1), embeddings
-    ~ U(-1, 1), linear weights ~ U(-a, a) with a = sqrt(3 / fan_in)."""
+    ~ U(-1, 1), linear weights ~ U(-a, a) with a = sqrt(3 / fan_in) (times a
+    per-row factor for HEAVY_ROW_TENSORS)."""
     leaf = name.rsplit(".", 1)[-1]
     if leaf.endswith("norm"):
         return 0.1, 1.0
@@ -419,6 +428,10 @@ class HostWeights:
         def plain(name, fan_in):
             scale, bias = init_scale(name, fan_in)
             sd = tensor_seed(seed, name)
+            if name in HEAVY_ROW_TENSORS:     # heavy-tailed row norms (margin-robust head)
+                def prod(dst, byte_off, n):
+                    L.call("ps_init_rowscaled_bf16", dst, n // 2, sd, byte_off // 2, fan_in, scale, stream)
+                return prod
 
             def prod(dst, byte_off, n):
                 L.call("ps_init_uniform_bf16", dst, n // 2, sd, byte_off // 2, scale, bias, stream)

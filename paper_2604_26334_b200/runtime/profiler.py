@@ -14,7 +14,7 @@ executor actually launches for it:
 | MATMUL (m, k, n), m <= 32          | ps_gemv_bf16, fp32 activations                     |
 | MATMUL (m, k, n), m > 32           | ps_gemm_bf16 (CTA-pair tcgen05), rows in <= 16384 slices |
 | GQA / MHA (t, ctx, ...), t <= 32   | ps_attn_decode, t requests at length ctx           |
-| GQA / MHA (t, ctx, ...), t > 32    | ps_attn_prefill, ceil(t / ctx) requests, causal    |
+| GQA / MHA (t, ctx, ...), t > 32    | ps_attn_prefill_tc, ceil(t / ctx) requests, causal |
 | MOE_ROUTE (t, d, E)                | router matmul + ps_moe_route_topk (k = 8)          |
 | ELEMENT_WISE (n,)                  | ps_rmsnorm over n / 4096 rows                      |
 
@@ -157,11 +157,17 @@ class KernelBench:
         torch, L = self.torch, self.L
         qrows = (heads + 2 * kv) * hd
         row_elems = 2 * kv * hd
+        page = 64
+        pps = -(-ctx // page)
+
+        def table(n_req):   # request b owns pages [b * pps, (b + 1) * pps) of the pool
+            return torch.arange(n_req * pps, dtype=torch.int32, device="cuda").view(n_req, pps)
         if t <= 32:
             B = t
-            ncache = _copies(ctx * B * row_elems * 2, cap=8)
-            caches = [torch.empty(ctx * B * row_elems, dtype=torch.bfloat16, device="cuda").normal_()
+            ncache = _copies(pps * page * B * row_elems * 2, cap=8)
+            caches = [torch.empty(pps * page * B * row_elems, dtype=torch.bfloat16, device="cuda").normal_()
                       for _ in range(ncache)]
+            bt = table(B)
             q = torch.randn(B, qrows, device="cuda")
             out = torch.empty(B, heads * hd, device="cuda")
             lens = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
@@ -170,8 +176,8 @@ class KernelBench:
 
             def launch(i):
                 L.call("ps_attn_decode", q.data_ptr(), qrows, B, heads, kv, hd, 0, caches[i].data_ptr(),
-                       row_elems, B * row_elems, lens.data_ptr(), ctx, 1.0 / math.sqrt(hd), out.data_ptr(),
-                       heads * hd, ws.data_ptr(), ws_floats, self.stream)
+                       row_elems, bt.data_ptr(), pps, page, lens.data_ptr(), ctx, 1.0 / math.sqrt(hd),
+                       out.data_ptr(), heads * hd, ws.data_ptr(), ws_floats, self.stream)
             return "ps_attn_decode", self._time(launch, ncache)
         nreq = math.ceil(t / ctx)
         new = [min(ctx, t - i * ctx) for i in range(nreq)]
@@ -179,17 +185,18 @@ class KernelBench:
         for v in new:
             q_start.append(q_start[-1] + v)
         p0 = [ctx - v for v in new]
-        cache = torch.empty(ctx * nreq * row_elems, dtype=torch.bfloat16, device="cuda").normal_()
+        cache = torch.empty(pps * page * nreq * row_elems, dtype=torch.bfloat16, device="cuda").normal_()
+        bt = table(nreq)
         q = torch.randn(t, qrows, device="cuda")
         out = torch.empty(t, heads * hd, dtype=torch.bfloat16, device="cuda")
         i_qs = torch.tensor(q_start, dtype=torch.int32, device="cuda")
         i_p0 = torch.tensor(p0, dtype=torch.int32, device="cuda")
 
         def launch(i):
-            L.call("ps_attn_prefill", q.data_ptr(), qrows, nreq, i_qs.data_ptr(), i_p0.data_ptr(), 0,
-                   max(new), heads, kv, hd, cache.data_ptr(), row_elems, nreq * row_elems,
+            L.call("ps_attn_prefill_tc", q.data_ptr(), qrows, nreq, i_qs.data_ptr(), i_p0.data_ptr(), 0,
+                   max(new), heads, kv, hd, cache.data_ptr(), row_elems, bt.data_ptr(), pps, page, nreq * pps,
                    1.0 / math.sqrt(hd), out.data_ptr(), heads * hd, 1, self.stream)
-        return "ps_attn_prefill", self._time(launch, 1)
+        return "ps_attn_prefill_tc", self._time(launch, 1)
 
     def moe_route(self, t: int, d: int, E: int, top_k: int = 8):
         torch, L = self.torch, self.L

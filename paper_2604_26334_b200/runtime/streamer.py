@@ -113,6 +113,26 @@ class CopyRing:
         # "arrived" is the copy-stream event, plus the helpers' sequence when striped
         return region, dst, (ev if seq is None else (ev, seq))
 
+    def upload_runs(self, src_base: int, runs: list, nbytes: int, tag: str) -> tuple[Region, int, int]:
+        """One region of `nbytes` filled by several copies: runs = [(offset, bytes)] of
+        the host range at `src_base`, each landing at the same offset in the region (a
+        paged KV window: pages keep their pool offsets). Returns (region, device
+        address, arrived event)."""
+        region = self._reserve(max(1, nbytes), tag)
+        dst = self.base + region.start
+        tr = self.tracer
+        total = sum(n for _, n in runs)
+        ev0 = tr.begin(self.stream) if tr is not None and total else None
+        for off, n in runs:
+            L.memcpy_async(dst + off, src_base + off, n, self.stream)
+        if ev0 is not None:
+            tr.end(f"{tag} ({total >> 20} MiB, {len(runs)} runs)", "h2d", ev0, self.stream)
+        ev = self.events.next()
+        L.call("ps_event_record", ev, self.stream)
+        self.bytes_copied += total
+        self.copies += len(runs)
+        return region, dst, ev
+
     def reserve_only(self, nbytes: int, tag: str) -> tuple[Region, int]:
         """Ring space without an upload (e.g. room for appended KV rows)."""
         region = self._reserve(nbytes, tag)

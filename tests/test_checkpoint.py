@@ -292,18 +292,28 @@ def test_gguf_rejects_bad_files(tmp_path):
 
 def test_exponent_coding_round_trip():
     """runtime/wcomp.py: 12-bit exponent-coded rows decode to the exact bf16 bits,
-    escapes (zeros, denormals, inf/nan, far exponents) included; the window covers
-    > 99.99 % of the initialiser's weights."""
+    escapes (zeros, denormals, inf/nan, far exponents) included, each row with its own
+    base exponent (a heavy-tailed head row needs no escapes); a matrix with a row of
+    more than MAX_ESCAPES escapes is refused (streams as bf16)."""
     from oracle import model_ref as M
     from paper_2604_26334_b200.runtime import wcomp
     bits = M.bf16_bits(0, "L0.w_gate", 256, 512).copy()
     bits[0, :4] = [0x0000, 0x8000, 0x0001, 0x7F80]       # +0, -0, denormal, inf
     bits[1, 7] = 0x7FC1                                  # nan
     bits[2, 9] = 0x4700                                  # 32768, far above the window
-    coded, base, off, ent = wcomp.encode(bits)
-    assert coded.shape == (256, 768) and coded.dtype == np.uint8
-    assert np.array_equal(wcomp.decode(coded, base, off, ent), bits)
-    assert len(ent) < 1e-3 * bits.size + 8
-    assert wcomp.coded_bytes(256, 512, len(ent)) < 0.76 * bits.nbytes + 4 * 257 + 4 * len(ent) + 1
+    res = wcomp.encode(bits)
+    assert res is not None
+    coded, tb = res
+    assert coded.shape == (256, 768 + tb) and coded.dtype == np.uint8 and tb % 16 == 0
+    assert np.array_equal(wcomp.decode(coded, 512), bits)
+    n_esc = (coded[:, 768:].copy().view(np.uint32)[:, 0] >> 8).sum()
+    assert n_esc < 1e-3 * bits.size + 1100               # row 2: everything below 2^15 / 2^14
+    assert wcomp._trailer_or_none(bits) == tb
+    head = M.bf16_bits(0, "lm_head", 512, 512)           # heavy-tailed rows: own windows
+    c2, tb2 = wcomp.encode(head)
+    assert np.array_equal(wcomp.decode(c2, 512), head) and tb2 <= 32
+    many = bits.copy()
+    many[5, :100] = 0x0001                               # 100 denormals in one row
+    assert wcomp.encode(many) is None and wcomp._trailer_or_none(many) is None
     with pytest.raises(ValueError):
         wcomp.encode(bits[:, :511])

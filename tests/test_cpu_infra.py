@@ -44,6 +44,33 @@ def test_oracle_initialiser_matches_python_restatement():
     np.testing.assert_array_equal(gu[1::2], model_ref.bf16_bits(7, "L0.w_up", 3, 64))
 
 
+def _py_head_row_scale(seed, row):
+    m = (1 << 64) - 1
+    z = (seed ^ 0xD1B54A32D192ED03) ^ ((row * 0x9E3779B97F4A7C15) & m)
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    z ^= z >> 31
+    u = np.float32((np.float32(z >> 40) + np.float32(0.5)) * np.float32(1.0 / 16777216.0))
+    s = np.float32(np.float32(1.0) / np.sqrt(u, dtype=np.float32))   # IEEE sqrt and div
+    return min(s, np.float32(64.0))
+
+
+def test_oracle_head_init_matches_python_restatement():
+    """The output head's heavy-tailed rows (margin-robust init): every element is the
+    uniform value with scale * s_row, s_row = min(u^-1/2, 64), all IEEE-rounded ops."""
+    from oracle import model_ref
+    rows, cols = 6, 64
+    bits = model_ref.bf16_bits(3, "lm_head", rows, cols)
+    sc, _ = model_ref.scale_bias("lm_head", cols)
+    sd = model_ref.seed_of(3, "lm_head")
+    want = np.array([_py_value(sd, i, np.float32(np.float32(sc) * _py_head_row_scale(sd, i // cols)), 0.0)
+                     for i in range(rows * cols)], np.uint16).reshape(rows, cols)
+    np.testing.assert_array_equal(bits, want)
+    # heavy tail: over many rows a few are scaled far above the median
+    big = model_ref.weight(0, "lm_head", 4096, 64).abs().amax(1).numpy()
+    assert big.max() > 20 * np.median(big)
+
+
 def test_oracle_norm_init_range():
     from oracle import model_ref
     w = model_ref.weight(0, "L3.attn_norm", 1, 4096).numpy()

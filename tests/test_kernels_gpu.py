@@ -136,6 +136,32 @@ def _rope_ref(x, pos, inv):
     return torch.cat([a * cos - b * sin, b * cos + a * sin], -1)
 
 
+PAGE = 64
+
+
+def paged(dense, lens, page_rows=PAGE, seed=0, spare=3):
+    """Dense per-request rows [cap, B, ...] -> (pool [pages * page_rows, row], block table
+    [B, pages per slot] int32) with the pages of all requests SHUFFLED over a pool with
+    `spare` unused pages; every row a request does not own (unused pages, rows past its
+    length) holds NaN, so a kernel that reads one is caught."""
+    cap, B = dense.shape[0], dense.shape[1]
+    row = dense[0, 0].numel()
+    pps = -(-cap // page_rows)
+    need = [-(-n // page_rows) for n in lens]
+    n_pages = sum(need) + spare
+    perm = np.random.default_rng(seed).permutation(n_pages)
+    pool = torch.full((n_pages * page_rows, row), float("nan"), device=dense.device).to(dense.dtype)
+    table = np.full((B, pps), -1, np.int32)
+    k = 0
+    for b, n in enumerate(lens):
+        for j in range(need[b]):
+            pg = int(perm[k]); k += 1
+            table[b, j] = pg
+            r0, r1 = j * page_rows, min(n, (j + 1) * page_rows)
+            pool[pg * page_rows:pg * page_rows + (r1 - r0)] = dense[r0:r1, b].reshape(r1 - r0, row)
+    return pool, torch.from_numpy(table).to(dense.device), n_pages
+
+
 @pytest.mark.parametrize("hd,h,kv,qk", [(128, 32, 8, False), (64, 8, 8, False), (128, 32, 4, True)])
 def test_qkv_rope_append(hd, h, kv, qk):
     lib = L()
@@ -146,13 +172,17 @@ def test_qkv_rope_append(hd, h, kv, qk):
     req = torch.tensor([2, 2, 2, 0, 1, 1], dtype=torch.int32, device="cuda")
     inv = 1.0 / (10000.0 ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
     ang = torch.arange(cap, dtype=torch.float64)[:, None] * inv[None, :]
-    table = torch.stack([torch.cos(ang), torch.sin(ang)], -1).float().cuda()
-    cache = torch.zeros(cap, B, 2 * kv * hd, dtype=torch.bfloat16, device="cuda")
+    rope = torch.stack([torch.cos(ang), torch.sin(ang)], -1).float().cuda()
+    # paged cache: request slot b owns pages table[b] (shuffled, 2 per slot)
+    pps = -(-cap // PAGE)
+    table = torch.tensor(np.random.default_rng(hd + h).permutation(B * pps).reshape(B, pps).astype(np.int32),
+                         device="cuda")
+    pool = torch.zeros(B * pps * PAGE, 2 * kv * hd, dtype=torch.bfloat16, device="cuda")
     qn = (1 + 0.1 * torch.randn(hd, device="cuda")).to(torch.bfloat16) if qk else None
     kn = (1 + 0.1 * torch.randn(hd, device="cuda")).to(torch.bfloat16) if qk else None
     src = qkv.clone()
     lib.call("ps_qkv_rope_append", qkv.data_ptr(), rows, T, h, kv, hd, pos.data_ptr(), req.data_ptr(),
-             cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd, table.data_ptr(),
+             pool.data_ptr(), 2 * kv * hd, table.data_ptr(), pps, PAGE, rope.data_ptr(),
              qn.data_ptr() if qk else 0, kn.data_ptr() if qk else 0, 1e-6, stream())
     torch.cuda.synchronize()
     q = src[:, : h * hd].view(T, h, hd)
@@ -165,7 +195,8 @@ def test_qkv_rope_append(hd, h, kv, qk):
     k = _rope_ref(k.cpu(), pos.cpu(), inv).cuda()
     assert rel_err(qkv[:, : h * hd].view(T, h, hd), q) < 1e-5
     for t in range(T):
-        row = cache[pos[t], req[t]].float()
+        p, b = int(pos[t]), int(req[t])
+        row = pool[int(table[b, p // PAGE]) * PAGE + p % PAGE].float()
         assert rel_err(row[: kv * hd].view(kv, hd), k[t]) < 8e-3
         assert rel_err(row[kv * hd:].view(kv, hd), v[t]) < 8e-3
 
@@ -186,16 +217,19 @@ def _attn_ref(q, K, V, qpos):
                                           (128, 32, 4, [1000]), (128, 32, 32, [16384, 129]),
                                           (128, 32, 8, [33, 128, 127, 1])])
 def test_attn_decode(hd, h, kv, lens):
+    """Split-KV decode over a paged cache with shuffled pages (NaN everywhere a request
+    does not own): every request's output matches fp32 attention over its own rows."""
     lib = L()
     B, cap = len(lens), max(lens)
     g = torch.Generator(device="cuda").manual_seed(sum(lens))
     cache = torch.randn(cap, B, 2, kv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    pool, table, _ = paged(cache, lens, seed=sum(lens))
     q = torch.randn(B, h * hd, device="cuda", generator=g)
     ln = torch.tensor(lens, dtype=torch.int32, device="cuda")
     out = torch.zeros(B, h * hd, device="cuda")
     ws = torch.zeros(max(1, lib.attn_decode_workspace(B, h, hd, cap)), device="cuda")
-    lib.call("ps_attn_decode", q.data_ptr(), h * hd, B, h, kv, hd, 0, cache.data_ptr(), 2 * kv * hd,
-             B * 2 * kv * hd, ln.data_ptr(), cap, 1 / math.sqrt(hd), out.data_ptr(), h * hd,
+    lib.call("ps_attn_decode", q.data_ptr(), h * hd, B, h, kv, hd, 0, pool.data_ptr(), 2 * kv * hd,
+             table.data_ptr(), table.shape[1], PAGE, ln.data_ptr(), cap, 1 / math.sqrt(hd), out.data_ptr(), h * hd,
              ws.data_ptr(), ws.numel(), stream())
     torch.cuda.synchronize()
     for b, n in enumerate(lens):
@@ -213,12 +247,14 @@ def test_attn_decode(hd, h, kv, lens):
 def test_attn_prefill(hd, h, kv, seqs, kernel):
     """kernel: the mma.sync flash attention or the tcgen05/TMEM/TMA one; varlen
     requests with p0 > 0 (chunked prefill), GQA groups 1-8, head dims 64 / 128,
-    partial query and key blocks."""
+    partial query and key blocks; paged cache with shuffled pages and NaN in every row a
+    request does not own (its last page's tail included)."""
     lib = L()
     B = len(seqs)
     cap = max(p0 + n for p0, n in seqs)
     g = torch.Generator(device="cuda").manual_seed(cap + B)
     cache = torch.randn(cap, B, 2, kv, hd, device="cuda", generator=g).to(torch.bfloat16)
+    pool, table, n_pages = paged(cache, [p0 + n for p0, n in seqs], seed=cap)
     T = sum(n for _, n in seqs)
     q = torch.randn(T, h * hd, device="cuda", generator=g)
     q_start = np.cumsum([0] + [n for _, n in seqs]).astype(np.int32)
@@ -227,12 +263,12 @@ def test_attn_prefill(hd, h, kv, seqs, kernel):
     out = torch.zeros(T, h * hd, device="cuda", dtype=torch.bfloat16)
     if kernel == "ps_attn_prefill":
         lib.call("ps_attn_prefill", q.data_ptr(), h * hd, B, qs.data_ptr(), p0.data_ptr(), 0,
-                 max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd,
-                 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
+                 max(n for _, n in seqs), h, kv, hd, pool.data_ptr(), 2 * kv * hd, table.data_ptr(),
+                 table.shape[1], PAGE, 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
     else:
         lib.call("ps_attn_prefill_tc", q.data_ptr(), h * hd, B, qs.data_ptr(), p0.data_ptr(), 0,
-                 max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd, cap,
-                 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
+                 max(n for _, n in seqs), h, kv, hd, pool.data_ptr(), 2 * kv * hd, table.data_ptr(),
+                 table.shape[1], PAGE, n_pages, 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, stream())
     torch.cuda.synchronize()
     for b, (s0, n) in enumerate(seqs):
         K = cache[: s0 + n, b, 0].float()
@@ -456,11 +492,12 @@ def test_expert_fetcher_publish_copy_wait():
 
 
 @pytest.mark.parametrize("N,K,t,epi", [(512, 4096, 1, 0), (1000, 2048, 2, 1), (640, 14336, 1, 0),
-                                       (256, 4096, 8, 2), (300, 512, 4, 0)])
+                                       (256, 4096, 8, 2), (300, 512, 4, 0), (4096, 768, 1, 1)])
 def test_gemv_coded_bit_identical(N, K, t, epi):
-    """ps_gemv_bf16c on exponent-coded weights (runtime/wcomp.py, 12 bits/weight) is
-    bit-identical to ps_gemv_bf16 on the bf16 weights, escapes included (zeros,
-    denormals, huge and tiny values outside the 15-exponent window)."""
+    """ps_gemv_bf16c on exponent-coded weights (runtime/wcomp.py, 12 bits/weight, per-row
+    base exponent, escapes in each row's trailer) is bit-identical to ps_gemv_bf16 on the
+    bf16 weights: zeros, denormals, huge and tiny values outside a row's 15-exponent
+    window, a row scaled by 2^20 (its own base) and a row with 40 escapes."""
     from paper_2604_26334_b200.runtime import wcomp
     lib = L()
     g = torch.Generator(device="cuda").manual_seed(N + K)
@@ -468,20 +505,20 @@ def test_gemv_coded_bit_identical(N, K, t, epi):
     W[0, :7] = 0.0
     W[1, 3] = 1e-30
     W[2, 11] = 3.0e4
+    W[3] *= 2.0 ** 20
+    W[4, 5:45] = 1e-12
     W[N - 1, K - 1] = -1e-38
     bits = W.view(torch.int16).cpu().numpy().view(np.uint16)
-    coded, base, off, ent = wcomp.encode(bits)
-    assert len(ent) >= 10
-    assert np.array_equal(wcomp.decode(coded, base, off, ent), bits)
+    coded, tb = wcomp.encode(bits)
+    assert tb >= 16 * 11                         # 40 escapes + header
+    assert np.array_equal(wcomp.decode(coded, K), bits)
     Wc = torch.from_numpy(coded).cuda()
-    d_off, d_ent = torch.from_numpy(off).cuda(), torch.from_numpy(ent).cuda()
     x = torch.randn(t, K, device="cuda", generator=g)
     rows = N // 2 if epi == 2 else N
     y0 = torch.randn(t, rows, device="cuda", generator=g)
     ya, yb = y0.clone(), y0.clone()
     s = stream()
     lib.call("ps_gemv_bf16_cfg", x.data_ptr(), K, t, W.data_ptr(), N, K, K, ya.data_ptr(), rows, epi, s, -1, 0, 0)
-    lib.call("ps_gemv_bf16c", x.data_ptr(), K, t, Wc.data_ptr(), N, K, base, d_off.data_ptr(), d_ent.data_ptr(),
-             yb.data_ptr(), rows, epi, s)
+    lib.call("ps_gemv_bf16c", x.data_ptr(), K, t, Wc.data_ptr(), N, K, coded.shape[1], yb.data_ptr(), rows, epi, s)
     torch.cuda.synchronize()
     assert torch.equal(ya, yb)

@@ -36,14 +36,14 @@ def test_l8_decode_prefill_switch_bytes():
     """Config 2: the decode tier pins 22 attention + 5 KV shards, tier 2048 pins 21
     attention: switching to prefill writes 5 KV caches home."""
     spec, m, plans, mm = _model("llama3.1-8b", budget=4e9)
-    rows = 2048
-    h2d, d2h = mm.bytes(1, 2048, rows)
-    row = rows * 1 * 2 * spec.n_kv_heads * spec.head_dim * 2
+    pages = 2048 // 64                      # one request's 2048 rows = 32 KV pages
+    h2d, d2h = mm.bytes(1, 2048, pages)
+    row = pages * 64 * 2 * spec.n_kv_heads * spec.head_dim * 2
     n_kv1 = sum(1 for p in plans[1].placements if p.residency is Residency.VRAM_PINNED
                 and mm.shards[p.shard_id].kind is ShardKind.KV_CACHE)
     assert d2h == n_kv1 * row
     assert h2d >= 0
-    back = mm.bytes(2048, 1, rows)
+    back = mm.bytes(2048, 1, pages)
     assert back[0] >= n_kv1 * row       # the KV caches come back
 
 

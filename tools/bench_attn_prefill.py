@@ -23,7 +23,9 @@ def run(kernel, h, kv, hd, seqs):
     torch.manual_seed(0)   # both kernels see the same inputs
     B = len(seqs)
     cap = max(p + n for p, n in seqs)
-    cache = torch.randn(cap, B, 2, kv, hd, device="cuda").to(torch.bfloat16)
+    pps = -(-cap // 64)                    # paged cache: request b owns pages [b * pps, (b + 1) * pps)
+    cache = torch.randn(B * pps * 64, 2, kv, hd, device="cuda").to(torch.bfloat16)
+    bt = torch.arange(B * pps, dtype=torch.int32, device="cuda").view(B, pps)
     T = sum(n for _, n in seqs)
     q = torch.randn(T, (h + 2 * kv) * hd, device="cuda")
     qs = torch.tensor(np.cumsum([0] + [n for _, n in seqs]).astype(np.int32), device="cuda")
@@ -35,11 +37,11 @@ def run(kernel, h, kv, hd, seqs):
         s = torch.cuda.current_stream().cuda_stream
         if kernel == "tc":
             L.call("ps_attn_prefill_tc", q.data_ptr(), ldq, B, qs.data_ptr(), p0.data_ptr(), 0,
-                   max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd, cap,
-                   1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, s)
+                   max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, bt.data_ptr(), pps, 64,
+                   B * pps, 1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, s)
         else:
             L.call("ps_attn_prefill", q.data_ptr(), ldq, B, qs.data_ptr(), p0.data_ptr(), 0,
-                   max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, B * 2 * kv * hd,
+                   max(n for _, n in seqs), h, kv, hd, cache.data_ptr(), 2 * kv * hd, bt.data_ptr(), pps, 64,
                    1 / math.sqrt(hd), out.data_ptr(), h * hd, 1, s)
     launch(); launch(); torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
