@@ -12,7 +12,11 @@ Inputs exceed L2: each pass streams ~13 GB of weights (L2 is 126 MB).
 
 --gpus N: one process per GPU (torchrun), each an independent replica of
 the same workload ("replicas only": the batch-1 path does not shard, and no
-collective is used); value = all ranks' tokens / max-over-ranks time.
+collective is used); value = all ranks' tokens / max-over-ranks time. The
+bookkeeping (barriers, one sum and one max of host scalars) runs on gloo: no NCCL.
+
+The run generates the config's full `gen` tokens (e.g. 2048 + 256): the timed
+steps are decode passes [W, W + K) of that run, and e2e covers every decode pass.
 
 --impl reference: the reference has no CPU inference path (it is a planner
 and simulator); the CPU arm times the fp32 CPU restatement (oracle/model_ref.py)
@@ -67,6 +71,8 @@ def parse():
     ap.add_argument("--gen", type=int)
     ap.add_argument("--batch", type=int)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-plan-faithful", action="store_true",
+                    help="skip the short PS_SPARE_PIN=0 PS_CODED=0 run reported as plan_faithful")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
     ap.add_argument("--stripe", action="store_true",
                     help="N>1: one request stream striped over every GPU's host link "
@@ -94,7 +100,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,memory.used")
 
     def __init__(self, index: int):
         self.index = index
@@ -133,6 +139,12 @@ class ClockSampler:
                 "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
+    def mem_used_max_gb(self):
+        """NVML memory.used (whole GPU: CUDA context, torch allocator, the arena) over the
+        sampled region, GB."""
+        vals = [float(s[7]) for s in self.samples if len(s) > 7 and s[7].replace(".", "").isdigit()]
+        return round(max(vals) * (1 << 20) / GB, 3) if vals else None
+
 
 def measure_h2d(L, nbytes=1 << 30, reps=5) -> float:
     """Pinned cudaMemcpyAsync H2D GB/s, best of `reps` (the link's roofline denominator)."""
@@ -154,42 +166,83 @@ def measure_h2d(L, nbytes=1 << 30, reps=5) -> float:
     return best
 
 
+def _ncu_traffic(name):
+    prof = os.path.join(REPO, "profiles", name)
+    if not os.path.exists(prof):
+        return None, None
+    with open(prof) as fh:
+        rec = json.loads(fh.readline())
+    return int(rec["traffic_bytes"]), f"profiles/{name} (ncu --set full)"
+
+
 def gemv_kernel_roofline(L, peaks) -> dict:
-    """The hot compute kernel on resident weights: K1 GEMV (bulk-copy kernel,
-    gemv_tma.cu) over the FFN gate/up matrix (28672 x 4096 bf16 = 234.9 MB per
-    launch), events on its stream, L2 flushed by a read-only pass between launches."""
+    """The hot compute kernels on VRAM-resident weights, timed on their stream with CUDA
+    events, L2 flushed by a read-only pass between launches: K1 GEMV (bulk-copy kernel,
+    gemv_tma.cu) over the FFN gate/up matrix (28672 x 4096 bf16 = 234.9 MB per launch),
+    and the same matrix exponent-coded (ps_gemv_bf16c, the kernel every streamed dense
+    piece of a decode pass runs: 176.6 MB per launch)."""
+    import numpy as np
     import torch
+    from paper_2604_26334_b200.runtime import wcomp
     N, K = 2 * 14336, 4096
     W = torch.empty(N, K, dtype=torch.bfloat16, device="cuda").normal_()
     x = torch.randn(1, K, device="cuda")
     y = torch.zeros(1, N // 2, device="cuda")
+    coded, _ = wcomp.encode(W.view(torch.int16).cpu().numpy().view(np.uint16))
+    Wc = torch.from_numpy(coded).cuda()
     flush = torch.ones(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > L2
     s = torch.cuda.current_stream().cuda_stream   # the flush runs on the same stream, so the
     e0, e1 = L.event_create(True), L.event_create(True)  # GPU is busy while the host enqueues
-    times = []
-    for i in range(12):
-        flush.sum()                   # evict W from L2 (read-only: leaves no dirty lines to write back)
-        L.call("ps_event_record", e0, s)
-        L.call("ps_gemv_bf16", x.data_ptr(), K, 1, W.data_ptr(), N, K, K, y.data_ptr(), N // 2, 2, s)
-        L.call("ps_event_record", e1, s)
-        L.call("ps_event_synchronize", e1)
-        if i >= 2:
-            times.append(L.event_elapsed_ms(e0, e1) / 1e3)
-    nbytes = N * K * 2 + K * 4 + (N // 2) * 4
-    avg = sum(times) / len(times)
-    achieved = nbytes / avg / GB
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic, tsrc = None, None
-    prof = os.path.join(REPO, "profiles", "r01_ncu_gemv_tma_235MB.jsonl")
-    if os.path.exists(prof):   # dram bytes read + written per launch, one ncu --set full capture
-        with open(prof) as fh:
-            rec = json.loads(fh.readline())
-        traffic, tsrc = int(rec["traffic_bytes"]), "profiles/r01_ncu_gemv_tma_235MB.jsonl (ncu --set full)"
+
+    def timed(launch):
+        times = []
+        for i in range(12):
+            flush.sum()               # evict W from L2 (read-only: leaves no dirty lines to write back)
+            L.call("ps_event_record", e0, s)
+            launch()
+            L.call("ps_event_record", e1, s)
+            L.call("ps_event_synchronize", e1)
+            if i >= 2:
+                times.append(L.event_elapsed_ms(e0, e1) / 1e3)
+        return sum(times) / len(times)
+    avg = timed(lambda: L.call("ps_gemv_bf16", x.data_ptr(), K, 1, W.data_ptr(), N, K, K, y.data_ptr(), N // 2, 2, s))
+    avg_c = timed(lambda: L.call("ps_gemv_bf16c", x.data_ptr(), K, 1, Wc.data_ptr(), N, K, coded.shape[1],
+                                 y.data_ptr(), N // 2, 2, s))
+    nbytes = N * K * 2 + K * 4 + (N // 2) * 4
+    nbytes_c = coded.nbytes + K * 4 + (N // 2) * 4
+    traffic, tsrc = _ncu_traffic("r02_ncu_gemv_bf16_235MB.jsonl")
+    traffic_c, tsrc_c = _ncu_traffic("r02_ncu_gemv_coded_177MB.jsonl")
     return {"kernel": "ps_gemv_bf16 (K1 bulk-copy kernel, SwiGLU epilogue) 28672x4096, t=1", "bound": "hbm",
-            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "algorithmic_bytes": nbytes,
+            "achieved": round(nbytes / avg / GB, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(nbytes / avg / GB / peak, 4), "algorithmic_bytes": nbytes,
             "avg_launch_us": round(avg * 1e6, 2), "traffic": traffic, "traffic_source": tsrc,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
+            "coded": {"kernel": "ps_gemv_bf16c (exponent-coded rows, same matrix), t=1", "bound": "hbm",
+                      "achieved": round(nbytes_c / avg_c / GB, 1), "peak": peak, "unit": "GB/s",
+                      "frac": round(nbytes_c / avg_c / GB / peak, 4), "algorithmic_bytes": nbytes_c,
+                      "avg_launch_us": round(avg_c * 1e6, 2), "traffic": traffic_c, "traffic_source": tsrc_c}}
+
+
+def reference_planning_seconds(args) -> dict:
+    """the reference's own CPU work for this config — the UNMODIFIED
+    `build_tier_table` (oracle/plan_oracle.py runs it in a subprocess from baseline/_ref),
+    single-threaded CPython on this host, wall seconds."""
+    from paper_2604_26334_b200.planning import catalog
+    from paper_2604_26334_b200.planning.graph import model_to_dict
+    from paper_2604_26334_b200.planning.hardware import machine_to_dict
+    cfg = [{"id": "bench", "model": model_to_dict(catalog.builtin_model(args.model)),
+            "machine": machine_to_dict(catalog.builtin_machine("b200")),
+            "budget": args.budget_gb * GB, "context": args.prompt + args.gen, "batch": args.batch}]
+    t0 = time.perf_counter()
+    r = subprocess.run([sys.executable, os.path.join(REPO, "oracle", "plan_oracle.py")], input=json.dumps(cfg),
+                       capture_output=True, text=True, timeout=600)
+    wall = time.perf_counter() - t0
+    if r.returncode != 0:
+        return {"error": r.stderr.strip()[-300:]}
+    rec = json.loads(r.stdout)[0]
+    return {"build_tier_table_s": round(rec["seconds"], 4), "process_wall_s": round(wall, 2), "cores": 1,
+            "ok": "sha256" in rec}
 
 
 def cpu_baseline_sample(eng, steps: int) -> dict:
@@ -254,7 +307,10 @@ def run_ours(args, rank: int, world: int) -> dict:
     h2d_peak = measure_h2d(L)
     B = args.batch
     ctx = args.prompt + args.gen
-    gen = min(args.gen, args.warmup + args.steps + 1)
+    gen = args.gen                      # the config's full generation
+    if args.warmup + args.steps > gen - 1:
+        raise SystemExit(f"--warmup {args.warmup} + --steps {args.steps} exceed the {gen - 1} decode passes "
+                         f"of prompt {args.prompt} + gen {gen}")
     shared = None
     if stripe:
         shared = blob_name
@@ -284,6 +340,9 @@ def run_ours(args, rank: int, world: int) -> dict:
         sh = eng.weights.shared
         if sh is not None and sh.creator:
             sh.unlink()    # every replica has it mapped: a crashed job leaks no /dev/shm
+        coded = getattr(eng.weights, "coded", None)
+        if coded is not None and coded.seg is not None and coded.seg.creator:
+            coded.seg.unlink()
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clocks:
         t0 = time.perf_counter()
@@ -303,18 +362,20 @@ def run_ours(args, rank: int, world: int) -> dict:
     zero_copy = sum(p[4] for p in timed) / max(1, len(timed))
     # replicas: sum of tokens over ranks / max over ranks of device seconds (no data collective)
     from paper_2604_26334_b200.runtime.replicas import aggregate
-    agg = (aggregate(B * len(timed), t_steps, device="cpu" if args.stripe_same_gpu else "cuda") if not stripe else
+    agg = (aggregate(B * len(timed), t_steps, device="cpu") if not stripe else
            {"seconds_max": t_steps, "value": B * len(timed) / t_steps})
     t_max, value = agg["seconds_max"], agg["value"]
     # end to end through the public API: all decode passes, host wall clock, tokens read back
     e2e_decode_wall = wall - res.ttft_s
     e2e = B * (gen - 1) / e2e_decode_wall
     if world > 1 and not stripe:   # whole job: tokens of every replica / slowest replica's wall
-        e2e = aggregate(B * (gen - 1), e2e_decode_wall,
-                        device="cpu" if args.stripe_same_gpu else "cuda")["value"]
+        e2e = aggregate(B * (gen - 1), e2e_decode_wall, device="cpu")["value"]
     kv_wb = sum(s.kv_writeback_bytes for s in timed_stats) / max(1, len(timed_stats))
     achieved = streamed / (t_steps / len(timed)) / GB
     plan_dec = eng.plans[eng.pick_tier(B)]
+    # the plan's own link bytes per decode step (what the reference's schedule streams):
+    # against those, the executor's caching + lossless coding can exceed 1.0
+    plan_bytes = plan_dec.pcie_h2d_bytes
     out = {
         "metric": metric_name(args), "value": round(value, 4),
         "unit": "tokens/s", "n_gpus": world,
@@ -325,7 +386,7 @@ def run_ours(args, rank: int, world: int) -> dict:
         "ttft_ms": round(res.ttft_s * 1e3, 2),
         "config": {"workload": args.workload + " (random-init weights)",
                    "model": args.model, "global_batch": world * B, "seq_len": ctx,
-                   "prompt": args.prompt, "gen": args.gen, "budget_gb": round(args.budget_gb, 4),
+                   "prompt": args.prompt, "gen": args.gen, "gen_run": gen, "budget_gb": round(args.budget_gb, 4),
                    "parallelism": (f"stripe{world}" if stripe else f"replicas{world}") if world > 1
                    else "single",
                    "decode_tier": eng.pick_tier(B), "decode_plan": plan_dec.kind.value,
@@ -335,7 +396,14 @@ def run_ours(args, rank: int, world: int) -> dict:
                      "unit": "GB/s", "frac": round(achieved / (h2d_peak * (world if stripe else 1)), 4),
                      "traffic": None, "algorithmic_bytes_per_step": int(streamed),
                      "peak_source": "pinned cudaMemcpyAsync 1 GiB best-of-5, measured in this run",
-                     "what": "copy-engine weight stream (dominant stage of every decode step)"},
+                     "what": "copy-engine weight stream (dominant stage of every decode step); "
+                             "achieved = bytes the executor moved per step / step time",
+                     "plan_bytes_per_step": int(plan_bytes),
+                     "plan_frac": round(plan_bytes / (t_steps / len(timed)) / GB /
+                                        (h2d_peak * (world if stripe else 1)), 4),
+                     "plan_frac_note": "the plan's streamed bytes per decode step (pkg/src/shardplan/planner.py "
+                                       "pcie_h2d_bytes) over the measured step time and link: > 1 means the "
+                                       "executor moves fewer bytes than the plan prices (spare pins, coding)"},
         "kernel_roofline": gemv_kernel_roofline(L, peaks),
         "e2e": {"value": round(e2e, 4), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(streamed), "d2h_bytes_per_step": int(kv_wb + 4 * B),
@@ -343,6 +411,9 @@ def run_ours(args, rank: int, world: int) -> dict:
                        "each token read back to pinned host memory"},
         "gpu_launches": None,
         "clocks": clocks.summary(),
+        "vram": {"arena_cap_gb": round(args.budget_gb, 4), "nvml_used_max_gb": clocks.mem_used_max_gb(),
+                 "note": "NVML memory.used of the whole GPU during the timed region: the capped arena plus "
+                         "the CUDA context and torch's allocator (bench buffers)"},
         "ttft": {"ms": round(res.ttft_s * 1e3, 2), "migration_bytes": int(res.migration_bytes),
                  "relocated_in_vram_bytes": int(ex.d2d_bytes),
                  "switches": [{"from": a, "to": b, "kv_pages": r, "moved": mv, "model_h2d": h, "model_d2h": dd}
@@ -372,7 +443,13 @@ def run_ours(args, rank: int, world: int) -> dict:
             out["cpu_baseline"] = cpu_baseline_sample(eng, args.cpu_sample_steps)
         except Exception as exc:  # reported, never fatal
             out["cpu_baseline"] = {"value": None, "error": repr(exc)[:300]}
+        try:
+            out["cpu_baseline"]["reference_planning"] = reference_planning_seconds(args)
+        except Exception as exc:
+            out["cpu_baseline"]["reference_planning"] = {"error": repr(exc)[:300]}
     eng.close()
+    if rank == 0 and world == 1 and not stripe and not args.no_plan_faithful:
+        out["plan_faithful"] = plan_faithful_run(args, prompts)
     if stripe:
         out["stripe"] = {"helpers": world - 1, "striped_pieces": leader.striped_pieces,
                          "striped_bytes": leader.striped_bytes, "wait_timeout_seq": leader.error_seq(),
@@ -381,6 +458,36 @@ def run_ours(args, rank: int, world: int) -> dict:
         import torch.distributed as dist
         dist.barrier()
     return out
+
+
+def plan_faithful_run(args, prompts) -> dict:
+    """The plan's residency exactly (PS_SPARE_PIN=0) and bf16 on the link (PS_CODED=0):
+    what the reference's schedule would move, run for real on a short generation."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    saved = {k: os.environ.get(k) for k in ("PS_SPARE_PIN", "PS_CODED")}
+    os.environ.update(PS_SPARE_PIN="0", PS_CODED="0")
+    try:
+        gen = min(args.gen, 10)
+        eng = Engine(args.model, budget_bytes=args.budget_gb * GB, context_len=args.prompt + args.gen,
+                     batch=args.batch)
+        eng.prepare([args.prompt] * args.batch, gen)
+        res = eng.generate(prompts, gen_len=gen)
+        dec = [p for p in res.passes if p[1] == args.batch and p[0] == eng.pick_tier(args.batch)][1:]
+        secs = sum(p[2] for p in dec)
+        link = sum(p[3] + p[4] for p in dec) / max(1, len(dec))
+        eng.close()
+        return {"value": round(args.batch * len(dec) / secs, 4) if secs else None, "unit": "tokens/s",
+                "steps": len(dec), "link_bytes_per_step": int(link), "ttft_ms": round(res.ttft_s * 1e3, 2),
+                "how": "PS_SPARE_PIN=0 PS_CODED=0: the plan's residency, bf16 on the link, "
+                       f"prompt {args.prompt} + {gen} tokens, decode passes 2.. timed"}
+    except Exception as exc:   # reported, never fatal
+        return {"value": None, "error": repr(exc)[:300]}
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def metric_name(args) -> str:
@@ -447,8 +554,9 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(0 if args.stripe_same_gpu else int(os.environ.get("LOCAL_RANK", 0)))
-        # striped mode only needs host-side control (barriers, a broadcast): gloo
-        dist.init_process_group("gloo" if (args.stripe or args.stripe_same_gpu) else "nccl")
+        # replicas and stripes only need host-side bookkeeping (barriers, a broadcast, a sum
+        # and a max of host scalars): gloo, no NCCL anywhere
+        dist.init_process_group("gloo")
     out = run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(out))

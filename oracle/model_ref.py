@@ -292,7 +292,7 @@ class RefModel:
         return (o * inv).permute(1, 0, 2).reshape(T, -1)
 
     @torch.no_grad()
-    def forward(self, tokens, cache, modes=None, logit_rows=None) -> torch.Tensor:
+    def forward(self, tokens, cache, modes=None, logit_rows=None, perturb=None) -> torch.Tensor:
         """Append `tokens` to one request's cache; returns fp32 logits [rows, V].
 
         `modes` (one character per token, default all "D") mirrors where the GPU pass
@@ -304,7 +304,11 @@ class RefModel:
                bf16, tcgen05 attention with a bf16 output, SwiGLU output rounded to bf16.
         The residual stream, router logits, expert hidden states and the output head
         are fp32 in every mode; K and V are stored as bf16. `logit_rows`: rows whose
-        logits to return (default all)."""
+        logits to return (default all). `perturb` = (seed, eps): multiply the embedded
+        inputs by (1 + eps * N(0, 1)) — the oracle's own numerical noise band: bf16
+        rounding points amplify a 1e-7 input change to ~1e-3 of max|logit|,
+        so positions whose top-2 margin lies inside that band have no well-defined
+        bf16 argmax."""
         tokens = torch.as_tensor(np.asarray(tokens, np.int64))
         T = tokens.numel()
         modes = "D" * T if modes is None else modes
@@ -318,6 +322,9 @@ class RefModel:
         p0 = cache[0]["k"].shape[0]
         pos = torch.arange(p0, p0 + T)
         x = self.embed[tokens].float()
+        if perturb is not None:
+            g = torch.Generator().manual_seed(int(perturb[0]))
+            x = x * (1 + float(perturb[1]) * torch.randn(x.shape, generator=g))
         for lw, c in zip(self.layers, cache):
             a = _round_rows(self._rms(x, self._w(lw["attn_norm"])), g_rows)
             q = (a @ self._w(lw["wq"]).T).view(T, self.h, self.hd)
@@ -368,13 +375,46 @@ class RefModel:
         return np.array(toks, np.int32), torch.stack(all_logits)
 
     @torch.no_grad()
-    def teacher_forced(self, prompt, continuation, modes=None):
+    def teacher_forced(self, prompt, continuation, modes=None, perturb=None):
         """Logits at each emitting position when the continuation is forced, in one
-        forward over prompt + continuation[:-1]; `modes` as in `forward`."""
+        forward over prompt + continuation[:-1]; `modes` / `perturb` as in `forward`."""
         cache = self.new_cache()
         seq = list(np.asarray(prompt)) + list(np.asarray(continuation))[:-1]
         rows = list(range(len(prompt) - 1, len(seq)))
-        return self.forward(seq, cache, modes, logit_rows=rows)
+        return self.forward(seq, cache, modes, logit_rows=rows, perturb=perturb)
+
+
+def greedy_parity(ref, prompt, got, modes, n_perturb: int = 1, eps: float = 1e-7) -> dict:
+    """Token parity of a GPU greedy run `got` against the oracle, teacher-forced.
+
+    The oracle runs with the GPU's per-pass rounding points (`modes`) and again with
+    its inputs perturbed by `eps` (n_perturb seeds; 1e-7 ~ the fp32 summation-order noise of the GPU); the spread at each position is the
+    oracle's own noise band (chaotic amplification by the bf16 rounding points). A
+    position is DECIDED when the oracle's top-1 / top-2 margin exceeds twice that band
+    and every perturbed run agrees on the argmax; there the GPU id must be the oracle's
+    EXACTLY. At an undecided (near-tie) position the GPU id must be one of the tied
+    candidates: its logit within twice the band of the top. Returns the counts and the
+    mirrored logits (numpy [len(got), V])."""
+    tf0 = ref.teacher_forced(prompt, got, modes).numpy()
+    band = np.zeros(len(got))
+    agree = np.ones(len(got), bool)
+    top0 = tf0.argmax(1)
+    for k in range(n_perturb):
+        tfk = ref.teacher_forced(prompt, got, modes, perturb=(1000 + k, eps)).numpy()
+        band = np.maximum(band, np.abs(tfk - tf0).max(1))
+        agree &= tfk.argmax(1) == top0
+    srt = np.sort(tf0, axis=1)
+    margin = srt[:, -1] - srt[:, -2]
+    decided = agree & (margin > 2 * band)
+    got = np.asarray(got)
+    exact_bad = [int(i) for i in np.nonzero(decided & (got != top0))[0]]
+    tie_bad = [int(i) for i in np.nonzero(~decided)[0]
+               if tf0[i, top0[i]] - tf0[i, got[i]] > 2 * band[i]]
+    scale = float(np.abs(tf0).max())
+    return {"positions": len(got), "decided": int(decided.sum()), "undecided": int((~decided).sum()),
+            "exact_mismatch": exact_bad, "tie_mismatch": tie_bad,
+            "equal": int((got == top0).sum()), "band_max": float(band.max()) / scale,
+            "min_margin": float(margin.min()) / scale, "logits": tf0}
 
 
 def _round_rows(x: torch.Tensor, rows: torch.Tensor) -> torch.Tensor:

@@ -31,7 +31,10 @@ namespace ps {
 
 constexpr int GT_STAGES = 5;
 constexpr int GT_STAGE_BYTES = 32768;
-constexpr int GT_CONSUMERS = 8;                      // consumer warps
+#ifndef PS_GT_CONSUMERS
+#define PS_GT_CONSUMERS 16
+#endif
+constexpr int GT_CONSUMERS = PS_GT_CONSUMERS;        // consumer warps (8 or 16)
 constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp
 
 // Per token count: columns per consumer thread (x kept in registers: CPT * T floats)
@@ -43,7 +46,8 @@ constexpr int gt_pow2_floor(int v) { return v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ?
 constexpr int GT_TRAILER_MAX = 256;
 
 template <int T, bool COMP = false> struct GtShape {
-  static constexpr int CPT = T <= 4 ? 16 : 8;
+  // 16 consumer warps: 8 columns per thread at every T (KC = 4096); 8 warps: 16 / 8
+  static constexpr int CPT = GT_CONSUMERS >= 16 ? 8 : (T <= 4 ? 16 : 8);
   static constexpr int KC = GT_CONSUMERS * 32 * CPT;
   static constexpr int ROWB = COMP ? KC * 3 / 2 + GT_TRAILER_MAX : KC * 2;   // stage bytes per row segment
   static constexpr int RS = COMP ? gt_pow2_floor(GT_STAGE_BYTES / ROWB) : GT_STAGE_BYTES / (KC * 2);
@@ -125,16 +129,20 @@ __device__ __forceinline__ uint32_t gt_pair(uint32_t smw, uint32_t sm_sel, uint3
   return (bb & 0x007F007Fu) | ((bb << 8) & 0x80008000u) | e7;
 }
 
-__device__ __forceinline__ uint4 gt_decode8(uint2 sm, uint32_t nb, uint32_t base7, const uint32_t* trailer,
-                                            int col) {
+// Fast path only: escapes (code 15) come out wrong and are patched by the caller once
+// per row when gt_escapes() flags any of the row's groups.
+__device__ __forceinline__ uint4 gt_decode8(uint2 sm, uint32_t nb, uint32_t base7) {
   const uint32_t lo = nb & 0x0F0F0F0Fu, hi = (nb >> 4) & 0x0F0F0F0Fu;   // codes 0,2,4,6 | 1,3,5,7
   uint4 v;
   v.x = gt_pair(sm.x, 0x4140u, lo, hi, 0x8480u, base7);
   v.y = gt_pair(sm.x, 0x4342u, lo, hi, 0x9591u, base7);
   v.z = gt_pair(sm.y, 0x4140u, lo, hi, 0xA6A2u, base7);
   v.w = gt_pair(sm.y, 0x4342u, lo, hi, 0xB7B3u, base7);
-  if (nb & (nb >> 1) & (nb >> 2) & (nb >> 3) & 0x11111111u) v = gt_patch_escapes(v, sm, nb, trailer, col);
   return v;
+}
+
+__device__ __forceinline__ uint32_t gt_escapes(uint32_t nb) {   // non-zero: some code is 15
+  return nb & (nb >> 1) & (nb >> 2) & (nb >> 3) & 0x11111111u;
 }
 
 template <int T, int EPI, bool COMP = false>
@@ -246,20 +254,32 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
 #pragma unroll
       for (int r = 0; r < RS; ++r) {
         uint4 w[CPT / 8];
+        if constexpr (COMP) {
+          const uint8_t* rowp = stage + r * ROWB;
+          const uint32_t* trailer = reinterpret_cast<const uint32_t*>(rowp + KC * 3 / 2);
+          const bool live = r < nr;
+          const uint32_t base7 = live ? ((trailer[0] & 0xFFu) * 0x10001u) << 7 : 0u;
+          uint2 sm[CPT / 8];
+          uint32_t nb[CPT / 8], esc = 0;
 #pragma unroll
-        for (int h = 0; h < CPT / 8; ++h) {
-          const int col = (h * GT_CONSUMERS * 32 + j) * 8;
-          if constexpr (COMP) {
-            if (r < nr && col < kc) {
-              const uint32_t* trailer = reinterpret_cast<const uint32_t*>(stage + r * ROWB + KC * 3 / 2);
-              const uint32_t base7 = ((trailer[0] & 0xFFu) * 0x10001u) << 7;
-              const uint2 sm = *reinterpret_cast<const uint2*>(stage + r * ROWB + col);
-              const uint32_t nb = *reinterpret_cast<const uint32_t*>(stage + r * ROWB + KC + col / 2);
-              w[h] = gt_decode8(sm, nb, base7, trailer, c * KC + col);
-            } else {
-              w[h] = make_uint4(0, 0, 0, 0);
-            }
-          } else {
+          for (int h = 0; h < CPT / 8; ++h) {
+            const int col = (h * GT_CONSUMERS * 32 + j) * 8;
+            const bool ok = live && col < kc;
+            sm[h] = ok ? *reinterpret_cast<const uint2*>(rowp + col) : make_uint2(0, 0);
+            nb[h] = ok ? *reinterpret_cast<const uint32_t*>(rowp + KC + col / 2) : 0u;
+            w[h] = ok ? gt_decode8(sm[h], nb[h], base7) : make_uint4(0, 0, 0, 0);
+            esc |= gt_escapes(nb[h]);
+          }
+          if (esc) {   // rare: one branch per row for all of this thread's groups
+#pragma unroll
+            for (int h = 0; h < CPT / 8; ++h)
+              if (gt_escapes(nb[h]))
+                w[h] = gt_patch_escapes(w[h], sm[h], nb[h], trailer, c * KC + (h * GT_CONSUMERS * 32 + j) * 8);
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < CPT / 8; ++h) {
+            const int col = (h * GT_CONSUMERS * 32 + j) * 8;
             w[h] = (r < nr && col < kc) ? *reinterpret_cast<const uint4*>(stage + (r * KC + col) * 2)
                                         : make_uint4(0, 0, 0, 0);
           }

@@ -299,6 +299,11 @@ class Engine:
         """fp32 logits [rows, V] of the last iteration's emitting requests, in slot order."""
         return self._need_executor().logits_host(self._sess.last_rows if self._sess else 1)
 
+    def last_sampled_slots(self) -> list:
+        """Request slots of the rows `logits()` returns (the last iteration's emitters)."""
+        s = self._need_session()
+        return list(s.last_sampled or [])
+
     def row_modes(self) -> list:
         """Per request: the numerics of the pass that computed each position so far
         (see GenerateResult.row_modes)."""
