@@ -148,6 +148,17 @@ int ps_attn_tc_watchdog(unsigned* code, int reset);
  * reset clears them. The executor raises on any non-zero word after every pass. */
 int ps_fault_status(unsigned* words /* [4] */, int reset);
 
+/* Decode GEMV for 9..32 tokens on the tcgen05 tensor cores (gemv_tc.cu): y[t, n] (epi)=
+ * x[t, :] . W[n, :] reading W ONCE (the CUDA-core GEMV takes 8 tokens per launch). W is
+ * bf16 [N x K] (row stride ldw elements) or, with coded = 1, exponent-coded rows of ldw
+ * bytes (the format of ps_gemv_bf16c). x is split into three bf16 planes (x1 + x2 + x3 =
+ * x to fp32 precision) and the three products accumulate in fp32 TMEM: fp32-faithful.
+ * Split-K partials are summed in a fixed order (deterministic). workspace: device bytes,
+ * >= ps_gemv_tc_workspace(N, K), 256-byte aligned. t <= 32, K % 64 == 0. */
+int ps_gemv_tc(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw, int coded,
+               float* y, int ldy, int epilogue, void* workspace, long long workspace_bytes, void* stream);
+int ps_gemv_tc_workspace(int N, int K, long long* bytes);
+
 /* Exponent-coded GEMV: y[t, n] (epi)= x[t, :] . W[n, :] with W in the 12-bit format of
  * runtime/wcomp.py: row n (stride ldw bytes) = K sign|mantissa bytes, K/2 bytes of 4-bit
  * exponent codes relative to the row's base (15 = escape), then a trailer of ldw - 1.5 K
@@ -206,6 +217,14 @@ int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot
                           const void* expert_base, long long expert_stride, long long gu_off,
                           long long down_off, int eff, int d, float* h, const float* w, float* y,
                           void* stream);
+/* The same on exponent-coded experts (runtime/wcomp.py rows; gu_row_bytes = 1.5 d +
+ * trailer, down_row_bytes = 1.5 eff + trailer, every expert of the group the same size):
+ * decoded in the consumer loops, bit-identical to ps_moe_decode_experts on the decoded
+ * weights. d and eff multiples of 256. */
+int ps_moe_decode_experts_c(const float* x, const int* ids, int k, const int* slot_of_expert,
+                            const void* expert_base, long long expert_stride, long long gu_off,
+                            long long down_off, int eff, int d, int gu_row_bytes, int down_row_bytes,
+                            float* h, const float* w, float* y, void* stream);
 
 /* ---- routed-expert fetcher (copy-engine uploads of router-selected experts) --
  * Replaces the zero-copy read of a streamed expert group in decode passes: the GPU

@@ -56,6 +56,7 @@ bool is_host_ptr(const void* p) {
 
 int ps_preload_gemv();
 int ps_preload_gemv_tma();
+int ps_preload_gemv_tc();
 int ps_preload_gemm();
 int ps_preload_attention();
 int ps_preload_elementwise();
@@ -113,7 +114,7 @@ int ps_fault_status(unsigned* words, int reset) {
 int ps_preload_kernels(int* n_loaded) {
   static int loaded = -1;
   if (loaded < 0)
-    loaded = ps_preload_gemv() + ps_preload_gemv_tma() + ps_preload_gemm() + ps_preload_attention() +
+    loaded = ps_preload_gemv() + ps_preload_gemv_tma() + ps_preload_gemv_tc() + ps_preload_gemm() + ps_preload_attention() +
              ps_preload_elementwise() + ps_preload_moe() + ps_preload_moe_decode() + ps_preload_fetcher() + ps_preload_striper() +
              ps_preload_attention_tc();
   if (n_loaded) *n_loaded = loaded;

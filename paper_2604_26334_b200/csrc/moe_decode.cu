@@ -28,10 +28,16 @@
 // Measured (tools/bench_moe_decode.py, Q30 shapes, warm): 11.2 + 8.0 us for the
 // 75.5 MB of 8 experts vs 50 us for the general chain; ncu: DRAM read = the
 // algorithmic bytes (profiles/r01_ncu_moe_decode_t1.jsonl).
+//
+// COMP variants (ps_moe_decode_experts_c): the experts arrive exponent-coded
+// (runtime/wcomp.py rows: sign|mantissa bytes, 4-bit codes, trailer) — 25 % fewer
+// bytes through the fetcher's copy engine — and each 8-column group is decoded in
+// the consumer loop (wcodec.cuh) before the same dot product: bit-identical outputs.
 #include <stdlib.h>
 
 #include "common.cuh"
 #include "mbarrier.cuh"
+#include "wcodec.cuh"
 #include "../../include/pshard.h"
 
 namespace ps {
@@ -52,6 +58,23 @@ __device__ __forceinline__ float2 md_dot8(uint4 w, const float2* x, float2 s) {
   return s;
 }
 
+// 8 weights of row `row` at column `col`: bf16 straight from the row, or decoded from
+// the coded row (K sign|mantissa bytes, K/2 code bytes, trailer at 1.5 K).
+template <bool COMP>
+__device__ __forceinline__ uint4 md_load8(const uint8_t* row, int col, int K) {
+  if constexpr (COMP) {
+    const uint32_t* trailer = reinterpret_cast<const uint32_t*>(row + K * 3 / 2);
+    const uint32_t base7 = ((trailer[0] & 0xFFu) * 0x10001u) << 7;
+    const uint2 sm = *reinterpret_cast<const uint2*>(row + col);
+    const uint32_t nb = *reinterpret_cast<const uint32_t*>(row + K + col / 2);
+    uint4 w = gt_decode8(sm, nb, base7);
+    if (gt_escapes(nb)) w = gt_patch_escapes(w, sm, nb, trailer, col);
+    return w;
+  } else {
+    return *reinterpret_cast<const uint4*>(row + col * 2);
+  }
+}
+
 // one stage = `bytes` in bulk copies of <= chunk bytes (all on the stage's barrier)
 __device__ __forceinline__ void md_copy(uint8_t* dst, const uint8_t* src, int bytes, int chunk, uint64_t* bar) {
   for (int o = 0; o < bytes; o += chunk) bulk_load(dst + o, src + o, (uint32_t)min(chunk, bytes - o), bar);
@@ -62,18 +85,17 @@ __device__ __forceinline__ void md_copy(uint8_t* dst, const uint8_t* src, int by
 // in the consumers' hands at once (each slot has one consumer, so phases stay
 // unambiguous). NG = K / 256 column groups per lane (0: generic).
 constexpr int GU_SLOT = MD_STAGES * MD_STAGE / MD_WARPS;
-template <int NG>
+template <int NG, bool COMP>
 __global__ void __launch_bounds__(MD_THREADS, 1)
 moe_gu_t1_kernel(const float* __restrict__ x, const int* __restrict__ ids, const int* __restrict__ slot_of_expert,
                  const unsigned char* __restrict__ base, long long expert_stride, long long mat_off, int N, int K,
-                 float* __restrict__ h, int C, int R, int chunk) {
+                 float* __restrict__ h, int C, int R, int chunk, int rowb) {
   constexpr int G = NG > 0 ? NG : MD_MAXG;
   extern __shared__ __align__(128) uint8_t smem[];
   const int j = blockIdx.x / C, c = blockIdx.x - j * C;
   const int r0 = c * R;
   if (r0 >= N) return;
   const int nrows = min(N, r0 + R) - r0;
-  const int rowb = K * 2;
   const int RS = GU_SLOT / rowb;
   const int nst = (nrows + RS - 1) / RS;
   uint8_t* ring = smem;
@@ -132,7 +154,7 @@ moe_gu_t1_kernel(const float* __restrict__ x, const int* __restrict__ ids, const
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int col = (g * 32 + lane) * 8;
-          if (NG > 0 || col < K) a2 = md_dot8(*reinterpret_cast<const uint4*>(row + col * 2), xr[g], a2);
+          if (NG > 0 || col < K) a2 = md_dot8(md_load8<COMP>(row, col, K), xr[g], a2);
         }
         v[q] = a2.x + a2.y;
       }
@@ -159,18 +181,17 @@ moe_gu_t1_kernel(const float* __restrict__ x, const int* __restrict__ ids, const
 // Consumer warp w owns experts w, w + 8, ...: it holds h[j] in registers and
 // takes that expert's rows MD_BATCH at a time (independent dot products,
 // interleaved warp reductions). NG = K / 256 column groups per lane (0: generic).
-template <int NG>
+template <int NG, bool COMP>
 __global__ void __launch_bounds__(MD_THREADS, 1)
 moe_down_t1_kernel(const float* __restrict__ h, const int* __restrict__ ids, const int* __restrict__ slot_of_expert,
                    const unsigned char* __restrict__ base, long long expert_stride, long long mat_off, int N,
                    int K, int R, const float* __restrict__ w, int k, float* __restrict__ y, int chunk,
-                   int slot_bytes) {
+                   int slot_bytes, int rowb) {
   constexpr int G = NG > 0 ? NG : MD_MAXG;
   extern __shared__ __align__(128) uint8_t smem[];
   const int r0 = blockIdx.x * R;
   if (r0 >= N) return;
   const int nrows = min(N, r0 + R) - r0;
-  const int rowb = K * 2;
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + MD_STAGES * MD_STAGE);   // k <= MD_MAXRING
   float* acc = reinterpret_cast<float*>(full + MD_MAXRING);                    // [k][R]
@@ -227,7 +248,7 @@ moe_down_t1_kernel(const float* __restrict__ h, const int* __restrict__ ids, con
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int col = (g * 32 + lane) * 8;
-          if (NG > 0 || col < K) a2 = md_dot8(*reinterpret_cast<const uint4*>(row + col * 2), xr[g], a2);
+          if (NG > 0 || col < K) a2 = md_dot8(md_load8<COMP>(row, col, K), xr[g], a2);
         }
         v[b] = a2.x + a2.y;
       }
@@ -259,17 +280,10 @@ static size_t md_smem(int R) { return (size_t)MD_STAGES * MD_STAGE + MD_WARPS * 
 
 using namespace ps;
 
-extern "C" {
-
-int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot_of_expert, const void* expert_base,
-                          long long expert_stride, long long gu_off, long long down_off, int eff, int d, float* h,
-                          const float* w, float* y, void* stream) {
-  PS_REQUIRE(k >= 1 && k <= 64, "ps_moe_decode_experts: k=%d", k);
-  PS_REQUIRE(d % 8 == 0 && eff % 8 == 0 && d <= 32 * 8 * MD_MAXG && eff <= 32 * 8 * MD_MAXG,
-             "ps_moe_decode_experts: d=%d eff=%d (multiples of 8, <= %d)", d, eff, 32 * 8 * MD_MAXG);
-  PS_REQUIRE((expert_stride | gu_off | down_off) % 16 == 0 &&
-                 (reinterpret_cast<uintptr_t>(expert_base) & 15) == 0,
-             "ps_moe_decode_experts: expert bytes must be 16-byte aligned");
+template <bool COMP>
+static int md_launch(const float* x, const int* ids, int k, const int* slot_of_expert, const void* expert_base,
+                     long long expert_stride, long long gu_off, long long down_off, int eff, int d, float* h,
+                     const float* w, float* y, cudaStream_t s, int gu_rowb, int down_rowb) {
   if (!g_md_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -282,52 +296,52 @@ int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot
     g_md_chunk = g_md_chunk < 1024 ? 1024 : (g_md_chunk & ~15);
   }
   auto base = static_cast<const unsigned char*>(expert_base);
-  cudaStream_t s = (cudaStream_t)stream;
   // gate/up: k groups x C CTAs; N = 2 * eff interleaved rows, even rows per CTA so
   // gate/up pairs never straddle CTAs
   const int C = g_md_sms / k > 0 ? g_md_sms / k : 1;
   const int Rg = 2 * ((eff + C - 1) / C);
   const size_t sg = md_smem(Rg);
   using GuKernel = void (*)(const float*, const int*, const int*, const unsigned char*, long long, long long, int, int,
-                           float*, int, int, int);
+                           float*, int, int, int, int);
   const int ngu = d % 256 ? 0 : d / 256;
-  GuKernel gk = moe_gu_t1_kernel<0>;
+  GuKernel gk = moe_gu_t1_kernel<0, COMP>;
   switch (ngu) {
-    case 1: gk = moe_gu_t1_kernel<1>; break;
-    case 2: gk = moe_gu_t1_kernel<2>; break;
-    case 4: gk = moe_gu_t1_kernel<4>; break;
-    case 8: gk = moe_gu_t1_kernel<8>; break;
-    default: gk = moe_gu_t1_kernel<0>; break;
+    case 1: gk = moe_gu_t1_kernel<1, COMP>; break;
+    case 2: gk = moe_gu_t1_kernel<2, COMP>; break;
+    case 4: gk = moe_gu_t1_kernel<4, COMP>; break;
+    case 8: gk = moe_gu_t1_kernel<8, COMP>; break;
+    default: gk = moe_gu_t1_kernel<0, COMP>; break;
   }
   static size_t set_gu[MD_MAXG + 1] = {};
   if (sg > set_gu[ngu]) {
     PS_CHECK_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sg));
     set_gu[ngu] = sg;
   }
+  PS_REQUIRE(GU_SLOT / gu_rowb >= 1, "ps_moe_decode_experts: gate/up rows of %d bytes exceed a ring slot", gu_rowb);
   gk<<<k * C, MD_THREADS, sg, s>>>(x, ids, slot_of_expert, base, expert_stride, gu_off, 2 * eff, d, h, C, Rg,
-                                   g_md_chunk);
+                                   g_md_chunk, gu_rowb);
   PS_CHECK_LAUNCH();
   // down + combine: row blocks of R rows, one ring slot per expert, all in flight
   int Rd = (d + g_md_sms - 1) / g_md_sms;
-  int slot_bytes = (Rd * eff * 2 + 127) / 128 * 128;
+  int slot_bytes = (Rd * down_rowb + 127) / 128 * 128;
   if (slot_bytes * k > MD_STAGES * MD_STAGE) {
-    Rd = (MD_STAGES * MD_STAGE / k) / (eff * 2);
-    slot_bytes = (Rd * eff * 2 + 127) / 128 * 128;
+    Rd = (MD_STAGES * MD_STAGE / k) / down_rowb;
+    slot_bytes = (Rd * down_rowb + 127) / 128 * 128;
   }
   PS_REQUIRE(k <= MD_MAXRING && Rd >= 1, "ps_moe_decode_experts: k=%d eff=%d do not fit the ring", k, eff);
   const size_t sd = (size_t)MD_STAGES * MD_STAGE + MD_MAXRING * 8 + (size_t)k * Rd * 4;
   PS_REQUIRE(sd <= 232448 - 1024, "ps_moe_decode_experts: k=%d eff=%d exceed shared memory", k, eff);
   using DownKernel = void (*)(const float*, const int*, const int*, const unsigned char*, long long, long long, int,
-                             int, int, const float*, int, float*, int, int);
+                             int, int, const float*, int, float*, int, int, int);
   const int ng = eff % 256 ? 0 : eff / 256;
-  DownKernel kern = moe_down_t1_kernel<0>;
+  DownKernel kern = moe_down_t1_kernel<0, COMP>;
   switch (ng) {
-    case 1: kern = moe_down_t1_kernel<1>; break;
-    case 2: kern = moe_down_t1_kernel<2>; break;
-    case 3: kern = moe_down_t1_kernel<3>; break;
-    case 4: kern = moe_down_t1_kernel<4>; break;
-    case 6: kern = moe_down_t1_kernel<6>; break;
-    case 8: kern = moe_down_t1_kernel<8>; break;
+    case 1: kern = moe_down_t1_kernel<1, COMP>; break;
+    case 2: kern = moe_down_t1_kernel<2, COMP>; break;
+    case 3: kern = moe_down_t1_kernel<3, COMP>; break;
+    case 4: kern = moe_down_t1_kernel<4, COMP>; break;
+    case 6: kern = moe_down_t1_kernel<6, COMP>; break;
+    case 8: kern = moe_down_t1_kernel<8, COMP>; break;
     default: break;
   }
   static size_t set_down[MD_MAXG + 1] = {};
@@ -336,26 +350,60 @@ int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot
     set_down[ng] = sd;
   }
   kern<<<(d + Rd - 1) / Rd, MD_THREADS, sd, s>>>(h, ids, slot_of_expert, base, expert_stride, down_off, d, eff, Rd, w,
-                                                 k, y, g_md_chunk, slot_bytes);
+                                                 k, y, g_md_chunk, slot_bytes, down_rowb);
   PS_CHECK_LAUNCH();
   return PS_OK;
+}
+
+static int md_check(int k, int eff, int d, long long expert_stride, long long gu_off, long long down_off,
+                    const void* expert_base) {
+  PS_REQUIRE(k >= 1 && k <= 64, "ps_moe_decode_experts: k=%d", k);
+  PS_REQUIRE(d % 8 == 0 && eff % 8 == 0 && d <= 32 * 8 * MD_MAXG && eff <= 32 * 8 * MD_MAXG,
+             "ps_moe_decode_experts: d=%d eff=%d (multiples of 8, <= %d)", d, eff, 32 * 8 * MD_MAXG);
+  PS_REQUIRE((expert_stride | gu_off | down_off) % 16 == 0 &&
+                 (reinterpret_cast<uintptr_t>(expert_base) & 15) == 0,
+             "ps_moe_decode_experts: expert bytes must be 16-byte aligned");
+  return PS_OK;
+}
+
+extern "C" {
+
+int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot_of_expert, const void* expert_base,
+                          long long expert_stride, long long gu_off, long long down_off, int eff, int d, float* h,
+                          const float* w, float* y, void* stream) {
+  int rc = md_check(k, eff, d, expert_stride, gu_off, down_off, expert_base);
+  if (rc) return rc;
+  return md_launch<false>(x, ids, k, slot_of_expert, expert_base, expert_stride, gu_off, down_off, eff, d, h, w, y,
+                          (cudaStream_t)stream, d * 2, eff * 2);
+}
+
+int ps_moe_decode_experts_c(const float* x, const int* ids, int k, const int* slot_of_expert,
+                            const void* expert_base, long long expert_stride, long long gu_off, long long down_off,
+                            int eff, int d, int gu_row_bytes, int down_row_bytes, float* h, const float* w, float* y,
+                            void* stream) {
+  int rc = md_check(k, eff, d, expert_stride, gu_off, down_off, expert_base);
+  if (rc) return rc;
+  PS_REQUIRE(d % 256 == 0 && eff % 256 == 0, "ps_moe_decode_experts_c: coded rows need d, eff multiples of 256");
+  const int tg = gu_row_bytes - d * 3 / 2, td = down_row_bytes - eff * 3 / 2;
+  PS_REQUIRE(tg >= 16 && tg <= 256 && tg % 16 == 0 && td >= 16 && td <= 256 && td % 16 == 0,
+             "ps_moe_decode_experts_c: coded row strides %d / %d (trailers %d / %d)", gu_row_bytes, down_row_bytes,
+             tg, td);
+  return md_launch<true>(x, ids, k, slot_of_expert, expert_base, expert_stride, gu_off, down_off, eff, d, h, w, y,
+                         (cudaStream_t)stream, gu_row_bytes, down_row_bytes);
 }
 
 }  // extern "C"
 
 int ps_preload_moe_decode() {
   int n = 0;
-  touch_kernel(moe_gu_t1_kernel<0>, n);
-  touch_kernel(moe_gu_t1_kernel<1>, n);
-  touch_kernel(moe_gu_t1_kernel<2>, n);
-  touch_kernel(moe_gu_t1_kernel<4>, n);
-  touch_kernel(moe_gu_t1_kernel<8>, n);
-  touch_kernel(moe_down_t1_kernel<0>, n);
-  touch_kernel(moe_down_t1_kernel<1>, n);
-  touch_kernel(moe_down_t1_kernel<2>, n);
-  touch_kernel(moe_down_t1_kernel<3>, n);
-  touch_kernel(moe_down_t1_kernel<4>, n);
-  touch_kernel(moe_down_t1_kernel<6>, n);
-  touch_kernel(moe_down_t1_kernel<8>, n);
+#define PS_MDP(C)                                                                      \
+  touch_kernel(moe_gu_t1_kernel<0, C>, n); touch_kernel(moe_gu_t1_kernel<1, C>, n);     \
+  touch_kernel(moe_gu_t1_kernel<2, C>, n); touch_kernel(moe_gu_t1_kernel<4, C>, n);     \
+  touch_kernel(moe_gu_t1_kernel<8, C>, n); touch_kernel(moe_down_t1_kernel<0, C>, n);   \
+  touch_kernel(moe_down_t1_kernel<1, C>, n); touch_kernel(moe_down_t1_kernel<2, C>, n); \
+  touch_kernel(moe_down_t1_kernel<3, C>, n); touch_kernel(moe_down_t1_kernel<4, C>, n); \
+  touch_kernel(moe_down_t1_kernel<6, C>, n); touch_kernel(moe_down_t1_kernel<8, C>, n);
+  PS_MDP(false) PS_MDP(true)
+#undef PS_MDP
   return n;
 }

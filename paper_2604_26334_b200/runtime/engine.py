@@ -170,8 +170,8 @@ class Engine:
         others map it), and the go / no-go rule uses only node totals, so every replica
         of a job decides the same. Anything else keeps bf16 streaming."""
         from .wcomp import CodedShards
-        dense = sum(b.nbytes for b in self.weights.layout.blobs.values()
-                    if b.kind in (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD))
+        kinds = (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD, ShardKind.MOE_EXPERT_GROUP)
+        dense = sum(b.nbytes for b in self.weights.layout.blobs.values() if b.kind in kinds)
         need = dense * 3 // 4
         shared = None
         meminfo = _meminfo()
@@ -186,8 +186,7 @@ class Engine:
             return
         t0 = time.perf_counter()
         try:
-            self.weights.coded = CodedShards(self.weights, (ShardKind.ATTENTION, ShardKind.FFN,
-                                                            ShardKind.OUTPUT_HEAD), shared=shared)
+            self.weights.coded = CodedShards(self.weights, kinds, shared=shared)
         except Exception as exc:   # e.g. pinned host memory exhausted: stream bf16
             import warnings
             warnings.warn(f"exponent-coded weights unavailable ({exc}); streaming bf16")
@@ -200,8 +199,7 @@ class Engine:
     def _ensure_executor(self, max_tokens: int) -> Executor:
         if self.executor is None:
             tiers_used = self.plans
-            if (os.environ.get("PS_CODED", "1") == "1" and self.spec.moe is None and
-                    getattr(self.weights, "coded", None) is None):
+            if (os.environ.get("PS_CODED", "1") == "1" and getattr(self.weights, "coded", None) is None):
                 self._build_coded()
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,

@@ -44,7 +44,8 @@ from .arena import VramArena
 from .model import Arch, HostWeights, rope_table
 from .streamer import CopyRing, EventPool
 
-GEMV_MAX_T = 32
+GEMV_MAX_T = 32            # passes of <= 32 tokens keep fp32 activations (GEMV kernels)
+GEMV_CORE_MAX_T = 8        # <= 8 tokens: CUDA-core bulk-copy GEMV; 9..32: tcgen05 one-pass GEMV
 KV_PAGE_ROWS = 64          # positions per KV page (a 64-row TMA box never straddles pages)
 
 
@@ -243,6 +244,8 @@ class Executor:
         if T > GEMV_MAX_T:
             spec += [("xn16", "xn16", T * d * 2), ("att16", "att16", T * self.h * self.hd * 2),
                      ("hid16", "hid16", T * self.ffn * 2)]
+        if T > GEMV_CORE_MAX_T:   # x planes + split-K partials of ps_gemv_tc
+            spec.append(("tcws", "gemv_tc_ws", self._tc_workspace_bytes()))
         spec += [("xs", "xs", B * d * 4), ("logits", "logits", B * self.V * 4)]
         # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
         ws = L.attn_decode_workspace(B, self.h, self.hd, self.cap)
@@ -258,10 +261,27 @@ class Executor:
                      ("m_slotmap", "moe_slot_of_expert", E * 4)]
         return spec
 
+    def _tc_workspace_bytes(self) -> int:
+        """Largest ps_gemv_tc workspace over the (N, K) of every matmul a pass can issue
+        (whole tensors and the row pieces of streamed ones)."""
+        if getattr(self, "_tcws_bytes", None) is None:
+            s = self.spec
+            ks = {self.d, self.h * self.hd, s.ffn_dim if s.moe is None else self.d}
+            ns = {self.qkv_rows, self.d, 2 * s.ffn_dim, self.V} | ({s.moe.n_experts} if s.moe else set())
+            ns |= set(range(128, 40064, 128))     # row pieces: split-K partials peak below 2 x SMs tiles
+            best = 0
+            for K in ks:
+                for N in ns:
+                    n = C.c_longlong()
+                    L.call("ps_gemv_tc_workspace", N, K, C.byref(n))
+                    best = max(best, n.value)
+            self._tcws_bytes = best
+        return self._tcws_bytes
+
     def _carve_activations(self, T: int) -> None:
         """Activation buffers for passes of <= T tokens (re-carved per tier, so a
         decode tier holds only what the plan's activation scratch allows)."""
-        self.xn16 = self.att16 = self.hid16 = 0
+        self.xn16 = self.att16 = self.hid16 = self.tcws = 0
         for attr, tag, n in self._activation_spec(T):
             setattr(self, attr, self.arena.alloc_high(tag, n))
         self.ws_floats = L.attn_decode_workspace(self.B, self.h, self.hd, self.cap)
@@ -484,7 +504,7 @@ class Executor:
         free = self.arena.free_bytes
         ring_bytes = max(0, min(self.ring_cap, free)) // 256 * 256
         self.chunk = min(self.chunk_cap, max(1 << 16, ring_bytes // 6 // 256 * 256))
-        staged = ("stream", "zerocopy") if tier > GEMV_MAX_T else ("stream",)
+        staged = ("stream", "zerocopy") if self.T_tier > GEMV_CORE_MAX_T else ("stream",)
         streams = any(m in staged for m, _ in self.residency.values()) or \
             any(m in staged for m in self.kv_mode.values())
         need = self.kv_layer_bytes + 3 * self.chunk
@@ -666,7 +686,9 @@ class Executor:
         right before its first consumer and released (sealed) after the last
         consumer that reads any tensor in it."""
         mode, dev = self.residency[sid]
-        if mode == "zerocopy" and T > GEMV_MAX_T:
+        if mode == "zerocopy" and T > GEMV_CORE_MAX_T:
+            # one pass over the weights: stage CPU-placed shards through the ring (copy
+            # engine, once) instead of re-reading host memory per 8 tokens or per tile
             mode = "stream"
         blob = self.w.layout.blobs[sid]
         own = {c.tensor: i for i, c in enumerate(consumers) if c.tensor is not None}
@@ -827,7 +849,16 @@ class Executor:
             if not t1:
                 L.call("ps_moe_plan", self.m_ids, P, E, self.m_plan, self.cs)
 
+        # routed experts exponent-coded through the fetcher (one-token kernels only)
+        cexp = None
+        if (t1 and fetched and self.coded is not None and os.environ.get("PS_CODED_EXPERTS", "1") != "0"):
+            cexp = getattr(self.coded, "experts", {}).get(sid)
+
         def decode_t1(ebase, slot_map):
+            if cexp is not None:
+                L.call("ps_moe_decode_experts_c", xn, self.m_ids, k, slot_map, ebase, sb, 0, cexp[2], eff, d,
+                       cexp[4], cexp[5], self.m_h, self.m_w, self.x, self.cs)
+                return
             L.call("ps_moe_decode_experts", xn, self.m_ids, k, slot_map, ebase, stride if not slot_map else sb,
                    0, down_off, eff, d, self.m_h, self.m_w, self.x, self.cs)
 
@@ -842,6 +873,9 @@ class Executor:
             host = self.w.shard_ptr(sid)
             _, _, _, ebytes = self._expert_geometry(sid, layer)
             slots, sb = self.expert_slots, self.expert_slot_bytes
+            src0, src_stride = host + e0.offset, stride
+            if cexp is not None:      # coded experts: 25 % fewer bytes per routed expert
+                src0, src_stride, ebytes = self.coded.shard_ptr(sid) + cexp[0], cexp[1], cexp[3]
             self.fetch_seq = (self.fetch_seq + 1) & 0xFFFFFFFF or 1
             seq = self.fetch_seq
             pre = self._prefix_dev.pop(sid, None)     # ffn_norm + router staged by gap filling
@@ -856,11 +890,11 @@ class Executor:
                 self.ring.seal(region, [self._record(self.cs)])
 
             def fetch(_p, _a, _b):
-                L.call("ps_fetcher_submit", self.fetcher, seq, host + e0.offset, stride, ebytes, slots, sb)
+                L.call("ps_fetcher_submit", self.fetcher, seq, src0, src_stride, ebytes, slots, sb)
                 L.call("ps_moe_publish", self.fetcher, self.m_ids, P, E, self.m_slotmap, seq, self.cs)
                 L.call("ps_wait_flag", self.fetcher, seq, self.cs)
                 if os.environ.get("PS_FETCH_DEBUG"):
-                    self._fetch_debug(layer, seq, P, E, host + e0.offset, stride, ebytes, slots, sb)
+                    self._fetch_debug(layer, seq, P, E, src0, src_stride, ebytes, slots, sb)
 
             def run(_p, _a, _b):
                 if t1:
@@ -1001,14 +1035,16 @@ class Executor:
     def _matmul(self, T, act, W, N, K, out, ldo, epi) -> None:
         """out (epi)= act @ W[:N]^T for T tokens: GEMV on fp32 act (T <= 32)
         or the tcgen05 GEMM on bf16 act."""
-        if self._coded_call is not None:
-            for t0 in range(0, T, 8):
-                L.call("ps_gemv_bf16c", act + t0 * K * 4, K, min(8, T - t0), W, N, K, self._coded_call,
-                       out + t0 * ldo * 4, ldo, epi, self.cs)
-        elif T <= GEMV_MAX_T:
-            L.call("ps_gemv_bf16", act, K, T, W, N, K, K, out, ldo, epi, self.cs)
-        else:
+        coded = self._coded_call
+        if T > GEMV_MAX_T:
             L.call("ps_gemm_bf16", act, T, K, K, W, N, K, out, ldo, epi, self.cs)
+        elif T > GEMV_CORE_MAX_T:      # one pass over W for the whole batch (tcgen05)
+            L.call("ps_gemv_tc", act, K, T, W, N, K, coded if coded is not None else K,
+                   1 if coded is not None else 0, out, ldo, epi, self.tcws, self._tcws_bytes, self.cs)
+        elif coded is not None:
+            L.call("ps_gemv_bf16c", act, K, T, W, N, K, coded, out, ldo, epi, self.cs)
+        else:
+            L.call("ps_gemv_bf16", act, K, T, W, N, K, K, out, ldo, epi, self.cs)
 
     def _upload(self, dst: int, arr: np.ndarray) -> None:
         arr = np.ascontiguousarray(arr, dtype=np.int32)
@@ -1200,11 +1236,7 @@ class Executor:
                 L.call("ps_rmsnorm", self.x, d, self.i_rows, R, p, d, eps, self.xs, d, 0, self.cs)
 
             def lm(p, r0, r1):
-                if self._coded_call is not None:
-                    self._matmul(R, self.xs, p, r1 - r0, d, self.logits + r0 * 4, self.V, L.PS_EPI_STORE)
-                    return
-                L.call("ps_gemv_bf16", self.xs, d, R, p, r1 - r0, d, d, self.logits + r0 * 4,
-                       self.V, L.PS_EPI_STORE, self.cs)
+                self._matmul(R, self.xs, p, r1 - r0, d, self.logits + r0 * 4, self.V, L.PS_EPI_STORE)
 
             self.tok_slot = (self.tok_slot + 1) % 8
             self.i_tok = self.i_tok_ring + self.tok_slot * self.B * 4

@@ -40,9 +40,11 @@ def row_bytes(k: int, trailer: int) -> int:
     return k * 3 // 2 + trailer
 
 
-def encode(bits: np.ndarray, out: np.ndarray | None = None, max_escapes: int = MAX_ESCAPES):
+def encode(bits: np.ndarray, out: np.ndarray | None = None, max_escapes: int = MAX_ESCAPES,
+           trailer: int | None = None):
     """bf16 bit patterns (uint16 [N, K], K % 32 == 0) -> (coded uint8 [N, row_bytes],
-    trailer bytes), or None when a row needs more than `max_escapes` escapes. `out`:
+    trailer bytes), or None when a row needs more than `max_escapes` escapes (or more
+    than a forced `trailer` holds: experts of one MoE group share one row size). `out`:
     optional destination (uint8, at least N * row_bytes) written in place."""
     bits = np.ascontiguousarray(bits, dtype=np.uint16)
     n, k = bits.shape
@@ -59,6 +61,10 @@ def encode(bits: np.ndarray, out: np.ndarray | None = None, max_escapes: int = M
     if top > max_escapes:
         return None
     tb = trailer_bytes(top)
+    if trailer is not None:
+        if trailer < tb:
+            return None
+        tb = trailer
     rb = row_bytes(k, tb)
     coded = (np.empty((n, rb), np.uint8) if out is None else out[:n * rb].reshape(n, rb))
     np.bitwise_or(hi & 0x80, lo & 0x7F, out=coded[:, :k])
@@ -129,8 +135,13 @@ class CodedShards:
         self.host = 0
         self.seg = None
         up = lambda n: (n + 255) // 256 * 256  # noqa: E731
+        from ..planning.graph import ShardKind
+        moe_kind = ShardKind.MOE_EXPERT_GROUP
+        # dense shards: every matrix; MoE expert groups: the expert matrices only (the
+        # router and norm are read from the bf16 blob by the routing step)
         mats = [(sid, name) for sid, blob in layout.blobs.items() if blob.kind in kinds
-                for name, t in blob.tensors.items() if t.rows > 1 and t.cols % 256 == 0]
+                for name, t in blob.tensors.items() if t.rows > 1 and t.cols % 256 == 0 and
+                (blob.kind is not moe_kind or ".e" in name)]
 
         def plan(job):   # the trailer each matrix needs (a counting pass, no output)
             sid, name = job
@@ -138,6 +149,18 @@ class CodedShards:
 
         with ThreadPoolExecutor(max_workers=threads) as pool:
             trailers = dict(pool.map(plan, mats))
+        # one row size per expert matrix kind within a group (uniform expert stride, so
+        # the fetcher copies expert e from e * stride): the group's largest trailer
+        self.experts = {}
+        for sid, blob in layout.blobs.items():
+            if blob.kind is not moe_kind or blob.kind not in kinds:
+                continue
+            for suffix in ("wgu", "wdown"):
+                names = [n for n in blob.tensors if n.endswith("." + suffix) and ".e" in n]
+                tbs = [trailers[(sid, n)] for n in names]
+                top = None if any(tb is None for tb in tbs) else max(tbs)
+                for n in names:
+                    trailers[(sid, n)] = top
         self.tensors, self.shard_off, self.shard_bytes = {}, {}, {}
         off = 0
         for sid, blob in layout.blobs.items():
@@ -156,6 +179,8 @@ class CodedShards:
             self.tensors[sid] = meta
             self.shard_bytes[sid] = t_off
             off += t_off
+            if blob.kind is moe_kind:
+                self._expert_geometry(sid, blob, meta)
         self.nbytes = max(1, off)
         self.n_uncoded = sum(1 for job in mats if trailers[job] is None)
         if shared is not None:
@@ -181,7 +206,7 @@ class CodedShards:
                 o, rb, is_coded = self.tensors[sid][name]
                 src = weights.host_view(sid, name)
                 if is_coded:
-                    res = encode(src, out=buf[o + self.shard_off[sid]:])
+                    res = encode(src, out=buf[o + self.shard_off[sid]:], trailer=rb - t.cols * 3 // 2)
                     assert res is not None and res[1] == rb - t.cols * 3 // 2
                 else:
                     start = self.shard_off[sid] + o
@@ -196,6 +221,23 @@ class CodedShards:
         if self.seg is not None:
             self.seg.mark_ready()
         self.coded_bytes = sum(self.shard_bytes.values())
+
+    def _expert_geometry(self, sid, blob, meta) -> None:
+        """experts[sid] = (offset of expert 0 in the coded shard, expert stride, offset of
+        wdown in an expert, bytes of one expert, gate/up row bytes, down row bytes), when
+        every expert matrix of the group is coded."""
+        layer = blob.layer
+        names = [f"L{layer}.e{e}.{m}" for e in range(2) for m in ("wgu", "wdown")]
+        if not all(n in meta and meta[n][2] for n in names if n in blob.tensors):
+            return
+        e0, d0 = meta[f"L{layer}.e0.wgu"][0], meta[f"L{layer}.e0.wdown"][0]
+        stride = (meta[f"L{layer}.e1.wgu"][0] - e0) if f"L{layer}.e1.wgu" in meta else None
+        if stride is None or any(not meta[n][2] for n in meta if ".e" in n):
+            return
+        wd = blob.tensors[f"L{layer}.e0.wdown"]
+        ebytes = d0 - e0 + wd.rows * meta[f"L{layer}.e0.wdown"][1]
+        self.experts[sid] = (e0, stride, d0 - e0, ebytes, meta[f"L{layer}.e0.wgu"][1],
+                             meta[f"L{layer}.e0.wdown"][1])
 
     def shard_ptr(self, sid: int) -> int:
         return self.host + self.shard_off[sid]

@@ -7,6 +7,7 @@ mma.sync flash attention) are bounded by bf16 input rounding (2^-8).
 Integer work (argmax, weight init) must be bit-exact.
 """
 
+import ctypes as C
 import math
 
 import numpy as np
@@ -520,5 +521,104 @@ def test_gemv_coded_bit_identical(N, K, t, epi):
     s = stream()
     lib.call("ps_gemv_bf16_cfg", x.data_ptr(), K, t, W.data_ptr(), N, K, K, ya.data_ptr(), rows, epi, s, -1, 0, 0)
     lib.call("ps_gemv_bf16c", x.data_ptr(), K, t, Wc.data_ptr(), N, K, coded.shape[1], yb.data_ptr(), rows, epi, s)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)
+
+
+@pytest.mark.parametrize("N,K,t,epi", [(6144, 4096, 32, 0), (4096, 14336, 32, 1), (28672, 4096, 16, 2),
+                                       (1000, 2048, 9, 0), (300, 512, 32, 1), (128256, 4096, 32, 0),
+                                       (4096, 768, 24, 2)])
+def test_gemv_tc_one_pass_fp32_faithful(N, K, t, epi):
+    """Decode batches of 9..32 tokens on tcgen05 (ps_gemv_tc): W read once, x split into
+    three bf16 planes -> fp32-faithful (within 2e-6 of an fp64 reference, like the fp32
+    CUDA-core GEMV); the exponent-coded variant is bit-identical to the bf16 one, escapes
+    and per-row bases included; split-K shapes (N / 128 < SMs) and partial row tiles."""
+    from paper_2604_26334_b200.runtime import wcomp
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(N + K + t)
+    W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.03
+    W[0, :7] = 0.0
+    W[3] *= 2.0 ** 20
+    W[N - 1, K - 1] = -1e-38
+    x = torch.randn(t, K, device="cuda", generator=g)
+    rows = N // 2 if epi == 2 else N
+    y0 = torch.randn(t, rows, device="cuda", generator=g)
+    ws_n = C.c_longlong()
+    lib.call("ps_gemv_tc_workspace", N, K, C.byref(ws_n))
+    ws = torch.empty(ws_n.value, dtype=torch.uint8, device="cuda")
+    ya, yb, yc = y0.clone(), y0.clone(), y0.clone()
+    s = stream()
+    lib.call("ps_gemv_tc", x.data_ptr(), K, t, W.data_ptr(), N, K, K, 0, ya.data_ptr(), rows, epi,
+             ws.data_ptr(), ws.numel(), s)
+    bits = W.view(torch.int16).cpu().numpy().view(np.uint16)
+    coded, tb = wcomp.encode(bits)
+    Wc = torch.from_numpy(coded).cuda()
+    lib.call("ps_gemv_tc", x.data_ptr(), K, t, Wc.data_ptr(), N, K, coded.shape[1], 1, yb.data_ptr(), rows, epi,
+             ws.data_ptr(), ws.numel(), s)
+    lib.call("ps_gemv_bf16", x.data_ptr(), K, t, W.data_ptr(), N, K, K, yc.data_ptr(), rows, epi, s)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)                      # coded == bf16, bit for bit
+    full = x.double() @ W.double().T                # [t, N]
+    if epi == 2:
+        ref = torch.nn.functional.silu(full[:, 0::2]) * full[:, 1::2]
+    elif epi == 1:
+        ref = y0.double() + full
+    else:
+        ref = full
+    scale = ref.abs().max()
+    assert float((ya.double() - ref).abs().max() / scale) < 2e-6
+    assert float((yc.double() - ref).abs().max() / scale) < 2e-6
+
+
+@pytest.mark.parametrize("E,k,d,eff", [(32, 8, 2048, 768), (16, 4, 512, 256)])
+def test_moe_decode_experts_coded_bit_identical(E, k, d, eff):
+    """ps_moe_decode_experts_c on exponent-coded experts (every expert of the group one
+    row size: the group's largest trailer) equals ps_moe_decode_experts on the bf16
+    experts bit for bit, escapes included, through a fetcher-style slot map."""
+    from paper_2604_26334_b200.runtime import wcomp
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(E * 7 + d)
+    x = torch.randn(1, d, device="cuda", generator=g)
+    Wgu = (torch.randn(E, 2 * eff, d, device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16)
+    Wd = (torch.randn(E, d, eff, device="cuda", generator=g) / eff ** 0.5).to(torch.bfloat16)
+    Wgu[1, 3, :5] = 0.0
+    Wd[2, 7] *= 2.0 ** 24
+    bits_gu = [Wgu[e].view(torch.int16).cpu().numpy().view(np.uint16) for e in range(E)]
+    bits_d = [Wd[e].view(torch.int16).cpu().numpy().view(np.uint16) for e in range(E)]
+    tg = max(wcomp._trailer_or_none(b) for b in bits_gu)
+    td = max(wcomp._trailer_or_none(b) for b in bits_d)
+    up = lambda n: (n + 255) // 256 * 256  # noqa: E731
+    gu_rb, d_rb = wcomp.row_bytes(d, tg), wcomp.row_bytes(eff, td)
+    down_off = up(2 * eff * gu_rb)
+    cstride = up(down_off + d * d_rb)
+    cblob = np.zeros(E * cstride, np.uint8)
+    for e in range(E):
+        wcomp.encode(bits_gu[e], out=cblob[e * cstride:], trailer=tg)
+        wcomp.encode(bits_d[e], out=cblob[e * cstride + down_off:], trailer=td)
+    blob = torch.cat([torch.cat([Wgu[e].reshape(-1), Wd[e].reshape(-1)]) for e in range(E)]).contiguous()
+    stride = (2 * eff * d + d * eff) * 2
+    ids = torch.tensor(np.random.default_rng(E).choice(E, k, replace=False).astype(np.int32), device="cuda")
+    ids[0] = 1
+    ids[1] = 2 if k > 1 else ids[1]
+    w = torch.rand(k, device="cuda", generator=g)
+    sb = up(stride)
+    slots = torch.zeros(k * sb, dtype=torch.uint8, device="cuda")
+    cslots = torch.zeros(k * sb, dtype=torch.uint8, device="cuda")
+    smap = torch.full((E,), -1, dtype=torch.int32, device="cuda")
+    cb = torch.from_numpy(cblob).cuda()
+    bb = blob.view(torch.uint8)
+    for j, e in enumerate(ids.tolist()):
+        sl = k - 1 - j
+        slots[sl * sb:sl * sb + stride] = bb[e * stride:(e + 1) * stride]
+        cslots[sl * sb:sl * sb + cstride] = cb[e * cstride:(e + 1) * cstride]
+        smap[e] = sl
+    h = torch.zeros(k, eff, device="cuda")
+    y0 = torch.randn(1, d, device="cuda", generator=g)
+    ya, yb = y0.clone(), y0.clone()
+    s = stream()
+    lib.call("ps_moe_decode_experts", x.data_ptr(), ids.data_ptr(), k, smap.data_ptr(), slots.data_ptr(), sb, 0,
+             2 * eff * d * 2, eff, d, h.data_ptr(), w.data_ptr(), ya.data_ptr(), s)
+    lib.call("ps_moe_decode_experts_c", x.data_ptr(), ids.data_ptr(), k, smap.data_ptr(), cslots.data_ptr(), sb, 0,
+             down_off, eff, d, gu_rb, d_rb, h.data_ptr(), w.data_ptr(), yb.data_ptr(), s)
     torch.cuda.synchronize()
     assert torch.equal(ya, yb)
