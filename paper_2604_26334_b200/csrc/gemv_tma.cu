@@ -33,7 +33,7 @@ namespace ps {
 constexpr int GT_STAGES = 5;
 constexpr int GT_STAGE_BYTES = 32768;
 #ifndef PS_GT_CONSUMERS
-#define PS_GT_CONSUMERS 16
+#define PS_GT_CONSUMERS 8
 #endif
 constexpr int GT_CONSUMERS = PS_GT_CONSUMERS;        // consumer warps (8 or 16)
 constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp

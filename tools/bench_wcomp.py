@@ -1,5 +1,5 @@
 """Exponent-coded weights (runtime/wcomp.py): coded GEMV `ps_gemv_bf16c` vs bf16 GEMV
-`ps_gemv_bf16` on L8 shapes (random-init weights of the oracle initialiser, the head
+`ps_gemv_bf16` (t <= 8; ps_gemv_tc, the one-pass tcgen05 kernel, for t > 8) on L8 shapes (random-init weights of the oracle initialiser, the head
 with its heavy-tailed rows), t in {1, 2, 4, 8}, plus host -> device time of a 64 MB ring
 piece as bf16 vs coded. Weights rotate over copies totalling > L2 (126 MB), so every
 launch reads HBM. Prints one JSON line per case; `frac` = coded bytes / time / HBM peak."""
@@ -48,6 +48,14 @@ def case(name, tensor, N, K, ts=(1, 2, 4, 8)):
                                        y.data_ptr(), N, 0, s) for w in dc])
         tbf = timed([lambda w=w: L.call("ps_gemv_bf16", x.data_ptr(), K, t, w.data_ptr(), N, K, K, y.data_ptr(), N,
                                         0, s) for w in db])
+        if t > 8:   # one-pass tensor-core GEMV (ps_gemv_tc), coded and bf16
+            ws_n = ctypes.c_longlong()
+            L.call("ps_gemv_tc_workspace", N, K, ctypes.byref(ws_n))
+            ws = torch.empty(ws_n.value, dtype=torch.uint8, device="cuda")
+            tc = timed([lambda w=w: L.call("ps_gemv_tc", x.data_ptr(), K, t, w.data_ptr(), N, K, coded.shape[1], 1,
+                                           y.data_ptr(), N, 0, ws.data_ptr(), ws.numel(), s) for w in dc])
+            tbf = timed([lambda w=w: L.call("ps_gemv_tc", x.data_ptr(), K, t, w.data_ptr(), N, K, K, 0,
+                                            y.data_ptr(), N, 0, ws.data_ptr(), ws.numel(), s) for w in db])
         gb = coded.nbytes / tc / 1e3
         print(json.dumps({"case": name, "N": N, "K": K, "t": t, "trailer": tb, "escapes": n_esc,
                           "coded_bytes": coded.nbytes, "bf16_bytes": bits.nbytes, "coded_us": round(tc, 2),
@@ -56,9 +64,9 @@ def case(name, tensor, N, K, ts=(1, 2, 4, 8)):
     return bits, coded
 
 
-bits, coded = case("ffn piece 64MB", "L0.w_gate", 8192, 4096)
-case("wgu 235MB", "L0.w_up", 28672, 4096, ts=(1, 8))
-case("wdown", "L0.w_down", 4096, 14336, ts=(1,))
+bits, coded = case("ffn piece 64MB", "L0.w_gate", 8192, 4096, ts=(1, 2, 4, 8, 32))
+case("wgu 235MB", "L0.w_up", 28672, 4096, ts=(1, 8, 16, 32))
+case("wdown", "L0.w_down", 4096, 14336, ts=(1, 32))
 case("lm_head (heavy rows)", "lm_head", 32768, 4096, ts=(1,))
 nb, nc = bits.nbytes, coded.nbytes
 hb, hc = L.host_alloc(nb, mapped=False), L.host_alloc(nc, mapped=False)
