@@ -148,6 +148,11 @@ int ps_attn_tc_watchdog(unsigned* code, int reset);
  * reset clears them. The executor raises on any non-zero word after every pass. */
 int ps_fault_status(unsigned* words /* [4] */, int reset);
 
+/* Coded rows (format of ps_gemv_bf16c, ld_in bytes each) -> bf16 rows (ld_out elements):
+ * a GEMM pass that streams coded pieces expands each piece in VRAM for the tcgen05 GEMM. */
+int ps_expand_coded(const void* coded, long long ld_in, int rows, int K, void* out, long long ld_out,
+                    void* stream);
+
 /* Decode GEMV for 9..32 tokens on the tcgen05 tensor cores (gemv_tc.cu): y[t, n] (epi)=
  * x[t, :] . W[n, :] reading W ONCE (the CUDA-core GEMV takes 8 tokens per launch). W is
  * bf16 [N x K] (row stride ldw elements) or, with coded = 1, exponent-coded rows of ldw

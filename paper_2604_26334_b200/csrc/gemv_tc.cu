@@ -10,16 +10,18 @@
 //   D[128 rows x 32 tokens] += W_tile[128 x 64] . X_tile[32 x 64]^T   (tcgen05.mma, M=128 N=32)
 //
 // with the fp32 activations split into three bf16 planes x = x1 + x2 + x3 (8 + 8 + 8
-// mantissa bits; the products with bf16 weights are exact in fp32), three MMAs per K step
-// accumulating in one fp32 TMEM tile: the decode numerics stay fp32-faithful (the bf16
-// rounding of a GEMM prefill pass would make batched decode tokens chaotic).
+// mantissa bits; the products with bf16 weights are exact in fp32), three MMAs per K step,
+// each plane into its OWN fp32 TMEM tile (the tensor core's accumulator keeps ~fp32 bits
+// relative to its own magnitude: added into x1's sum, the 2^-16-sized x3 products would
+// be truncated away), summed x1 + (x2 + x3) in the epilogue: the decode numerics stay
+// fp32-faithful (bf16 activations would make batched decode tokens chaotic).
 //
 // CTA = 128 weight rows x one K range (split-K when N / 128 is small: partials reduced in a
 // fixed order by a second kernel, deterministic). Warp roles:
 //   warp 0       TMA producer: W tile (bf16: one 128B-swizzled box; coded: the rows' sign|
 //                mantissa bytes and codes as two plain boxes) + the three x planes
 //   warp 1       MMA issuer (one lane), 4 K steps x 3 planes per stage
-//   warp 2       TMEM allocator (32 columns)
+//   warp 2       TMEM allocator (128 columns: three 32-column plane accumulators)
 //   warps 4..11  (coded) decode the staged rows into the swizzled bf16 W tile; warps 4..7
 //                drain TMEM in the epilogue (store / residual add / SwiGLU, or partials)
 #include <cuda.h>
@@ -173,7 +175,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -219,7 +221,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
         for (int k = 0; k < TG_K / 16; ++k)
 #pragma unroll
           for (int p = 0; p < 3; ++p)
-            tg_mma(tmem, da + 2 * k, tg_desc(st + TG_A + p * (TG_B / 3)) + 2 * k, (i | k | p) != 0);
+            tg_mma(tmem + p * TG_N, da + 2 * k, tg_desc(st + TG_A + p * (TG_B / 3)) + 2 * k, (i | k) != 0);
         tg_commit(&empty[s]);
       }
       tg_commit(acc_full);
@@ -244,8 +246,13 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int q = warp - 4;
       const int row = m0 + q * 32 + lane;
-      float v[32];
-      tg_ld32(tmem + ((uint32_t)(q * 32) << 16), v);
+      float v[32], v1[32], v2[32];
+      const uint32_t lanes = (uint32_t)(q * 32) << 16;
+      tg_ld32(tmem + lanes, v);
+      tg_ld32(tmem + lanes + TG_N, v1);
+      tg_ld32(tmem + lanes + 2 * TG_N, v2);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += v1[i] + v2[i];
       if (partial == nullptr) {
         tg_epilogue<EPI>(v, row, N, t, y, ldy);
       } else if (row < N) {
@@ -259,7 +266,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
   __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
   }
 }
 

@@ -359,6 +359,42 @@ extern "C" int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int
   return launch_tmac_epi<8>(epilogue, x, ldx, t, Wc, N, K, ldw, y, ldy, s);
 }
 
+namespace ps {
+// Coded rows -> bf16 rows (GEMM passes that stream coded pieces: the tcgen05 GEMM reads
+// bf16 operands). One thread per 8 weights; rows of ld_in bytes in, K bf16 out.
+__global__ void expand_coded_kernel(const uint8_t* __restrict__ in, long long ld_in, int rows, int K,
+                                    __nv_bfloat16* __restrict__ out, long long ld_out) {
+  const long long groups = (long long)rows * (K / 8);
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(g / (K / 8)), col = (int)(g % (K / 8)) * 8;
+    const uint8_t* row = in + r * ld_in;
+    const uint32_t* trailer = reinterpret_cast<const uint32_t*>(row + (long long)K * 3 / 2);
+    const uint32_t base7 = ((trailer[0] & 0xFFu) * 0x10001u) << 7;
+    const uint2 sm = *reinterpret_cast<const uint2*>(row + col);
+    const uint32_t nb = *reinterpret_cast<const uint32_t*>(row + K + col / 2);
+    uint4 w = gt_decode8(sm, nb, base7);
+    if (gt_escapes(nb)) w = gt_patch_escapes(w, sm, nb, trailer, col);
+    *reinterpret_cast<uint4*>(out + r * ld_out + col) = w;
+  }
+}
+}  // namespace ps
+
+extern "C" int ps_expand_coded(const void* coded, long long ld_in, int rows, int K, void* out, long long ld_out,
+                               void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K % 256 == 0 && ld_out % 8 == 0 && ld_in >= (long long)K * 3 / 2 + 16,
+             "ps_expand_coded: K %d, ld_in %lld, ld_out %lld", K, ld_in, ld_out);
+  PS_REQUIRE(((uintptr_t)coded & 15) == 0 && ((uintptr_t)out & 15) == 0, "ps_expand_coded: alignment");
+  if (rows <= 0) return PS_OK;
+  const long long groups = (long long)rows * (K / 8);
+  const int blocks = (int)((groups + 255) / 256 < 148 * 16 ? (groups + 255) / 256 : 148 * 16);
+  expand_coded_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(coded), ld_in, rows, K,
+                                                                static_cast<__nv_bfloat16*>(out), ld_out);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
 int ps_preload_gemv_tma() {
   using namespace ps;
   int n = 0;
@@ -371,5 +407,6 @@ int ps_preload_gemv_tma() {
   touch_kernel(gemv_tma_kernel<T, PS_EPI_SWIGLU, true>, n);
   PS_T(1) PS_T(2) PS_T(4) PS_T(8)
 #undef PS_T
+  touch_kernel(expand_coded_kernel, n);
   return n;
 }

@@ -246,6 +246,8 @@ class Executor:
                      ("hid16", "hid16", T * self.ffn * 2)]
         if T > GEMV_CORE_MAX_T:   # x planes + split-K partials of ps_gemv_tc
             spec.append(("tcws", "gemv_tc_ws", self._tc_workspace_bytes()))
+        if T > GEMV_MAX_T and self._coded_prefill():   # one coded piece expanded to bf16 for the GEMM
+            spec.append(("expand", "coded_expand", self._expand_bytes()))
         spec += [("xs", "xs", B * d * 4), ("logits", "logits", B * self.V * 4)]
         # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
         ws = L.attn_decode_workspace(B, self.h, self.hd, self.cap)
@@ -260,6 +262,15 @@ class Executor:
                      ("m_h", "moe_h", P * eff * 4), ("m_out", "moe_out", P * d * 4),
                      ("m_slotmap", "moe_slot_of_expert", E * 4)]
         return spec
+
+    def _expand_bytes(self) -> int:
+        """The bf16 expansion buffer of coded GEMM pieces: one ring piece at most, and at
+        most 1/32 of the budget (small budgets keep their ring)."""
+        return max(1 << 20, min(self.chunk_cap, int(self.arena.capacity) // 32)) // 256 * 256
+
+    def _coded_prefill(self) -> bool:
+        """GEMM (prefill) passes stream coded pieces and expand them in VRAM (PS_CODED_PREFILL)."""
+        return getattr(self, "coded", None) is not None and os.environ.get("PS_CODED_PREFILL", "1") != "0"
 
     def _tc_workspace_bytes(self) -> int:
         """Largest ps_gemv_tc workspace over the (N, K) of every matmul a pass can issue
@@ -281,7 +292,7 @@ class Executor:
     def _carve_activations(self, T: int) -> None:
         """Activation buffers for passes of <= T tokens (re-carved per tier, so a
         decode tier holds only what the plan's activation scratch allows)."""
-        self.xn16 = self.att16 = self.hid16 = self.tcws = 0
+        self.xn16 = self.att16 = self.hid16 = self.tcws = self.expand = 0
         for attr, tag, n in self._activation_spec(T):
             setattr(self, attr, self.arena.alloc_high(tag, n))
         self.ws_floats = L.attn_decode_workspace(self.B, self.h, self.hd, self.cap)
@@ -730,12 +741,16 @@ class Executor:
             advance_to(len(consumers))
             return
 
-        coded = (self.coded is not None and T <= GEMV_MAX_T and sid in self.coded.tensors and
-                 self.striper is None and sid not in self._piece_override)
+        coded = (self.coded is not None and sid in self.coded.tensors and self.striper is None and
+                 sid not in self._piece_override and (T <= GEMV_MAX_T or bool(self.expand)))
+        expand = coded and T > GEMV_MAX_T   # GEMM pass: coded piece -> bf16 in VRAM -> tcgen05 GEMM
         evens = {c.tensor for c in consumers if c.even_rows}
         if coded:
             meta = self.coded.tensors[sid]
-            pieces = self._pieces_coded(sid, names, evens)
+            # an expanded piece (rows x K bf16) must fit the expand buffer: coded rows are
+            # >= 0.75 of their bf16 size, so 0.74 of it in coded bytes always does
+            pieces = self._pieces_coded(sid, names, evens,
+                                        chunk=int(0.74 * min(self.chunk, self._expand_bytes())) if expand else None)
             host = self.coded.shard_ptr(sid)
         else:
             pieces = self._piece_override.pop(sid, None) or self._pieces(sid, names, evens)
@@ -783,7 +798,10 @@ class Executor:
                     self.ptrs[name] = ptr
                 if name in own:
                     advance_to(own[name])
-                    if coded and m[2]:   # the consumer's GEMV reads coded rows (stride m[1] bytes)
+                    if coded and m[2] and expand:
+                        L.call("ps_expand_coded", ptr, m[1], r1 - r0, t.cols, self.expand, t.cols, self.cs)
+                        ptr = self.expand
+                    elif coded and m[2]:   # the consumer's GEMV reads coded rows (stride m[1] bytes)
                         self._coded_call = m[1]
                     try:
                         self._traced(name, consumers[ci].fn, ptr, r0, r1)
