@@ -159,7 +159,9 @@ int ps_expand_coded(const void* coded, long long ld_in, int rows, int K, void* o
  * bytes (the format of ps_gemv_bf16c). x is split into three bf16 planes (x1 + x2 + x3 =
  * x to fp32 precision) and the three products accumulate in fp32 TMEM: fp32-faithful.
  * Split-K partials are summed in a fixed order (deterministic). workspace: device bytes,
- * >= ps_gemv_tc_workspace(N, K), 256-byte aligned. t <= 32, K % 64 == 0. */
+ * 256-byte aligned, at least the x planes (3 * 32 * K * 2 bytes); ps_gemv_tc_workspace(N, K)
+ * is the size at which the split-K choice is unconstrained (smaller: fewer splits, the
+ * same results up to summation order). t <= 32, K % 64 == 0. */
 int ps_gemv_tc(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw, int coded,
                float* y, int ldy, int epilogue, void* workspace, long long workspace_bytes, void* stream);
 int ps_gemv_tc_workspace(int N, int K, long long* bytes);

@@ -344,9 +344,12 @@ static int tg_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void*
 
 static int g_tg_sms = 0;
 
+static long long tg_planes_bytes(int K) { return ((3LL * TG_N * K * 2 + 255) / 256) * 256; }
+
 // K split so that the grid covers the SMs at least twice over (split-K only when the
-// row tiles alone do not); every split a multiple of TG_K columns.
-static void tg_split(int N, int K, int* splits, int* k_per_split) {
+// row tiles alone do not), and so that the partials fit `workspace` bytes after the x
+// planes (< 0: no limit); every split a multiple of TG_K columns.
+static void tg_split(int N, int K, int* splits, int* k_per_split, long long workspace = -1) {
   if (!g_tg_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -356,7 +359,9 @@ static void tg_split(int N, int K, int* splits, int* k_per_split) {
   const int tiles = (N + TG_M - 1) / TG_M;
   const int kb = K / TG_K;
   int s = 1;
-  while (tiles * s < g_tg_sms && s < 8 && kb / (2 * s) >= 8) s *= 2;
+  while (tiles * s < g_tg_sms && s < 8 && kb / (2 * s) >= 8 &&
+         (workspace < 0 || tg_planes_bytes(K) + 2LL * s * TG_N * N * 4 <= workspace))
+    s *= 2;
   const int per = (kb + s - 1) / s;
   *splits = (kb + per - 1) / per;
   *k_per_split = per * TG_K;
@@ -365,9 +370,8 @@ static void tg_split(int N, int K, int* splits, int* k_per_split) {
 static long long tg_workspace(int N, int K) {
   int splits, kps;
   tg_split(N, K, &splits, &kps);
-  const long long planes = 3LL * TG_N * K * 2;
   const long long part = splits > 1 ? (long long)splits * TG_N * N * 4 : 0;
-  return ((planes + 255) / 256) * 256 + part;
+  return tg_planes_bytes(K) + part;
 }
 
 template <int EPI, bool COMP>
@@ -410,14 +414,15 @@ extern "C" int ps_gemv_tc(const float* x, int ldx, int t, const void* W, int N, 
   PS_REQUIRE(epilogue != PS_EPI_SWIGLU || N % 2 == 0, "ps_gemv_tc: SWIGLU needs an even N");
   PS_REQUIRE(((uintptr_t)W & 15) == 0 && ((uintptr_t)workspace & 255) == 0, "ps_gemv_tc: alignment");
   if (N <= 0) return PS_OK;
-  const long long need = tg_workspace(N, K);
-  PS_REQUIRE(workspace != nullptr && workspace_bytes >= need, "ps_gemv_tc: workspace %lld < %lld bytes",
-             workspace_bytes, need);
+  // the workspace must hold the x planes; split-K partials use what is left (fewer splits
+  // in a small workspace: same result, fewer CTAs)
+  PS_REQUIRE(workspace != nullptr && workspace_bytes >= tg_planes_bytes(K),
+             "ps_gemv_tc: workspace %lld < %lld bytes (x planes)", workspace_bytes, tg_planes_bytes(K));
   int splits, kps;
-  tg_split(N, K, &splits, &kps);
+  tg_split(N, K, &splits, &kps, workspace_bytes);
   cudaStream_t s = (cudaStream_t)stream;
   auto planes = static_cast<__nv_bfloat16*>(workspace);
-  float* partial = reinterpret_cast<float*>(static_cast<char*>(workspace) + ((3LL * TG_N * K * 2 + 255) / 256) * 256);
+  float* partial = reinterpret_cast<float*>(static_cast<char*>(workspace) + tg_planes_bytes(K));
   split_x3_kernel<<<dim3((K + 255) / 256, TG_N), 256, 0, s>>>(x, ldx, t, K, planes);
   PS_CHECK_LAUNCH();
   CUtensorMap mw, mc, mt, mx;

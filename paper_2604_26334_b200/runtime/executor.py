@@ -265,28 +265,28 @@ class Executor:
 
     def _expand_bytes(self) -> int:
         """The bf16 expansion buffer of coded GEMM pieces: one ring piece at most, and at
-        most 1/32 of the budget (small budgets keep their ring)."""
-        return max(1 << 20, min(self.chunk_cap, int(self.arena.capacity) // 32)) // 256 * 256
+        most 1/64 of the budget (small budgets keep their ring)."""
+        return max(64 << 10, min(self.chunk_cap, int(self.arena.capacity) // 64)) // 256 * 256
 
     def _coded_prefill(self) -> bool:
         """GEMM (prefill) passes stream coded pieces and expand them in VRAM (PS_CODED_PREFILL)."""
         return getattr(self, "coded", None) is not None and os.environ.get("PS_CODED_PREFILL", "1") != "0"
 
     def _tc_workspace_bytes(self) -> int:
-        """Largest ps_gemv_tc workspace over the (N, K) of every matmul a pass can issue
-        (whole tensors and the row pieces of streamed ones)."""
+        """ps_gemv_tc workspace: the x planes of the widest K, plus split-K partials up to
+        the size that leaves every shape its best split (~4.9 MB), capped at 1/128 of the
+        budget (small budgets run fewer splits; results differ only in summation order)."""
         if getattr(self, "_tcws_bytes", None) is None:
             s = self.spec
-            ks = {self.d, self.h * self.hd, s.ffn_dim if s.moe is None else self.d}
-            ns = {self.qkv_rows, self.d, 2 * s.ffn_dim, self.V} | ({s.moe.n_experts} if s.moe else set())
-            ns |= set(range(128, 40064, 128))     # row pieces: split-K partials peak below 2 x SMs tiles
-            best = 0
-            for K in ks:
-                for N in ns:
-                    n = C.c_longlong()
-                    L.call("ps_gemv_tc_workspace", N, K, C.byref(n))
-                    best = max(best, n.value)
-            self._tcws_bytes = best
+            kmax = max(self.d, self.h * self.hd, s.ffn_dim if s.moe is None else self.d)
+            planes = (3 * 32 * kmax * 2 + 255) // 256 * 256
+            ideal = C.c_longlong()
+            best = planes
+            for K in {self.d, self.h * self.hd, s.ffn_dim if s.moe is None else self.d}:
+                for N in list(range(128, 40064, 128)) + [self.qkv_rows, 2 * s.ffn_dim, self.V]:
+                    L.call("ps_gemv_tc_workspace", N, K, C.byref(ideal))
+                    best = max(best, ideal.value)
+            self._tcws_bytes = int(max(planes, min(best, int(self.arena.capacity) // 128))) // 256 * 256
         return self._tcws_bytes
 
     def _carve_activations(self, T: int) -> None:
@@ -725,7 +725,14 @@ class Executor:
 
         if mode in ("pinned", "zerocopy"):
             base = dev if mode == "pinned" else self.w.shard_ptr(sid)
-            if mode == "zerocopy":
+            zc_coded = (mode == "zerocopy" and self.coded is not None and sid in self.coded.tensors and
+                        getattr(self.coded, "mapped", False) and
+                        os.environ.get("PS_CODED_ZEROCOPY", "1") != "0")
+            if zc_coded:   # the bulk-copy GEMV reads the coded rows straight from host memory
+                base = self.coded.shard_ptr(sid)
+                meta = self.coded.tensors[sid]
+                self._stat.zero_copy_bytes += self.coded.shard_bytes[sid]
+            elif mode == "zerocopy":
                 self._stat.zero_copy_bytes += blob.nbytes
             live = []
 
@@ -733,10 +740,16 @@ class Executor:
                 pass
             for name in names:
                 t = blob.tensors[name]
-                self.ptrs[name] = base + t.offset
+                off = meta[name][0] if zc_coded else t.offset
+                self.ptrs[name] = base + off
                 if name in own:
                     advance_to(own[name])
-                    self._traced(name, consumers[ci].fn, base + t.offset, 0, t.rows)
+                    if zc_coded and meta[name][2]:
+                        self._coded_call = meta[name][1]
+                    try:
+                        self._traced(name, consumers[ci].fn, base + off, 0, t.rows)
+                    finally:
+                        self._coded_call = None
                     ci += 1
             advance_to(len(consumers))
             return

@@ -196,7 +196,9 @@ class CodedShards:
                 self.coded_bytes = sum(self.shard_bytes.values())
                 return
         else:
-            self.host = L.host_alloc(self.nbytes, mapped=False)
+            # mapped: a CPU-placed (zero-copy) shard's GEMV reads its coded rows from here
+            self.host = L.host_alloc(self.nbytes, mapped=True)
+        self.mapped = True        # both private (mapped alloc) and shared (registered mapped)
         try:
             buf = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint8 * self.nbytes).from_address(self.host))
 

@@ -44,11 +44,12 @@ def case(name, tensor, N, K, ts=(1, 2, 4, 8)):
     for t in ts:
         x = torch.randn(t, K, device="cuda")
         y = torch.zeros(t, N, device="cuda")
-        tc = timed([lambda w=w: L.call("ps_gemv_bf16c", x.data_ptr(), K, t, w.data_ptr(), N, K, coded.shape[1],
-                                       y.data_ptr(), N, 0, s) for w in dc])
-        tbf = timed([lambda w=w: L.call("ps_gemv_bf16", x.data_ptr(), K, t, w.data_ptr(), N, K, K, y.data_ptr(), N,
-                                        0, s) for w in db])
-        if t > 8:   # one-pass tensor-core GEMV (ps_gemv_tc), coded and bf16
+        if t <= 8:
+            tc = timed([lambda w=w: L.call("ps_gemv_bf16c", x.data_ptr(), K, t, w.data_ptr(), N, K, coded.shape[1],
+                                           y.data_ptr(), N, 0, s) for w in dc])
+            tbf = timed([lambda w=w: L.call("ps_gemv_bf16", x.data_ptr(), K, t, w.data_ptr(), N, K, K, y.data_ptr(),
+                                            N, 0, s) for w in db])
+        else:   # one-pass tensor-core GEMV (ps_gemv_tc), coded and bf16
             ws_n = ctypes.c_longlong()
             L.call("ps_gemv_tc_workspace", N, K, ctypes.byref(ws_n))
             ws = torch.empty(ws_n.value, dtype=torch.uint8, device="cuda")
