@@ -153,6 +153,15 @@ int ps_fault_status(unsigned* words /* [4] */, int reset);
 int ps_expand_coded(const void* coded, long long ld_in, int rows, int K, void* out, long long ld_out,
                     void* stream);
 
+/* GPU encoder of the exponent-coded rows (csrc/wencode.cu), byte-identical to
+ * runtime/wcomp.py encode: per row of a bf16 [N x K] matrix (row stride ld elements,
+ * K % 256 == 0) the window base and escape count, then the coded rows (ld_out bytes each,
+ * trailer_bytes >= 16 * ceil((1 + max count) / 4)). Replaces the numpy encoder at model
+ * load (no reference counterpart: the link format is this build's). */
+int ps_wencode_stats(const void* bits, int N, int K, long long ld, int* base_out, int* count_out, void* stream);
+int ps_wencode_rows(const void* bits, int N, int K, long long ld, const int* base, int trailer_bytes, void* out,
+                    long long ld_out, void* stream);
+
 /* Decode GEMV for 9..32 tokens on the tcgen05 tensor cores (gemv_tc.cu): y[t, n] (epi)=
  * x[t, :] . W[n, :] reading W ONCE (the CUDA-core GEMV takes 8 tokens per launch). W is
  * bf16 [N x K] (row stride ldw elements) or, with coded = 1, exponent-coded rows of ldw

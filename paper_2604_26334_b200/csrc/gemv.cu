@@ -13,7 +13,9 @@
 // cover HBM latency even for the ~50 MB ring pieces of a decode pass, and
 // sizes the grid to the resident-CTA capacity (148 SMs x 6), looping over
 // tiles (grid-stride) so warps do not retire after one short burst.
-// The same kernel reads host-mapped weights (K8, zero-copy over PCIe).
+// ps_gemv_bf16 itself dispatches to the bulk-copy kernel (gemv_tma.cu) for device and
+// host-mapped (K8, zero-copy) weights alike; this register-burst kernel stays reachable
+// through ps_gemv_bf16_cfg (rows 2 | 4) as the test and tuning baseline.
 //
 // Epilogues: STORE (y = acc), ACCUM (y += acc, fused residual add),
 // SWIGLU (rows interleaved gate/up: y[t, j] = silu(acc[2j]) * acc[2j+1]).
@@ -221,12 +223,11 @@ static int gemv_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, 
   return PS_OK;
 }
 
-bool is_host_ptr(const void* p);
 int gemv_tma_launch(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
                     int ldy, int epi, cudaStream_t s, int grid_cap);
 
-// rows == 0 selects the bulk-copy kernel (gemv_tma.cu) for device-resident weights;
-// host-mapped weights (zero-copy, K8) and rows = 2 | 4 use the register-burst kernel.
+// rows == 0 selects the bulk-copy kernel (gemv_tma.cu) for device-resident and host-mapped
+// (zero-copy, K8) weights; rows = 2 | 4 use the register-burst kernel below.
 static int gemv_checked(const float* x, int ldx, int t, const void* W, int N, int K, long long ldw, float* y,
                         int ldy, int epilogue, void* stream, int rows, int ksplit, int grid_cap) {
   PS_REQUIRE(t >= 1 && t <= 32, "ps_gemv_bf16: t=%d outside [1, 32]", t);
@@ -240,7 +241,11 @@ static int gemv_checked(const float* x, int ldx, int t, const void* W, int N, in
   cudaStream_t s = (cudaStream_t)stream;
   for (int t0 = 0; t0 < t; t0 += 8) {  // tokens in chunks of 8 (W re-read per chunk)
     int tt = t - t0 < 8 ? t - t0 : 8;
-    if ((rows == 0 && !is_host_ptr(W)) || rows == -1) {  // -1: bulk-copy kernel even on host memory
+    // rows 0 (ps_gemv_bf16): the bulk-copy kernel, device or host-mapped weights alike, so a
+    // zero-copy shard gives bit-identical outputs to its exponent-coded twin (ps_gemv_bf16c,
+    // same decomposition) and to a VRAM copy; SM reads of host memory cap at ~50 GB/s
+    // whatever the kernel. rows 2 | 4: the register-burst kernel (tests).
+    if (rows == 0 || rows == -1) {
       int rc = gemv_tma_launch(x + (long long)t0 * ldx, ldx, tt, Wb, N, K, ldw, y + (long long)t0 * ldy, ldy,
                                epilogue, s, grid_cap);
       if (rc) return rc;

@@ -32,11 +32,18 @@ namespace ps {
 
 constexpr int GT_STAGES = 5;
 constexpr int GT_STAGE_BYTES = 32768;
-#ifndef PS_GT_CONSUMERS
-#define PS_GT_CONSUMERS 8
+#ifndef PS_GT_CONSUMERS_LO
+#define PS_GT_CONSUMERS_LO 16
 #endif
-constexpr int GT_CONSUMERS = PS_GT_CONSUMERS;        // consumer warps (8 or 16)
-constexpr int GT_THREADS = 32 * (1 + GT_CONSUMERS);  // + producer warp
+#ifndef PS_GT_CONSUMERS_HI
+#define PS_GT_CONSUMERS_HI 8
+#endif
+// Consumer warps per token count, the same for bf16 and coded rows (identical
+// decomposition = bit-identical outputs): 16 at t <= 4 — the coded decode is a dependent
+// ALU chain, and 2 warps per scheduler left it latency-bound (ncu r02: "wait" stalls 1.0
+// per issue, 2.2 active warps per scheduler) — and 8 at t = 8 (16 regressed there).
+constexpr int gt_consumers(int T) { return T <= 4 ? PS_GT_CONSUMERS_LO : PS_GT_CONSUMERS_HI; }
+constexpr int gt_threads(int T) { return 32 * (1 + gt_consumers(T)); }  // + producer warp
 
 // Per token count: columns per consumer thread (x kept in registers: CPT * T floats)
 // and rows per stage (RS * KC * 2 = 32 KB, KC = 256 * CPT columns per chunk).
@@ -47,9 +54,10 @@ constexpr int gt_pow2_floor(int v) { return v >= 16 ? 16 : v >= 8 ? 8 : v >= 4 ?
 constexpr int GT_TRAILER_MAX = 256;
 
 template <int T, bool COMP = false> struct GtShape {
+  static constexpr int NC = gt_consumers(T);
   // 16 consumer warps: 8 columns per thread at every T (KC = 4096); 8 warps: 16 / 8
-  static constexpr int CPT = GT_CONSUMERS >= 16 ? 8 : (T <= 4 ? 16 : 8);
-  static constexpr int KC = GT_CONSUMERS * 32 * CPT;
+  static constexpr int CPT = NC >= 16 ? 8 : (T <= 4 ? 16 : 8);
+  static constexpr int KC = NC * 32 * CPT;
   static constexpr int ROWB = COMP ? KC * 3 / 2 + GT_TRAILER_MAX : KC * 2;   // stage bytes per row segment
   static constexpr int RS = COMP ? gt_pow2_floor(GT_STAGE_BYTES / ROWB) : GT_STAGE_BYTES / (KC * 2);
   static constexpr int V = RS * T;  // partial sums reduced per stage
@@ -88,11 +96,12 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[V], int lane) {
 }
 
 template <int T, int EPI, bool COMP = false>
-__global__ void __launch_bounds__(GT_THREADS, 1)
+__global__ void __launch_bounds__(gt_threads(T), 1)
 gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W, int N, int K,
                 long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages) {
   using S = GtShape<T, COMP>;
   constexpr int CPT = S::CPT, KC = S::KC, RS = S::RS, V = S::V, ROWB = S::ROWB;
+  constexpr int GT_CONSUMERS = S::NC, GT_THREADS = gt_threads(T);
   const uint8_t* Wb = reinterpret_cast<const uint8_t*>(W);   // COMP: ldw is in bytes
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;
@@ -294,6 +303,7 @@ static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, i
     g_tma_stages = v < 2 ? 2 : (v > 12 ? 12 : v);
   }
   const int stages = g_tma_stages;
+  constexpr int GT_CONSUMERS = gt_consumers(T), GT_THREADS = gt_threads(T);
   // the per-row accumulators share shared memory with the ring
   const int max_rows = ((232448 - stages * (GT_STAGE_BYTES + 16)) / (GT_CONSUMERS * T * 4)) & ~1;
   int rows_per_cta = 2 * ((pairs + grid - 1) / grid);

@@ -90,7 +90,8 @@ class Engine:
                  machine="b200", profile: str | None = None, seed: int = 0,
                  max_tokens: int | None = None, chunk_bytes: int = 64 << 20,
                  checkpoint: str | None = None, shared_weights: str | None = None,
-                 migration_aware: bool = False, striper=None, kv_page_seed: int | None = None):
+                 migration_aware: bool = False, striper=None, kv_page_seed: int | None = None,
+                 host_format: str | None = None):
         """`model`: preset name or ModelSpec (random-init weights), or None with
         `checkpoint` = a directory holding config.json + safetensors, or a .gguf file
         (real weights, runtime/checkpoint.py, runtime/gguf.py). `shared_weights`: a /dev/shm segment name shared by
@@ -123,7 +124,10 @@ class Engine:
             self.table = TierTable(self.spec.name, self.machine.name, self.budget,
                                    self.context_len,
                                    {t: TierEntry(t, p) for t, p in self.plans.items()})
-        self.weights = HostWeights(self.spec, self.arch, shared=shared_weights)
+        if host_format is None:
+            host_format = self._auto_host_format(ckpt, shared_weights, striper)
+        self.host_format = host_format
+        self.weights = HostWeights(self.spec, self.arch, shared=shared_weights, host_format=host_format)
         t0 = time.perf_counter()
         if ckpt is not None:
             if self.weights.shared is None or self.weights.shared.creator:
@@ -161,6 +165,25 @@ class Engine:
             if best_cost is None or cost < best_cost:
                 best, best_cost = tier, cost
         return best
+
+    def _auto_host_format(self, ckpt, shared_weights, striper) -> str:
+        """'coded' (no bf16 host blob, runtime/model.py) when the bf16 blob and its coded
+        copy do not fit host memory together but the coded copy alone does (Llama-3.3-70B
+        on a 196 GB box: 141 + 106 GB), for a dense random-init model with a private host
+        copy; else 'bf16'. PS_HOST_FORMAT overrides."""
+        env = os.environ.get("PS_HOST_FORMAT")
+        if env:
+            return env
+        if (self.spec.moe is not None or ckpt is not None or shared_weights is not None or striper is not None
+                or os.environ.get("PS_CODED", "1") != "1"):
+            return "bf16"
+        from .model import WeightLayout
+        lay = WeightLayout(self.spec, self.arch)
+        avail = _meminfo().get("MemAvailable", 0)
+        coded = lay.total_bytes * 3 // 4 + lay.embed_bytes
+        if avail and coded > 0.5 * avail and coded < 0.75 * avail:
+            return "coded"
+        return "bf16"
 
     def _build_coded(self) -> None:
         """Exponent-coded copies of the dense shards (runtime/wcomp.py) that decode
@@ -206,6 +229,7 @@ class Engine:
                                      self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes,
                                      kv_page_seed=self.kv_page_seed)
             self.migration.pins_fn = self.executor.pins_for   # include the spare pins
+            self.migration.phys_fn = self.executor.phys_bytes  # coded-resident shards
             if self.striper is not None:
                 if self.weights.shared is None:
                     raise SpecError("striped streaming needs node-shared weights (shared_weights=...)")

@@ -134,8 +134,9 @@ class PassSpec:
 class PassStats:
     tier: int
     T: int
-    bytes_streamed: int = 0
+    bytes_streamed: int = 0      # every H2D byte of the pass (weights + KV windows)
     copies: int = 0
+    kv_bytes: int = 0            # of which KV-cache pages (never coded)
     kv_writeback_bytes: int = 0
     zero_copy_bytes: int = 0
     kernel_calls: int = 0
@@ -219,7 +220,13 @@ class Executor:
         # exponent-coded dense shards (runtime/wcomp.py) for GEMV passes that stream
         # them; every coded row carries its own base exponent and escapes (in-band)
         self.coded = getattr(weights, "coded", None)
+        # host_format="coded": the coded shards are the only host copy, so every path reads them
+        self.coded_only = getattr(weights, "host_format", "bf16") == "coded"
+        self._coded_res_on = self.coded is not None and (self.coded_only or
+                                                         os.environ.get("PS_CODED_RESIDENT", "1") != "0")
         self._coded_call = None
+        self._zc_direct = False
+        self.stage_zc = False
         self.persist_high = self.arena.high       # activations + ring are carved below, per tier
         self.residency: dict[int, tuple] = {}
         self.tier = None
@@ -246,7 +253,8 @@ class Executor:
                      ("hid16", "hid16", T * self.ffn * 2)]
         if T > GEMV_CORE_MAX_T:   # x planes + split-K partials of ps_gemv_tc
             spec.append(("tcws", "gemv_tc_ws", self._tc_workspace_bytes()))
-        if T > GEMV_MAX_T and self._coded_prefill():   # one coded piece expanded to bf16 for the GEMM
+        if T > GEMV_MAX_T and (self._coded_prefill() or getattr(self, "_coded_res_on", False)):
+            # one coded piece (streamed or VRAM-resident) expanded to bf16 for the GEMM
             spec.append(("expand", "coded_expand", self._expand_bytes()))
         spec += [("xs", "xs", B * d * 4), ("logits", "logits", B * self.V * 4)]
         # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
@@ -270,7 +278,8 @@ class Executor:
 
     def _coded_prefill(self) -> bool:
         """GEMM (prefill) passes stream coded pieces and expand them in VRAM (PS_CODED_PREFILL)."""
-        return getattr(self, "coded", None) is not None and os.environ.get("PS_CODED_PREFILL", "1") != "0"
+        return getattr(self, "coded", None) is not None and (
+            getattr(self, "coded_only", False) or os.environ.get("PS_CODED_PREFILL", "1") != "0")
 
     def _tc_workspace_bytes(self) -> int:
         """ps_gemv_tc workspace: the x planes of the widest K, plus split-K partials up to
@@ -326,7 +335,21 @@ class Executor:
     def _phys_bytes(self, shard) -> int:
         if shard.kind is ShardKind.KV_CACHE:
             return self.kv_layer_bytes
+        if self.coded_resident(shard.id):
+            return self.coded.shard_bytes[shard.id]
         return self.w.layout.blobs[shard.id].nbytes
+
+    def phys_bytes(self, sid: int) -> int:
+        """VRAM bytes shard `sid` takes when resident (the migration model's size)."""
+        return self._phys_bytes(self.shards[sid])
+
+    def coded_resident(self, sid: int) -> bool:
+        """Dense weight shards live in VRAM in their exponent-coded form (runtime/wcomp.py,
+        0.75 x the bytes): GEMV passes read the coded rows, GEMM passes expand them to bf16
+        piece by piece. The freed budget caches more shards (spare pins), so fewer bytes
+        cross the link per token. MoE expert groups stay bf16 (PS_CODED_RESIDENT=0: all)."""
+        return (self._coded_res_on and sid in self.coded.tensors and
+                self.shard_kind[sid] is not ShardKind.MOE_EXPERT_GROUP)
 
     def _pinned_bytes(self, plan: SchedulePlan) -> int:
         return sum((self._phys_bytes(self.shards[p.shard_id]) + 255) // 256 * 256
@@ -485,7 +508,8 @@ class Executor:
             self.d2d_bytes += nbytes
         for sid in h2d:
             dev, nbytes = new[sid]
-            L.memcpy_async(dev, self.w.shard_ptr(sid), nbytes, self.cs)
+            src = self.coded.shard_ptr(sid) if self.coded_resident(sid) else self.w.shard_ptr(sid)
+            L.memcpy_async(dev, src, nbytes, self.cs)
             moved += nbytes
         for layer, dev in self.kv_vram.items():
             moved += self._copy_pages(dev, self._kv_host_ptr(layer), live, self.cs)
@@ -515,10 +539,15 @@ class Executor:
         free = self.arena.free_bytes
         ring_bytes = max(0, min(self.ring_cap, free)) // 256 * 256
         self.chunk = min(self.chunk_cap, max(1 << 16, ring_bytes // 6 // 256 * 256))
-        staged = ("stream", "zerocopy") if self.T_tier > GEMV_CORE_MAX_T else ("stream",)
-        streams = any(m in staged for m, _ in self.residency.values()) or \
-            any(m in staged for m in self.kv_mode.values())
         need = self.kv_layer_bytes + 3 * self.chunk
+        streams = any(m == "stream" for m, _ in self.residency.values()) or \
+            any(m == "stream" for m in self.kv_mode.values())
+        # passes of 9..32 tokens stage CPU-placed shards through the ring (one pass over
+        # them); a budget whose ring cannot hold that keeps reading them zero-copy
+        self.stage_zc = self.T_tier > GEMV_CORE_MAX_T and ring_bytes >= need and \
+            any(m == "zerocopy" for m, _ in self.residency.values())
+        if self.T_tier > GEMV_MAX_T:   # GEMM passes cannot read host memory: staging is required
+            streams = streams or any(m == "zerocopy" for m, _ in self.residency.values())
         if streams and ring_bytes < need:
             raise InfeasibleBudget(float(self.arena.capacity),
                                    float(self.arena.capacity - free + need), "copy-engine ring")
@@ -697,10 +726,14 @@ class Executor:
         right before its first consumer and released (sealed) after the last
         consumer that reads any tensor in it."""
         mode, dev = self.residency[sid]
+        self._zc_direct = False
         if mode == "zerocopy" and T > GEMV_CORE_MAX_T:
-            # one pass over the weights: stage CPU-placed shards through the ring (copy
-            # engine, once) instead of re-reading host memory per 8 tokens or per tile
-            mode = "stream"
+            if T > GEMV_MAX_T or self.stage_zc:
+                # one pass over the weights: stage CPU-placed shards through the ring (copy
+                # engine, once) instead of re-reading host memory per 8 tokens or per tile
+                mode = "stream"
+            else:   # no room for a ring: the CUDA-core GEMV reads them zero-copy
+                self._zc_direct = True
         blob = self.w.layout.blobs[sid]
         own = {c.tensor: i for i, c in enumerate(consumers) if c.tensor is not None}
         readers: dict = {}
@@ -727,24 +760,42 @@ class Executor:
             base = dev if mode == "pinned" else self.w.shard_ptr(sid)
             zc_coded = (mode == "zerocopy" and self.coded is not None and sid in self.coded.tensors and
                         getattr(self.coded, "mapped", False) and
-                        os.environ.get("PS_CODED_ZEROCOPY", "1") != "0")
+                        (self.coded_only or os.environ.get("PS_CODED_ZEROCOPY", "1") != "0"))
+            res_coded = mode == "pinned" and self.coded_resident(sid)
             if zc_coded:   # the bulk-copy GEMV reads the coded rows straight from host memory
                 base = self.coded.shard_ptr(sid)
-                meta = self.coded.tensors[sid]
                 self._stat.zero_copy_bytes += self.coded.shard_bytes[sid]
             elif mode == "zerocopy":
                 self._stat.zero_copy_bytes += blob.nbytes
+            coded_rows = zc_coded or res_coded
+            if coded_rows:
+                meta = self.coded.tensors[sid]
+            evens = {c.tensor for c in consumers if c.even_rows}
             live = []
 
             def done(i):
                 pass
             for name in names:
                 t = blob.tensors[name]
-                off = meta[name][0] if zc_coded else t.offset
+                off = meta[name][0] if coded_rows else t.offset
                 self.ptrs[name] = base + off
                 if name in own:
                     advance_to(own[name])
-                    if zc_coded and meta[name][2]:
+                    if coded_rows and meta[name][2] and T > GEMV_MAX_T:
+                        # GEMM pass over a coded-resident matrix: rows expanded to bf16 in
+                        # pieces of the expand buffer, one GEMM per piece (stream order
+                        # keeps the next expansion behind the previous GEMM)
+                        step = max(1, self._expand_bytes() // (t.cols * 2))
+                        if name in evens:
+                            step = max(2, step & ~1)
+                        for r0 in range(0, t.rows, step):
+                            r1 = min(t.rows, r0 + step)
+                            L.call("ps_expand_coded", base + off + r0 * meta[name][1], meta[name][1],
+                                   r1 - r0, t.cols, self.expand, t.cols, self.cs)
+                            self._traced(name, consumers[ci].fn, self.expand, r0, r1)
+                        ci += 1
+                        continue
+                    if coded_rows and meta[name][2]:
                         self._coded_call = meta[name][1]
                     try:
                         self._traced(name, consumers[ci].fn, base + off, 0, t.rows)
@@ -875,7 +926,10 @@ class Executor:
 
         def route(base):
             norm(base + t_norm.offset)
+            # a router read from host memory takes the CUDA-core GEMV (no tensor map over it)
+            self._zc_direct = base == self.w.shard_ptr(sid)
             self._matmul(T, xn, base + t_router.offset, E, d, self.m_logits, E, L.PS_EPI_STORE)
+            self._zc_direct = False
             L.call("ps_moe_route_topk", self.m_logits, E, T, E, k, 1, self.m_ids, self.m_w, self.cs)
             if not t1:
                 L.call("ps_moe_plan", self.m_ids, P, E, self.m_plan, self.cs)
@@ -1069,11 +1123,13 @@ class Executor:
         coded = self._coded_call
         if T > GEMV_MAX_T:
             L.call("ps_gemm_bf16", act, T, K, K, W, N, K, out, ldo, epi, self.cs)
-        elif T > GEMV_CORE_MAX_T:      # one pass over W for the whole batch (tcgen05)
+        elif T > GEMV_CORE_MAX_T and not self._zc_direct:   # one pass over W for the batch (tcgen05)
             L.call("ps_gemv_tc", act, K, T, W, N, K, coded if coded is not None else K,
                    1 if coded is not None else 0, out, ldo, epi, self.tcws, self._tcws_bytes, self.cs)
-        elif coded is not None:
-            L.call("ps_gemv_bf16c", act, K, T, W, N, K, coded, out, ldo, epi, self.cs)
+        elif coded is not None:   # t <= 8 per launch (zero-copy rows at 9..32 tokens: chunks of 8)
+            for t0 in range(0, T, GEMV_CORE_MAX_T):
+                L.call("ps_gemv_bf16c", act + t0 * K * 4, K, min(GEMV_CORE_MAX_T, T - t0), W, N, K, coded,
+                       out + t0 * ldo * 4, ldo, epi, self.cs)
         else:
             L.call("ps_gemv_bf16", act, K, T, W, N, K, K, out, ldo, epi, self.cs)
 
@@ -1204,6 +1260,7 @@ class Executor:
                 kv_pool_pages = kv_span
                 up = sum(c for _, c in kv_read) * self.page_bytes
                 self._stat.bytes_streamed += up
+                self._stat.kv_bytes += up
                 self._stat.copies += len(kv_read)
                 self._wait(arrived)
 

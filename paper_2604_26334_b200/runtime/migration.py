@@ -98,6 +98,7 @@ class MigrationModel:
         self.spec, self.plans = spec, plans
         # tier -> shard ids in carve order; the executor's pins_for adds its spare pins
         self.pins_fn = pins_fn
+        self.phys_fn = None
         self.shards = build_shards(spec, context_len, batch)
         self.batch = batch
         from .executor import KV_PAGE_ROWS
@@ -109,6 +110,8 @@ class MigrationModel:
     def _phys(self, shard) -> int:
         if shard.kind is ShardKind.KV_CACHE:
             return self.kv_layer_bytes
+        if self.phys_fn is not None:     # the executor's resident size (coded shards: smaller)
+            return self.phys_fn(shard.id)
         return self.blob_bytes[shard.id]
 
     def pinned_offsets(self, tier: int) -> dict:

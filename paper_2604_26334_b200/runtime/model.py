@@ -321,10 +321,24 @@ class HostWeights:
     that created it generates, the others wait for it.
     """
 
-    def __init__(self, spec: ModelSpec, arch: Arch, shared: str | None = None):
+    def __init__(self, spec: ModelSpec, arch: Arch, shared: str | None = None, host_format: str = "bf16"):
+        """`host_format="coded"`: no bf16 blob on the host at all — `generate()` produces
+        every tensor on the GPU and keeps only its exponent-coded form (runtime/wcomp.py,
+        ~0.75 x the bytes; dense models), for models whose bf16 and coded copies do not
+        fit host memory together. The embedding table stays bf16."""
         self.spec, self.arch = spec, arch
         self.layout = WeightLayout(spec, arch)
         self.shared = None
+        self.coded = None
+        self.host_format = host_format
+        if host_format not in ("bf16", "coded"):
+            raise ValueError(f"host_format {host_format!r}")
+        if host_format == "coded":
+            if spec.moe is not None or shared is not None:
+                raise ValueError("host_format='coded' is for dense models with a private host copy")
+            self.base = 0
+            self.embed = L.host_alloc(self.layout.embed_bytes, mapped=True)
+            return
         if shared is not None:
             total = _align(self.layout.total_bytes) + self.layout.embed_bytes
             try:
@@ -341,6 +355,14 @@ class HostWeights:
             self.embed = L.host_alloc(self.layout.embed_bytes, mapped=True)
 
     def close(self) -> None:
+        if self.coded is not None:
+            self.coded.close()
+            self.coded = None
+        if self.host_format == "coded":
+            if self.embed:
+                L.host_free(self.embed)
+                self.embed = 0
+            return
         if self.shared is not None:
             if self.base:
                 self.base = self.embed = 0
@@ -358,14 +380,24 @@ class HostWeights:
             pass
 
     def shard_ptr(self, shard_id: int) -> int:
+        if not self.base:
+            raise RuntimeError("no bf16 host blob (host_format='coded'): read the coded shards")
         return self.base + self.layout.blobs[shard_id].offset
 
     def tensor_ptr(self, shard_id: int, name: str) -> int:
         return self.shard_ptr(shard_id) + self.layout.tensor(shard_id, name).offset
 
     def host_view(self, shard_id: int, name: str) -> np.ndarray:
-        """uint16 view (bf16 bits) of one tensor in the pinned blob."""
+        """uint16 view (bf16 bits) of one tensor in the pinned blob (host_format='coded':
+        a decoded copy, for tests and the CPU oracle)."""
         t = self.layout.tensor(shard_id, name)
+        if self.host_format == "coded":
+            from .wcomp import decode
+            off, rb, is_coded = self.coded.tensors[shard_id][name]
+            addr = self.coded.shard_ptr(shard_id) + off
+            raw = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint8 * (t.rows * rb)).from_address(addr))
+            raw = raw.reshape(t.rows, rb)
+            return decode(raw, t.cols) if is_coded else raw.view(np.uint16).copy()
         buf = (np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint16 * (t.rows * t.cols))
                                      .from_address(self.tensor_ptr(shard_id, name))))
         return buf.reshape(t.rows, t.cols)
@@ -401,6 +433,9 @@ class HostWeights:
         return buf.reshape(self.spec.vocab_size, self.spec.d_model)
 
     def generate(self, staging_bytes: int = 256 << 20) -> None:
+        if self.host_format == "coded":
+            self._generate_coded(staging_bytes)
+            return
         if self.shared is not None and not self.shared.creator:
             self.shared.wait_ready()          # another replica of this node fills it
             return
@@ -408,62 +443,81 @@ class HostWeights:
         if self.shared is not None:
             self.shared.mark_ready()
 
-    def _generate(self, staging_bytes: int) -> None:
-        import torch
-        seed = self.arch.seed
-        stream = torch.cuda.current_stream().cuda_stream
-        stage = torch.empty(staging_bytes, dtype=torch.uint8, device="cuda")
-        sptr = stage.data_ptr()
-        row_cap_bytes = staging_bytes
-
-        def emit(dst_host: int, nbytes: int, producer) -> None:
-            done = 0
-            while done < nbytes:
-                n = min(row_cap_bytes, nbytes - done)
-                producer(sptr, done, n)
-                L.memcpy_async(dst_host + done, sptr, n, stream)
-                L.call("ps_stream_synchronize", stream)
-                done += n
+    def tensor_filler(self, t: TensorSlot, stream: int):
+        """fill(dst_dev, r0, r1): the deterministic init of rows [r0, r1) of tensor `t`
+        (bf16, row-major) written to device memory at dst_dev."""
+        seed, cols = self.arch.seed, t.cols
 
         def plain(name, fan_in):
             scale, bias = init_scale(name, fan_in)
             sd = tensor_seed(seed, name)
             if name in HEAVY_ROW_TENSORS:     # heavy-tailed row norms (margin-robust head)
-                def prod(dst, byte_off, n):
-                    L.call("ps_init_rowscaled_bf16", dst, n // 2, sd, byte_off // 2, fan_in, scale, stream)
-                return prod
+                return lambda dst, e0, n: L.call("ps_init_rowscaled_bf16", dst, n, sd, e0, fan_in, scale, stream)
+            return lambda dst, e0, n: L.call("ps_init_uniform_bf16", dst, n, sd, e0, scale, bias, stream)
 
-            def prod(dst, byte_off, n):
-                L.call("ps_init_uniform_bf16", dst, n // 2, sd, byte_off // 2, scale, bias, stream)
-            return prod
+        kind = t.init[0]
+        if kind == "plain":
+            prod = plain(t.init[1], cols)
+            return lambda dst, r0, r1: prod(dst, r0 * cols, (r1 - r0) * cols)
+        if kind == "concat":
+            parts, first = [], 0
+            for name, rows in t.init[1]:
+                parts.append((first, first + rows, plain(name, cols)))
+                first += rows
+
+            def fill(dst, r0, r1):
+                for a, b, prod in parts:
+                    lo, hi = max(a, r0), min(b, r1)
+                    if lo < hi:
+                        prod(dst + (lo - r0) * cols * 2, (lo - a) * cols, (hi - lo) * cols)
+            return fill
+        if kind == "interleaved":
+            name_a, name_b = t.init[1], t.init[2]
+            scale, bias = init_scale(name_a, cols)
+            sa, sb = tensor_seed(seed, name_a), tensor_seed(seed, name_b)
+            rows_each = t.rows // 2
+            return lambda dst, r0, r1: L.call("ps_init_interleaved_bf16", dst, rows_each, r0, r1 - r0, cols, sa,
+                                              sb, scale, bias, stream)
+        raise ValueError(f"unknown init {t.init!r}")
+
+    def _generate_coded(self, staging_bytes: int) -> None:
+        """Embedding table as bf16; every shard generated on the GPU and stored coded."""
+        import torch
+
+        from .wcomp import CodedShards
+        stream = torch.cuda.current_stream().cuda_stream
+        stage = torch.empty(staging_bytes, dtype=torch.uint8, device="cuda")
+        emb = TensorSlot("embed", 0, self.spec.vocab_size, self.spec.d_model, ("plain", "embed"))
+        fill = self.tensor_filler(emb, stream)
+        step = max(1, staging_bytes // (emb.cols * 2))
+        for r0 in range(0, emb.rows, step):
+            r1 = min(emb.rows, r0 + step)
+            fill(stage.data_ptr(), r0, r1)
+            L.memcpy_async(self.embed + r0 * emb.cols * 2, stage.data_ptr(), (r1 - r0) * emb.cols * 2, stream)
+            L.call("ps_stream_synchronize", stream)
+        del stage
+        kinds = {b.kind for b in self.layout.blobs.values()}
+        self.coded = CodedShards(self, kinds, chunk_bytes=staging_bytes)
+
+    def _generate(self, staging_bytes: int) -> None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+        stage = torch.empty(staging_bytes, dtype=torch.uint8, device="cuda")
+        sptr = stage.data_ptr()
+
+        def emit_rows(dst_host: int, t: TensorSlot) -> None:
+            fill = self.tensor_filler(t, stream)
+            step = max(1, staging_bytes // (t.cols * 2))
+            for r0 in range(0, t.rows, step):
+                r1 = min(t.rows, r0 + step)
+                fill(sptr, r0, r1)
+                L.memcpy_async(dst_host + r0 * t.cols * 2, sptr, (r1 - r0) * t.cols * 2, stream)
+                L.call("ps_stream_synchronize", stream)
 
         for sid, blob in self.layout.blobs.items():
             for t in blob.tensors.values():
-                dst = self.base + blob.offset + t.offset
-                kind = t.init[0]
-                if kind == "plain":
-                    emit(dst, t.nbytes, plain(t.init[1], t.cols))
-                elif kind == "concat":
-                    cur = dst
-                    for name, rows in t.init[1]:
-                        emit(cur, rows * t.cols * 2, plain(name, t.cols))
-                        cur += rows * t.cols * 2
-                elif kind == "interleaved":
-                    name_a, name_b = t.init[1], t.init[2]
-                    scale, bias = init_scale(name_a, t.cols)
-                    sa, sb = tensor_seed(seed, name_a), tensor_seed(seed, name_b)
-                    rows_each, cols = t.rows // 2, t.cols
-                    row_bytes = cols * 2
-
-                    def prod(dst_dev, byte_off, n, rows_each=rows_each, cols=cols, sa=sa, sb=sb,
-                             scale=scale, bias=bias, row_bytes=row_bytes):
-                        L.call("ps_init_interleaved_bf16", dst_dev, rows_each, byte_off // row_bytes,
-                               n // row_bytes, cols, sa, sb, scale, bias, stream)
-                    # chunks must hold whole rows
-                    saved = row_cap_bytes
-                    row_cap_bytes = max(row_bytes, (saved // row_bytes) * row_bytes)
-                    emit(dst, t.nbytes, prod)
-                    row_cap_bytes = saved
-        emit(self.embed, self.layout.embed_bytes, plain("embed", self.spec.d_model))
+                emit_rows(self.base + blob.offset + t.offset, t)
+        emb = TensorSlot("embed", 0, self.spec.vocab_size, self.spec.d_model, ("plain", "embed"))
+        emit_rows(self.embed, emb)
         del stage
         torch.cuda.synchronize()

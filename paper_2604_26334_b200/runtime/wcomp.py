@@ -124,7 +124,8 @@ class CodedShards:
     coded)`, coded = True), norm vectors, other tensors and matrices with too many
     escapes as raw bf16 (coded = False, row_bytes = 2 K)."""
 
-    def __init__(self, weights, kinds, threads: int = 16, shared: str | None = None):
+    def __init__(self, weights, kinds, threads: int = 16, shared: str | None = None, use_gpu: bool = True,
+                 chunk_bytes: int = 256 << 20):
         """`shared`: name of a node-wide /dev/shm segment (model.SharedHostBlob): the
         replica that creates it encodes, the others map it and wait for the ready flag,
         so a node holds ONE coded copy however many replicas stream from it."""
@@ -143,12 +144,36 @@ class CodedShards:
                 for name, t in blob.tensors.items() if t.rows > 1 and t.cols % 256 == 0 and
                 (blob.kind is not moe_kind or ".e" in name)]
 
+        gpu = None
+        # host_format="coded" (runtime/model.py): no bf16 blob; tensors come from their
+        # device-side init, generated once per pass
+        generated = getattr(weights, "host_format", "bf16") == "coded"
+        if use_gpu or generated:
+            import torch
+            if torch.cuda.is_available():
+                gpu = GpuEncoder(chunk_bytes)
+        if generated and gpu is None:
+            raise RuntimeError("host_format='coded' encodes on the GPU")
+        self.encoder = "gpu" if gpu is not None else "numpy"
+
+        def source(sid, name):
+            if generated:
+                return weights.tensor_filler(layout.blobs[sid].tensors[name], gpu.stream)
+            return weights.tensor_ptr(sid, name)
+
         def plan(job):   # the trailer each matrix needs (a counting pass, no output)
             sid, name = job
+            if gpu is not None:
+                t = layout.blobs[sid].tensors[name]
+                top = gpu.max_escapes(source(sid, name), t.rows, t.cols)
+                return job, None if top > MAX_ESCAPES else trailer_bytes(top)
             return job, _trailer_or_none(weights.host_view(sid, name))
 
-        with ThreadPoolExecutor(max_workers=threads) as pool:
-            trailers = dict(pool.map(plan, mats))
+        if gpu is not None:
+            trailers = dict(plan(job) for job in mats)
+        else:
+            with ThreadPoolExecutor(max_workers=threads) as pool:
+                trailers = dict(pool.map(plan, mats))
         # one row size per expert matrix kind within a group (uniform expert stride, so
         # the fetcher copies expert e from e * stride): the group's largest trailer
         self.experts = {}
@@ -188,11 +213,14 @@ class CodedShards:
             self.seg = SharedHostBlob(shared, self.nbytes)
             self.host = self.seg.addr
             if not self.seg.creator:
+                if gpu is not None:
+                    gpu.close()
                 try:
                     self.seg.wait_ready()          # another replica of this node encodes
                 except BaseException:
                     self.close()
                     raise
+                self.mapped = True                 # registered mapped by SharedHostBlob
                 self.coded_bytes = sum(self.shard_bytes.values())
                 return
         else:
@@ -206,8 +234,18 @@ class CodedShards:
                 sid, name = item
                 t = layout.blobs[sid].tensors[name]
                 o, rb, is_coded = self.tensors[sid][name]
+                if generated:
+                    dst = self.host + self.shard_off[sid] + o
+                    if is_coded:
+                        gpu.encode_to(source(sid, name), t.rows, t.cols, rb - t.cols * 3 // 2, dst)
+                    else:
+                        gpu.bf16_to(source(sid, name), t.rows, t.cols, dst)
+                    return
                 src = weights.host_view(sid, name)
-                if is_coded:
+                if is_coded and gpu is not None:
+                    gpu.encode_to(source(sid, name), t.rows, t.cols, rb - t.cols * 3 // 2,
+                                  self.host + self.shard_off[sid] + o)
+                elif is_coded:
                     res = encode(src, out=buf[o + self.shard_off[sid]:], trailer=rb - t.cols * 3 // 2)
                     assert res is not None and res[1] == rb - t.cols * 3 // 2
                 else:
@@ -215,11 +253,18 @@ class CodedShards:
                     buf[start:start + t.rows * t.cols * 2] = src.reshape(-1).view(np.uint8)
 
             items = [(sid, name) for sid, meta in self.tensors.items() for name in meta]
-            with ThreadPoolExecutor(max_workers=threads) as pool:
-                list(pool.map(work, items))
+            if gpu is not None:
+                for item in items:
+                    work(item)
+            else:
+                with ThreadPoolExecutor(max_workers=threads) as pool:
+                    list(pool.map(work, items))
         except BaseException:
             self.close()
             raise
+        finally:
+            if gpu is not None:
+                gpu.close()
         if self.seg is not None:
             self.seg.mark_ready()
         self.coded_bytes = sum(self.shard_bytes.values())
@@ -252,6 +297,83 @@ class CodedShards:
         elif self.host:
             L.host_free(self.host)
             self.host = 0
+
+
+class GpuEncoder:
+    """`encode` on the GPU (csrc/wencode.cu: ps_wencode_stats + ps_wencode_rows), byte-
+    identical to the numpy encoder: matrices go up in row chunks of <= `chunk_bytes`
+    through a device staging buffer, coded rows come back with one D2H per chunk.
+    Used at model load (before the capped arena exists, so the staging is not budget)."""
+
+    def __init__(self, chunk_bytes: int = 256 << 20):
+        import torch
+
+        from . import lib as L
+        self.L = L
+        self.torch = torch
+        self.stream = torch.cuda.current_stream().cuda_stream
+        self.chunk_bytes = chunk_bytes
+        self.src = torch.empty(chunk_bytes, dtype=torch.uint8, device="cuda")
+        self.out = torch.empty(chunk_bytes * 3 // 4 + (chunk_bytes // 512) * 256 + 4096, dtype=torch.uint8,
+                               device="cuda")
+        self.rows_cap = 1 << 16
+        self._ints(self.rows_cap)
+
+    def _ints(self, n: int) -> None:
+        self.base = self.torch.empty(n, dtype=self.torch.int32, device="cuda")
+        self.count = self.torch.empty(n, dtype=self.torch.int32, device="cuda")
+        self.rows_cap = n
+
+    def _chunks(self, n: int, k: int):
+        step = max(1, min(self.chunk_bytes // (2 * k), self.rows_cap))
+        for r0 in range(0, n, step):
+            yield r0, min(n, r0 + step)
+
+    def _source(self, src, k: int):
+        """fill(dst_dev, r0, r1) for a pinned host matrix address or a device filler."""
+        if callable(src):
+            return src
+        return lambda dst, r0, r1: self.L.memcpy_async(dst, src + r0 * k * 2, (r1 - r0) * k * 2, self.stream)
+
+    def _stats(self, fill, r0: int, r1: int, k: int) -> None:
+        fill(self.src.data_ptr(), r0, r1)
+        self.L.call("ps_wencode_stats", self.src.data_ptr(), r1 - r0, k, k, self.base.data_ptr(),
+                    self.count.data_ptr(), self.stream)
+
+    def max_escapes(self, src, n: int, k: int) -> int:
+        """Largest per-row escape count of a bf16 matrix [n, k]: `src` is its pinned host
+        address, or fill(dst_dev, r0, r1) producing its rows on the device."""
+        fill, top = self._source(src, k), 0
+        for r0, r1 in self._chunks(n, k):
+            self._stats(fill, r0, r1, k)
+            top = max(top, int(self.count[:r1 - r0].max().item()))
+        return top
+
+    def bf16_to(self, src, n: int, k: int, dst_host: int) -> None:
+        """The raw bf16 rows of a device-filled matrix copied to `dst_host`."""
+        fill = self._source(src, k)
+        for r0, r1 in self._chunks(n, k):
+            fill(self.src.data_ptr(), r0, r1)
+            self.L.memcpy_async(dst_host + r0 * k * 2, self.src.data_ptr(), (r1 - r0) * k * 2, self.stream)
+        self.L.call("ps_stream_synchronize", self.stream)
+
+    def encode_to(self, src, n: int, k: int, tb: int, dst_host: int) -> None:
+        """Coded rows (trailer `tb` bytes) of a bf16 matrix (`src` as in max_escapes)
+        written to `dst_host` (n * row_bytes(k, tb) bytes, pinned)."""
+        L = self.L
+        rb = row_bytes(k, tb)
+        fill = self._source(src, k)
+        for r0, r1 in self._chunks(n, k):
+            if (r1 - r0) * rb > self.out.numel():
+                raise ValueError("GpuEncoder: output staging too small")
+            self._stats(fill, r0, r1, k)
+            L.call("ps_wencode_rows", self.src.data_ptr(), r1 - r0, k, k, self.base.data_ptr(), tb,
+                   self.out.data_ptr(), rb, self.stream)
+            L.memcpy_async(dst_host + r0 * rb, self.out.data_ptr(), (r1 - r0) * rb, self.stream)
+        L.call("ps_stream_synchronize", self.stream)   # stream order protects the staging reuse
+
+    def close(self) -> None:
+        self.src = self.out = self.base = self.count = None
 
 
 def _trailer_or_none(bits: np.ndarray) -> int | None:

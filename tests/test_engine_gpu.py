@@ -578,7 +578,7 @@ def test_batched_decode_one_pass_coded_vs_bf16(monkeypatch, frac, batch):
                      chunk_bytes=1 << 20)
         res = eng.generate(prompts, gen_len=8)
         ex = eng.executor
-        link = sum(s.bytes_streamed for s in ex.stats if s.T == batch)
+        link = sum(s.bytes_streamed - s.kv_bytes for s in ex.stats if s.T == batch)   # weight bytes
         out[coded] = ([t.tolist() for t in res.tokens], eng.logits().copy(), link, res.row_modes)
         eng.close()
     assert out["1"][0] == out["0"][0]
@@ -662,3 +662,91 @@ def test_coded_zero_copy_head_same_tokens_fewer_bytes(monkeypatch):
     assert out["1"][0] == out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1])
     assert out["0"][2] > 0 and out["1"][2] < 0.8 * out["0"][2], (out["0"][2], out["1"][2])
+
+
+@pytest.mark.parametrize("frac,batch", [(0.5, 1), (0.35, 1), (0.6, 16)])
+def test_coded_residency_same_tokens_fewer_link_bytes(monkeypatch, frac, batch):
+    """Dense shards held in VRAM in their exponent-coded form (PS_CODED_RESIDENT=1): GEMV
+    passes read the coded rows (ps_gemv_bf16c / ps_gemv_tc), GEMM passes expand them to
+    bf16 piece by piece (ps_expand_coded) ahead of the tcgen05 GEMM. Both reproduce the
+    bf16 operands exactly, so tokens and logits equal bf16 residency; the freed budget
+    caches more shards, so decode passes move no more link bytes (fewer whenever another
+    shard fits), and the migration model still predicts every switch."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model("tiny-llama")
+    prompts = [_prompt(128 if batch == 1 else 40, spec.vocab_size, seed=70 + i) for i in range(batch)]
+    out = {}
+    for cr in ("0", "1"):
+        monkeypatch.setenv("PS_CODED_RESIDENT", cr)
+        eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=batch,
+                     chunk_bytes=1 << 20)
+        res = eng.generate(prompts, gen_len=10)
+        ex = eng.executor
+        dec = [s for s in ex.stats if s.T <= 32 and s.T == batch]
+        link = sum(s.bytes_streamed + s.zero_copy_bytes for s in dec) / max(1, len(dec))
+        res_bytes = sum(ex.phys_bytes(sid) for sid, r in ex.residency.items() if r[0] == "pinned")
+        n_res = sum(1 for sid, r in ex.residency.items() if r[0] == "pinned" and ex.coded_resident(sid))
+        for prev, tier, rows, moved, (h2d, d2h) in res.switches:
+            assert moved == h2d + d2h, (prev, tier, rows, moved, h2d, d2h)
+        out[cr] = ([t.tolist() for t in res.tokens], eng.logits().copy(), link, res_bytes, n_res)
+        eng.close()
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert out["1"][4] > 0 and out["0"][4] == 0, "no shard was coded-resident"
+    assert out["1"][2] <= out["0"][2], (out["0"][2], out["1"][2])
+
+
+@pytest.mark.parametrize("frac,prompt_len,batch", [(0.5, 128, 1), (0.25, 20, 1), (0.6, 40, 12)])
+def test_coded_only_host_format_same_tokens(frac, prompt_len, batch):
+    """host_format='coded': the weights are generated on the GPU and only their exponent-
+    coded form is kept on the host (no bf16 blob, the Llama-3.3-70B configuration on a
+    196 GB box). Prefill (expanded pieces), decode (coded GEMV / one-pass tcgen05 GEMV),
+    zero-copy and pinned shards all read the coded copy: same tokens and logits as the
+    bf16 host blob, and the decoded host view equals the bf16 blob bit for bit."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model("tiny-llama")
+    prompts = [_prompt(prompt_len, spec.vocab_size, seed=90 + i) for i in range(batch)]
+    out = {}
+    for fmt in ("bf16", "coded"):
+        eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=batch,
+                     chunk_bytes=1 << 20, host_format=fmt)
+        res = eng.generate(prompts, gen_len=8)
+        w = eng.weights
+        views = {(sid, n): w.host_view(sid, n).copy() for sid, b in w.layout.blobs.items() for n in b.tensors}
+        out[fmt] = ([t.tolist() for t in res.tokens], eng.logits().copy(), views, w.embed_view().copy())
+        if fmt == "coded":
+            assert w.base == 0 and w.coded is not None and w.coded.encoder == "gpu"
+        eng.close()
+    assert out["coded"][0] == out["bf16"][0]
+    assert np.array_equal(out["coded"][1], out["bf16"][1])
+    assert np.array_equal(out["coded"][3], out["bf16"][3])
+    for key, v in out["bf16"][2].items():
+        assert np.array_equal(out["coded"][2][key], v), key
+
+
+def test_gpu_encoded_blob_equals_numpy_encoded():
+    """CodedShards built by the GPU encoder (model load) is byte-identical to the numpy
+    encoder's blob for the same weights (tiny-llama and tiny-moe, experts included)."""
+    from paper_2604_26334_b200.planning.graph import ShardKind
+    from paper_2604_26334_b200.runtime.model import HostWeights, arch_for
+    from paper_2604_26334_b200.runtime.wcomp import CodedShards
+    import ctypes
+    for name in ("tiny-llama", "tiny-moe"):
+        spec = catalog.builtin_model(name)
+        hw = HostWeights(spec, arch_for(spec))
+        hw.generate()
+        kinds = (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD, ShardKind.MOE_EXPERT_GROUP)
+        a = CodedShards(hw, kinds, use_gpu=True)
+        b = CodedShards(hw, kinds, use_gpu=False)
+        assert a.encoder == "gpu" and b.encoder == "numpy"
+        assert a.tensors == b.tensors and a.nbytes == b.nbytes
+        ba = np.ctypeslib.as_array((ctypes.c_uint8 * a.nbytes).from_address(a.host))
+        bb = np.ctypeslib.as_array((ctypes.c_uint8 * b.nbytes).from_address(b.host))
+        for sid, meta in a.tensors.items():   # every tensor's bytes (alignment padding aside)
+            for tname, (off, rb, _) in meta.items():
+                o = a.shard_off[sid] + off
+                n = hw.layout.blobs[sid].tensors[tname].rows * rb
+                assert np.array_equal(ba[o:o + n], bb[o:o + n]), (name, tname)
+        a.close()
+        b.close()
+        hw.close()

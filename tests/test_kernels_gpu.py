@@ -622,3 +622,53 @@ def test_moe_decode_experts_coded_bit_identical(E, k, d, eff):
              down_off, eff, d, gu_rb, d_rb, h.data_ptr(), w.data_ptr(), yb.data_ptr(), s)
     torch.cuda.synchronize()
     assert torch.equal(ya, yb)
+
+
+@pytest.mark.parametrize("N,K", [(300, 4096), (64, 14336), (1000, 256), (5, 2048)])
+def test_gpu_encoder_byte_identical(N, K):
+    """ps_wencode_stats + ps_wencode_rows (csrc/wencode.cu) produce exactly the bytes of
+    wcomp.encode (the numpy reference): per-row bases, the best-covering window of a row
+    with an outlier (recheck path), escapes in ascending column order, 0xFF padding, and
+    the same escape counts; also through GpuEncoder's chunked H2D / D2H path."""
+    from paper_2604_26334_b200.runtime import wcomp
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K)
+    W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.03
+    W[0, :7] = 0.0
+    W[1, 3] = 1e-30
+    W[2, 11] = 3.0e4                      # one outlier far above the bulk: recheck picks the bulk's window
+    W[3] *= 2.0 ** 20
+    W[4, 5:45] = 1e-12                    # 40 escapes below the window
+    W[N - 1, K - 1] = -1e-38
+    W[min(N - 1, 5), :20] *= 2.0 ** -30   # 20 weights far below the window
+    bits = W.view(torch.int16).cpu().numpy().view(np.uint16)
+    want = wcomp.encode(bits, max_escapes=1 << 20)
+    assert want is not None
+    coded, tb = want
+    base = torch.empty(N, dtype=torch.int32, device="cuda")
+    count = torch.empty(N, dtype=torch.int32, device="cuda")
+    s = stream()
+    lib.call("ps_wencode_stats", W.data_ptr(), N, K, K, base.data_ptr(), count.data_ptr(), s)
+    torch.cuda.synchronize()
+    exp = ((bits >> 7) & 0xFF).astype(np.uint8)
+    assert np.array_equal(base.cpu().numpy(), wcomp.row_bases(exp).astype(np.int32))
+    top = int(count.max().item())
+    assert wcomp.trailer_bytes(top) == tb
+    out = torch.full((N, coded.shape[1]), 0x5A, dtype=torch.uint8, device="cuda")
+    lib.call("ps_wencode_rows", W.data_ptr(), N, K, K, base.data_ptr(), tb, out.data_ptr(), coded.shape[1], s)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), coded)
+    if top <= wcomp.MAX_ESCAPES:   # GpuEncoder: chunked through pinned host memory
+        host_src = lib.host_alloc(bits.nbytes, mapped=False)
+        host_dst = lib.host_alloc(coded.nbytes, mapped=False)
+        try:
+            C.memmove(host_src, bits.ctypes.data, bits.nbytes)
+            enc = wcomp.GpuEncoder(chunk_bytes=max(2 * K, (N // 3) * 2 * K))
+            assert enc.max_escapes(host_src, N, K) == top
+            enc.encode_to(host_src, N, K, tb, host_dst)
+            enc.close()
+            got = np.ctypeslib.as_array((C.c_uint8 * coded.nbytes).from_address(host_dst)).reshape(coded.shape)
+            assert np.array_equal(got, coded)
+        finally:
+            lib.host_free(host_src)
+            lib.host_free(host_dst)
