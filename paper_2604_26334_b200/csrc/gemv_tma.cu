@@ -33,15 +33,15 @@ namespace ps {
 constexpr int GT_STAGES = 5;
 constexpr int GT_STAGE_BYTES = 32768;
 #ifndef PS_GT_CONSUMERS_LO
-#define PS_GT_CONSUMERS_LO 16
+#define PS_GT_CONSUMERS_LO 8
 #endif
 #ifndef PS_GT_CONSUMERS_HI
 #define PS_GT_CONSUMERS_HI 8
 #endif
 // Consumer warps per token count, the same for bf16 and coded rows (identical
-// decomposition = bit-identical outputs): 16 at t <= 4 — the coded decode is a dependent
-// ALU chain, and 2 warps per scheduler left it latency-bound (ncu r02: "wait" stalls 1.0
-// per issue, 2.2 active warps per scheduler) — and 8 at t = 8 (16 regressed there).
+// decomposition = bit-identical outputs). 8: an A/B with 16 at t <= 4 (tools/
+// bench_gemv_nc.py, r02) gained the coded kernel 3 % on the 235 MB matrix and cost the
+// bf16 kernel 5-12 % on 25-64 MB pieces; 16 regressed t = 8 outright.
 constexpr int gt_consumers(int T) { return T <= 4 ? PS_GT_CONSUMERS_LO : PS_GT_CONSUMERS_HI; }
 constexpr int gt_threads(int T) { return 32 * (1 + gt_consumers(T)); }  // + producer warp
 
@@ -64,6 +64,22 @@ template <int T, bool COMP = false> struct GtShape {
   // warp_reduce_scatter halves V each step: a non-power-of-two V would drop values
   static_assert(RS >= 1 && (V & (V - 1)) == 0, "rows x tokens per stage must be a power of two");
 };
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
 
 // 8 bf16 weights x 8 fp32 activations, packed fp32x2 FMA (two partial sums).
 __device__ __forceinline__ float2 dot8x2(uint4 w, const float2* x, float2 s) {
@@ -177,6 +193,10 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
   const bool writer = V >= 32 || (lane & ((32 / V) - 1)) == 0;
   int it = 0, s = 0;
   uint32_t ph = 0;
+  const uint32_t ring_s = smem_u32(ring);
+  int colb[CPT / 8];   // this thread's 8-column groups within a chunk
+#pragma unroll
+  for (int h = 0; h < CPT / 8; ++h) colb[h] = (h * GT_CONSUMERS * 32 + j) * 8;
   for (int c = 0; c < nchunks; ++c) {
     const int kc = min(KC, K - c * KC);
     float2 xr[T][CPT / 2];
@@ -202,6 +222,44 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
       mbar_wait(&full[s], ph);
       const uint8_t* stage = ring + s * GT_STAGE_BYTES;
       float v[V];
+      if (nr == RS && kc == KC) {
+        // full block (all but a CTA's last one): no bounds tests, shared loads by 32-bit
+        // address; the same values and accumulation order as the general path below
+        const uint32_t sa = ring_s + s * GT_STAGE_BYTES;
+#pragma unroll
+        for (int r = 0; r < RS; ++r) {
+          uint4 w[CPT / 8];
+          if constexpr (COMP) {
+            const uint32_t ra = sa + r * ROWB;
+            const uint32_t hdr = lds_u32(ra + KC * 3 / 2);       // base | n_escapes << 8
+            const uint32_t base7 = ((hdr & 0xFFu) * 0x10001u) << 7;
+            uint2 sm[CPT / 8];
+            uint32_t nb[CPT / 8];
+#pragma unroll
+            for (int h = 0; h < CPT / 8; ++h) {
+              sm[h] = lds_v2(ra + colb[h]);
+              nb[h] = lds_u32(ra + KC + colb[h] / 2);
+              w[h] = gt_decode8(sm[h], nb[h], base7);
+            }
+            if (hdr >> 8) {   // the row has escapes (warp-uniform): patch the groups holding one
+              const uint32_t* trailer = reinterpret_cast<const uint32_t*>(stage + r * ROWB + KC * 3 / 2);
+#pragma unroll
+              for (int h = 0; h < CPT / 8; ++h)
+                if (gt_escapes(nb[h])) w[h] = gt_patch_escapes(w[h], sm[h], nb[h], trailer, c * KC + colb[h]);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < CPT / 8; ++h) w[h] = lds_v4(sa + r * KC * 2 + colb[h] * 2);
+          }
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int h = 0; h < CPT / 8; ++h) p = dot8x2(w[h], &xr[t][h * 4], p);
+            v[r * T + t] = p.x + p.y;
+          }
+        }
+      } else {
 #pragma unroll
       for (int r = 0; r < RS; ++r) {
         uint4 w[CPT / 8];
@@ -242,6 +300,7 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
           for (int h = 0; h < CPT / 8; ++h) p = dot8x2(w[h], &xr[t][h * 4], p);
           v[r * T + t] = p.x + p.y;
         }
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading the stage

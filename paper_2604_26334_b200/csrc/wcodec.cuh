@@ -9,10 +9,9 @@
 namespace ps {
 
 // 8 coded weights -> 8 bf16 (uint4). sm: their sign|mantissa bytes, nb: their eight
-// 4-bit codes, base7 = (base | base << 16) << 7 of the row. Two weights per 32-bit
-// word: one PRMT spreads the two sm bytes to the halves, one PRMT the two codes, one
-// IMAD adds the base and shifts, one LOP3-class merge. A code of 15 (escape) sends the
-// group to gt_patch_escapes, which reads the exponent from the row's trailer.
+// 4-bit codes, base7 = (base | base << 16) << 7 of the row (gt_pair below). A code of 15
+// (escape) sends the group to gt_patch_escapes, which reads the exponent from the row's
+// trailer.
 static __device__ __noinline__ uint4 gt_patch_escapes(uint4 v, uint2 sm, uint32_t nb, const uint32_t* __restrict__ trailer,
                                                int col) {
   const uint32_t n = trailer[0] >> 8;
@@ -43,12 +42,16 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+// Two weights per 32-bit word, four instructions: one sign-replicating PRMT lays the two
+// sm bytes out as [b0, sign(b0) x 8, b1, sign(b1) x 8] (so & 0x807F keeps sign << 15 |
+// mantissa per half), one PRMT spreads the two codes, one IMAD adds the base and shifts,
+// one LOP3 merges: (bb & 0x807F807F) | e7.
 __device__ __forceinline__ uint32_t gt_pair(uint32_t smw, uint32_t sm_sel, uint32_t lo, uint32_t hi, uint32_t e_sel,
                                             uint32_t base7) {
-  const uint32_t bb = prmt(smw, 0u, sm_sel);                  // [b0, 0, b1, 0]
+  const uint32_t bb = prmt(smw, 0u, sm_sel);                  // [b0, s0, b1, s1]
   const uint32_t ep = prmt(lo, hi, e_sel);                    // [code0, 0, code1, 0]
   const uint32_t e7 = ep * 128u + base7;                       // (code + base) << 7, per half
-  return (bb & 0x007F007Fu) | ((bb << 8) & 0x80008000u) | e7;
+  return (bb & 0x807F807Fu) | e7;
 }
 
 // Fast path only: escapes (code 15) come out wrong and are patched by the caller once
@@ -56,10 +59,10 @@ __device__ __forceinline__ uint32_t gt_pair(uint32_t smw, uint32_t sm_sel, uint3
 __device__ __forceinline__ uint4 gt_decode8(uint2 sm, uint32_t nb, uint32_t base7) {
   const uint32_t lo = nb & 0x0F0F0F0Fu, hi = (nb >> 4) & 0x0F0F0F0Fu;   // codes 0,2,4,6 | 1,3,5,7
   uint4 v;
-  v.x = gt_pair(sm.x, 0x4140u, lo, hi, 0x8480u, base7);
-  v.y = gt_pair(sm.x, 0x4342u, lo, hi, 0x9591u, base7);
-  v.z = gt_pair(sm.y, 0x4140u, lo, hi, 0xA6A2u, base7);
-  v.w = gt_pair(sm.y, 0x4342u, lo, hi, 0xB7B3u, base7);
+  v.x = gt_pair(sm.x, 0x9180u, lo, hi, 0x8480u, base7);
+  v.y = gt_pair(sm.x, 0xB3A2u, lo, hi, 0x9591u, base7);
+  v.z = gt_pair(sm.y, 0x9180u, lo, hi, 0xA6A2u, base7);
+  v.w = gt_pair(sm.y, 0xB3A2u, lo, hi, 0xB7B3u, base7);
   return v;
 }
 

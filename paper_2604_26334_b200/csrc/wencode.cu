@@ -11,10 +11,9 @@
 //   ps_wencode_rows:  sign|mantissa bytes, 4-bit codes (low nibble = even column), and the
 //                     trailer [base | n << 8, (col << 8 | exp) ascending, 0xFFFFFFFF ...]
 //
-// One CTA of 256 threads per row; thread i owns the contiguous columns
-// [i * K / 256, (i + 1) * K / 256), so an exclusive scan of per-thread escape counts
-// places every escape at its ascending-column slot. Bound: HBM (K*2 in, K*1.5 + trailer
-// out per row), far from the host link that feeds it.
+// One CTA per row; thread i of n owns the contiguous columns [i * K / n, (i + 1) * K / n),
+// so a scan of per-thread escape counts places every escape at its ascending-column
+// slot. Bound: HBM (K*2 in, K*1.5 + trailer out per row), far from the host link.
 #include "common.cuh"
 #include "../../include/pshard.h"
 
@@ -90,14 +89,17 @@ wencode_stats_kernel(const uint16_t* __restrict__ bits, int K, long long ld, int
   }
 }
 
+// blockDim.x threads (256, or 128 when K / 256 is odd) so each thread owns an even number
+// of columns: a code byte (two nibbles) never straddles two threads
 __global__ void __launch_bounds__(WE_THREADS)
 wencode_rows_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const int* __restrict__ base_in,
                     int tb, uint8_t* __restrict__ out, long long ld_out) {
   __shared__ int scan[WE_THREADS];
+  const int nt = blockDim.x;
   const uint16_t* row = bits + blockIdx.x * ld;
   uint8_t* o = out + blockIdx.x * ld_out;
   const int base = base_in[blockIdx.x];
-  const int per = K / WE_THREADS;          // K % 256 == 0: even, so code pairs stay in a thread
+  const int per = K / nt;
   const int c0 = threadIdx.x * per;
   int mine = 0;
   for (int c = c0; c < c0 + per; c += 2) {
@@ -109,16 +111,16 @@ wencode_rows_kernel(const uint16_t* __restrict__ bits, int K, long long ld, cons
     o[c + 1] = (uint8_t)(((b >> 8) & 0x80) | (b & 0x7F));
     o[K + c / 2] = (uint8_t)((xa ? 15 : ea) | ((xb ? 15 : eb) << 4));
   }
-  // exclusive scan of the escape counts in thread (= column) order
+  // inclusive scan of the escape counts in thread (= column) order
   scan[threadIdx.x] = mine;
   __syncthreads();
-  for (int off = 1; off < WE_THREADS; off <<= 1) {
+  for (int off = 1; off < nt; off <<= 1) {
     const int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
     __syncthreads();
     scan[threadIdx.x] += v;
     __syncthreads();
   }
-  const int total = scan[WE_THREADS - 1];
+  const int total = scan[nt - 1];
   int slot = 1 + scan[threadIdx.x] - mine;
   uint32_t* tr = reinterpret_cast<uint32_t*>(o + (long long)K * 3 / 2);
   if (mine) {
@@ -127,7 +129,7 @@ wencode_rows_kernel(const uint16_t* __restrict__ bits, int K, long long ld, cons
       if (e - base < 0 || e - base > 14) tr[slot++] = ((uint32_t)c << 8) | (uint32_t)e;
     }
   }
-  for (int w = 1 + total + threadIdx.x; w < tb / 4; w += WE_THREADS) tr[w] = 0xFFFFFFFFu;
+  for (int w = 1 + total + threadIdx.x; w < tb / 4; w += nt) tr[w] = 0xFFFFFFFFu;
   if (threadIdx.x == 0) tr[0] = (uint32_t)base | ((uint32_t)total << 8);
 }
 
@@ -151,7 +153,8 @@ extern "C" int ps_wencode_rows(const void* bits, int N, int K, long long ld, con
   PS_REQUIRE(trailer_bytes >= 16 && trailer_bytes % 16 == 0 && ld_out >= (long long)K * 3 / 2 + trailer_bytes,
              "ps_wencode_rows: trailer %d, ld_out %lld", trailer_bytes, ld_out);
   if (N <= 0) return PS_OK;
-  wencode_rows_kernel<<<N, WE_THREADS, 0, (cudaStream_t)stream>>>(static_cast<const uint16_t*>(bits), K, ld, base,
+  const int nt = (K / 256) % 2 == 0 ? WE_THREADS : WE_THREADS / 2;
+  wencode_rows_kernel<<<N, nt, 0, (cudaStream_t)stream>>>(static_cast<const uint16_t*>(bits), K, ld, base,
                                                                   trailer_bytes, static_cast<uint8_t*>(out), ld_out);
   PS_CHECK_LAUNCH();
   return PS_OK;

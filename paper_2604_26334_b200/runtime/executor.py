@@ -439,7 +439,9 @@ class Executor:
         low = sum(up(self._phys_bytes(self.shards[sid])) for sid in out)
         free = self.arena.capacity - high - low
         n_slots, slot = self._slot_bytes(T, modes, free)
-        kv_streams = any(m == "stream" and self.shards[sid].kind is ShardKind.KV_CACHE
+        # a GEMM pass stages zero-copy KV through the ring too
+        kv_staged = ("stream", "zerocopy") if T > GEMV_MAX_T else ("stream",)
+        kv_streams = any(m in kv_staged and self.shards[sid].kind is ShardKind.KV_CACHE
                          for sid, m in modes.items())
         keep = self.ring_keep_pieces if T > GEMV_MAX_T else self.ring_keep_pieces_decode
         ring_keep = min(self.ring_cap, keep * self.chunk_cap + (self.kv_layer_bytes if kv_streams else 0))
@@ -538,16 +540,17 @@ class Executor:
         self._carve_expert_slots(tier, modes)
         free = self.arena.free_bytes
         ring_bytes = max(0, min(self.ring_cap, free)) // 256 * 256
-        self.chunk = min(self.chunk_cap, max(1 << 16, ring_bytes // 6 // 256 * 256))
-        need = self.kv_layer_bytes + 3 * self.chunk
-        streams = any(m == "stream" for m, _ in self.residency.values()) or \
-            any(m == "stream" for m in self.kv_mode.values())
+        gemm = self.T_tier > GEMV_MAX_T   # GEMM passes cannot read host memory: staging is required
+        staged = ("stream", "zerocopy") if gemm else ("stream",)
+        kv_win = self.kv_layer_bytes if any(m in staged for m in self.kv_mode.values()) else 0
+        # pieces of <= 1/6 of what the KV window leaves, so three always fit beside it
+        self.chunk = min(self.chunk_cap, max(1 << 16, (ring_bytes - kv_win) // 6 // 256 * 256))
+        need = kv_win + 3 * self.chunk
+        streams = kv_win > 0 or any(m in staged for m, _ in self.residency.values())
         # passes of 9..32 tokens stage CPU-placed shards through the ring (one pass over
         # them); a budget whose ring cannot hold that keeps reading them zero-copy
         self.stage_zc = self.T_tier > GEMV_CORE_MAX_T and ring_bytes >= need and \
             any(m == "zerocopy" for m, _ in self.residency.values())
-        if self.T_tier > GEMV_MAX_T:   # GEMM passes cannot read host memory: staging is required
-            streams = streams or any(m == "zerocopy" for m, _ in self.residency.values())
         if streams and ring_bytes < need:
             raise InfeasibleBudget(float(self.arena.capacity),
                                    float(self.arena.capacity - free + need), "copy-engine ring")
@@ -757,13 +760,17 @@ class Executor:
                 ci += 1
 
         if mode in ("pinned", "zerocopy"):
-            base = dev if mode == "pinned" else self.w.shard_ptr(sid)
             zc_coded = (mode == "zerocopy" and self.coded is not None and sid in self.coded.tensors and
                         getattr(self.coded, "mapped", False) and
                         (self.coded_only or os.environ.get("PS_CODED_ZEROCOPY", "1") != "0"))
             res_coded = mode == "pinned" and self.coded_resident(sid)
-            if zc_coded:   # the bulk-copy GEMV reads the coded rows straight from host memory
+            if mode == "pinned":
+                base = dev
+            elif zc_coded:   # the bulk-copy GEMV reads the coded rows straight from host memory
                 base = self.coded.shard_ptr(sid)
+            else:
+                base = self.w.shard_ptr(sid)
+            if zc_coded:
                 self._stat.zero_copy_bytes += self.coded.shard_bytes[sid]
             elif mode == "zerocopy":
                 self._stat.zero_copy_bytes += blob.nbytes
@@ -806,7 +813,8 @@ class Executor:
             return
 
         coded = (self.coded is not None and sid in self.coded.tensors and self.striper is None and
-                 sid not in self._piece_override and (T <= GEMV_MAX_T or bool(self.expand)))
+                 sid not in self._piece_override and
+                 (T <= GEMV_MAX_T or (bool(self.expand) and self._coded_prefill())))
         expand = coded and T > GEMV_MAX_T   # GEMM pass: coded piece -> bf16 in VRAM -> tcgen05 GEMM
         evens = {c.tensor for c in consumers if c.even_rows}
         if coded:

@@ -182,7 +182,7 @@ class CodedShards:
                 continue
             for suffix in ("wgu", "wdown"):
                 names = [n for n in blob.tensors if n.endswith("." + suffix) and ".e" in n]
-                tbs = [trailers[(sid, n)] for n in names]
+                tbs = [trailers.get((sid, n)) for n in names]   # absent: not codable (K % 256)
                 top = None if any(tb is None for tb in tbs) else max(tbs)
                 for n in names:
                     trailers[(sid, n)] = top

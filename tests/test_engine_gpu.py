@@ -632,6 +632,7 @@ def test_coded_prefill_same_tokens_fewer_bytes(monkeypatch, frac):
     spec = catalog.builtin_model("tiny-llama")
     prompt = _prompt(128, spec.vocab_size, seed=33)
     out = {}
+    monkeypatch.setenv("PS_CODED_RESIDENT", "0")   # keep the prefill streaming (coded residency pins more)
     for cp in ("0", "1"):
         monkeypatch.setenv("PS_CODED_PREFILL", cp)
         eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, chunk_bytes=1 << 20)
