@@ -162,6 +162,23 @@ int ps_wencode_stats(const void* bits, int N, int K, long long ld, int* base_out
 int ps_wencode_rows(const void* bits, int N, int K, long long ld, const int* base, int trailer_bytes, void* out,
                     long long ld_out, void* stream);
 
+/* Huffman-coded exponents ("hx", csrc/hx.cu, format in runtime/hxcodec.py): ~10.1 bits
+ * per bf16 weight, lossless. ps_hx_expand decodes `rows` rows (whole 64-row blocks;
+ * block_off[b] = byte offset of block b from `piece`, device memory) to bf16 rows of
+ * ld_out elements, with the matrix's 4096-entry lookup table (uint16 symbol | length << 8).
+ * Encoder passes: ps_hx_stats (row max exponent + histogram of rowmax - exponent),
+ * ps_hx_sizes (bits per 256-weight sub-block, bytes per row, given the code table
+ * uint32 length << 16 | bit-reversed code), ps_hx_write (the coded rows at row_off into a
+ * zeroed buffer). No reference counterpart: the link format is this build's. */
+int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, const void* lut, void* out,
+                 long long ld_out, void* stream);
+int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist, void* stream);
+int ps_hx_sizes(const void* bits, int N, int K, long long ld, const int* rowmax, const unsigned* table,
+                unsigned short* sublen, unsigned* rowbytes, void* stream);
+int ps_hx_write(const void* bits, int N, int K, long long ld, const int* rowmax, const unsigned* table,
+                const unsigned short* sublen, const unsigned* rowbytes, const unsigned long long* row_off, void* out,
+                void* stream);
+
 /* Decode GEMV for 9..32 tokens on the tcgen05 tensor cores (gemv_tc.cu): y[t, n] (epi)=
  * x[t, :] . W[n, :] reading W ONCE (the CUDA-core GEMV takes 8 tokens per launch). W is
  * bf16 [N x K] (row stride ldw elements) or, with coded = 1, exponent-coded rows of ldw

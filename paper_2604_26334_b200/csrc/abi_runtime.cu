@@ -65,6 +65,7 @@ int ps_preload_moe_decode();
 extern "C" int ps_preload_fetcher();
 int ps_preload_striper();
 int ps_preload_attention_tc();
+int ps_preload_hx();
 
 namespace ps {
 int g_pdl = 0;
@@ -116,7 +117,7 @@ int ps_preload_kernels(int* n_loaded) {
   if (loaded < 0)
     loaded = ps_preload_gemv() + ps_preload_gemv_tma() + ps_preload_gemv_tc() + ps_preload_gemm() + ps_preload_attention() +
              ps_preload_elementwise() + ps_preload_moe() + ps_preload_moe_decode() + ps_preload_fetcher() + ps_preload_striper() +
-             ps_preload_attention_tc();
+             ps_preload_attention_tc() + ps_preload_hx();
   if (n_loaded) *n_loaded = loaded;
   return PS_OK;
 }

@@ -222,7 +222,8 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
       mbar_wait(&full[s], ph);
       const uint8_t* stage = ring + s * GT_STAGE_BYTES;
       float v[V];
-      if (nr == RS && kc == KC) {
+      // (coded rows at 64 values per stage: the second copy of the loop spills; general path)
+      if (!(COMP && V > 32) && nr == RS && kc == KC) {
         // full block (all but a CTA's last one): no bounds tests, shared loads by 32-bit
         // address; the same values and accumulation order as the general path below
         const uint32_t sa = ring_s + s * GT_STAGE_BYTES;

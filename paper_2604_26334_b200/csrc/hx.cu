@@ -1,0 +1,240 @@
+// Huffman-coded exponents ("hx", runtime/hxcodec.py): ~10.1 bits per bf16 weight on the
+// host link and in VRAM, lossless. The decoder expands a run of 64-row blocks to bf16 in
+// VRAM ahead of the bf16 kernels (bulk-copy GEMV, one-pass tcgen05 GEMV, tcgen05 GEMM),
+// which therefore see exactly the bf16 weights: results are bit-identical to bf16.
+//
+//   ps_hx_expand  decode: CTA per 64-row block, one thread per 256-weight sub-block
+//                 (bit offset = prefix of the row header's sub-block lengths); a 4096-entry
+//                 table (symbol | length << 8) in shared memory turns the next 12 bits of
+//                 the LSB-first stream into a symbol; exponent = rowmax - symbol
+//   ps_hx_stats   encoder pass 1: row max exponent + histogram of d = rowmax - exponent
+//   ps_hx_sizes   encoder pass 2: bits per sub-block, bytes per row (host: Huffman code,
+//                 row and block offsets)
+//   ps_hx_write   encoder pass 3: block headers, row headers, sign|mantissa bytes, the
+//                 bit streams (atomicOr into a zeroed buffer: sub-blocks share words)
+//
+// Bound: link bytes. The expand kernel runs at HBM-class speed (it writes 2 bytes per
+// weight and reads ~1.26), microseconds per piece against the milliseconds a piece takes
+// to cross PCIe; prefill passes run it ahead of the GEMM on every piece.
+#include "common.cuh"
+#include "../../include/pshard.h"
+
+namespace ps {
+
+constexpr int HX_SUB = 256, HX_BLOCK_ROWS = 64, HX_LUT = 4096, HX_THREADS = 256;
+
+__device__ __forceinline__ int hx_header_bytes(int K) { return ((4 + 2 * (K / HX_SUB)) + 15) / 16 * 16; }
+
+// expand: blocks [blockIdx.x] of a piece; blk[b] = byte offset of block b from `piece`
+__global__ void __launch_bounds__(HX_THREADS)
+hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
+                 const uint16_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
+  __shared__ uint16_t lut[HX_LUT];
+  __shared__ uint32_t row_start[HX_BLOCK_ROWS];
+  extern __shared__ uint32_t sub_off[];   // [64][K / 256] bit offsets
+  const int nsub = K / HX_SUB;
+  const int hb = hx_header_bytes(K);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(lut_g);
+    uint4* dst = reinterpret_cast<uint4*>(lut);
+    for (int i = threadIdx.x; i < HX_LUT / 8; i += HX_THREADS) dst[i] = src[i];
+  }
+  const uint8_t* block = piece + blk[blockIdx.x];
+  const int r0 = blockIdx.x * HX_BLOCK_ROWS;
+  const int nr = min(HX_BLOCK_ROWS, rows - r0);
+  if (threadIdx.x < 32) {   // row starts: exclusive scan of the 64 row sizes (one warp)
+    const uint32_t* sizes = reinterpret_cast<const uint32_t*>(block);
+    uint32_t a = threadIdx.x < nr ? sizes[threadIdx.x] : 0u;
+    uint32_t b = threadIdx.x + 32 < nr ? sizes[threadIdx.x + 32] : 0u;
+    uint32_t sa = a, sb = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ua = __shfl_up_sync(0xffffffffu, sa, o), ub = __shfl_up_sync(0xffffffffu, sb, o);
+      if ((int)threadIdx.x >= o) { sa += ua; sb += ub; }
+    }
+    const uint32_t tot_a = __shfl_sync(0xffffffffu, sa, 31);
+    row_start[threadIdx.x] = 256 + sa - a;
+    row_start[threadIdx.x + 32] = 256 + tot_a + sb - b;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nr; r += HX_THREADS) {   // sub-block bit offsets per row
+    const uint16_t* hdr = reinterpret_cast<const uint16_t*>(block + row_start[r]);
+    uint32_t acc = 0;
+    for (int s = 0; s < nsub; ++s) {
+      sub_off[r * nsub + s] = acc;
+      acc += hdr[2 + s];
+    }
+  }
+  __syncthreads();
+  for (int task = threadIdx.x; task < nr * nsub; task += HX_THREADS) {
+    const int r = task / nsub, s = task - (task / nsub) * nsub;
+    const uint8_t* row = block + row_start[r];
+    const uint32_t rowmax = reinterpret_cast<const uint16_t*>(row)[0];
+    const uint8_t* sm = row + hb + s * HX_SUB;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(row + hb + K);
+    uint32_t pos = sub_off[r * nsub + s];
+    uint4* o = reinterpret_cast<uint4*>(out + (long long)(r0 + r) * ld_out + s * HX_SUB);
+    for (int c = 0; c < HX_SUB; c += 16) {
+      const uint4 m = *reinterpret_cast<const uint4*>(sm + c);   // 16 sign|mantissa bytes
+      const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t idx = pos >> 5;
+        const uint32_t peek = __funnelshift_r(sw[idx], sw[idx + 1], pos & 31) & (HX_LUT - 1);
+        const uint32_t e = lut[peek];
+        pos += e >> 8;
+        const uint32_t b = (mw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+        const uint32_t h = ((b & 0x80u) << 8) | (((rowmax - (e & 0xFFu)) & 0xFFu) << 7) | (b & 0x7Fu);
+        if (i & 1) w[i >> 1] |= h << 16; else w[i >> 1] = h;
+      }
+      o[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+      o[c / 8 + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
+}
+
+__device__ __forceinline__ int hx_exp(uint16_t b) { return (b >> 7) & 0xFF; }
+
+__global__ void __launch_bounds__(HX_THREADS)
+hx_stats_kernel(const uint16_t* __restrict__ bits, int K, long long ld, int* __restrict__ rowmax,
+                unsigned long long* __restrict__ hist) {
+  __shared__ int red[HX_THREADS / 32];
+  __shared__ unsigned int h[256];
+  const uint16_t* row = bits + blockIdx.x * ld;
+  h[threadIdx.x] = 0;
+  int mx = 0;
+  for (int c = threadIdx.x; c < K; c += HX_THREADS) mx = max(mx, hx_exp(row[c]));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0;
+  for (int i = 0; i < HX_THREADS / 32; ++i) mx = max(mx, red[i]);
+  for (int c = threadIdx.x; c < K; c += HX_THREADS) atomicAdd(&h[mx - hx_exp(row[c])], 1u);
+  __syncthreads();
+  if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+  if (threadIdx.x == 0) rowmax[blockIdx.x] = mx;
+}
+
+__global__ void __launch_bounds__(HX_THREADS)
+hx_sizes_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const int* __restrict__ rowmax,
+                const uint32_t* __restrict__ table, uint16_t* __restrict__ sublen, uint32_t* __restrict__ rowbytes) {
+  __shared__ uint32_t tot;
+  const uint16_t* row = bits + blockIdx.x * ld;
+  const int nsub = K / HX_SUB, mx = rowmax[blockIdx.x];
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  for (int s = threadIdx.x; s < nsub; s += HX_THREADS) {
+    uint32_t n = 0;
+    for (int c = s * HX_SUB; c < (s + 1) * HX_SUB; ++c) n += table[mx - hx_exp(row[c])] >> 16;
+    sublen[(long long)blockIdx.x * nsub + s] = (uint16_t)n;
+    atomicAdd(&tot, n);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t stream = ((tot + 7) / 8 + 8 + 15) / 16 * 16;   // >= 8 spare bytes: the decoder reads a word ahead
+    rowbytes[blockIdx.x] = (uint32_t)hx_header_bytes(K) + (uint32_t)K + stream;
+  }
+}
+
+__global__ void __launch_bounds__(HX_THREADS)
+hx_write_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const int* __restrict__ rowmax,
+                const uint32_t* __restrict__ table, const uint16_t* __restrict__ sublen,
+                const uint32_t* __restrict__ rowbytes, const unsigned long long* __restrict__ row_off, int N,
+                uint8_t* __restrict__ out) {
+  const int r = blockIdx.x;
+  const uint16_t* row = bits + r * ld;
+  const int nsub = K / HX_SUB, mx = rowmax[r], hb = hx_header_bytes(K);
+  uint8_t* o = out + row_off[r];
+  if (r % HX_BLOCK_ROWS == 0) {   // the block header: 64 row sizes (0 past N)
+    uint32_t* bh = reinterpret_cast<uint32_t*>(o - 256);
+    for (int i = threadIdx.x; i < HX_BLOCK_ROWS; i += HX_THREADS) bh[i] = r + i < N ? rowbytes[r + i] : 0u;
+  }
+  uint16_t* hdr = reinterpret_cast<uint16_t*>(o);
+  for (int i = threadIdx.x; i < hb / 2; i += HX_THREADS)
+    hdr[i] = i == 0 ? (uint16_t)mx : (i >= 2 && i < 2 + nsub ? sublen[(long long)r * nsub + i - 2] : 0);
+  for (int c = threadIdx.x; c < K; c += HX_THREADS) {
+    const uint16_t b = row[c];
+    o[hb + c] = (uint8_t)(((b >> 8) & 0x80) | (b & 0x7F));
+  }
+  uint32_t* sw = reinterpret_cast<uint32_t*>(o + hb + K);
+  for (int s = threadIdx.x; s < nsub; s += HX_THREADS) {
+    uint32_t pos = 0;
+    for (int i = 0; i < s; ++i) pos += sublen[(long long)r * nsub + i];
+    for (int c = s * HX_SUB; c < (s + 1) * HX_SUB; ++c) {
+      const uint32_t t = table[mx - hx_exp(row[c])];
+      const uint32_t len = t >> 16, code = t & 0xFFFFu;
+      const uint32_t sh = pos & 31, idx = pos >> 5;
+      atomicOr(&sw[idx], code << sh);
+      if (sh + len > 32) atomicOr(&sw[idx + 1], code >> (32 - sh));
+      pos += len;
+    }
+  }
+}
+
+}  // namespace ps
+
+extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, const void* lut,
+                            void* out, long long ld_out, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K > 0 && K % HX_SUB == 0 && ld_out >= K && ld_out % 8 == 0, "ps_hx_expand: K %d, ld_out %lld", K,
+             ld_out);
+  PS_REQUIRE(((uintptr_t)piece & 15) == 0 && ((uintptr_t)out & 15) == 0 && ((uintptr_t)lut & 15) == 0,
+             "ps_hx_expand: piece, out and lut must be 16-byte aligned");
+  if (rows <= 0) return PS_OK;
+  const int nblocks = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
+  const size_t smem = (size_t)HX_BLOCK_ROWS * (K / HX_SUB) * 4;
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_set = smem;
+  }
+  hx_expand_kernel<<<nblocks, HX_THREADS, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint16_t*>(lut),
+      static_cast<__nv_bfloat16*>(out), ld_out);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+extern "C" int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist,
+                           void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K > 0 && ld >= K, "ps_hx_stats: K %d ld %lld", K, ld);
+  if (N <= 0) return PS_OK;
+  hx_stats_kernel<<<N, HX_THREADS, 0, (cudaStream_t)stream>>>(static_cast<const uint16_t*>(bits), K, ld, rowmax,
+                                                               hist);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+extern "C" int ps_hx_sizes(const void* bits, int N, int K, long long ld, const int* rowmax, const unsigned* table,
+                           unsigned short* sublen, unsigned* rowbytes, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K > 0 && K % HX_SUB == 0 && ld >= K, "ps_hx_sizes: K %d ld %lld", K, ld);
+  if (N <= 0) return PS_OK;
+  hx_sizes_kernel<<<N, HX_THREADS, 0, (cudaStream_t)stream>>>(static_cast<const uint16_t*>(bits), K, ld, rowmax,
+                                                               table, sublen, rowbytes);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+extern "C" int ps_hx_write(const void* bits, int N, int K, long long ld, const int* rowmax, const unsigned* table,
+                           const unsigned short* sublen, const unsigned* rowbytes, const unsigned long long* row_off,
+                           void* out, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K > 0 && K % HX_SUB == 0 && ld >= K, "ps_hx_write: K %d ld %lld", K, ld);
+  if (N <= 0) return PS_OK;
+  hx_write_kernel<<<N, HX_THREADS, 0, (cudaStream_t)stream>>>(static_cast<const uint16_t*>(bits), K, ld, rowmax,
+                                                               table, sublen, rowbytes, row_off, N,
+                                                               static_cast<uint8_t*>(out));
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+int ps_preload_hx() {
+  using namespace ps;
+  int n = 0;
+  touch_kernel(hx_expand_kernel, n);
+  return n;
+}

@@ -12,20 +12,20 @@ namespace ps {
 // 4-bit codes, base7 = (base | base << 16) << 7 of the row (gt_pair below). A code of 15
 // (escape) sends the group to gt_patch_escapes, which reads the exponent from the row's
 // trailer.
-static __device__ __noinline__ uint4 gt_patch_escapes(uint4 v, uint2 sm, uint32_t nb, const uint32_t* __restrict__ trailer,
-                                               int col) {
+static __device__ __forceinline__ uint4 gt_patch_escapes(uint4 v, uint2 sm, uint32_t nb,
+                                                         const uint32_t* __restrict__ trailer, int col) {
   const uint32_t n = trailer[0] >> 8;
   uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  const uint32_t smw[2] = {sm.x, sm.y};
-#pragma unroll 1
-  for (int i = 0; i < 8; ++i) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {   // unrolled: every index below is a constant (no local memory)
     if (((nb >> (4 * i)) & 0xFu) != 15u) continue;
     uint32_t e = 0;
+#pragma unroll 1
     for (uint32_t j = 1; j <= n; ++j) {
       const uint32_t ent = trailer[j];
       if ((int)(ent >> 8) == col + i) { e = ent & 0xFFu; break; }
     }
-    const uint32_t b = (smw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+    const uint32_t b = (((i < 4) ? sm.x : sm.y) >> (8 * (i & 3))) & 0xFFu;
     const uint32_t half = ((b & 0x80u) << 8) | (e << 7) | (b & 0x7Fu);
     const int sh = 16 * (i & 1);
     w[i >> 1] = (w[i >> 1] & ~(0xFFFFu << sh)) | (half << sh);

@@ -1,0 +1,183 @@
+"""Huffman-coded exponents ("hx"): ~10.1 bits per bf16 weight, lossless.
+
+The 12-bit format (runtime/wcomp.py) spends 4 bits on an exponent whose entropy over
+these weights is ~2 bits. hx codes it with a per-matrix canonical
+Huffman code instead, keeping the sign|mantissa byte raw:
+
+    symbol  d = rowmax_r - exponent      (rowmax_r = the row's largest exponent)
+    code    canonical Huffman over the matrix's histogram of d, lengths <= 12 bits,
+            packed LSB-first (bit-reversed codes), so a decoder peeks 12 bits and
+            looks the symbol up in a 4096-entry table
+
+Layout of one [N, K] matrix (K % 256 == 0), rows in blocks of 64:
+
+    block   64 x uint32 row byte sizes (rows past N: 0), then the block's rows
+    row     header: uint16 rowmax, uint16 0, uint16 bit length of each 256-weight
+            sub-block (K / 256 of them), padded to 16 bytes
+            K bytes sign << 7 | mantissa
+            the bit stream, padded (after >= 8 spare bytes) to 16 bytes
+
+Every 64-row block is self-contained: a ring piece is a run of whole blocks, and the
+decoder (`ps_hx_expand`, csrc/hx.cu) needs only the block offsets of its piece and
+the matrix's code table (256 x uint32: length << 16 | bit-reversed code). A sub-block
+decodes independently of its neighbours (its bit offset is a prefix sum of the
+header's lengths), so one thread decodes 256 weights.
+
+This module is the format's CPU reference (encoder + decoder, test sizes only); the
+GPU encoder (`ps_hx_stats` / `ps_hx_sizes` / `ps_hx_write`) must produce the same bytes.
+"""
+
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+MAX_LEN = 12
+SUB = 256                 # weights per independently decodable sub-block
+BLOCK_ROWS = 64
+
+
+def code_lengths(hist: np.ndarray, max_len: int = MAX_LEN) -> np.ndarray:
+    """Huffman code lengths (uint8 [256]) for a symbol histogram, limited to max_len
+    bits by package-merge; symbols with count 0 get length 0. A single used symbol gets
+    length 1. Deterministic: ties break on the symbol index."""
+    hist = np.asarray(hist, dtype=np.int64)
+    used = [int(s) for s in np.nonzero(hist)[0]]
+    lengths = np.zeros(256, np.uint8)
+    if not used:
+        return lengths
+    if len(used) == 1:
+        lengths[used[0]] = 1
+        return lengths
+    # package-merge (boundary-free form): max_len rounds of pairing
+    leaves = sorted((int(hist[s]), s) for s in used)
+    items = [(w, (s,)) for w, s in leaves]
+    cur = list(items)
+    for _ in range(max_len - 1):
+        pk = [(cur[i][0] + cur[i + 1][0], cur[i][1] + cur[i + 1][1]) for i in range(0, len(cur) - 1, 2)]
+        cur = sorted(items + pk, key=lambda t: (t[0], len(t[1]), t[1]))
+    take = cur[:2 * len(used) - 2]
+    for _, syms in take:
+        for s in syms:
+            lengths[s] += 1
+    return lengths
+
+
+def canonical_table(lengths: np.ndarray) -> np.ndarray:
+    """uint32 [256]: length << 16 | code bit-reversed (LSB-first), canonical order
+    (by length, then symbol); 0 for unused symbols."""
+    table = np.zeros(256, np.uint32)
+    order = sorted((int(lengths[s]), s) for s in range(256) if lengths[s])
+    code, prev = 0, 0
+    for ln, s in order:
+        code <<= (ln - prev)
+        prev = ln
+        rev = int(f"{code:0{ln}b}"[::-1], 2)
+        table[s] = (ln << 16) | rev
+        code += 1
+    return table
+
+
+def _exp(bits: np.ndarray) -> np.ndarray:
+    return ((bits >> 7) & 0xFF).astype(np.int32)
+
+
+def histogram(bits: np.ndarray) -> tuple:
+    """(rowmax int32 [N], histogram int64 [256] of d = rowmax - exponent)."""
+    e = _exp(bits)
+    rowmax = e.max(axis=1)
+    d = rowmax[:, None] - e
+    return rowmax, np.bincount(d.reshape(-1), minlength=256).astype(np.int64)
+
+
+def header_bytes(k: int) -> int:
+    return -(-(4 + 2 * (k // SUB)) // 16) * 16
+
+
+def row_bytes(k: int, nbits: int) -> int:
+    return header_bytes(k) + k + -(-(-(-nbits // 8) + 8) // 16) * 16
+
+
+def encode(bits: np.ndarray, table: np.ndarray | None = None):
+    """bf16 bits uint16 [N, K] -> (blob uint8, block offsets uint64 [nblocks + 1], table).
+    Pure Python bit packing: test sizes only."""
+    bits = np.ascontiguousarray(bits, dtype=np.uint16)
+    n, k = bits.shape
+    if k % SUB:
+        raise ValueError("K must be a multiple of 256")
+    rowmax, hist = histogram(bits)
+    if table is None:
+        table = canonical_table(code_lengths(hist))
+    e = _exp(bits)
+    d = rowmax[:, None] - e
+    lens = (table[d] >> 16).astype(np.int64)
+    codes = (table[d] & 0xFFFF).astype(np.int64)
+    sublen = lens.reshape(n, k // SUB, SUB).sum(axis=2)            # bits per sub-block
+    rbytes = [row_bytes(k, int(sublen[r].sum())) for r in range(n)]
+    nblocks = -(-n // BLOCK_ROWS)
+    offs = np.zeros(nblocks + 1, np.uint64)
+    for b in range(nblocks):
+        offs[b + 1] = offs[b] + 256 + sum(rbytes[b * BLOCK_ROWS:(b + 1) * BLOCK_ROWS])
+    blob = np.zeros(int(offs[-1]), np.uint8)
+    hb = header_bytes(k)
+    sm = (((bits >> 8) & 0x80) | (bits & 0x7F)).astype(np.uint8)
+    for b in range(nblocks):
+        r0, r1 = b * BLOCK_ROWS, min(n, (b + 1) * BLOCK_ROWS)
+        pos = int(offs[b])
+        blob[pos:pos + 4 * (r1 - r0)] = np.array(rbytes[r0:r1], np.uint32).view(np.uint8)
+        pos += 256
+        for r in range(r0, r1):
+            hdr = np.zeros(hb // 2, np.uint16)
+            hdr[0] = rowmax[r]
+            hdr[2:2 + k // SUB] = sublen[r]
+            blob[pos:pos + hb] = hdr.view(np.uint8)
+            blob[pos + hb:pos + hb + k] = sm[r]
+            acc, nacc, out = 0, 0, bytearray()
+            for c in range(k):
+                acc |= int(codes[r, c]) << nacc
+                nacc += int(lens[r, c])
+                while nacc >= 8:
+                    out.append(acc & 0xFF)
+                    acc >>= 8
+                    nacc -= 8
+            if nacc:
+                out.append(acc & 0xFF)
+            s0 = pos + hb + k
+            blob[s0:s0 + len(out)] = np.frombuffer(bytes(out), np.uint8)
+            pos += rbytes[r]
+    return blob, offs, table
+
+
+def decode(blob: np.ndarray, offs: np.ndarray, table: np.ndarray, n: int, k: int) -> np.ndarray:
+    """Inverse of `encode` (CPU reference of ps_hx_expand): uint16 bf16 bits [N, K]."""
+    lut = {}
+    for s in range(256):
+        if table[s]:
+            lut[(int(table[s]) >> 16, int(table[s]) & 0xFFFF)] = s
+    out = np.zeros((n, k), np.uint16)
+    hb = header_bytes(k)
+    for b in range(len(offs) - 1):
+        pos = int(offs[b])
+        r0, r1 = b * BLOCK_ROWS, min(n, (b + 1) * BLOCK_ROWS)
+        sizes = blob[pos:pos + 4 * (r1 - r0)].view(np.uint32)
+        pos += 256
+        for i, r in enumerate(range(r0, r1)):
+            hdr = blob[pos:pos + hb].view(np.uint16)
+            rowmax = int(hdr[0])
+            sm = blob[pos + hb:pos + hb + k].astype(np.uint16)
+            stream = blob[pos + hb + k:pos + int(sizes[i])]
+            bitpos = 0
+            for c in range(k):
+                code, ln = 0, 0
+                while (ln, code) not in lut:
+                    byte = int(stream[bitpos >> 3])
+                    code |= ((byte >> (bitpos & 7)) & 1) << ln
+                    ln += 1
+                    bitpos += 1
+                    if ln > MAX_LEN:
+                        raise ValueError("bad code")
+                e = rowmax - lut[(ln, code)]
+                out[r, c] = ((sm[c] & 0x80) << 8) | (e << 7) | (sm[c] & 0x7F)
+            pos += int(sizes[i])
+    return out
