@@ -29,8 +29,6 @@ GPU encoder (`ps_hx_stats` / `ps_hx_sizes` / `ps_hx_write`) must produce the sam
 
 from __future__ import annotations
 
-import heapq
-
 import numpy as np
 
 MAX_LEN = 12
@@ -181,3 +179,98 @@ def decode(blob: np.ndarray, offs: np.ndarray, table: np.ndarray, n: int, k: int
                 out[r, c] = ((sm[c] & 0x80) << 8) | (e << 7) | (sm[c] & 0x7F)
             pos += int(sizes[i])
     return out
+
+
+def lookup_table(table: np.ndarray) -> np.ndarray:
+    """The decoder's 4096-entry table (uint16: symbol | length << 8) for a code table:
+    every 12-bit LSB-first window whose low `length` bits are a symbol's reversed code."""
+    lut = np.zeros(1 << MAX_LEN, np.uint16)
+    for s in range(256):
+        t = int(table[s])
+        if not t:
+            continue
+        ln, rev = t >> 16, t & 0xFFFF
+        lut[rev | (np.arange(1 << (MAX_LEN - ln)) << ln)] = s | (ln << 8)
+    return lut
+
+
+class HxMatrix:
+    """One hx-coded matrix: its geometry, code table, decoder table, block offsets
+    (uint64 [nblocks + 1], bytes from the matrix start) and size."""
+
+    def __init__(self, n: int, k: int, table: np.ndarray, block_off: np.ndarray):
+        self.n, self.k, self.table = n, k, table
+        self.lut = lookup_table(table)
+        self.block_off = block_off
+        self.nbytes = int(block_off[-1])
+
+    def blocks_for_rows(self, r0: int, r1: int) -> tuple:
+        """(first block, end block) covering rows [r0, r1) (r0 on a block boundary)."""
+        return r0 // BLOCK_ROWS, -(-r1 // BLOCK_ROWS)
+
+
+class GpuHxEncoder:
+    """The hx encoder on the GPU (csrc/hx.cu: ps_hx_stats, ps_hx_sizes, ps_hx_write),
+    byte-identical to `encode`. A matrix is staged whole in device memory (model load,
+    before the capped arena exists); `src` is its pinned host address or a device
+    filler fill(dst_dev, r0, r1) (host_format='coded' generation)."""
+
+    def __init__(self):
+        import torch
+
+        from . import lib as L
+        self.L, self.torch = L, torch
+        self.stream = torch.cuda.current_stream().cuda_stream
+
+    def _stage(self, src, n: int, k: int):
+        t = self.torch.empty(n * k, dtype=self.torch.int16, device="cuda")
+        if callable(src):
+            step = max(1, (256 << 20) // (2 * k))
+            for r0 in range(0, n, step):
+                src(t.data_ptr() + r0 * k * 2, r0, min(n, r0 + step))
+        else:
+            self.L.memcpy_async(t.data_ptr(), src, n * k * 2, self.stream)
+        return t
+
+    def _sizes(self, bits, n: int, k: int, table: np.ndarray | None):
+        torch, L = self.torch, self.L
+        rowmax = torch.empty(n, dtype=torch.int32, device="cuda")
+        hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+        L.call("ps_hx_stats", bits.data_ptr(), n, k, k, rowmax.data_ptr(), hist.data_ptr(), self.stream)
+        if table is None:
+            table = canonical_table(code_lengths(hist.cpu().numpy()))
+        tab = torch.from_numpy(table.view(np.int32)).cuda()
+        sublen = torch.empty(n * (k // SUB), dtype=torch.int16, device="cuda")
+        rowbytes = torch.empty(n, dtype=torch.int32, device="cuda")
+        L.call("ps_hx_sizes", bits.data_ptr(), n, k, k, rowmax.data_ptr(), tab.data_ptr(), sublen.data_ptr(),
+               rowbytes.data_ptr(), self.stream)
+        return table, tab, rowmax, sublen, rowbytes
+
+    def plan(self, src, n: int, k: int) -> HxMatrix:
+        bits = self._stage(src, n, k)
+        table, _, _, _, rowbytes = self._sizes(bits, n, k, None)
+        rb = rowbytes.cpu().numpy().view(np.uint32).astype(np.uint64)
+        nb = -(-n // BLOCK_ROWS)
+        per_block = np.zeros(nb, np.uint64)
+        np.add.at(per_block, np.arange(n) // BLOCK_ROWS, rb)
+        block_off = np.zeros(nb + 1, np.uint64)
+        np.cumsum(per_block + 256, out=block_off[1:])
+        return HxMatrix(n, k, table, block_off)
+
+    def write(self, src, m: HxMatrix, dst_host: int) -> None:
+        """Encode the matrix again (same table) and copy its m.nbytes bytes to dst_host."""
+        torch, L = self.torch, self.L
+        n, k = m.n, m.k
+        bits = self._stage(src, n, k)
+        _, tab, rowmax, sublen, rowbytes = self._sizes(bits, n, k, m.table)
+        rb = rowbytes.cpu().numpy().view(np.uint32).astype(np.uint64)
+        row_off = np.empty(n, np.uint64)
+        for b in range(len(m.block_off) - 1):
+            r0, r1 = b * BLOCK_ROWS, min(n, (b + 1) * BLOCK_ROWS)
+            row_off[r0:r1] = m.block_off[b] + 256 + np.concatenate(([0], np.cumsum(rb[r0:r1 - 1])))
+        ro = torch.from_numpy(row_off.view(np.int64)).cuda()
+        out = torch.zeros(m.nbytes, dtype=torch.uint8, device="cuda")
+        L.call("ps_hx_write", bits.data_ptr(), n, k, k, rowmax.data_ptr(), tab.data_ptr(), sublen.data_ptr(),
+               rowbytes.data_ptr(), ro.data_ptr(), out.data_ptr(), self.stream)
+        L.memcpy_async(dst_host, out.data_ptr(), m.nbytes, self.stream)
+        L.call("ps_stream_synchronize", self.stream)

@@ -1,0 +1,49 @@
+"""CPU tests of the Huffman-exponent link format (runtime/hxcodec.py): the reference
+encoder/decoder round-trips bf16 bits exactly, code lengths respect the 12-bit limit
+and Kraft's inequality with equality, and the decoder table covers every window."""
+
+import numpy as np
+import pytest
+
+from paper_2604_26334_b200.runtime import hxcodec as hx
+
+
+def _bits(n, k, seed):
+    rng = np.random.default_rng(seed)
+    w = ((rng.random((n, k)) * 2 - 1) * np.sqrt(3 / k)).astype(np.float32)
+    w[0, :5] = 0.0
+    if n > 2:
+        w[1, 3] = 1e-30
+        w[2, 7] = 3e4
+    return (w.view(np.uint32) >> 16).astype(np.uint16)
+
+
+@pytest.mark.parametrize("n,k", [(1, 256), (3, 512), (70, 768), (130, 256)])
+def test_round_trip(n, k):
+    bits = _bits(n, k, n + k)
+    blob, offs, table = hx.encode(bits)
+    assert blob.nbytes == int(offs[-1]) and int(offs[0]) == 0
+    assert np.array_equal(hx.decode(blob, offs, table, n, k), bits)
+
+
+def test_code_lengths_limited_and_complete():
+    rng = np.random.default_rng(1)
+    for trial in range(30):
+        hist = np.zeros(256, np.int64)
+        m = int(rng.integers(2, 256))
+        hist[rng.choice(256, m, replace=False)] = (rng.pareto(0.5, m) * 10 + 1).astype(np.int64)
+        ln = hx.code_lengths(hist)
+        used = ln[hist > 0].astype(int)
+        assert (ln[hist == 0] == 0).all() and used.max() <= hx.MAX_LEN and used.min() >= 1
+        assert abs(sum(2.0 ** -used) - 1.0) < 1e-12
+        lut = hx.lookup_table(hx.canonical_table(ln))
+        assert (lut >> 8).min() >= 1          # every 12-bit window decodes to some symbol
+
+
+def test_geometric_exponents_cost_about_ten_bits():
+    """Uniform-init weights (exponents roughly geometric below the row max) code at ~10.4
+    bits per weight (the 12-bit format: 12.03)."""
+    bits = _bits(64, 4096, 5)
+    blob, _, _ = hx.encode(bits)
+    per = blob.nbytes * 8 / bits.size
+    assert 9.9 < per < 10.6, per

@@ -672,3 +672,48 @@ def test_gpu_encoder_byte_identical(N, K):
         finally:
             lib.host_free(host_src)
             lib.host_free(host_dst)
+
+
+@pytest.mark.parametrize("N,K", [(130, 768), (70, 512), (1, 256), (65, 1024)])
+def test_hx_encoder_and_expand_exact(N, K):
+    """Huffman-coded exponents (csrc/hx.cu): the GPU encoder (ps_hx_stats / sizes / write)
+    writes exactly the bytes of the CPU reference (runtime/hxcodec.encode), and
+    ps_hx_expand restores the bf16 bits exactly — whole matrix and a run of blocks
+    starting mid-matrix — zeros, denormals, an outlier row and 2^20-scaled rows included."""
+    from paper_2604_26334_b200.runtime import hxcodec as hx
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(N * 13 + K)
+    W = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) * 0.03
+    W[0, :7] = 0.0
+    if N > 3:
+        W[1, 3] = 1e-30
+        W[2, 11] = 3.0e4
+        W[3] *= 2.0 ** 20
+    bits = W.view(torch.int16).cpu().numpy().view(np.uint16)
+    blob, offs, table = hx.encode(bits)
+    enc = hx.GpuHxEncoder()
+    fill = lambda dst, r0, r1: lib.memcpy_async(dst, W.data_ptr() + r0 * K * 2, (r1 - r0) * K * 2,  # noqa: E731
+                                                stream())
+    m = enc.plan(fill, N, K)
+    assert np.array_equal(m.table, table) and np.array_equal(m.block_off, offs)
+    host = lib.host_alloc(m.nbytes, mapped=False)
+    try:
+        enc.write(fill, m, host)
+        got = np.ctypeslib.as_array((C.c_uint8 * m.nbytes).from_address(host)).copy()
+    finally:
+        lib.host_free(host)
+    assert np.array_equal(got, blob)
+    dev = torch.from_numpy(blob).cuda()
+    lut = torch.from_numpy(m.lut.view(np.int16)).cuda()
+    for b0 in (0, 1):
+        if b0 * hx.BLOCK_ROWS >= N:
+            continue
+        nb = len(offs) - 1 - b0
+        rel = torch.from_numpy((offs[b0:-1] - offs[b0]).astype(np.uint32).view(np.int32)).cuda()
+        rows = N - b0 * hx.BLOCK_ROWS
+        out = torch.full((rows, K), -1, dtype=torch.int16, device="cuda")
+        lib.call("ps_hx_expand", dev.data_ptr() + int(offs[b0]), rel.data_ptr(), rows, K, lut.data_ptr(),
+                 out.data_ptr(), K, stream())
+        torch.cuda.synchronize()
+        assert nb >= 1
+        assert np.array_equal(out.cpu().numpy().view(np.uint16), bits[b0 * hx.BLOCK_ROWS:]), b0
