@@ -185,6 +185,42 @@ class Engine:
             return "coded"
         return "bf16"
 
+    def _needs_coded12(self) -> bool:
+        """The 12-bit coded copy serves what hx does not: CPU-placed (zero-copy) shards and
+        routed experts. Built when some plan places a shard on the CPU backend, for MoE
+        models, or when hx is off (PS_HX=0)."""
+        from ..planning.vocab import Backend
+        if self.spec.moe is not None or os.environ.get("PS_HX", "1") == "0":
+            return True
+        return any(p.exec_backend is Backend.CPU for plan in self.plans.values() for p in plan.placements)
+
+    def _build_hx(self) -> None:
+        """hx copies (runtime/hxcodec.py, ~0.65 x the dense bytes, encoded on the GPU) of
+        the dense shards: decode passes and prefill passes stream them, resident shards
+        are held in that form. Node-shared with node-shared weights; skipped (bf16 /
+        12-bit streaming) when host memory is short."""
+        from .hxcodec import HxShards
+        kinds = (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD)
+        dense = sum(b.nbytes for b in self.weights.layout.blobs.values() if b.kind in kinds)
+        need = dense * 2 // 3
+        shared = None
+        meminfo = _meminfo()
+        if self.weights.shared is not None:
+            shared = os.path.basename(self.weights.shared.path) + "_hx"
+        elif meminfo.get("MemAvailable", 0) and need > 0.5 * meminfo["MemAvailable"]:
+            self.hx_skipped = "host memory: hx copy exceeds half of MemAvailable"
+            return
+        t0 = time.perf_counter()
+        try:
+            self.weights.hx = HxShards(self.weights, kinds, shared=shared)
+        except Exception as exc:   # e.g. pinned host memory exhausted
+            import warnings
+            warnings.warn(f"hx-coded weights unavailable ({exc}); streaming without them")
+            self.weights.hx = None
+            self.hx_skipped = repr(exc)[:200]
+            return
+        self.hx_seconds = time.perf_counter() - t0
+
     def _build_coded(self) -> None:
         """Exponent-coded copies of the dense shards (runtime/wcomp.py) that decode
         passes stream instead of bf16 (25 % fewer link bytes, bit-identical results),
@@ -222,8 +258,12 @@ class Engine:
     def _ensure_executor(self, max_tokens: int) -> Executor:
         if self.executor is None:
             tiers_used = self.plans
-            if (os.environ.get("PS_CODED", "1") == "1" and getattr(self.weights, "coded", None) is None):
+            if (os.environ.get("PS_CODED", "1") == "1" and getattr(self.weights, "coded", None) is None
+                    and self.weights.host_format == "bf16" and self._needs_coded12()):
                 self._build_coded()
+            if (os.environ.get("PS_CODED", "1") == "1" and os.environ.get("PS_HX", "1") != "0"
+                    and getattr(self.weights, "hx", None) is None and self.weights.host_format == "bf16"):
+                self._build_hx()
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,
                                      self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes,
@@ -478,4 +518,8 @@ class Engine:
         if coded is not None:
             coded.close()
             self.weights.coded = None
+        hx = getattr(self.weights, "hx", None)
+        if hx is not None:
+            hx.close()
+            self.weights.hx = None
         self.weights.close()

@@ -225,6 +225,14 @@ class Executor:
         self._coded_res_on = self.coded is not None and (self.coded_only or
                                                          os.environ.get("PS_CODED_RESIDENT", "1") != "0")
         self._coded_call = None
+        # Huffman-coded exponents (runtime/hxcodec.py, ~10.4 bits/weight): dense shards
+        # resident and streamed in hx form, expanded to bf16 piece by piece (PS_HX=0: off)
+        self.hx = getattr(weights, "hx", None)
+        self._hx_on = self.hx is not None and (self.coded_only or os.environ.get("PS_HX", "1") != "0")
+        if self._hx_on:
+            self.hx_lut = self.arena.alloc_high("hx_luts", self.hx.luts.nbytes)
+            self._h2d_sync(self.hx_lut, self.hx.luts)
+            self.hx_meta = self.arena.alloc_high("hx_blocks", 4096)
         self._zc_direct = False
         self.stage_zc = False
         self.persist_high = self.arena.high       # activations + ring are carved below, per tier
@@ -253,8 +261,10 @@ class Executor:
                      ("hid16", "hid16", T * self.ffn * 2)]
         if T > GEMV_CORE_MAX_T:   # x planes + split-K partials of ps_gemv_tc
             spec.append(("tcws", "gemv_tc_ws", self._tc_workspace_bytes()))
-        if T > GEMV_MAX_T and (self._coded_prefill() or getattr(self, "_coded_res_on", False)):
-            # one coded piece (streamed or VRAM-resident) expanded to bf16 for the GEMM
+        if getattr(self, "_hx_on", False) or (
+                T > GEMV_MAX_T and (self._coded_prefill() or getattr(self, "_coded_res_on", False))):
+            # one coded piece (streamed or VRAM-resident) expanded to bf16 for the GEMM, or,
+            # with hx, for every pass (hx rows are only ever read through this buffer)
             spec.append(("expand", "coded_expand", self._expand_bytes()))
         spec += [("xs", "xs", B * d * 4), ("logits", "logits", B * self.V * 4)]
         # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
@@ -272,8 +282,14 @@ class Executor:
         return spec
 
     def _expand_bytes(self) -> int:
-        """The bf16 expansion buffer of coded GEMM pieces: one ring piece at most, and at
-        most 1/64 of the budget (small budgets keep their ring)."""
+        """The bf16 expansion buffer. hx: <= 32 MB and 1/128 of the budget, >= one 64-row
+        block of the widest matrix; 12-bit coded GEMM pieces: one ring piece at most, and
+        at most 1/64 of the budget (small budgets keep their ring)."""
+        if getattr(self, "_hx_on", False):
+            kmax = max((m.k for meta in self.hx.tensors.values() for _, m in meta.values() if m is not None),
+                       default=256)
+            floor = 64 * kmax * 2
+            return max(floor, min(32 << 20, int(self.arena.capacity) // 128)) // 256 * 256
         return max(64 << 10, min(self.chunk_cap, int(self.arena.capacity) // 64)) // 256 * 256
 
     def _coded_prefill(self) -> bool:
@@ -320,24 +336,41 @@ class Executor:
         self.i_tok = self.i_tok_ring
         rope = rope_table(self.arch, self.hd, self.cap)
         self.rope = a.alloc_high("rope", rope.nbytes)
-        self.host_stage = L.host_alloc(max(1 << 20, rope.nbytes, T * 4 + 4096), mapped=False)
+        self.host_stage_bytes = max(1 << 20, rope.nbytes, T * 4 + 4096)
+        self.host_stage = L.host_alloc(self.host_stage_bytes, mapped=False)
         self._h2d_sync(self.rope, rope)
         self.host_tok = L.host_alloc(4 * B * 4096, mapped=False)
         self.host_tok_i = 0
 
     def _h2d_sync(self, dst: int, arr: np.ndarray) -> None:
         arr = np.ascontiguousarray(arr)
-        L.call("ps_stream_synchronize", self.cs)
-        C.memmove(self.host_stage, arr.ctypes.data, arr.nbytes)
-        L.memcpy_async(dst, self.host_stage, arr.nbytes, self.cs)
+        src = arr.ctypes.data
+        for o in range(0, arr.nbytes, self.host_stage_bytes):
+            n = min(self.host_stage_bytes, arr.nbytes - o)
+            L.call("ps_stream_synchronize", self.cs)
+            C.memmove(self.host_stage, src + o, n)
+            L.memcpy_async(dst + o, self.host_stage, n, self.cs)
         L.call("ps_stream_synchronize", self.cs)
 
     def _phys_bytes(self, shard) -> int:
         if shard.kind is ShardKind.KV_CACHE:
             return self.kv_layer_bytes
+        if self.hx_resident(shard.id):
+            return self.hx.shard_bytes[shard.id]
         if self.coded_resident(shard.id):
             return self.coded.shard_bytes[shard.id]
         return self.w.layout.blobs[shard.id].nbytes
+
+    def _zc_readable(self, sid: int) -> bool:
+        """A CPU-placed shard can be read zero-copy: the bf16 blob or its 12-bit coded
+        copy is on the host (an hx-only host copy must be staged through the ring)."""
+        if self.w.base:
+            return True
+        return (self.coded is not None and sid in self.coded.tensors and getattr(self.coded, "mapped", False))
+
+    def hx_resident(self, sid: int) -> bool:
+        """Dense shards held in VRAM hx-coded (~0.65 x bf16), expanded per use."""
+        return self._hx_on and sid in self.hx.tensors
 
     def phys_bytes(self, sid: int) -> int:
         """VRAM bytes shard `sid` takes when resident (the migration model's size)."""
@@ -348,7 +381,7 @@ class Executor:
         0.75 x the bytes): GEMV passes read the coded rows, GEMM passes expand them to bf16
         piece by piece. The freed budget caches more shards (spare pins), so fewer bytes
         cross the link per token. MoE expert groups stay bf16 (PS_CODED_RESIDENT=0: all)."""
-        return (self._coded_res_on and sid in self.coded.tensors and
+        return (self._coded_res_on and sid in self.coded.tensors and not self.hx_resident(sid) and
                 self.shard_kind[sid] is not ShardKind.MOE_EXPERT_GROUP)
 
     def _pinned_bytes(self, plan: SchedulePlan) -> int:
@@ -510,7 +543,8 @@ class Executor:
             self.d2d_bytes += nbytes
         for sid in h2d:
             dev, nbytes = new[sid]
-            src = self.coded.shard_ptr(sid) if self.coded_resident(sid) else self.w.shard_ptr(sid)
+            src = (self.hx.shard_ptr(sid) if self.hx_resident(sid) else
+                   self.coded.shard_ptr(sid) if self.coded_resident(sid) else self.w.shard_ptr(sid))
             L.memcpy_async(dev, src, nbytes, self.cs)
             moved += nbytes
         for layer, dev in self.kv_vram.items():
@@ -522,6 +556,8 @@ class Executor:
             if s.kind is ShardKind.KV_CACHE:
                 self.kv_mode[s.layer_index] = mode
             else:
+                if mode == "zerocopy" and not self._zc_readable(sid):
+                    mode = "stream"      # no host form the SMs can read (hx-only host copy)
                 self.residency[sid] = (mode, 0)
         self._carve_ring(tier, modes)
         L.call("ps_stream_synchronize", self.cs)
@@ -692,6 +728,56 @@ class Executor:
             out.append((start, end, items))
         return out
 
+    def _pieces_hx(self, sid: int, names: list, chunk: int | None = None) -> list:
+        """`_pieces` over the shard's hx layout: a matrix splits only between its 64-row
+        blocks (runtime/hxcodec.py), raw tensors (norm vectors) whole."""
+        chunk = chunk or self.chunk
+        blob = self.w.layout.blobs[sid]
+        meta = self.hx.tensors[sid]
+        out, items, start, end, big = [], [], None, 0, False
+        for name in names:
+            t = blob.tensors[name]
+            off, m = meta[name]
+            if m is None:
+                units = [(0, t.rows, off, off + t.rows * t.cols * 2)]
+            else:
+                nb = len(m.block_off) - 1
+                step = max(1, int(chunk * nb // max(1, m.nbytes)))
+                units = [(b * 64, min(t.rows, (b + step) * 64), off + int(m.block_off[b]),
+                          off + int(m.block_off[min(nb, b + step)])) for b in range(0, nb, step)]
+            for r, r1, b0, b1 in units:
+                if big and t.rows > 1 and b1 - start > chunk:
+                    out.append((start, end, items))
+                    items, start, big = [], None, False
+                if start is None:
+                    start = b0
+                items.append((name, r, r1))
+                big = big or t.rows > 1
+                end = b1
+        if items:
+            out.append((start, end, items))
+        return out
+
+    def _hx_consume(self, sid: int, name: str, m, ptr: int, r0: int, r1: int, fn) -> None:
+        """Run consumer `fn` over rows [r0, r1) of hx matrix `m` (r0 on a 64-row block;
+        `ptr` = device address of that block): expand to bf16 into the expand buffer in
+        runs of whole blocks, one consumer call per run. Stream order keeps each
+        expansion behind the previous consumer."""
+        from .hxcodec import BLOCK_ROWS
+        rows_fit = max(BLOCK_ROWS, (self._expand_bytes() // (m.k * 2)) // BLOCK_ROWS * BLOCK_ROWS)
+        rows_fit = min(rows_fit, 999 * BLOCK_ROWS)          # block offsets fit one small upload
+        lut = self.hx_lut + self.hx.lut_off[(sid, name)]
+        base = int(m.block_off[r0 // BLOCK_ROWS])
+        ra = r0
+        while ra < r1:
+            rb = min(r1, ra + rows_fit)
+            ba, bb = ra // BLOCK_ROWS, -(-rb // BLOCK_ROWS)
+            first = int(m.block_off[ba])
+            self._upload(self.hx_meta, (m.block_off[ba:bb] - first).astype(np.int64))
+            L.call("ps_hx_expand", ptr + first - base, self.hx_meta, rb - ra, m.k, lut, self.expand, m.k, self.cs)
+            self._traced(name, fn, self.expand, ra, rb)
+            ra = rb
+
     def _pieces_coded(self, sid: int, names: list, even: set, chunk: int | None = None) -> list:
         """`_pieces` over the shard's exponent-coded layout (row bytes 1.5 x cols)."""
         chunk = chunk or self.chunk
@@ -764,6 +850,24 @@ class Executor:
                         getattr(self.coded, "mapped", False) and
                         (self.coded_only or os.environ.get("PS_CODED_ZEROCOPY", "1") != "0"))
             res_coded = mode == "pinned" and self.coded_resident(sid)
+            if mode == "pinned" and self.hx_resident(sid):
+                meta = self.hx.tensors[sid]
+
+                def done(i):
+                    pass
+                for name in names:
+                    t = blob.tensors[name]
+                    off, m = meta[name]
+                    self.ptrs[name] = dev + off
+                    if name in own:
+                        advance_to(own[name])
+                        if m is not None:
+                            self._hx_consume(sid, name, m, dev + off, 0, t.rows, consumers[ci].fn)
+                        else:
+                            self._traced(name, consumers[ci].fn, dev + off, 0, t.rows)
+                        ci += 1
+                advance_to(len(consumers))
+                return
             if mode == "pinned":
                 base = dev
             elif zc_coded:   # the bulk-copy GEMV reads the coded rows straight from host memory
@@ -812,12 +916,18 @@ class Executor:
             advance_to(len(consumers))
             return
 
-        coded = (self.coded is not None and sid in self.coded.tensors and self.striper is None and
+        hxs = (self._hx_on and sid in self.hx.tensors and self.striper is None and
+               sid not in self._piece_override)
+        coded = (not hxs and self.coded is not None and sid in self.coded.tensors and self.striper is None and
                  sid not in self._piece_override and
                  (T <= GEMV_MAX_T or (bool(self.expand) and self._coded_prefill())))
         expand = coded and T > GEMV_MAX_T   # GEMM pass: coded piece -> bf16 in VRAM -> tcgen05 GEMM
         evens = {c.tensor for c in consumers if c.even_rows}
-        if coded:
+        if hxs:
+            hmeta = self.hx.tensors[sid]
+            pieces = self._pieces_hx(sid, names)
+            host = self.hx.shard_ptr(sid)
+        elif coded:
             meta = self.coded.tensors[sid]
             # an expanded piece (rows x K bf16) must fit the expand buffer: coded rows are
             # >= 0.75 of their bf16 size, so 0.74 of it in coded bytes always does
@@ -861,7 +971,11 @@ class Executor:
             self._wait(arrived)
             for name, r0, r1 in items:
                 t = blob.tensors[name]
-                if coded:
+                hm = None
+                if hxs:
+                    o, hm = hmeta[name]
+                    ptr = pdev + (o - b0) + (int(hm.block_off[r0 // 64]) if hm is not None else r0 * t.cols * 2)
+                elif coded:
                     m = meta[name]
                     ptr = pdev + (m[0] + r0 * m[1] - b0)
                 else:
@@ -870,6 +984,14 @@ class Executor:
                     self.ptrs[name] = ptr
                 if name in own:
                     advance_to(own[name])
+                    if hm is not None:
+                        self._hx_consume(sid, name, hm, ptr, r0, r1, consumers[ci].fn)
+                        if t.rows > 1:
+                            discharge(entry, ("rows", name))
+                        if r1 == t.rows:
+                            done(ci)
+                            ci += 1
+                        continue
                     if coded and m[2] and expand:
                         L.call("ps_expand_coded", ptr, m[1], r1 - r0, t.cols, self.expand, t.cols, self.cs)
                         ptr = self.expand

@@ -274,3 +274,104 @@ class GpuHxEncoder:
                rowbytes.data_ptr(), ro.data_ptr(), out.data_ptr(), self.stream)
         L.memcpy_async(dst_host, out.data_ptr(), m.nbytes, self.stream)
         L.call("ps_stream_synchronize", self.stream)
+
+
+from .wcomp import GpuEncoder  # noqa: E402  (raw-tensor copies of generated weights)
+
+
+class HxShards:
+    """hx-coded copies of a model's dense weight shards (attention, FFN, head) in pinned
+    host memory: matrices with K % 256 == 0 as hx blobs, everything else (norm vectors)
+    raw bf16, tensors 256-byte aligned in blob order. `tensors[sid][name]` = (offset,
+    HxMatrix) or (offset, None) for raw bytes; `luts` holds every matrix's 8 KB decoder
+    table back to back (`lut_off[(sid, name)]`), uploaded once to VRAM by the executor.
+
+    Source: the bf16 host blob, or — host_format='coded' (runtime/model.py) — each
+    tensor's deterministic init run on the GPU (no bf16 blob on the host at all).
+    `shared`: a node-wide /dev/shm segment (model.SharedHostBlob): every replica plans
+    the layout (GPU, ~1 s), the creator writes, the others wait for the ready flag."""
+
+    def __init__(self, weights, kinds, shared: str | None = None):
+        from ..planning.graph import ShardKind
+        from . import lib as L
+        self.host, self.seg = 0, None
+        layout = weights.layout
+        generated = getattr(weights, "host_format", "bf16") == "coded"
+        enc = GpuHxEncoder()
+        up = lambda n: (n + 255) // 256 * 256  # noqa: E731
+
+        def source(sid, name):
+            t = layout.blobs[sid].tensors[name]
+            if generated:
+                return weights.tensor_filler(t, enc.stream)
+            return weights.tensor_ptr(sid, name)
+
+        self.tensors, self.shard_off, self.shard_bytes, self.lut_off = {}, {}, {}, {}
+        luts, off = [], 0
+        for sid, blob in layout.blobs.items():
+            if blob.kind not in kinds or blob.kind is ShardKind.MOE_EXPERT_GROUP:
+                continue
+            self.shard_off[sid] = off
+            t_off, meta = 0, {}
+            for name, t in blob.tensors.items():
+                if t.rows > 1 and t.cols % SUB == 0:
+                    m = enc.plan(source(sid, name), t.rows, t.cols)
+                    meta[name] = (t_off, m)
+                    self.lut_off[(sid, name)] = len(luts) * m.lut.nbytes
+                    luts.append(m.lut)
+                    t_off += up(m.nbytes)
+                else:
+                    meta[name] = (t_off, None)
+                    t_off += up(t.rows * t.cols * 2)
+            self.tensors[sid] = meta
+            self.shard_bytes[sid] = t_off
+            off += t_off
+        self.nbytes = max(1, off)
+        self.luts = np.concatenate(luts) if luts else np.zeros(8, np.uint16)
+        if shared is not None:
+            from .model import SharedHostBlob
+            self.seg = SharedHostBlob(shared, self.nbytes)
+            self.host = self.seg.addr
+            if not self.seg.creator:
+                try:
+                    self.seg.wait_ready()          # another replica of this node writes
+                except BaseException:
+                    self.close()
+                    raise
+                return
+        else:
+            self.host = L.host_alloc(self.nbytes, mapped=True)
+        try:
+            for sid, meta in self.tensors.items():
+                for name, (o, m) in meta.items():
+                    dst = self.host + self.shard_off[sid] + o
+                    t = layout.blobs[sid].tensors[name]
+                    if m is not None:
+                        enc.write(source(sid, name), m, dst)
+                    elif generated:
+                        GpuEncoder(chunk_bytes=max(1 << 20, t.rows * t.cols * 2)).bf16_to(
+                            source(sid, name), t.rows, t.cols, dst)
+                    else:
+                        import ctypes
+                        ctypes.memmove(dst, weights.tensor_ptr(sid, name), t.rows * t.cols * 2)
+        except BaseException:
+            self.close()
+            raise
+        if self.seg is not None:
+            self.seg.mark_ready()
+
+    @property
+    def hx_bytes(self) -> int:
+        return sum(self.shard_bytes.values())
+
+    def shard_ptr(self, sid: int) -> int:
+        return self.host + self.shard_off[sid]
+
+    def close(self) -> None:
+        from . import lib as L
+        if self.seg is not None:
+            self.seg.close()
+            self.seg, self.host = None, 0
+        elif self.host:
+            L.host_free(self.host)
+            self.host = 0

@@ -323,13 +323,14 @@ class HostWeights:
 
     def __init__(self, spec: ModelSpec, arch: Arch, shared: str | None = None, host_format: str = "bf16"):
         """`host_format="coded"`: no bf16 blob on the host at all — `generate()` produces
-        every tensor on the GPU and keeps only its exponent-coded form (runtime/wcomp.py,
-        ~0.75 x the bytes; dense models), for models whose bf16 and coded copies do not
+        every tensor on the GPU and keeps only its hx-coded form (runtime/hxcodec.py,
+        ~0.65 x the bytes; dense models), for models whose bf16 blob and coded copy do not
         fit host memory together. The embedding table stays bf16."""
         self.spec, self.arch = spec, arch
         self.layout = WeightLayout(spec, arch)
         self.shared = None
         self.coded = None
+        self.hx = None
         self.host_format = host_format
         if host_format not in ("bf16", "coded"):
             raise ValueError(f"host_format {host_format!r}")
@@ -358,6 +359,9 @@ class HostWeights:
         if self.coded is not None:
             self.coded.close()
             self.coded = None
+        if self.hx is not None:
+            self.hx.close()
+            self.hx = None
         if self.host_format == "coded":
             if self.embed:
                 L.host_free(self.embed)
@@ -391,13 +395,22 @@ class HostWeights:
         """uint16 view (bf16 bits) of one tensor in the pinned blob (host_format='coded':
         a decoded copy, for tests and the CPU oracle)."""
         t = self.layout.tensor(shard_id, name)
-        if self.host_format == "coded":
-            from .wcomp import decode
-            off, rb, is_coded = self.coded.tensors[shard_id][name]
-            addr = self.coded.shard_ptr(shard_id) + off
-            raw = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint8 * (t.rows * rb)).from_address(addr))
-            raw = raw.reshape(t.rows, rb)
-            return decode(raw, t.cols) if is_coded else raw.view(np.uint16).copy()
+        if self.host_format == "coded":   # decode the hx copy on the GPU (ps_hx_expand)
+            import torch
+            off, m = self.hx.tensors[shard_id][name]
+            addr = self.hx.shard_ptr(shard_id) + off
+            if m is None:
+                raw = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint8 * (t.rows * t.cols * 2)).from_address(addr))
+                return raw.view(np.uint16).reshape(t.rows, t.cols).copy()
+            stream = torch.cuda.current_stream().cuda_stream
+            blob = torch.empty(m.nbytes, dtype=torch.uint8, device="cuda")
+            L.memcpy_async(blob.data_ptr(), addr, m.nbytes, stream)
+            offs = torch.from_numpy(m.block_off[:-1].astype(np.int32)).cuda()
+            lut = torch.from_numpy(m.lut.view(np.int16)).cuda()
+            out = torch.empty(t.rows, t.cols, dtype=torch.int16, device="cuda")
+            L.call("ps_hx_expand", blob.data_ptr(), offs.data_ptr(), t.rows, t.cols, lut.data_ptr(),
+                   out.data_ptr(), t.cols, stream)
+            return out.cpu().numpy().view(np.uint16)
         buf = (np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint16 * (t.rows * t.cols))
                                      .from_address(self.tensor_ptr(shard_id, name))))
         return buf.reshape(t.rows, t.cols)
@@ -484,7 +497,7 @@ class HostWeights:
         """Embedding table as bf16; every shard generated on the GPU and stored coded."""
         import torch
 
-        from .wcomp import CodedShards
+        from .hxcodec import HxShards
         stream = torch.cuda.current_stream().cuda_stream
         stage = torch.empty(staging_bytes, dtype=torch.uint8, device="cuda")
         emb = TensorSlot("embed", 0, self.spec.vocab_size, self.spec.d_model, ("plain", "embed"))
@@ -497,7 +510,7 @@ class HostWeights:
             L.call("ps_stream_synchronize", stream)
         del stage
         kinds = {b.kind for b in self.layout.blobs.values()}
-        self.coded = CodedShards(self, kinds, chunk_bytes=staging_bytes)
+        self.hx = HxShards(self, kinds)
 
     def _generate(self, staging_bytes: int) -> None:
         import torch

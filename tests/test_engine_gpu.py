@@ -633,6 +633,7 @@ def test_coded_prefill_same_tokens_fewer_bytes(monkeypatch, frac):
     prompt = _prompt(128, spec.vocab_size, seed=33)
     out = {}
     monkeypatch.setenv("PS_CODED_RESIDENT", "0")   # keep the prefill streaming (coded residency pins more)
+    monkeypatch.setenv("PS_HX", "0")               # the 12-bit path under test (hx would take it)
     for cp in ("0", "1"):
         monkeypatch.setenv("PS_CODED_PREFILL", cp)
         eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, chunk_bytes=1 << 20)
@@ -677,6 +678,7 @@ def test_coded_residency_same_tokens_fewer_link_bytes(monkeypatch, frac, batch):
     spec = catalog.builtin_model("tiny-llama")
     prompts = [_prompt(128 if batch == 1 else 40, spec.vocab_size, seed=70 + i) for i in range(batch)]
     out = {}
+    monkeypatch.setenv("PS_HX", "0")               # the 12-bit residency under test
     for cr in ("0", "1"):
         monkeypatch.setenv("PS_CODED_RESIDENT", cr)
         eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=batch,
@@ -699,11 +701,11 @@ def test_coded_residency_same_tokens_fewer_link_bytes(monkeypatch, frac, batch):
 
 @pytest.mark.parametrize("frac,prompt_len,batch", [(0.5, 128, 1), (0.25, 20, 1), (0.6, 40, 12)])
 def test_coded_only_host_format_same_tokens(frac, prompt_len, batch):
-    """host_format='coded': the weights are generated on the GPU and only their exponent-
-    coded form is kept on the host (no bf16 blob, the Llama-3.3-70B configuration on a
-    196 GB box). Prefill (expanded pieces), decode (coded GEMV / one-pass tcgen05 GEMV),
-    zero-copy and pinned shards all read the coded copy: same tokens and logits as the
-    bf16 host blob, and the decoded host view equals the bf16 blob bit for bit."""
+    """host_format='coded': the weights are generated on the GPU and only their hx-coded
+    form is kept on the host (no bf16 blob, the Llama-3.3-70B configuration on a 196 GB
+    box). Prefill, decode, pinned and (staged) CPU-placed shards all read the hx copy
+    through ps_hx_expand: same tokens and logits as the bf16 host blob, and the decoded
+    host view equals the bf16 blob bit for bit."""
     from paper_2604_26334_b200.runtime.engine import Engine
     spec = catalog.builtin_model("tiny-llama")
     prompts = [_prompt(prompt_len, spec.vocab_size, seed=90 + i) for i in range(batch)]
@@ -716,7 +718,7 @@ def test_coded_only_host_format_same_tokens(frac, prompt_len, batch):
         views = {(sid, n): w.host_view(sid, n).copy() for sid, b in w.layout.blobs.items() for n in b.tensors}
         out[fmt] = ([t.tolist() for t in res.tokens], eng.logits().copy(), views, w.embed_view().copy())
         if fmt == "coded":
-            assert w.base == 0 and w.coded is not None and w.coded.encoder == "gpu"
+            assert w.base == 0 and w.hx is not None and w.coded is None
         eng.close()
     assert out["coded"][0] == out["bf16"][0]
     assert np.array_equal(out["coded"][1], out["bf16"][1])
@@ -751,3 +753,35 @@ def test_gpu_encoded_blob_equals_numpy_encoded():
         a.close()
         b.close()
         hw.close()
+
+
+@pytest.mark.parametrize("frac,prompt_len,batch", [(0.5, 24, 1), (0.35, 128, 1), (0.25, 20, 1), (0.6, 30, 12)])
+def test_hx_same_tokens_fewer_bytes(monkeypatch, frac, prompt_len, batch):
+    """Huffman-coded exponents (hx, ~10.4 bits/weight) for resident and streamed dense
+    shards, expanded to bf16 in VRAM ahead of the bf16 kernels (PS_HX=1) against the
+    12-bit format (PS_HX=0): identical tokens and logits (the kernels see the same bf16
+    weights), fewer link bytes per decode pass, fewer resident bytes; GEMV, one-pass
+    tcgen05 GEMV (batched) and GEMM (prompt 128) passes, and the migration model still
+    predicts every tier switch."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model("tiny-llama")
+    prompts = [_prompt(prompt_len, spec.vocab_size, seed=120 + i) for i in range(batch)]
+    out = {}
+    for h in ("0", "1"):
+        monkeypatch.setenv("PS_HX", h)
+        eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=batch,
+                     chunk_bytes=1 << 20)
+        res = eng.generate(prompts, gen_len=10)
+        ex = eng.executor
+        dec = [st for st in ex.stats if st.T == batch]
+        link = sum(st.bytes_streamed - st.kv_bytes for st in dec) / max(1, len(dec))
+        res_bytes = sum(ex.phys_bytes(sid) for sid, r in ex.residency.items() if r[0] == "pinned")
+        n_hx = sum(1 for sid, r in ex.residency.items() if r[0] == "pinned" and ex.hx_resident(sid))
+        for prev, tier, rows, moved, (h2d, d2h) in res.switches:
+            assert moved == h2d + d2h, (prev, tier, rows, moved, h2d, d2h)
+        out[h] = ([t.tolist() for t in res.tokens], eng.logits().copy(), link, res_bytes, n_hx)
+        eng.close()
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert out["1"][4] > 0 and out["0"][4] == 0
+    assert out["1"][2] <= out["0"][2], (out["0"][2], out["1"][2])
