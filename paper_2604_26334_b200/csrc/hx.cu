@@ -3,10 +3,11 @@
 // VRAM ahead of the bf16 kernels (bulk-copy GEMV, one-pass tcgen05 GEMV, tcgen05 GEMM),
 // which therefore see exactly the bf16 weights: results are bit-identical to bf16.
 //
-//   ps_hx_expand  decode: CTA per 64-row block, one thread per 256-weight sub-block
-//                 (bit offset = prefix of the row header's sub-block lengths); a 4096-entry
-//                 table (symbol | length << 8) in shared memory turns the next 12 bits of
-//                 the LSB-first stream into a symbol; exponent = rowmax - symbol
+//   ps_hx_expand  decode: one thread per 256-weight sub-block (bit offset = prefix of the
+//                 row header's sub-block lengths), CTAs of 256 sub-blocks of one 64-row
+//                 block; a 4096-entry table (symbol | length << 8) in shared memory turns
+//                 the next 12 bits of the LSB-first stream into a symbol; exponent =
+//                 rowmax - symbol
 //   ps_hx_stats   encoder pass 1: row max exponent + histogram of d = rowmax - exponent
 //   ps_hx_sizes   encoder pass 2: bits per sub-block, bytes per row (host: Huffman code,
 //                 row and block offsets)
@@ -25,13 +26,15 @@ constexpr int HX_SUB = 256, HX_BLOCK_ROWS = 64, HX_LUT = 4096, HX_THREADS = 256;
 
 __device__ __forceinline__ int hx_header_bytes(int K) { return ((4 + 2 * (K / HX_SUB)) + 15) / 16 * 16; }
 
-// expand: blocks [blockIdx.x] of a piece; blk[b] = byte offset of block b from `piece`
+// expand: CTA (b, part) decodes tasks [part * 256, part * 256 + 256) of block b of a piece,
+// task = (row r, sub-block s), r = task / (K / 256); blk[b] = byte offset of block b from
+// `piece`. Each thread keeps a 64-bit bit buffer (refilled one word at a time, never
+// reading past the stream's padding) and resolves one symbol per 4096-entry table lookup.
 __global__ void __launch_bounds__(HX_THREADS)
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
                  const uint16_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
   __shared__ uint16_t lut[HX_LUT];
   __shared__ uint32_t row_start[HX_BLOCK_ROWS];
-  extern __shared__ uint32_t sub_off[];   // [64][K / 256] bit offsets
   const int nsub = K / HX_SUB;
   const int hb = hx_header_bytes(K);
   {
@@ -57,40 +60,41 @@ hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__
     row_start[threadIdx.x + 32] = 256 + tot_a + sb - b;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < nr; r += HX_THREADS) {   // sub-block bit offsets per row
-    const uint16_t* hdr = reinterpret_cast<const uint16_t*>(block + row_start[r]);
-    uint32_t acc = 0;
-    for (int s = 0; s < nsub; ++s) {
-      sub_off[r * nsub + s] = acc;
-      acc += hdr[2 + s];
-    }
-  }
-  __syncthreads();
-  for (int task = threadIdx.x; task < nr * nsub; task += HX_THREADS) {
-    const int r = task / nsub, s = task - (task / nsub) * nsub;
-    const uint8_t* row = block + row_start[r];
-    const uint32_t rowmax = reinterpret_cast<const uint16_t*>(row)[0];
-    const uint8_t* sm = row + hb + s * HX_SUB;
-    const uint32_t* sw = reinterpret_cast<const uint32_t*>(row + hb + K);
-    uint32_t pos = sub_off[r * nsub + s];
-    uint4* o = reinterpret_cast<uint4*>(out + (long long)(r0 + r) * ld_out + s * HX_SUB);
-    for (int c = 0; c < HX_SUB; c += 16) {
-      const uint4 m = *reinterpret_cast<const uint4*>(sm + c);   // 16 sign|mantissa bytes
-      const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
-      uint32_t w[8];
+  const int task = blockIdx.y * HX_THREADS + threadIdx.x;
+  const int r = task / nsub, s = task - (task / nsub) * nsub;
+  if (r >= nr) return;
+  const uint8_t* row = block + row_start[r];
+  const uint16_t* hdr = reinterpret_cast<const uint16_t*>(row);
+  const uint32_t rowmax = hdr[0];
+  uint32_t pos = 0;
+  for (int i = 0; i < s; ++i) pos += hdr[2 + i];
+  const uint8_t* sm = row + hb + s * HX_SUB;
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
+  uint64_t buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
+  int avail = 64 - (int)(pos & 31);
+  uint32_t nextw = p[2];   // one word of look-ahead: a refill never waits on memory
+  p += 3;
+  uint4* o = reinterpret_cast<uint4*>(out + (long long)(r0 + r) * ld_out + s * HX_SUB);
+  uint4 m_next = *reinterpret_cast<const uint4*>(sm);
+#pragma unroll 1
+  for (int c = 0; c < HX_SUB; c += 16) {
+    const uint4 m = m_next;                                     // 16 sign|mantissa bytes
+    if (c + 16 < HX_SUB) m_next = *reinterpret_cast<const uint4*>(sm + c + 16);
+    const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+    uint32_t w[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t idx = pos >> 5;
-        const uint32_t peek = __funnelshift_r(sw[idx], sw[idx + 1], pos & 31) & (HX_LUT - 1);
-        const uint32_t e = lut[peek];
-        pos += e >> 8;
-        const uint32_t b = (mw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-        const uint32_t h = ((b & 0x80u) << 8) | (((rowmax - (e & 0xFFu)) & 0xFFu) << 7) | (b & 0x7Fu);
-        if (i & 1) w[i >> 1] |= h << 16; else w[i >> 1] = h;
-      }
-      o[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
-      o[c / 8 + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    for (int i = 0; i < 16; ++i) {
+      if (avail < 12) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
+      const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
+      const int len = (int)(e >> 8);
+      buf >>= len;
+      avail -= len;
+      const uint32_t b = (mw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+      const uint32_t h = ((b & 0x80u) << 8) | (((rowmax - (e & 0xFFu)) & 0xFFu) << 7) | (b & 0x7Fu);
+      if (i & 1) w[i >> 1] |= h << 16; else w[i >> 1] = h;
     }
+    o[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+    o[c / 8 + 1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
@@ -133,7 +137,7 @@ hx_sizes_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const in
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t stream = ((tot + 7) / 8 + 8 + 15) / 16 * 16;   // >= 8 spare bytes: the decoder reads a word ahead
+    const uint32_t stream = ((tot + 7) / 8 + 16 + 15) / 16 * 16;   // >= 16 spare bytes: the decoder reads ahead
     rowbytes[blockIdx.x] = (uint32_t)hx_header_bytes(K) + (uint32_t)K + stream;
   }
 }
@@ -184,13 +188,8 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
              "ps_hx_expand: piece, out and lut must be 16-byte aligned");
   if (rows <= 0) return PS_OK;
   const int nblocks = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
-  const size_t smem = (size_t)HX_BLOCK_ROWS * (K / HX_SUB) * 4;
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    smem_set = smem;
-  }
-  hx_expand_kernel<<<nblocks, HX_THREADS, smem, (cudaStream_t)stream>>>(
+  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + HX_THREADS - 1) / HX_THREADS;
+  hx_expand_kernel<<<dim3(nblocks, parts), HX_THREADS, 0, (cudaStream_t)stream>>>(
       static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint16_t*>(lut),
       static_cast<__nv_bfloat16*>(out), ld_out);
   PS_CHECK_LAUNCH();

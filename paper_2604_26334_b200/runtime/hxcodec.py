@@ -15,7 +15,8 @@ Layout of one [N, K] matrix (K % 256 == 0), rows in blocks of 64:
     row     header: uint16 rowmax, uint16 0, uint16 bit length of each 256-weight
             sub-block (K / 256 of them), padded to 16 bytes
             K bytes sign << 7 | mantissa
-            the bit stream, padded (after >= 8 spare bytes) to 16 bytes
+            the bit stream, padded (after >= 16 spare bytes: the decoder reads two
+            words ahead) to 16 bytes
 
 Every 64-row block is self-contained: a ring piece is a run of whole blocks, and the
 decoder (`ps_hx_expand`, csrc/hx.cu) needs only the block offsets of its piece and
@@ -94,7 +95,7 @@ def header_bytes(k: int) -> int:
 
 
 def row_bytes(k: int, nbits: int) -> int:
-    return header_bytes(k) + k + -(-(-(-nbits // 8) + 8) // 16) * 16
+    return header_bytes(k) + k + -(-(-(-nbits // 8) + 16) // 16) * 16
 
 
 def encode(bits: np.ndarray, table: np.ndarray | None = None):
