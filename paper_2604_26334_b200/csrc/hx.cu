@@ -3,11 +3,11 @@
 // VRAM ahead of the bf16 kernels (bulk-copy GEMV, one-pass tcgen05 GEMV, tcgen05 GEMM),
 // which therefore see exactly the bf16 weights: results are bit-identical to bf16.
 //
-//   ps_hx_expand  decode: one thread per 256-weight sub-block (bit offset = prefix of the
-//                 row header's sub-block lengths), CTAs of 256 sub-blocks of one 64-row
-//                 block; a 4096-entry table (symbol | length << 8) in shared memory turns
-//                 the next 12 bits of the LSB-first stream into a symbol; exponent =
-//                 rowmax - symbol
+//   ps_hx_expand  decode: one lane per 256-weight sub-block (bit offset = prefix of the
+//                 row header's sub-block lengths) decodes its exponents into shared memory
+//                 (a 4096-entry table, symbol | length << 8, turns the next 12 bits of the
+//                 LSB-first stream into a symbol; exponent = rowmax - symbol), then the
+//                 warp assembles bf16 rows with coalesced loads and stores
 //   ps_hx_stats   encoder pass 1: row max exponent + histogram of d = rowmax - exponent
 //   ps_hx_sizes   encoder pass 2: bits per sub-block, bytes per row (host: Huffman code,
 //                 row and block offsets)
@@ -26,75 +26,120 @@ constexpr int HX_SUB = 256, HX_BLOCK_ROWS = 64, HX_LUT = 4096, HX_THREADS = 256;
 
 __device__ __forceinline__ int hx_header_bytes(int K) { return ((4 + 2 * (K / HX_SUB)) + 15) / 16 * 16; }
 
-// expand: CTA (b, part) decodes tasks [part * 256, part * 256 + 256) of block b of a piece,
-// task = (row r, sub-block s), r = task / (K / 256); blk[b] = byte offset of block b from
-// `piece`. Each thread keeps a 64-bit bit buffer (refilled one word at a time, never
-// reading past the stream's padding) and resolves one symbol per 4096-entry table lookup.
-__global__ void __launch_bounds__(HX_THREADS)
+// expand: CTA (b, part) of HX_EXP_WARPS warps takes tasks [part * 32 * HX_EXP_WARPS, ...)
+// of block b of a piece, task = (row r, sub-block s), r = task / (K / 256); blk[b] = byte
+// offset of block b from `piece`. Two phases per warp of 32 tasks:
+//   1. each lane decodes ITS sub-block's 256 exponents (serial: the bit stream is a chain)
+//      into a shared-memory row of its own (65 words: conflict-free), from a 64-bit bit
+//      buffer with one word of look-ahead, one 4096-entry table lookup per symbol;
+//   2. the warp assembles the 32 sub-blocks one at a time, lane l taking 8 columns: the
+//      sign|mantissa loads (256 B) and the bf16 stores (512 B) are coalesced.
+constexpr int HX_EXP_WARPS = 4;
+constexpr int HX_EXP_ROW_WORDS = HX_SUB / 4 + 1;   // 64 exponent words + 1 (bank offset)
+
+__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
                  const uint16_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
   __shared__ uint16_t lut[HX_LUT];
   __shared__ uint32_t row_start[HX_BLOCK_ROWS];
+  __shared__ uint32_t exps[HX_EXP_WARPS][32][HX_EXP_ROW_WORDS];
   const int nsub = K / HX_SUB;
   const int hb = hx_header_bytes(K);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
     const uint4* src = reinterpret_cast<const uint4*>(lut_g);
     uint4* dst = reinterpret_cast<uint4*>(lut);
-    for (int i = threadIdx.x; i < HX_LUT / 8; i += HX_THREADS) dst[i] = src[i];
+    for (int i = threadIdx.x; i < HX_LUT / 8; i += 32 * HX_EXP_WARPS) dst[i] = src[i];
   }
   const uint8_t* block = piece + blk[blockIdx.x];
   const int r0 = blockIdx.x * HX_BLOCK_ROWS;
   const int nr = min(HX_BLOCK_ROWS, rows - r0);
-  if (threadIdx.x < 32) {   // row starts: exclusive scan of the 64 row sizes (one warp)
+  if (warp == 0) {   // row starts: exclusive scan of the 64 row sizes
     const uint32_t* sizes = reinterpret_cast<const uint32_t*>(block);
-    uint32_t a = threadIdx.x < nr ? sizes[threadIdx.x] : 0u;
-    uint32_t b = threadIdx.x + 32 < nr ? sizes[threadIdx.x + 32] : 0u;
+    uint32_t a = lane < nr ? sizes[lane] : 0u;
+    uint32_t b = lane + 32 < nr ? sizes[lane + 32] : 0u;
     uint32_t sa = a, sb = b;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t ua = __shfl_up_sync(0xffffffffu, sa, o), ub = __shfl_up_sync(0xffffffffu, sb, o);
-      if ((int)threadIdx.x >= o) { sa += ua; sb += ub; }
+      if (lane >= o) { sa += ua; sb += ub; }
     }
     const uint32_t tot_a = __shfl_sync(0xffffffffu, sa, 31);
-    row_start[threadIdx.x] = 256 + sa - a;
-    row_start[threadIdx.x + 32] = 256 + tot_a + sb - b;
+    row_start[lane] = 256 + sa - a;
+    row_start[lane + 32] = 256 + tot_a + sb - b;
   }
   __syncthreads();
-  const int task = blockIdx.y * HX_THREADS + threadIdx.x;
-  const int r = task / nsub, s = task - (task / nsub) * nsub;
-  if (r >= nr) return;
-  const uint8_t* row = block + row_start[r];
-  const uint16_t* hdr = reinterpret_cast<const uint16_t*>(row);
-  const uint32_t rowmax = hdr[0];
-  uint32_t pos = 0;
-  for (int i = 0; i < s; ++i) pos += hdr[2 + i];
-  const uint8_t* sm = row + hb + s * HX_SUB;
-  const uint32_t* p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
-  uint64_t buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
-  int avail = 64 - (int)(pos & 31);
-  uint32_t nextw = p[2];   // one word of look-ahead: a refill never waits on memory
-  p += 3;
-  uint4* o = reinterpret_cast<uint4*>(out + (long long)(r0 + r) * ld_out + s * HX_SUB);
-  uint4 m_next = *reinterpret_cast<const uint4*>(sm);
+  const int task0 = (blockIdx.y * HX_EXP_WARPS + warp) * 32;
+  if (task0 >= nr * nsub) return;   // whole warp (no block-level barrier below)
+  uint32_t* my = exps[warp][lane];
+  // ---- phase 1: this lane's sub-block -> 256 exponents in shared memory
+  {
+    const int task = task0 + lane;
+    const int r = task / nsub, s = task - (task / nsub) * nsub;
+    if (r < nr) {
+      const uint8_t* row = block + row_start[r];
+      const uint16_t* hdr = reinterpret_cast<const uint16_t*>(row);
+      const uint32_t rowmax = hdr[0];
+      uint32_t pos = 0;
+      for (int i = 0; i < s; ++i) pos += hdr[2 + i];
+      // 64-bit bit buffer, refilled one word at a time with one word of look-ahead; the
+      // refill test runs once per two symbols (a lane refills every ~14 symbols, but in a
+      // warp SOME lane almost always does, so a per-symbol test costs every lane the
+      // refill path): after it the buffer holds >= 32 bits, enough for two 12-bit codes
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
+      uint64_t buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
+      int avail = 64 - (int)(pos & 31);
+      uint32_t nextw = p[2];
+      p += 3;
 #pragma unroll 1
-  for (int c = 0; c < HX_SUB; c += 16) {
-    const uint4 m = m_next;                                     // 16 sign|mantissa bytes
-    if (c + 16 < HX_SUB) m_next = *reinterpret_cast<const uint4*>(sm + c + 16);
-    const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
-    uint32_t w[8];
+      for (int c = 0; c < HX_SUB / 4; ++c) {
+        uint32_t word = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (avail < 12) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
-      const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
-      const int len = (int)(e >> 8);
-      buf >>= len;
-      avail -= len;
-      const uint32_t b = (mw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-      const uint32_t h = ((b & 0x80u) << 8) | (((rowmax - (e & 0xFFu)) & 0xFFu) << 7) | (b & 0x7Fu);
-      if (i & 1) w[i >> 1] |= h << 16; else w[i >> 1] = h;
+        for (int i = 0; i < 4; ++i) {
+          if ((i & 1) == 0 && avail < 32) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
+          const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
+          const int len = (int)(e >> 8);
+          buf >>= len;
+          avail -= len;
+          word |= ((rowmax - (e & 0xFFu)) & 0xFFu) << (8 * i);
+        }
+        my[c] = word;
+      }
     }
-    o[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
-    o[c / 8 + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  __syncwarp();
+  // ---- phase 2: sub-block j of this warp, lane -> columns [8 lane, 8 lane + 8); the
+  // sign|mantissa loads of 8 sub-blocks are issued together (one memory latency per 8)
+  const int ntask = min(32, nr * nsub - task0);
+#pragma unroll 1
+  for (int j0 = 0; j0 < ntask; j0 += 8) {
+    uint2 mm[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int task = task0 + j0 + u;
+      const int r = task / nsub, s = task - (task / nsub) * nsub;
+      mm[u] = j0 + u < ntask ? *reinterpret_cast<const uint2*>(block + row_start[r] + hb + s * HX_SUB + 8 * lane)
+                             : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u;
+      if (j >= ntask) break;
+      const int task = task0 + j;
+      const int r = task / nsub, s = task - (task / nsub) * nsub;
+      const uint32_t e0 = exps[warp][j][2 * lane], e1 = exps[warp][j][2 * lane + 1];
+      const uint32_t mw[2] = {mm[u].x, mm[u].y}, ew[2] = {e0, e1};
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t b = (mw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+        const uint32_t ex = (ew[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+        const uint32_t h = ((b & 0x80u) << 8) | (ex << 7) | (b & 0x7Fu);
+        if (i & 1) w[i >> 1] |= h << 16; else w[i >> 1] = h;
+      }
+      *reinterpret_cast<uint4*>(out + (long long)(r0 + r) * ld_out + s * HX_SUB + 8 * lane) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
@@ -137,7 +182,7 @@ hx_sizes_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const in
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t stream = ((tot + 7) / 8 + 16 + 15) / 16 * 16;   // >= 16 spare bytes: the decoder reads ahead
+    const uint32_t stream = ((tot + 7) / 8 + 24 + 15) / 16 * 16;   // >= 24 spare bytes: the decoder reads ahead
     rowbytes[blockIdx.x] = (uint32_t)hx_header_bytes(K) + (uint32_t)K + stream;
   }
 }
@@ -188,8 +233,9 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
              "ps_hx_expand: piece, out and lut must be 16-byte aligned");
   if (rows <= 0) return PS_OK;
   const int nblocks = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
-  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + HX_THREADS - 1) / HX_THREADS;
-  hx_expand_kernel<<<dim3(nblocks, parts), HX_THREADS, 0, (cudaStream_t)stream>>>(
+  const int per_cta = 32 * HX_EXP_WARPS;
+  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + per_cta - 1) / per_cta;
+  hx_expand_kernel<<<dim3(nblocks, parts), per_cta, 0, (cudaStream_t)stream>>>(
       static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint16_t*>(lut),
       static_cast<__nv_bfloat16*>(out), ld_out);
   PS_CHECK_LAUNCH();

@@ -15,8 +15,8 @@ Layout of one [N, K] matrix (K % 256 == 0), rows in blocks of 64:
     row     header: uint16 rowmax, uint16 0, uint16 bit length of each 256-weight
             sub-block (K / 256 of them), padded to 16 bytes
             K bytes sign << 7 | mantissa
-            the bit stream, padded (after >= 16 spare bytes: the decoder reads two
-            words ahead) to 16 bytes
+            the bit stream, padded (after >= 24 spare bytes: the decoder reads up
+            to 95 bits ahead) to 16 bytes
 
 Every 64-row block is self-contained: a ring piece is a run of whole blocks, and the
 decoder (`ps_hx_expand`, csrc/hx.cu) needs only the block offsets of its piece and
@@ -95,7 +95,7 @@ def header_bytes(k: int) -> int:
 
 
 def row_bytes(k: int, nbits: int) -> int:
-    return header_bytes(k) + k + -(-(-(-nbits // 8) + 16) // 16) * 16
+    return header_bytes(k) + k + -(-(-(-nbits // 8) + 24) // 16) * 16
 
 
 def encode(bits: np.ndarray, table: np.ndarray | None = None):
