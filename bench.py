@@ -224,6 +224,23 @@ def gemv_kernel_roofline(L, peaks) -> dict:
                       "avg_launch_us": round(avg_c * 1e6, 2), "traffic": traffic_c, "traffic_source": tsrc_c}}
 
 
+def link_format(eng) -> str:
+    """How dense weights cross the link and sit in VRAM in this run (runtime/hxcodec.py,
+    runtime/wcomp.py)."""
+    w = eng.weights
+    parts = []
+    hx = getattr(w, "hx", None)
+    if hx is not None and os.environ.get("PS_HX", "1") != "0":
+        dense = sum(w.layout.blobs[sid].nbytes for sid in hx.tensors)
+        parts.append(f"hx: dense shards Huffman-coded ({8 * 2 * hx.hx_bytes / dense:.2f} bits/weight, lossless), "
+                     f"streamed and VRAM-resident in that form, expanded to bf16 per 64-row block run; "
+                     f"encoded on the GPU in {getattr(eng, 'hx_seconds', 0.0):.1f}s")
+    if getattr(w, "coded", None) is not None:
+        parts.append(f"12-bit exponent-coded copy for zero-copy shards / routed experts "
+                     f"(encoded in {getattr(eng, 'coded_seconds', 0.0):.1f}s)")
+    return "; ".join(parts) if parts else "bf16"
+
+
 def reference_planning_seconds(args) -> dict:
     """the reference's own CPU work for this config — the UNMODIFIED
     `build_tier_table` (oracle/plan_oracle.py runs it in a subprocess from baseline/_ref),
@@ -420,10 +437,10 @@ def run_ours(args, rank: int, world: int) -> dict:
                               for a, b, r, mv, (h, dd) in res.switches],
                  "prefill_pass_ms": round(res.passes[0][2] * 1e3, 2) if res.passes else None},
         "model_load_s": round(eng.load_seconds, 2),
-        "link_format": ("exponent-coded dense shards in decode passes (12 bits/weight, lossless; "
-                        f"encoded in {getattr(eng, 'coded_seconds', 0.0):.1f}s at load)"
-                        if getattr(eng.weights, "coded", None) is not None else "bf16"),
-        "host_weights": "shared /dev/shm segment per node" if shared else "private pinned blob",
+        "link_format": link_format(eng),
+        "host_weights": ("no bf16 blob: hx-coded shards generated and encoded on the GPU (host_format=coded)"
+                         if eng.weights.host_format == "coded" else
+                         "shared /dev/shm segment per node" if shared else "private pinned blob"),
         "residency": {
             "spare_pinned_shards": len(eng.executor.spare_pinned),
             "spare_pinned_bytes": int(sum(eng.executor._phys_bytes(eng.executor.shards[sid])

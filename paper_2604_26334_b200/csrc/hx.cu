@@ -5,8 +5,8 @@
 //
 //   ps_hx_expand  decode: one lane per 256-weight sub-block (bit offset = prefix of the
 //                 row header's sub-block lengths) decodes its exponents into shared memory
-//                 (a 4096-entry table, symbol | length << 8, turns the next 12 bits of the
-//                 LSB-first stream into a symbol; exponent = rowmax - symbol), then the
+//                 (a 4096-entry table turns the next 12 bits of the LSB-first stream into
+//                 one symbol, or two when both codes fit; exponent = rowmax - symbol), then the
 //                 warp assembles bf16 rows with coalesced loads and stores
 //   ps_hx_stats   encoder pass 1: row max exponent + histogram of d = rowmax - exponent
 //   ps_hx_sizes   encoder pass 2: bits per sub-block, bytes per row (host: Huffman code,
@@ -39,17 +39,18 @@ constexpr int HX_EXP_ROW_WORDS = HX_SUB / 4 + 1;   // 64 exponent words + 1 (ban
 
 __global__ void __launch_bounds__(32 * HX_EXP_WARPS)
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
-                 const uint16_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
-  __shared__ uint16_t lut[HX_LUT];
+                 const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
+  __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | len1 << 16 | len1+len2 << 20 | two << 25
   __shared__ uint32_t row_start[HX_BLOCK_ROWS];
-  __shared__ uint32_t exps[HX_EXP_WARPS][32][HX_EXP_ROW_WORDS];
+  extern __shared__ uint32_t hx_exps[];   // [warp][lane][65] exponent rows (dynamic: > 48 KB static)
+  auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);
   const int nsub = K / HX_SUB;
   const int hb = hx_header_bytes(K);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   {
     const uint4* src = reinterpret_cast<const uint4*>(lut_g);
     uint4* dst = reinterpret_cast<uint4*>(lut);
-    for (int i = threadIdx.x; i < HX_LUT / 8; i += 32 * HX_EXP_WARPS) dst[i] = src[i];
+    for (int i = threadIdx.x; i < HX_LUT / 4; i += 32 * HX_EXP_WARPS) dst[i] = src[i];
   }
   const uint8_t* block = piece + blk[blockIdx.x];
   const int r0 = blockIdx.x * HX_BLOCK_ROWS;
@@ -83,27 +84,33 @@ hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__
       uint32_t pos = 0;
       for (int i = 0; i < s; ++i) pos += hdr[2 + i];
       // 64-bit bit buffer, refilled one word at a time with one word of look-ahead; the
-      // refill test runs once per two symbols (a lane refills every ~14 symbols, but in a
-      // warp SOME lane almost always does, so a per-symbol test costs every lane the
-      // refill path): after it the buffer holds >= 32 bits, enough for two 12-bit codes
+      // refill test runs once per two lookups (a lane refills every few lookups, but in
+      // a warp SOME lane almost always does, so a per-lookup test costs every lane the
+      // refill path): after it the buffer holds >= 32 bits, enough for two 12-bit
+      // windows. One lookup resolves one symbol, or two when both codes fit the window.
       const uint32_t* p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
       uint64_t buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
       int avail = 64 - (int)(pos & 31);
       uint32_t nextw = p[2];
       p += 3;
+      uint8_t* myb = reinterpret_cast<uint8_t*>(my);
+      int k = 0;
 #pragma unroll 1
-      for (int c = 0; c < HX_SUB / 4; ++c) {
-        uint32_t word = 0;
+      while (k < HX_SUB) {
+        if (avail < 32) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if ((i & 1) == 0 && avail < 32) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
-          const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
-          const int len = (int)(e >> 8);
-          buf >>= len;
-          avail -= len;
-          word |= ((rowmax - (e & 0xFFu)) & 0xFFu) << (8 * i);
+        for (int t = 0; t < 2; ++t) {
+          if (k < HX_SUB) {
+            const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
+            const bool both = (e >> 25) != 0u && k < HX_SUB - 1;
+            const int len = both ? (int)((e >> 20) & 0x1Fu) : (int)((e >> 16) & 0xFu);
+            myb[k] = (uint8_t)(rowmax - (e & 0xFFu));
+            if (both) myb[k + 1] = (uint8_t)(rowmax - ((e >> 8) & 0xFFu));
+            buf >>= len;
+            avail -= len;
+            k += both ? 2 : 1;
+          }
         }
-        my[c] = word;
       }
     }
   }
@@ -235,8 +242,14 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
   const int nblocks = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
   const int per_cta = 32 * HX_EXP_WARPS;
   const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + per_cta - 1) / per_cta;
-  hx_expand_kernel<<<dim3(nblocks, parts), per_cta, 0, (cudaStream_t)stream>>>(
-      static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint16_t*>(lut),
+  constexpr int smem = HX_EXP_WARPS * 32 * HX_EXP_ROW_WORDS * 4;
+  static bool smem_set = false;
+  if (!smem_set) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_set = true;
+  }
+  hx_expand_kernel<<<dim3(nblocks, parts), per_cta, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint32_t*>(lut),
       static_cast<__nv_bfloat16*>(out), ld_out);
   PS_CHECK_LAUNCH();
   return PS_OK;

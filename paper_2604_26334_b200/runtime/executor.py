@@ -247,6 +247,33 @@ class Executor:
         self.stats: list[PassStats] = []
         self.host_tokens: list = []
         self._prev_sample_slots = None
+        self._hx_res_on = self._hx_on
+        # (host_format='coded': the hx copy is the only one there is to upload)
+        if self._hx_on and not self.coded_only and os.environ.get("PS_HX_RESIDENT", "auto") != "1":
+            self._hx_res_on = self._hx_residency_pays(os.environ.get("PS_HX_RESIDENT") == "0")
+
+    def _hx_residency_pays(self, forced_off: bool) -> bool:
+        """Hold resident dense shards hx-coded only when that frees budget the decode tier
+        turns into fewer link bytes (more shards cached). Otherwise every token would pay
+        the per-use expansions for nothing — the tiny model at 50 % (its one streamed
+        shard, the head, does not fit either way) or Qwen3-30B-A3B (its dense shards fit
+        as they are, and an expansion would sit on the per-layer routing chain)."""
+        if forced_off:
+            return False
+        dec = min((t for t in self.plans if t >= self.B), default=max(self.plans))
+
+        def link_bytes(hx_res: bool) -> int:
+            self._hx_res_on = hx_res
+            pins = set(self.pins_for(dec))
+            _, modes = self._plan_modes(self.plans[dec])
+            total = 0
+            for sid in modes:
+                if sid in pins or self.shard_kind[sid] is ShardKind.KV_CACHE:
+                    continue
+                total += self.hx.shard_bytes.get(sid, self.w.layout.blobs[sid].nbytes)
+            return total
+        with_hx, without = link_bytes(True), link_bytes(False)
+        return with_hx < 0.99 * without
 
     # ------------------------------------------------------------------ layout
     def _activation_spec(self, T: int) -> list:
@@ -369,8 +396,9 @@ class Executor:
         return (self.coded is not None and sid in self.coded.tensors and getattr(self.coded, "mapped", False))
 
     def hx_resident(self, sid: int) -> bool:
-        """Dense shards held in VRAM hx-coded (~0.65 x bf16), expanded per use."""
-        return self._hx_on and sid in self.hx.tensors
+        """Dense shards held in VRAM hx-coded (~0.65 x bf16), expanded per use
+        (`_hx_residency_pays`; PS_HX_RESIDENT=1 / 0 forces it on / off)."""
+        return self._hx_on and getattr(self, "_hx_res_on", True) and sid in self.hx.tensors
 
     def phys_bytes(self, sid: int) -> int:
         """VRAM bytes shard `sid` takes when resident (the migration model's size)."""

@@ -182,6 +182,21 @@ def decode(blob: np.ndarray, offs: np.ndarray, table: np.ndarray, n: int, k: int
     return out
 
 
+def pair_table(table: np.ndarray) -> np.ndarray:
+    """The decoder's 4096-entry table (uint32) of `ps_hx_expand`: for every 12-bit
+    LSB-first window, s1 | s2 << 8 | len1 << 16 | (len1 + len2) << 20 | two << 25 — the
+    first symbol and, when the second code also lies inside the window, the second."""
+    single = lookup_table(table).astype(np.uint32)
+    x = np.arange(1 << MAX_LEN, dtype=np.uint32)
+    s1, l1 = single & 0xFF, single >> 8
+    rest = x >> l1
+    e2 = single[rest]
+    s2, l2 = e2 & 0xFF, e2 >> 8
+    two = (l2 <= MAX_LEN - l1).astype(np.uint32)
+    return (s1 | (np.where(two, s2, 0) << 8) | (l1 << 16) | (np.where(two, l1 + l2, l1) << 20)
+            | (two << 25)).astype(np.uint32)
+
+
 def lookup_table(table: np.ndarray) -> np.ndarray:
     """The decoder's 4096-entry table (uint16: symbol | length << 8) for a code table:
     every 12-bit LSB-first window whose low `length` bits are a symbol's reversed code."""
@@ -201,7 +216,7 @@ class HxMatrix:
 
     def __init__(self, n: int, k: int, table: np.ndarray, block_off: np.ndarray):
         self.n, self.k, self.table = n, k, table
-        self.lut = lookup_table(table)
+        self.lut = pair_table(table)
         self.block_off = block_off
         self.nbytes = int(block_off[-1])
 
@@ -284,7 +299,7 @@ class HxShards:
     """hx-coded copies of a model's dense weight shards (attention, FFN, head) in pinned
     host memory: matrices with K % 256 == 0 as hx blobs, everything else (norm vectors)
     raw bf16, tensors 256-byte aligned in blob order. `tensors[sid][name]` = (offset,
-    HxMatrix) or (offset, None) for raw bytes; `luts` holds every matrix's 8 KB decoder
+    HxMatrix) or (offset, None) for raw bytes; `luts` holds every matrix's 16 KB decoder
     table back to back (`lut_off[(sid, name)]`), uploaded once to VRAM by the executor.
 
     Source: the bf16 host blob, or — host_format='coded' (runtime/model.py) — each

@@ -406,7 +406,7 @@ class HostWeights:
             blob = torch.empty(m.nbytes, dtype=torch.uint8, device="cuda")
             L.memcpy_async(blob.data_ptr(), addr, m.nbytes, stream)
             offs = torch.from_numpy(m.block_off[:-1].astype(np.int32)).cuda()
-            lut = torch.from_numpy(m.lut.view(np.int16)).cuda()
+            lut = torch.from_numpy(m.lut.view(np.int32)).cuda()
             out = torch.empty(t.rows, t.cols, dtype=torch.int16, device="cuda")
             L.call("ps_hx_expand", blob.data_ptr(), offs.data_ptr(), t.rows, t.cols, lut.data_ptr(),
                    out.data_ptr(), t.cols, stream)

@@ -47,3 +47,24 @@ def test_geometric_exponents_cost_about_ten_bits():
     blob, _, _ = hx.encode(bits)
     per = blob.nbytes * 8 / bits.size
     assert 9.9 < per < 10.6, per
+
+
+def test_pair_table_decodes_like_single_lookups():
+    """The kernel's two-symbol table (hxcodec.pair_table) resolves each 12-bit window to
+    the same first symbol and length as the single table, and a second symbol only when
+    its whole code lies inside the window (then equal to decoding the rest)."""
+    rng = np.random.default_rng(3)
+    hist = np.zeros(256, np.int64)
+    hist[:30] = (1e6 * 0.55 ** np.arange(30)).astype(np.int64) + 1
+    table = hx.canonical_table(hx.code_lengths(hist))
+    single, pair = hx.lookup_table(table).astype(np.int64), hx.pair_table(table).astype(np.int64)
+    for x in rng.integers(0, 4096, 2000):
+        s1, l1 = single[x] & 0xFF, single[x] >> 8
+        e = pair[x]
+        assert e & 0xFF == s1 and (e >> 16) & 0xF == l1
+        if e >> 25:
+            rest = x >> l1
+            s2, l2 = single[rest] & 0xFF, single[rest] >> 8
+            assert l1 + l2 <= hx.MAX_LEN and (e >> 8) & 0xFF == s2 and (e >> 20) & 0x1F == l1 + l2
+        else:
+            assert (single[x >> l1] >> 8) > hx.MAX_LEN - l1

@@ -704,7 +704,7 @@ def test_hx_encoder_and_expand_exact(N, K):
         lib.host_free(host)
     assert np.array_equal(got, blob)
     dev = torch.from_numpy(blob).cuda()
-    lut = torch.from_numpy(m.lut.view(np.int16)).cuda()
+    lut = torch.from_numpy(m.lut.view(np.int32)).cuda()
     for b0 in (0, 1):
         if b0 * hx.BLOCK_ROWS >= N:
             continue

@@ -43,7 +43,7 @@ for N, K in [(28672, 4096), (4096, 14336), (6144, 4096)]:
     L.memcpy_async(blob.data_ptr(), host, m.nbytes, s)
     torch.cuda.synchronize()
     L.host_free(host)
-    lut = torch.from_numpy(m.lut.view(np.int16)).cuda()
+    lut = torch.from_numpy(m.lut.view(np.int32)).cuda()
     out = torch.empty(N, K, dtype=torch.bfloat16, device="cuda")
     for run_rows in (N, 3584, 1024):
         run_rows = min(N, run_rows)
