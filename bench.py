@@ -213,6 +213,35 @@ def gemv_kernel_roofline(L, peaks) -> dict:
     nbytes_c = coded.nbytes + K * 4 + (N // 2) * 4
     traffic, tsrc = _ncu_traffic("r02_ncu_gemv_bf16_235MB.jsonl")
     traffic_c, tsrc_c = _ncu_traffic("r02_ncu_gemv_coded_177MB.jsonl")
+    # hx: the same matrix Huffman-coded, expanded to bf16 in runs the size of a decode
+    # pass's expand buffer (32 MB at 4 GB), the step every hx-coded weight goes through
+    from paper_2604_26334_b200.runtime import hxcodec as hx
+    enc = hx.GpuHxEncoder()
+    fill = lambda dst, r0, r1: L.memcpy_async(dst, W.data_ptr() + r0 * K * 2, (r1 - r0) * K * 2, s)  # noqa: E731
+    m = enc.plan(fill, N, K)
+    hbuf = L.host_alloc(m.nbytes, mapped=False)
+    enc.write(fill, m, hbuf)
+    blob = torch.empty(m.nbytes, dtype=torch.uint8, device="cuda")
+    L.memcpy_async(blob.data_ptr(), hbuf, m.nbytes, s)
+    torch.cuda.synchronize()
+    L.host_free(hbuf)
+    lut = torch.from_numpy(m.lut.view(np.int32)).cuda()
+    Wx = torch.empty_like(W)
+    run_rows = (32 << 20) // (K * 2)
+    runs = []
+    for r0 in range(0, N, run_rows):
+        ba, bb = r0 // 64, -(-min(N, r0 + run_rows) // 64)
+        runs.append((r0, min(N, r0 + run_rows), int(m.block_off[ba]),
+                     torch.from_numpy((m.block_off[ba:bb] - m.block_off[ba]).astype(np.int32)).cuda()))
+
+    def expand():
+        for r0, r1, b0, rel in runs:
+            L.call("ps_hx_expand", blob.data_ptr() + b0, rel.data_ptr(), r1 - r0, K, lut.data_ptr(),
+                   Wx.data_ptr() + r0 * K * 2, K, s)
+    avg_x = timed(expand)
+    assert torch.equal(Wx, W), "ps_hx_expand is not exact"
+    traffic_x, tsrc_x = _ncu_traffic("r02_ncu_hx_expand_235MB.jsonl")
+    nbytes_x = m.nbytes + N * K * 2
     return {"kernel": "ps_gemv_bf16 (K1 bulk-copy kernel, SwiGLU epilogue) 28672x4096, t=1", "bound": "hbm",
             "achieved": round(nbytes / avg / GB, 1), "peak": peak, "unit": "GB/s",
             "frac": round(nbytes / avg / GB / peak, 4), "algorithmic_bytes": nbytes,
@@ -221,7 +250,16 @@ def gemv_kernel_roofline(L, peaks) -> dict:
             "coded": {"kernel": "ps_gemv_bf16c (exponent-coded rows, same matrix), t=1", "bound": "hbm",
                       "achieved": round(nbytes_c / avg_c / GB, 1), "peak": peak, "unit": "GB/s",
                       "frac": round(nbytes_c / avg_c / GB / peak, 4), "algorithmic_bytes": nbytes_c,
-                      "avg_launch_us": round(avg_c * 1e6, 2), "traffic": traffic_c, "traffic_source": tsrc_c}}
+                      "avg_launch_us": round(avg_c * 1e6, 2), "traffic": traffic_c, "traffic_source": tsrc_c},
+            "hx_expand": {"kernel": f"ps_hx_expand (Huffman-coded rows -> bf16, same matrix, {len(runs)} runs of "
+                                    f"{run_rows} rows = the 32 MB expand buffer)", "bound": "hbm",
+                          "achieved": round(nbytes_x / avg_x / GB, 1), "peak": peak, "unit": "GB/s",
+                          "frac": round(nbytes_x / avg_x / GB / peak, 4), "algorithmic_bytes": nbytes_x,
+                          "bits_per_weight": round(m.nbytes * 8 / (N * K), 3),
+                          "avg_us_per_matrix": round(avg_x * 1e6, 2), "traffic": traffic_x,
+                          "traffic_source": tsrc_x,
+                          "note": "algorithmic bytes = coded read + bf16 written; latency-bound (a serial "
+                                  "Huffman chain per 256-weight sub-block), hidden under the link in decode"}}
 
 
 def link_format(eng) -> str:

@@ -195,6 +195,7 @@ gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant_
         const uint32_t ph = (i / TG_STAGES) & 1;
         const int k0 = (kb0 + i) * TG_K;
         mbar_wait(&empty[s], ph ^ 1);
+        fence_proxy_async_smem();   // consumers' generic reads -> the next bulk copy
         uint8_t* st = sm + s * STG;
         mbar_expect_tx(&full[s], (uint32_t)(TG_B + (COMP ? TG_CS + TG_CN : TG_A)));
         if (COMP) {

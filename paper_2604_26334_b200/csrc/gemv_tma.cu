@@ -153,6 +153,7 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
           const int rb = r0 + b * RS;
           const int nr = min(RS, r1 - rb);
           mbar_wait(&empty[s], ph ^ 1);
+          fence_proxy_async_smem();   // consumers' generic reads -> the next bulk copy
           uint8_t* dst = ring + s * GT_STAGE_BYTES;
           if constexpr (COMP) {
             const uint32_t tb = (uint32_t)(ldw - (long long)K * 3 / 2);   // the row's trailer

@@ -28,6 +28,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Orders this CTA's earlier generic-proxy shared-memory accesses (consumers that read a
+// ring slot, released through an mbarrier the caller just waited on) before the
+// async-proxy writes (cp.async.bulk) the caller issues next into the same slot.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // shared::cluster address of the same smem variable in CTA `rank` of this cluster
 __device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t rank) {
   uint32_t r;

@@ -118,6 +118,7 @@ moe_gu_t1_kernel(const float* __restrict__ x, const int* __restrict__ ids, const
         const int s = b % MD_WARPS;
         const int nr = min(RS, nrows - b * RS);
         mbar_wait(&empty[s], (uint32_t)(((b / MD_WARPS) & 1) ^ 1));
+        fence_proxy_async_smem();   // consumers' generic reads -> the next bulk copy
         mbar_expect_tx(&full[s], (uint32_t)(nr * rowb));
         md_copy(ring + s * GU_SLOT, W + (long long)b * RS * rowb, nr * rowb, chunk, &full[s]);
       }

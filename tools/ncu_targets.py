@@ -4,7 +4,8 @@ captures (round-2 evidence: profiles/r02_ncu_*). Usage: python tools/ncu_targets
 targets: gemv_bf16 | gemv_coded (28672 x 4096, t = 1, SwiGLU: the bench's kernel_roofline
 matrix), gemv_tc_bf16 | gemv_tc_coded (same matrix, t = 32), moe_coded (Qwen3-30B-A3B
 one-token experts, k = 8, coded), attn_tc (Llama-3.3-70B 4096-token causal prefill over a
-paged cache), expand (8192 x 4096 coded piece -> bf16)."""
+paged cache), expand (8192 x 4096 coded piece -> bf16), hx_expand (one 32 MB run of the
+235 MB matrix, Huffman-coded -> bf16)."""
 import ctypes
 import math
 import os
@@ -56,6 +57,26 @@ elif target == "expand":
         L.call("ps_expand_coded", Wc.data_ptr(), rb, N, K, out.data_ptr(), K, s)
     torch.cuda.synchronize()
     assert torch.equal(out, W)
+elif target == "hx_expand":   # the 235 MB matrix, Huffman-coded, expanded in 32 MB runs (decode pass)
+    from paper_2604_26334_b200.runtime import hxcodec as hx
+    N, K = 28672, 4096
+    W = ((torch.rand(N, K, device="cuda", generator=g) * 2 - 1) * math.sqrt(3 / K)).to(torch.bfloat16)
+    enc = hx.GpuHxEncoder()
+    fill = lambda dst, r0, r1: L.memcpy_async(dst, W.data_ptr() + r0 * K * 2, (r1 - r0) * K * 2, s)  # noqa: E731
+    m = enc.plan(fill, N, K)
+    host = L.host_alloc(m.nbytes, mapped=False)
+    enc.write(fill, m, host)
+    blob = torch.empty(m.nbytes, dtype=torch.uint8, device="cuda")
+    L.memcpy_async(blob.data_ptr(), host, m.nbytes, s)
+    torch.cuda.synchronize()
+    lut = torch.from_numpy(m.lut.view(np.int32)).cuda()
+    out = torch.empty(N, K, dtype=torch.bfloat16, device="cuda")
+    rr = (32 << 20) // (K * 2)
+    rel = torch.from_numpy((m.block_off[:rr // 64] - m.block_off[0]).astype(np.int32)).cuda()
+    for _ in range(reps):
+        L.call("ps_hx_expand", blob.data_ptr(), rel.data_ptr(), rr, K, lut.data_ptr(), out.data_ptr(), K, s)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:rr], W[:rr])
 elif target == "moe_coded":
     E, k, d, eff = 32, 8, 2048, 768
     gu = [mat(2 * eff, d) for _ in range(E)]
