@@ -173,6 +173,7 @@ class Executor:
         # cache streamed / CPU-placed weight shards in budget the ring does not need
         # (PS_SPARE_PIN=0 runs the plan's residency exactly)
         self.spare_pin = os.environ.get("PS_SPARE_PIN", "1") != "0"
+        self.spread_pins = os.environ.get("PS_SPREAD_PINS", "1") != "0"
         # ring kept for streaming, in pieces of chunk_cap: a GEMM (prefill) pass computes
         # for ms on each piece and wants a deep ring; a GEMV (decode) pass consumes a
         # piece in microseconds, so two keep the link busy and the rest of the budget
@@ -515,10 +516,17 @@ class Executor:
 
         def value(sid):   # link bytes saved per token per VRAM byte
             return k_frac if self.shard_kind[sid] is ShardKind.MOE_EXPERT_GROUP else 1.0
-        # equal value per byte packs best largest-first (first-fit decreasing)
+        # equal value per byte packs best largest-first (first-fit decreasing); among equal
+        # shards, layers in bit-reversed order (0, L/2, L/4, 3L/4, ...): the cached layers
+        # spread over the pass, so no long run of resident compute (at batch 32, ~1 ms a
+        # layer) outlasts the ring's look-ahead and idles the link
+        nbits = max(1, (self.spec.n_layers - 1).bit_length())
+
+        def spread(layer):
+            return int(format(layer, f"0{nbits}b")[::-1], 2) if self.spread_pins else layer
         cands = sorted((sid for sid in modes if self.shard_kind[sid] is not ShardKind.KV_CACHE),
                        key=lambda sid: (-value(sid), -self._phys_bytes(self.shards[sid]),
-                                        self.shards[sid].priority, self.shards[sid].layer_index, sid))
+                                        self.shards[sid].priority, spread(self.shards[sid].layer_index), sid))
         for sid in cands:
             b = up(self._phys_bytes(self.shards[sid]))
             if b <= spare:
