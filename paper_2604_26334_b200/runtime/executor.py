@@ -389,6 +389,18 @@ class Executor:
             return self.coded.shard_bytes[shard.id]
         return self.w.layout.blobs[shard.id].nbytes
 
+    def _hx_stream_on(self) -> bool:
+        """Stream hx pieces: when the expand buffer takes runs of useful size (>= 4 MB; a
+        30 MB budget's 1/128 would expand a piece in ~100 tiny launches — such budgets
+        stream the 12-bit rows, read directly by the GEMV), or on an hx-only host copy
+        (PS_HX_STREAM=1 / 0 forces it)."""
+        if not self._hx_on:
+            return False
+        env = os.environ.get("PS_HX_STREAM")
+        if env in ("0", "1") and not self.coded_only:
+            return env == "1"
+        return self.coded_only or self._expand_bytes() >= (4 << 20) or self.coded is None
+
     def _zc_readable(self, sid: int) -> bool:
         """A CPU-placed shard can be read zero-copy: the bf16 blob or its 12-bit coded
         copy is on the host (an hx-only host copy must be staged through the ring)."""
@@ -619,10 +631,16 @@ class Executor:
         self.chunk = min(self.chunk_cap, max(1 << 16, (ring_bytes - kv_win) // 6 // 256 * 256))
         need = kv_win + 3 * self.chunk
         streams = kv_win > 0 or any(m in staged for m, _ in self.residency.values())
-        # passes of 9..32 tokens stage CPU-placed shards through the ring (one pass over
-        # them); a budget whose ring cannot hold that keeps reading them zero-copy
-        self.stage_zc = self.T_tier > GEMV_CORE_MAX_T and ring_bytes >= need and \
-            any(m == "zerocopy" for m, _ in self.residency.values())
+        # CPU-placed shards go through the ring when it fits: passes of 9..32 tokens read
+        # them once (not per 8 tokens); a one-token pass gets the copy engine (55.6 vs
+        # ~50 GB/s for SM reads of host memory) and, above all, overlap — the copies run
+        # while the resident layers compute, where a zero-copy read of the head could only
+        # start after them (PS_STAGE_ZC=0: zero-copy at <= 8 tokens). A budget whose ring
+        # cannot hold that keeps reading them zero-copy.
+        small = os.environ.get("PS_STAGE_ZC", "1") != "0"
+        self.stage_zc = (self.T_tier > GEMV_CORE_MAX_T or small) and ring_bytes >= need and \
+            any(m == "zerocopy" and self.shard_kind[sid] is not ShardKind.MOE_EXPERT_GROUP
+                for sid, (m, _) in self.residency.items())
         if streams and ring_bytes < need:
             raise InfeasibleBudget(float(self.arena.capacity),
                                    float(self.arena.capacity - free + need), "copy-engine ring")
@@ -852,7 +870,7 @@ class Executor:
         consumer that reads any tensor in it."""
         mode, dev = self.residency[sid]
         self._zc_direct = False
-        if mode == "zerocopy" and T > GEMV_CORE_MAX_T:
+        if mode == "zerocopy" and (T > GEMV_CORE_MAX_T or self.stage_zc):
             if T > GEMV_MAX_T or self.stage_zc:
                 # one pass over the weights: stage CPU-placed shards through the ring (copy
                 # engine, once) instead of re-reading host memory per 8 tokens or per tile
@@ -952,7 +970,7 @@ class Executor:
             advance_to(len(consumers))
             return
 
-        hxs = (self._hx_on and sid in self.hx.tensors and self.striper is None and
+        hxs = (self._hx_stream_on() and sid in self.hx.tensors and self.striper is None and
                sid not in self._piece_override)
         coded = (not hxs and self.coded is not None and sid in self.coded.tensors and self.striper is None and
                  sid not in self._piece_override and
@@ -1314,7 +1332,8 @@ class Executor:
         weight it reads is VRAM-resident or host-mapped (no ring copies, no fetched
         experts, no stripes), so the only producers of a kernel's inputs are earlier
         kernels on the compute stream."""
-        if T > GEMV_MAX_T or os.environ.get("PS_PDL", "1") == "0" or self.striper is not None:
+        if (T > GEMV_MAX_T or os.environ.get("PS_PDL", "1") == "0" or self.striper is not None
+                or self.stage_zc):
             return False
         if os.environ.get("PS_PDL_STREAMED", "0") == "1":   # experiment: ring + fetcher passes too
             return True

@@ -768,6 +768,7 @@ def test_hx_same_tokens_fewer_bytes(monkeypatch, frac, prompt_len, batch):
     prompts = [_prompt(prompt_len, spec.vocab_size, seed=120 + i) for i in range(batch)]
     out = {}
     monkeypatch.setenv("PS_HX_RESIDENT", "1")   # resident hx even where it frees no link bytes
+    monkeypatch.setenv("PS_HX_STREAM", "1")     # and hx pieces through the small test budgets' buffers
     for h in ("0", "1"):
         monkeypatch.setenv("PS_HX", h)
         eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, batch=batch,
