@@ -631,13 +631,14 @@ class Executor:
         self.chunk = min(self.chunk_cap, max(1 << 16, (ring_bytes - kv_win) // 6 // 256 * 256))
         need = kv_win + 3 * self.chunk
         streams = kv_win > 0 or any(m in staged for m, _ in self.residency.values())
-        # CPU-placed shards go through the ring when it fits: passes of 9..32 tokens read
-        # them once (not per 8 tokens); a one-token pass gets the copy engine (55.6 vs
-        # ~50 GB/s for SM reads of host memory) and, above all, overlap — the copies run
-        # while the resident layers compute, where a zero-copy read of the head could only
-        # start after them (PS_STAGE_ZC=0: zero-copy at <= 8 tokens). A budget whose ring
+        # CPU-placed shards go through the ring when it fits in passes of 9..32 tokens:
+        # read once, not per 8 tokens. One-token passes keep reading them zero-copy:
+        # staging would buy the copy engine (55.6 vs ~50 GB/s) and overlap with the
+        # resident layers, but config 1's 8 MB ring cuts its 25 MB head into ~19 pieces
+        # (a GEMV launch and an event wait each) and ends programmatic dependent launch:
+        # 1337 -> 1121 tokens/s measured (PS_STAGE_ZC=1 turns it on). A budget whose ring
         # cannot hold that keeps reading them zero-copy.
-        small = os.environ.get("PS_STAGE_ZC", "1") != "0"
+        small = os.environ.get("PS_STAGE_ZC", "0") == "1"
         self.stage_zc = (self.T_tier > GEMV_CORE_MAX_T or small) and ring_bytes >= need and \
             any(m == "zerocopy" and self.shard_kind[sid] is not ShardKind.MOE_EXPERT_GROUP
                 for sid, (m, _) in self.residency.items())
