@@ -480,6 +480,7 @@ def run_ours(args, rank: int, world: int) -> dict:
                          if eng.weights.host_format == "coded" else
                          "shared /dev/shm segment per node" if shared else "private pinned blob"),
         "residency": {
+            "resident_form": getattr(eng.executor, "resident_form", "bf16"),
             "spare_pinned_shards": len(eng.executor.spare_pinned),
             "spare_pinned_bytes": int(sum(eng.executor._phys_bytes(eng.executor.shards[sid])
                                           for sid in eng.executor.spare_pinned)),

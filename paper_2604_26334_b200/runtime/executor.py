@@ -236,6 +236,7 @@ class Executor:
             self.hx_meta = self.arena.alloc_high("hx_blocks", 4096)
         self._zc_direct = False
         self.stage_zc = False
+        self.stage_small = False
         self.persist_high = self.arena.high       # activations + ring are carved below, per tier
         self.residency: dict[int, tuple] = {}
         self.tier = None
@@ -255,32 +256,67 @@ class Executor:
         self.host_tokens: list = []
         self._prev_sample_slots = None
         self._hx_res_on = self._hx_on
-        # (host_format='coded': the hx copy is the only one there is to upload)
-        if self._hx_on and not self.coded_only and os.environ.get("PS_HX_RESIDENT", "auto") != "1":
-            self._hx_res_on = self._hx_residency_pays(os.environ.get("PS_HX_RESIDENT") == "0")
+        self._choose_resident_form()
 
-    def _hx_residency_pays(self, forced_off: bool) -> bool:
-        """Hold resident dense shards hx-coded only when that frees budget the decode tier
-        turns into fewer link bytes (more shards cached). Otherwise every token would pay
-        the per-use expansions for nothing — the tiny model at 50 % (its one streamed
-        shard, the head, does not fit either way) or Qwen3-30B-A3B (its dense shards fit
-        as they are, and an expansion would sit on the per-layer routing chain)."""
-        if forced_off:
-            return False
+    def _choose_resident_form(self) -> None:
+        """The form VRAM-resident dense shards take: bf16, 12-bit coded or hx. A coded form
+        frees budget (0.75 / 0.64 x the bytes) that the decode tier may turn into more
+        cached shards and fewer link bytes, but every use then pays a decode (12-bit: in
+        the GEMV's inner loop; hx: an expansion pass). The cheapest form whose decode-tier
+        link bytes are within 1 % of the best is taken: hx for Llama-3.1-8B @ 4 GB; bf16
+        for the tiny model at 50 % (its one streamed shard, the head, fits in no form) and
+        for Qwen3-30B-A3B (its dense shards fit as they are; a decode would sit on the
+        per-layer routing chain). PS_HX_RESIDENT / PS_CODED_RESIDENT = 1 force a form, = 0
+        exclude it; host_format='coded' has only the hx copy to upload."""
+        hx_env = os.environ.get("PS_HX_RESIDENT", "auto")
+        c12_env = os.environ.get("PS_CODED_RESIDENT", "auto")
+        has_hx, has_c12 = self._hx_on, self._coded_res_on
+        if self.coded_only or (has_hx and hx_env == "1"):
+            self._hx_res_on, self._coded_res_on = has_hx, False
+            self.resident_form = "hx" if has_hx else "bf16"
+            return
+        if has_c12 and c12_env == "1":
+            self._hx_res_on, self._coded_res_on = False, True
+            self.resident_form = "c12"
+            return
+        forms = ["bf16"]
+        if has_c12 and c12_env != "0":
+            forms.append("c12")
+        if has_hx and hx_env != "0":
+            forms.append("hx")
         dec = min((t for t in self.plans if t >= self.B), default=max(self.plans))
+        T = min(dec, self.Tmax)
+        k_frac = min(1.0, T * self.moe.top_k / self.moe.n_experts) if self.moe is not None else 1.0
 
-        def link_bytes(hx_res: bool) -> int:
-            self._hx_res_on = hx_res
+        def link_bytes(form: str) -> float:
+            self._hx_res_on, self._coded_res_on = form == "hx", form == "c12"
             pins = set(self.pins_for(dec))
             _, modes = self._plan_modes(self.plans[dec])
-            total = 0
+            total = 0.0
             for sid in modes:
-                if sid in pins or self.shard_kind[sid] is ShardKind.KV_CACHE:
+                kind = self.shard_kind[sid]
+                if sid in pins or kind is ShardKind.KV_CACHE:
                     continue
-                total += self.hx.shard_bytes.get(sid, self.w.layout.blobs[sid].nbytes)
+                nb = self.w.layout.blobs[sid].nbytes
+                total += nb * k_frac if kind is ShardKind.MOE_EXPERT_GROUP else nb
             return total
-        with_hx, without = link_bytes(True), link_bytes(False)
-        return with_hx < 0.99 * without
+        def fits(form: str) -> bool:   # the plan's own pins beside every tier's buffers
+            self._hx_res_on, self._coded_res_on = form == "hx", form == "c12"
+            up = lambda n: (n + 255) // 256 * 256  # noqa: E731
+            for tier, plan in self.plans.items():
+                high = (self.arena.capacity - self.persist_high) + \
+                    sum(up(n) for _, _, n in self._activation_spec(min(tier, self.Tmax)))
+                pinned, _ = self._plan_modes(plan)
+                low = sum(up(self._phys_bytes(self.shards[p.shard_id])) for p in pinned)
+                if low + high > self.arena.capacity:
+                    return False
+            return True
+        feasible = [f for f in forms if fits(f)] or forms[-1:]
+        lb = {f: link_bytes(f) for f in feasible}
+        best = min(lb.values())
+        pick = next(f for f in feasible if lb[f] <= 1.01 * best)
+        self._hx_res_on, self._coded_res_on = pick == "hx", pick == "c12"
+        self.resident_form = pick
 
     # ------------------------------------------------------------------ layout
     def _activation_spec(self, T: int) -> list:
@@ -295,8 +331,7 @@ class Executor:
                      ("hid16", "hid16", T * self.ffn * 2)]
         if T > GEMV_CORE_MAX_T:   # x planes + split-K partials of ps_gemv_tc
             spec.append(("tcws", "gemv_tc_ws", self._tc_workspace_bytes()))
-        if getattr(self, "_hx_on", False) or (
-                T > GEMV_MAX_T and (self._coded_prefill() or getattr(self, "_coded_res_on", False))):
+        if self._hx_used() or (T > GEMV_MAX_T and (self._coded_prefill() or getattr(self, "_coded_res_on", False))):
             # one coded piece (streamed or VRAM-resident) expanded to bf16 for the GEMM, or,
             # with hx, for every pass (hx rows are only ever read through this buffer)
             spec.append(("expand", "coded_expand", self._expand_bytes()))
@@ -315,15 +350,22 @@ class Executor:
                      ("m_slotmap", "moe_slot_of_expert", E * 4)]
         return spec
 
+    def _hx_expand_bytes(self) -> int:
+        """hx expansion buffer: <= 32 MB and 1/128 of the budget, >= one 64-row block of
+        the widest matrix."""
+        kmax = max((m.k for meta in self.hx.tensors.values() for _, m in meta.values() if m is not None),
+                   default=256)
+        return max(64 * kmax * 2, min(32 << 20, int(self.arena.capacity) // 128)) // 256 * 256
+
+    def _hx_used(self) -> bool:
+        return getattr(self, "_hx_on", False) and (getattr(self, "_hx_res_on", False) or self._hx_stream_on())
+
     def _expand_bytes(self) -> int:
-        """The bf16 expansion buffer. hx: <= 32 MB and 1/128 of the budget, >= one 64-row
-        block of the widest matrix; 12-bit coded GEMM pieces: one ring piece at most, and
-        at most 1/64 of the budget (small budgets keep their ring)."""
-        if getattr(self, "_hx_on", False):
-            kmax = max((m.k for meta in self.hx.tensors.values() for _, m in meta.values() if m is not None),
-                       default=256)
-            floor = 64 * kmax * 2
-            return max(floor, min(32 << 20, int(self.arena.capacity) // 128)) // 256 * 256
+        """The bf16 expansion buffer: the hx size when hx rows are in use, else (12-bit
+        coded GEMM pieces) one ring piece at most and at most 1/64 of the budget (small
+        budgets keep their ring)."""
+        if self._hx_used():
+            return self._hx_expand_bytes()
         return max(64 << 10, min(self.chunk_cap, int(self.arena.capacity) // 64)) // 256 * 256
 
     def _coded_prefill(self) -> bool:
@@ -405,7 +447,7 @@ class Executor:
         env = os.environ.get("PS_HX_STREAM")
         if env in ("0", "1") and not self.coded_only:
             return env == "1"
-        return self.coded_only or self._expand_bytes() >= (4 << 20) or self.coded is None
+        return self.coded_only or self._hx_expand_bytes() >= (4 << 20) or self.coded is None
 
     def _zc_readable(self, sid: int) -> bool:
         """A CPU-placed shard can be read zero-copy: the bf16 blob or its 12-bit coded
@@ -416,7 +458,7 @@ class Executor:
 
     def hx_resident(self, sid: int) -> bool:
         """Dense shards held in VRAM hx-coded (~0.65 x bf16), expanded per use
-        (`_hx_residency_pays`; PS_HX_RESIDENT=1 / 0 forces it on / off)."""
+        (`_choose_resident_form`)."""
         return self._hx_on and getattr(self, "_hx_res_on", True) and sid in self.hx.tensors
 
     def phys_bytes(self, sid: int) -> int:
@@ -646,7 +688,7 @@ class Executor:
         # (a GEMV launch and an event wait each) and ends programmatic dependent launch:
         # 1337 -> 1121 tokens/s measured (PS_STAGE_ZC=1 turns it on). A budget whose ring
         # cannot hold that keeps reading them zero-copy.
-        small = os.environ.get("PS_STAGE_ZC", "0") == "1"
+        small = self.stage_small = os.environ.get("PS_STAGE_ZC", "0") == "1"
         self.stage_zc = (self.T_tier > GEMV_CORE_MAX_T or small) and ring_bytes >= need and \
             any(m == "zerocopy" and self.shard_kind[sid] is not ShardKind.MOE_EXPERT_GROUP
                 for sid, (m, _) in self.residency.items())
@@ -879,7 +921,7 @@ class Executor:
         consumer that reads any tensor in it."""
         mode, dev = self.residency[sid]
         self._zc_direct = False
-        if mode == "zerocopy" and (T > GEMV_CORE_MAX_T or self.stage_zc):
+        if mode == "zerocopy" and (T > GEMV_CORE_MAX_T or (self.stage_zc and self.stage_small)):
             if T > GEMV_MAX_T or self.stage_zc:
                 # one pass over the weights: stage CPU-placed shards through the ring (copy
                 # engine, once) instead of re-reading host memory per 8 tokens or per tile
@@ -1342,7 +1384,7 @@ class Executor:
         experts, no stripes), so the only producers of a kernel's inputs are earlier
         kernels on the compute stream."""
         if (T > GEMV_MAX_T or os.environ.get("PS_PDL", "1") == "0" or self.striper is not None
-                or self.stage_zc):
+                or (self.stage_zc and self.stage_small)):
             return False
         if os.environ.get("PS_PDL_STREAMED", "0") == "1":   # experiment: ring + fetcher passes too
             return True

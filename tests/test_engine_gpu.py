@@ -639,7 +639,7 @@ def test_coded_prefill_same_tokens_fewer_bytes(monkeypatch, frac):
         eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160, chunk_bytes=1 << 20)
         res = eng.generate([prompt], gen_len=6)
         pre = [s for s in eng.executor.stats if s.T > 32]
-        out[cp] = (res.tokens[0].tolist(), eng.logits().copy(), sum(s.bytes_streamed for s in pre))
+        out[cp] = (res.tokens[0].tolist(), eng.logits().copy(), sum(s.bytes_streamed - s.kv_bytes for s in pre))
         eng.close()
     assert out["1"][0] == out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1])
