@@ -173,6 +173,13 @@ int ps_wencode_rows(const void* bits, int N, int K, long long ld, const int* bas
  * zeroed buffer). No reference counterpart: the link format is this build's. */
 int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, const void* lut, void* out,
                  long long ld_out, void* stream);
+/* The k routed experts of a MoE layer fetched hx-coded into slots (rank j in slot j, slot
+ * stride slot_stride): each slot's span carries the uint32 block offsets of the matrix at
+ * word hdr_word and the matrix at mat_off; expands `rows` x K into scratch expert j at
+ * out_off (bf16 rows of K), for the bf16 one-token expert kernels. */
+int ps_hx_expand_experts(const void* slots, long long slot_stride, int k, int hdr_word, long long mat_off, int rows,
+                         int K, const void* lut, void* scratch, long long scratch_stride, long long out_off,
+                         void* stream);
 int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist, void* stream);
 int ps_hx_sizes(const void* bits, int N, int K, long long ld, const int* rowmax, const unsigned* table,
                 unsigned short* sublen, unsigned* rowbytes, void* stream);

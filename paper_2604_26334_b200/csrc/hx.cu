@@ -37,9 +37,11 @@ __device__ __forceinline__ int hx_header_bytes(int K) { return ((4 + 2 * (K / HX
 constexpr int HX_EXP_WARPS = 4;
 constexpr int HX_EXP_ROW_WORDS = HX_SUB / 4 + 1;   // 64 exponent words + 1 (bank offset)
 
-__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
-hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
-                 const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
+// One CTA's share (`part`) of one 64-row block: `block` = the block's bytes, `nr` rows,
+// `out` = bf16 row 0 of the block (ld_out elements per row), lut_g = the 4096-entry table.
+__device__ __forceinline__ void hx_expand_block(const uint8_t* __restrict__ block, int nr, int K, int part,
+                                                const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out,
+                                                long long ld_out) {
   __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | len1 << 16 | len1+len2 << 20 | two << 25
   __shared__ uint32_t row_start[HX_BLOCK_ROWS];
   extern __shared__ uint32_t hx_exps[];   // [warp][lane][65] exponent rows (dynamic: > 48 KB static)
@@ -52,9 +54,7 @@ hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__
     uint4* dst = reinterpret_cast<uint4*>(lut);
     for (int i = threadIdx.x; i < HX_LUT / 4; i += 32 * HX_EXP_WARPS) dst[i] = src[i];
   }
-  const uint8_t* block = piece + blk[blockIdx.x];
-  const int r0 = blockIdx.x * HX_BLOCK_ROWS;
-  const int nr = min(HX_BLOCK_ROWS, rows - r0);
+  const int r0 = 0;
   if (warp == 0) {   // row starts: exclusive scan of the 64 row sizes
     const uint32_t* sizes = reinterpret_cast<const uint32_t*>(block);
     uint32_t a = lane < nr ? sizes[lane] : 0u;
@@ -70,7 +70,7 @@ hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__
     row_start[lane + 32] = 256 + tot_a + sb - b;
   }
   __syncthreads();
-  const int task0 = (blockIdx.y * HX_EXP_WARPS + warp) * 32;
+  const int task0 = (part * HX_EXP_WARPS + warp) * 32;
   if (task0 >= nr * nsub) return;   // whole warp (no block-level barrier below)
   uint32_t* my = exps[warp][lane];
   // ---- phase 1: this lane's sub-block -> 256 exponents in shared memory
@@ -148,6 +148,33 @@ hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__
           make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
+}
+
+
+__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
+hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
+                 const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
+  const int r0 = blockIdx.x * HX_BLOCK_ROWS;
+  hx_expand_block(piece + blk[blockIdx.x], min(HX_BLOCK_ROWS, rows - r0), K, blockIdx.y, lut_g,
+                  out + (long long)r0 * ld_out, ld_out);
+}
+
+// The routed experts of one MoE layer, fetched hx-coded into slots (expert rank j in slot
+// j): each slot holds a span [uint32 block offsets of the matrix][...][hx matrix], the
+// offsets at hdr_word (n_blocks of them), the matrix at mat_off. CTA (j * n_blocks + b,
+// part) expands block b of expert j's matrix into scratch expert j (out_off bytes into
+// it, rows of K bf16): the bf16 one-token expert kernels then read the scratch slots.
+__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
+hx_expand_experts_kernel(const uint8_t* __restrict__ slots, long long slot_stride, int hdr_word, long long mat_off,
+                         int rows, int K, const uint32_t* __restrict__ lut_g, uint8_t* __restrict__ scratch,
+                         long long scratch_stride, long long out_off) {
+  const int nb = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
+  const int j = blockIdx.x / nb, b = blockIdx.x - (blockIdx.x / nb) * nb;
+  const uint8_t* span = slots + j * slot_stride;
+  const uint32_t off = reinterpret_cast<const uint32_t*>(span)[hdr_word + b];
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(scratch + j * scratch_stride + out_off) +
+                       (long long)b * HX_BLOCK_ROWS * K;
+  hx_expand_block(span + mat_off + off, min(HX_BLOCK_ROWS, rows - b * HX_BLOCK_ROWS), K, blockIdx.y, lut_g, out, K);
 }
 
 __device__ __forceinline__ int hx_exp(uint16_t b) { return (b >> 7) & 0xFF; }
@@ -255,6 +282,31 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
   return PS_OK;
 }
 
+extern "C" int ps_hx_expand_experts(const void* slots, long long slot_stride, int k, int hdr_word,
+                                    long long mat_off, int rows, int K, const void* lut, void* scratch,
+                                    long long scratch_stride, long long out_off, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K > 0 && K % HX_SUB == 0 && rows > 0 && k >= 0, "ps_hx_expand_experts: K %d rows %d k %d", K, rows, k);
+  PS_REQUIRE(((uintptr_t)slots & 15) == 0 && (slot_stride & 255) == 0 && (mat_off & 15) == 0 &&
+             ((uintptr_t)scratch & 15) == 0 && (scratch_stride & 15) == 0 && (out_off & 15) == 0,
+             "ps_hx_expand_experts: alignment");
+  if (k == 0) return PS_OK;
+  const int nb = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
+  const int per_cta = 32 * HX_EXP_WARPS;
+  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + per_cta - 1) / per_cta;
+  constexpr int smem = HX_EXP_WARPS * 32 * HX_EXP_ROW_WORDS * 4;
+  static bool smem_set = false;
+  if (!smem_set) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_experts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_set = true;
+  }
+  hx_expand_experts_kernel<<<dim3(k * nb, parts), per_cta, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(slots), slot_stride, hdr_word, mat_off, rows, K, static_cast<const uint32_t*>(lut),
+      static_cast<uint8_t*>(scratch), scratch_stride, out_off);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
 extern "C" int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist,
                            void* stream) {
   using namespace ps;
@@ -294,5 +346,6 @@ int ps_preload_hx() {
   using namespace ps;
   int n = 0;
   touch_kernel(hx_expand_kernel, n);
+  touch_kernel(hx_expand_experts_kernel, n);
   return n;
 }

@@ -186,11 +186,14 @@ class Engine:
         return "bf16"
 
     def _needs_coded12(self) -> bool:
-        """The 12-bit coded copy serves what hx does not: CPU-placed (zero-copy) shards and
-        routed experts. Built when some plan places a shard on the CPU backend, for MoE
-        models, or when hx is off (PS_HX=0)."""
+        """The 12-bit coded copy serves what hx does not: CPU-placed (zero-copy) shards, and
+        routed experts when the hx copy has none. Built when some plan places a shard on
+        the CPU backend, for MoE models without hx experts, or when hx is off (PS_HX=0)."""
         from ..planning.vocab import Backend
-        if self.spec.moe is not None or os.environ.get("PS_HX", "1") == "0":
+        hx = getattr(self.weights, "hx", None)
+        if os.environ.get("PS_HX", "1") == "0" or hx is None:
+            return True
+        if self.spec.moe is not None and (not hx.experts or os.environ.get("PS_HX_EXPERTS", "1") == "0"):
             return True
         return any(p.exec_backend is Backend.CPU for plan in self.plans.values() for p in plan.placements)
 
@@ -200,7 +203,7 @@ class Engine:
         are held in that form. Node-shared with node-shared weights; skipped (bf16 /
         12-bit streaming) when host memory is short."""
         from .hxcodec import HxShards
-        kinds = (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD)
+        kinds = (ShardKind.ATTENTION, ShardKind.FFN, ShardKind.OUTPUT_HEAD, ShardKind.MOE_EXPERT_GROUP)
         dense = sum(b.nbytes for b in self.weights.layout.blobs.values() if b.kind in kinds)
         need = dense * 2 // 3
         shared = None
@@ -258,12 +261,12 @@ class Engine:
     def _ensure_executor(self, max_tokens: int) -> Executor:
         if self.executor is None:
             tiers_used = self.plans
-            if (os.environ.get("PS_CODED", "1") == "1" and getattr(self.weights, "coded", None) is None
-                    and self.weights.host_format == "bf16" and self._needs_coded12()):
-                self._build_coded()
             if (os.environ.get("PS_CODED", "1") == "1" and os.environ.get("PS_HX", "1") != "0"
                     and getattr(self.weights, "hx", None) is None and self.weights.host_format == "bf16"):
                 self._build_hx()
+            if (os.environ.get("PS_CODED", "1") == "1" and getattr(self.weights, "coded", None) is None
+                    and self.weights.host_format == "bf16" and self._needs_coded12()):
+                self._build_coded()
             self.executor = Executor(self.weights, self.arch, tiers_used, self.budget,
                                      self.batch, self.context_len,
                                      self.max_tokens or max_tokens, chunk_bytes=self.chunk_bytes,

@@ -339,6 +339,11 @@ class Executor:
         # split-KV partials of ps_attn_decode (any pass with <= 32 tokens, whatever the tier)
         ws = L.attn_decode_workspace(B, self.h, self.hd, self.cap)
         spec.append(("ws", "attn_ws", max(1, ws) * 4))
+        if self.moe is not None and self._hx_experts_on(T):
+            # bf16 scratch experts the hx-coded routed experts expand into (blob layout)
+            sid0 = next(iter(self.hx.experts))
+            _, estride, _, _ = self._expert_geometry(sid0, self.shards[sid0].layer_index)
+            spec.append(("hx_escratch", "hx_expert_scratch", self.moe.top_k * estride))
         if self.moe is not None:
             E, k, eff = self.moe.n_experts, self.moe.top_k, self.moe.expert_ffn_dim
             P = T * k
@@ -393,7 +398,7 @@ class Executor:
     def _carve_activations(self, T: int) -> None:
         """Activation buffers for passes of <= T tokens (re-carved per tier, so a
         decode tier holds only what the plan's activation scratch allows)."""
-        self.xn16 = self.att16 = self.hid16 = self.tcws = self.expand = 0
+        self.xn16 = self.att16 = self.hid16 = self.tcws = self.expand = self.hx_escratch = 0
         for attr, tag, n in self._activation_spec(T):
             setattr(self, attr, self.arena.alloc_high(tag, n))
         self.ws_floats = L.attn_decode_workspace(self.B, self.h, self.hd, self.cap)
@@ -448,6 +453,11 @@ class Executor:
         if env in ("0", "1") and not self.coded_only:
             return env == "1"
         return self.coded_only or self._hx_expand_bytes() >= (4 << 20) or self.coded is None
+
+    def _hx_experts_on(self, T: int) -> bool:
+        """One-token MoE passes fetch routed experts hx-coded (PS_HX_EXPERTS=0: off)."""
+        return (T == 1 and self._hx_on and bool(getattr(self.hx, "experts", None)) and self.fetch_enabled and
+                os.environ.get("PS_HX_EXPERTS", "1") != "0")
 
     def _zc_readable(self, sid: int) -> bool:
         """A CPU-placed shard can be read zero-copy: the bf16 blob or its 12-bit coded
@@ -1169,12 +1179,25 @@ class Executor:
             if not t1:
                 L.call("ps_moe_plan", self.m_ids, P, E, self.m_plan, self.cs)
 
-        # routed experts exponent-coded through the fetcher (one-token kernels only)
-        cexp = None
-        if (t1 and fetched and self.coded is not None and os.environ.get("PS_CODED_EXPERTS", "1") != "0"):
+        # routed experts coded through the fetcher (one-token kernels only): hx-coded
+        # (expanded to bf16 scratch slots on arrival), else 12-bit (decoded in the kernels)
+        cexp = hxe = None
+        if t1 and fetched and self._hx_experts_on(1):
+            hxe = self.hx.experts.get(sid)
+        if (hxe is None and t1 and fetched and self.coded is not None and
+                os.environ.get("PS_CODED_EXPERTS", "1") != "0"):
             cexp = getattr(self.coded, "experts", {}).get(sid)
 
         def decode_t1(ebase, slot_map):
+            if hxe is not None:   # the k routed spans -> bf16 scratch experts (blob layout)
+                sc, sst = self.hx_escratch, stride
+                L.call("ps_hx_expand_experts", ebase, sb, k, 0, hxe["gu_off"], hxe["gu_rows"], hxe["gu_k"],
+                       self.hx_lut + self.hx.lut_off[(sid, "wgu")], sc, sst, 0, self.cs)
+                L.call("ps_hx_expand_experts", ebase, sb, k, hxe["nb_gu"], hxe["dn_off"], hxe["dn_rows"],
+                       hxe["dn_k"], self.hx_lut + self.hx.lut_off[(sid, "wdown")], sc, sst, down_off, self.cs)
+                L.call("ps_moe_decode_experts", xn, self.m_ids, k, slot_map, sc, sst, 0, down_off, eff, d,
+                       self.m_h, self.m_w, self.x, self.cs)
+                return
             if cexp is not None:
                 L.call("ps_moe_decode_experts_c", xn, self.m_ids, k, slot_map, ebase, sb, 0, cexp[2], eff, d,
                        cexp[4], cexp[5], self.m_h, self.m_w, self.x, self.cs)
@@ -1194,7 +1217,9 @@ class Executor:
             _, _, _, ebytes = self._expert_geometry(sid, layer)
             slots, sb = self.expert_slots, self.expert_slot_bytes
             src0, src_stride = host + e0.offset, stride
-            if cexp is not None:      # coded experts: 25 % fewer bytes per routed expert
+            if hxe is not None:       # hx experts: ~35 % fewer bytes per routed expert
+                src0, src_stride, ebytes = self.hx.shard_ptr(sid), hxe["stride"], hxe["stride"]
+            elif cexp is not None:    # coded experts: 25 % fewer bytes per routed expert
                 src0, src_stride, ebytes = self.coded.shard_ptr(sid) + cexp[0], cexp[1], cexp[3]
             self.fetch_seq = (self.fetch_seq + 1) & 0xFFFFFFFF or 1
             seq = self.fetch_seq

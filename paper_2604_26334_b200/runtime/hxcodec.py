@@ -216,9 +216,16 @@ class HxMatrix:
 
     def __init__(self, n: int, k: int, table: np.ndarray, block_off: np.ndarray):
         self.n, self.k, self.table = n, k, table
-        self.lut = pair_table(table)
+        self._lut = None
         self.block_off = block_off
         self.nbytes = int(block_off[-1])
+
+    @property
+    def lut(self) -> np.ndarray:
+        """The decoder table (pair_table), built on first use."""
+        if self._lut is None:
+            self._lut = pair_table(self.table)
+        return self._lut
 
     def blocks_for_rows(self, r0: int, r1: int) -> tuple:
         """(first block, end block) covering rows [r0, r1) (r0 on a block boundary)."""
@@ -262,9 +269,20 @@ class GpuHxEncoder:
                rowbytes.data_ptr(), self.stream)
         return table, tab, rowmax, sublen, rowbytes
 
-    def plan(self, src, n: int, k: int) -> HxMatrix:
+    def histogram(self, src, n: int, k: int) -> np.ndarray:
+        """Histogram (int64 [256]) of d = rowmax - exponent over a matrix."""
+        torch, L = self.torch, self.L
         bits = self._stage(src, n, k)
-        table, _, _, _, rowbytes = self._sizes(bits, n, k, None)
+        rowmax = torch.empty(n, dtype=torch.int32, device="cuda")
+        hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+        L.call("ps_hx_stats", bits.data_ptr(), n, k, k, rowmax.data_ptr(), hist.data_ptr(), self.stream)
+        return hist.cpu().numpy()
+
+    def plan(self, src, n: int, k: int, table: np.ndarray | None = None) -> HxMatrix:
+        """Layout of the matrix coded with its own Huffman code, or with `table` (a code
+        shared by several matrices, e.g. the experts of one MoE layer)."""
+        bits = self._stage(src, n, k)
+        table, _, _, _, rowbytes = self._sizes(bits, n, k, table)
         rb = rowbytes.cpu().numpy().view(np.uint32).astype(np.uint64)
         nb = -(-n // BLOCK_ROWS)
         per_block = np.zeros(nb, np.uint64)
@@ -323,9 +341,18 @@ class HxShards:
             return weights.tensor_ptr(sid, name)
 
         self.tensors, self.shard_off, self.shard_bytes, self.lut_off = {}, {}, {}, {}
+        self.experts = {}      # MoE group sid -> expert span geometry (see _plan_experts)
         luts, off = [], 0
         for sid, blob in layout.blobs.items():
-            if blob.kind not in kinds or blob.kind is ShardKind.MOE_EXPERT_GROUP:
+            if blob.kind is ShardKind.MOE_EXPERT_GROUP and blob.kind in kinds:
+                geo = self._plan_experts(enc, source, sid, blob, luts)
+                if geo is not None:
+                    self.experts[sid] = geo
+                    self.shard_off[sid] = off
+                    self.shard_bytes[sid] = geo["n_experts"] * geo["stride"]
+                    off += self.shard_bytes[sid]
+                continue
+            if blob.kind not in kinds:
                 continue
             self.shard_off[sid] = off
             t_off, meta = 0, {}
@@ -358,6 +385,8 @@ class HxShards:
         else:
             self.host = L.host_alloc(self.nbytes, mapped=True)
         try:
+            for sid, geo in self.experts.items():
+                self._write_experts(enc, source, sid, geo)
             for sid, meta in self.tensors.items():
                 for name, (o, m) in meta.items():
                     dst = self.host + self.shard_off[sid] + o
@@ -376,9 +405,60 @@ class HxShards:
         if self.seg is not None:
             self.seg.mark_ready()
 
+    def _plan_experts(self, enc, source, sid, blob, luts) -> dict | None:
+        """Routed experts of one MoE group, hx-coded with one Huffman code per matrix kind
+        (gate/up, down) shared by the group's experts, so one decoder table serves every
+        expert a layer routes to. Expert e is a uniform-stride span
+            [uint32 block offsets of gate/up, then of down | pad to 256]
+            [gate/up hx, padded to the group's largest][down hx, padded likewise]
+        (the padding is < 0.5 % here), so the fetcher copies expert e from e * stride, and
+        the expansion kernel finds each block from the offsets that travel with it."""
+        layer = blob.layer
+        names = {kind: [f"L{layer}.e{e}.{kind}" for e in range(sum(1 for n in blob.tensors
+                                                                   if n.endswith(".wgu")))]
+                 for kind in ("wgu", "wdown")}
+        ts = {n: blob.tensors[n] for kind in names for n in names[kind]}
+        if any(t.cols % SUB for t in ts.values()):
+            return None
+        plans, tables = {}, {}
+        for kind, ns in names.items():
+            hist = sum(enc.histogram(source(sid, n), ts[n].rows, ts[n].cols) for n in ns)
+            tables[kind] = canonical_table(code_lengths(hist))
+            for n in ns:
+                plans[n] = enc.plan(source(sid, n), ts[n].rows, ts[n].cols, table=tables[kind])
+        up = lambda v: (v + 255) // 256 * 256  # noqa: E731
+        g0 = plans[names["wgu"][0]]
+        d0 = plans[names["wdown"][0]]
+        nb_gu, nb_dn = len(g0.block_off) - 1, len(d0.block_off) - 1
+        H = up(4 * (nb_gu + nb_dn))
+        G = up(max(plans[n].nbytes for n in names["wgu"]))
+        D = up(max(plans[n].nbytes for n in names["wdown"]))
+        geo = {"n_experts": len(names["wgu"]), "stride": H + G + D, "gu_off": H, "dn_off": H + G,
+               "nb_gu": nb_gu, "nb_dn": nb_dn, "gu_rows": g0.n, "dn_rows": d0.n, "gu_k": g0.k, "dn_k": d0.k,
+               "names": names, "plans": plans, "actual_bytes": sum(H + plans[g].nbytes + plans[d].nbytes
+                                                                   for g, d in zip(names["wgu"], names["wdown"]))}
+        for kind in ("wgu", "wdown"):
+            lut = pair_table(tables[kind])
+            self.lut_off[(sid, kind)] = len(luts) * lut.nbytes
+            luts.append(lut)
+        return geo
+
+    def _write_experts(self, enc, source, sid, geo) -> None:
+        import ctypes
+        base = self.host + self.shard_off[sid]
+        ctypes.memset(base, 0, self.shard_bytes[sid])
+        for e, (g, d) in enumerate(zip(geo["names"]["wgu"], geo["names"]["wdown"])):
+            span = base + e * geo["stride"]
+            mg, md = geo["plans"][g], geo["plans"][d]
+            hdr = np.concatenate([mg.block_off[:-1], md.block_off[:-1]]).astype(np.uint32)
+            ctypes.memmove(span, hdr.ctypes.data, hdr.nbytes)
+            enc.write(source(sid, g), mg, span + geo["gu_off"])
+            enc.write(source(sid, d), md, span + geo["dn_off"])
+
     @property
     def hx_bytes(self) -> int:
-        return sum(self.shard_bytes.values())
+        """Bytes of the dense shards' hx copies."""
+        return sum(self.shard_bytes[sid] for sid in self.tensors)
 
     def shard_ptr(self, sid: int) -> int:
         return self.host + self.shard_off[sid]

@@ -604,6 +604,7 @@ def test_moe_coded_experts_same_tokens_fewer_bytes(monkeypatch):
     spec = dataclasses.replace(base, moe=MoeSpec(base.moe.n_experts, base.moe.top_k, 256))
     prompt = _prompt(24, spec.vocab_size, seed=17)
     out = {}
+    monkeypatch.setenv("PS_HX", "0")     # the 12-bit experts under test (hx experts would take them)
     for ce in ("0", "1"):
         monkeypatch.setenv("PS_CODED_EXPERTS", ce)
         # at 100 % of the weights the decode plan streams both expert groups (GPU_ONLY):
@@ -787,3 +788,37 @@ def test_hx_same_tokens_fewer_bytes(monkeypatch, frac, prompt_len, batch):
     assert np.array_equal(out["1"][1], out["0"][1])
     assert out["1"][4] > 0 and out["0"][4] == 0
     assert out["1"][2] <= out["0"][2], (out["0"][2], out["1"][2])
+
+
+def test_moe_hx_experts_same_tokens_fewer_bytes(monkeypatch):
+    """One-token MoE decode with the routed experts fetched hx-coded (one Huffman code per
+    matrix kind shared by a layer's experts, uniform-stride spans carrying their block
+    offsets) and expanded into bf16 scratch slots (ps_hx_expand_experts) ahead of the
+    bf16 expert kernels: same tokens and logits as 12-bit experts (PS_HX_EXPERTS=0), fewer
+    fetched bytes, decided-exact against the oracle."""
+    import dataclasses
+    from oracle.model_ref import RefModel, hp_from_spec
+    from paper_2604_26334_b200.planning.graph import MoeSpec
+    from paper_2604_26334_b200.runtime.engine import Engine
+    from paper_2604_26334_b200.runtime.model import arch_for
+    base = catalog.builtin_model("tiny-moe")
+    spec = dataclasses.replace(base, moe=MoeSpec(base.moe.n_experts, base.moe.top_k, 256))
+    prompt = _prompt(24, spec.vocab_size, seed=18)
+    out = {}
+    for he in ("0", "1"):
+        monkeypatch.setenv("PS_HX_EXPERTS", he)
+        eng = Engine(spec, budget_bytes=1.0 * total_model_bytes(spec), context_len=160)
+        res = eng.generate([prompt], gen_len=12)
+        st = eng.executor.fetcher_stats()
+        hx = eng.weights.hx
+        out[he] = (res.tokens[0].tolist(), eng.logits().copy(), st, bool(hx and hx.experts), res.row_modes[0])
+        eng.close()
+    assert out["1"][3], "no expert group was hx-coded"
+    assert out["1"][2]["experts_copied"] == out["0"][2]["experts_copied"] > 0
+    # (tiny experts: the per-expert header and padding weigh more than at Qwen3 sizes,
+    # where a span is 0.87 x the 12-bit expert)
+    assert out["1"][2]["bytes_copied"] < 0.97 * out["0"][2]["bytes_copied"], (out["0"][2], out["1"][2])
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
+    ref = RefModel(hp_from_spec(spec, arch_for(spec)), seed=0)
+    assert_exact_parity(ref, prompt, np.array(out["1"][0]), out["1"][4])
