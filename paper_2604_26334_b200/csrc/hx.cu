@@ -35,25 +35,19 @@ __device__ __forceinline__ int hx_header_bytes(int K) { return ((4 + 2 * (K / HX
 //   2. the warp assembles the 32 sub-blocks one at a time, lane l taking 8 columns: the
 //      sign|mantissa loads (256 B) and the bf16 stores (512 B) are coalesced.
 constexpr int HX_EXP_WARPS = 4;
-constexpr int HX_EXP_ROW_WORDS = HX_SUB / 4 + 1;   // 64 exponent words + 1 (bank offset)
+constexpr int HX_CHUNK = 64;                        // symbols per decode round
+constexpr int HX_EXP_ROW_WORDS = HX_CHUNK / 4 + 1;  // 16 exponent words + 1 (bank offset)
 
 // One CTA's share (`part`) of one 64-row block: `block` = the block's bytes, `nr` rows,
-// `out` = bf16 row 0 of the block (ld_out elements per row), lut_g = the 4096-entry table.
-__device__ __forceinline__ void hx_expand_block(const uint8_t* __restrict__ block, int nr, int K, int part,
-                                                const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out,
-                                                long long ld_out) {
-  __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | len1 << 16 | len1+len2 << 20 | two << 25
-  __shared__ uint32_t row_start[HX_BLOCK_ROWS];
-  extern __shared__ uint32_t hx_exps[];   // [warp][lane][65] exponent rows (dynamic: > 48 KB static)
-  auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);
+// `out` = bf16 row 0 of the block (ld_out elements per row); lut = the 4096-entry table
+// already in shared memory. Every thread reaches both barriers (the CTA loops over items).
+__device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block, int nr, int K, int part,
+                                               const uint32_t* __restrict__ lut, uint32_t* __restrict__ row_start,
+                                               uint32_t (*exps)[32][HX_EXP_ROW_WORDS],
+                                               __nv_bfloat16* __restrict__ out, long long ld_out) {
   const int nsub = K / HX_SUB;
   const int hb = hx_header_bytes(K);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(lut_g);
-    uint4* dst = reinterpret_cast<uint4*>(lut);
-    for (int i = threadIdx.x; i < HX_LUT / 4; i += 32 * HX_EXP_WARPS) dst[i] = src[i];
-  }
   const int r0 = 0;
   if (warp == 0) {   // row starts: exclusive scan of the 64 row sizes
     const uint32_t* sizes = reinterpret_cast<const uint32_t*>(block);
@@ -71,16 +65,27 @@ __device__ __forceinline__ void hx_expand_block(const uint8_t* __restrict__ bloc
   }
   __syncthreads();
   const int task0 = (part * HX_EXP_WARPS + warp) * 32;
-  if (task0 >= nr * nsub) return;   // whole warp (no block-level barrier below)
-  uint32_t* my = exps[warp][lane];
-  // ---- phase 1: this lane's sub-block -> 256 exponents in shared memory
-  {
+  if (task0 < nr * nsub) {   // (warps past the block's tasks skip to the closing barrier)
+    // Four rounds of 64 symbols: each lane decodes the next 64 exponents of ITS sub-block
+    // (serial: the bit stream is a chain) into its 64-byte shared row (17 words:
+    // conflict-free), then the warp assembles those 64 columns of all 32 sub-blocks —
+    // 8 lanes per sub-block, 16-B coalesced loads and stores. A 2 KB buffer per warp
+    // instead of 8 KB keeps ~2x the warps resident to hide the decode chain.
+    uint32_t* my = exps[warp][lane];
+    uint8_t* myb = reinterpret_cast<uint8_t*>(my);
+    const int ntask = min(32, nr * nsub - task0);
     const int task = task0 + lane;
     const int r = task / nsub, s = task - (task / nsub) * nsub;
-    if (r < nr) {
+    const bool live = lane < ntask;
+    uint32_t rowmax = 0;
+    const uint32_t* p = nullptr;
+    uint64_t buf = 0;
+    int avail = 64;
+    uint32_t nextw = 0;
+    if (live) {
       const uint8_t* row = block + row_start[r];
       const uint16_t* hdr = reinterpret_cast<const uint16_t*>(row);
-      const uint32_t rowmax = hdr[0];
+      rowmax = hdr[0];
       uint32_t pos = 0;
       for (int i = 0; i < s; ++i) pos += hdr[2 + i];
       // 64-bit bit buffer, refilled one word at a time with one word of look-ahead; the
@@ -88,93 +93,123 @@ __device__ __forceinline__ void hx_expand_block(const uint8_t* __restrict__ bloc
       // a warp SOME lane almost always does, so a per-lookup test costs every lane the
       // refill path): after it the buffer holds >= 32 bits, enough for two 12-bit
       // windows. One lookup resolves one symbol, or two when both codes fit the window.
-      const uint32_t* p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
-      uint64_t buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
-      int avail = 64 - (int)(pos & 31);
-      uint32_t nextw = p[2];
+      p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
+      buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
+      avail = 64 - (int)(pos & 31);
+      nextw = p[2];
       p += 3;
-      uint8_t* myb = reinterpret_cast<uint8_t*>(my);
-      int k = 0;
+    }
+    const int q = lane >> 3, l8 = lane & 7;   // phase 2: sub-block 4 i + q, columns 8 l8 ..
 #pragma unroll 1
-      while (k < HX_SUB) {
-        if (avail < 32) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
+    for (int c0 = 0; c0 < HX_SUB; c0 += HX_CHUNK) {
+      if (live) {
+        int k = 0;
+#pragma unroll 1
+        while (k < HX_CHUNK) {
+          if (avail < 32) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (k < HX_SUB) {
-            const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
-            const bool both = (e >> 25) != 0u && k < HX_SUB - 1;
-            const int len = both ? (int)((e >> 20) & 0x1Fu) : (int)((e >> 16) & 0xFu);
-            myb[k] = (uint8_t)(rowmax - (e & 0xFFu));
-            if (both) myb[k + 1] = (uint8_t)(rowmax - ((e >> 8) & 0xFFu));
-            buf >>= len;
-            avail -= len;
-            k += both ? 2 : 1;
+          for (int t = 0; t < 2; ++t) {
+            if (k < HX_CHUNK) {
+              const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
+              const bool both = (e >> 25) != 0u && k < HX_CHUNK - 1;
+              const int len = both ? (int)((e >> 20) & 0x1Fu) : (int)((e >> 16) & 0xFu);
+              myb[k] = (uint8_t)(rowmax - (e & 0xFFu));
+              if (both) myb[k + 1] = (uint8_t)(rowmax - ((e >> 8) & 0xFFu));
+              buf >>= len;
+              avail -= len;
+              k += both ? 2 : 1;
+            }
           }
         }
       }
-    }
-  }
-  __syncwarp();
-  // ---- phase 2: sub-block j of this warp, lane -> columns [8 lane, 8 lane + 8); the
-  // sign|mantissa loads of 8 sub-blocks are issued together (one memory latency per 8)
-  const int ntask = min(32, nr * nsub - task0);
-#pragma unroll 1
-  for (int j0 = 0; j0 < ntask; j0 += 8) {
-    uint2 mm[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int task = task0 + j0 + u;
-      const int r = task / nsub, s = task - (task / nsub) * nsub;
-      mm[u] = j0 + u < ntask ? *reinterpret_cast<const uint2*>(block + row_start[r] + hb + s * HX_SUB + 8 * lane)
-                             : make_uint2(0u, 0u);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int j = j0 + u;
-      if (j >= ntask) break;
-      const int task = task0 + j;
-      const int r = task / nsub, s = task - (task / nsub) * nsub;
-      const uint32_t e0 = exps[warp][j][2 * lane], e1 = exps[warp][j][2 * lane + 1];
-      const uint32_t mw[2] = {mm[u].x, mm[u].y}, ew[2] = {e0, e1};
-      uint32_t w[4];
+      __syncwarp();
+      uint2 mm[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const uint32_t b = (mw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-        const uint32_t ex = (ew[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-        const uint32_t h = ((b & 0x80u) << 8) | (ex << 7) | (b & 0x7Fu);
-        if (i & 1) w[i >> 1] |= h << 16; else w[i >> 1] = h;
+        const int j = 4 * i + q;
+        const int tj = task0 + j, rj = tj / nsub, sj = tj - (tj / nsub) * nsub;
+        mm[i] = j < ntask ? *reinterpret_cast<const uint2*>(block + row_start[rj] + hb + sj * HX_SUB + c0 + 8 * l8)
+                          : make_uint2(0u, 0u);
       }
-      *reinterpret_cast<uint4*>(out + (long long)(r0 + r) * ld_out + s * HX_SUB + 8 * lane) =
-          make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = 4 * i + q;
+        if (j < ntask) {
+          const int tj = task0 + j, rj = tj / nsub, sj = tj - (tj / nsub) * nsub;
+          const uint32_t e0 = exps[warp][j][2 * l8], e1 = exps[warp][j][2 * l8 + 1];
+          const uint32_t mw[2] = {mm[i].x, mm[i].y}, ew[2] = {e0, e1};
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t b = (mw[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+            const uint32_t ex = (ew[u >> 2] >> (8 * (u & 3))) & 0xFFu;
+            const uint32_t h = ((b & 0x80u) << 8) | (ex << 7) | (b & 0x7Fu);
+            if (u & 1) w[u >> 1] |= h << 16; else w[u >> 1] = h;
+          }
+          *reinterpret_cast<uint4*>(out + (long long)(r0 + rj) * ld_out + sj * HX_SUB + c0 + 8 * l8) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      __syncwarp();   // the next round overwrites the rows
     }
   }
+  __syncthreads();   // row_start / exps are reused by the CTA's next item
 }
 
+// The table is loaded once per CTA and CTAs loop over items (one part of a 64-row block):
+// a CTA per item read the 16 KB table per 128 sub-blocks (32 KB of weights) — ncu r02:
+// the top stall of the expert expansion.
+__device__ __forceinline__ void hx_load_lut(const uint32_t* __restrict__ lut_g, uint32_t* lut) {
+  const uint4* src = reinterpret_cast<const uint4*>(lut_g);
+  uint4* dst = reinterpret_cast<uint4*>(lut);
+  for (int i = threadIdx.x; i < HX_LUT / 4; i += 32 * HX_EXP_WARPS) dst[i] = src[i];
+  __syncthreads();
+}
 
 __global__ void __launch_bounds__(32 * HX_EXP_WARPS)
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
                  const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
-  const int r0 = blockIdx.x * HX_BLOCK_ROWS;
-  hx_expand_block(piece + blk[blockIdx.x], min(HX_BLOCK_ROWS, rows - r0), K, blockIdx.y, lut_g,
-                  out + (long long)r0 * ld_out, ld_out);
+  __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | len1 << 16 | len1+len2 << 20 | two << 25
+  __shared__ uint32_t row_start[HX_BLOCK_ROWS];
+  extern __shared__ uint32_t hx_exps[];   // [warp][lane][65] exponent rows (dynamic: > 48 KB static)
+  auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);
+  hx_load_lut(lut_g, lut);
+  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + 32 * HX_EXP_WARPS - 1) / (32 * HX_EXP_WARPS);
+  const int nb = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
+  for (int item = blockIdx.x; item < nb * parts; item += gridDim.x) {
+    const int b = item / parts, part = item - b * parts;
+    const int r0 = b * HX_BLOCK_ROWS;
+    hx_expand_item(piece + blk[b], min(HX_BLOCK_ROWS, rows - r0), K, part, lut, row_start, exps,
+                   out + (long long)r0 * ld_out, ld_out);
+  }
 }
 
 // The routed experts of one MoE layer, fetched hx-coded into slots (expert rank j in slot
 // j): each slot holds a span [uint32 block offsets of the matrix][...][hx matrix], the
-// offsets at hdr_word (n_blocks of them), the matrix at mat_off. CTA (j * n_blocks + b,
-// part) expands block b of expert j's matrix into scratch expert j (out_off bytes into
-// it, rows of K bf16): the bf16 one-token expert kernels then read the scratch slots.
+// offsets at hdr_word (n_blocks of them), the matrix at mat_off. Item (j, b, part) expands
+// block b of expert j's matrix into scratch expert j (out_off bytes into it, rows of K
+// bf16): the bf16 one-token expert kernels then read the scratch slots.
 __global__ void __launch_bounds__(32 * HX_EXP_WARPS)
-hx_expand_experts_kernel(const uint8_t* __restrict__ slots, long long slot_stride, int hdr_word, long long mat_off,
-                         int rows, int K, const uint32_t* __restrict__ lut_g, uint8_t* __restrict__ scratch,
-                         long long scratch_stride, long long out_off) {
+hx_expand_experts_kernel(const uint8_t* __restrict__ slots, long long slot_stride, int k, int hdr_word,
+                         long long mat_off, int rows, int K, const uint32_t* __restrict__ lut_g,
+                         uint8_t* __restrict__ scratch, long long scratch_stride, long long out_off) {
+  __shared__ uint32_t lut[HX_LUT];
+  __shared__ uint32_t row_start[HX_BLOCK_ROWS];
+  extern __shared__ uint32_t hx_exps[];
+  auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);
+  hx_load_lut(lut_g, lut);
+  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + 32 * HX_EXP_WARPS - 1) / (32 * HX_EXP_WARPS);
   const int nb = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
-  const int j = blockIdx.x / nb, b = blockIdx.x - (blockIdx.x / nb) * nb;
-  const uint8_t* span = slots + j * slot_stride;
-  const uint32_t off = reinterpret_cast<const uint32_t*>(span)[hdr_word + b];
-  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(scratch + j * scratch_stride + out_off) +
+  for (int item = blockIdx.x; item < k * nb * parts; item += gridDim.x) {
+    const int part = item % parts, jb = item / parts;
+    const int j = jb / nb, b = jb - (jb / nb) * nb;
+    const uint8_t* span = slots + j * slot_stride;
+    const uint32_t off = reinterpret_cast<const uint32_t*>(span)[hdr_word + b];
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(scratch + j * scratch_stride + out_off) +
                        (long long)b * HX_BLOCK_ROWS * K;
-  hx_expand_block(span + mat_off + off, min(HX_BLOCK_ROWS, rows - b * HX_BLOCK_ROWS), K, blockIdx.y, lut_g, out, K);
+    hx_expand_item(span + mat_off + off, min(HX_BLOCK_ROWS, rows - b * HX_BLOCK_ROWS), K, part, lut, row_start,
+                   exps, o, K);
+  }
 }
 
 __device__ __forceinline__ int hx_exp(uint16_t b) { return (b >> 7) & 0xFF; }
@@ -256,6 +291,18 @@ hx_write_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const in
   }
 }
 
+// resident CTAs of the expand kernels (8 per SM at ~25 KB of shared memory each)
+static int hx_grid_cap() {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = 8 * (sms > 0 ? sms : 148);
+  }
+  return cap;
+}
+
 }  // namespace ps
 
 extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, const void* lut,
@@ -275,7 +322,8 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
     PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     smem_set = true;
   }
-  hx_expand_kernel<<<dim3(nblocks, parts), per_cta, smem, (cudaStream_t)stream>>>(
+  const int grid = min(nblocks * parts, hx_grid_cap());
+  hx_expand_kernel<<<grid, per_cta, smem, (cudaStream_t)stream>>>(
       static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint32_t*>(lut),
       static_cast<__nv_bfloat16*>(out), ld_out);
   PS_CHECK_LAUNCH();
@@ -300,8 +348,9 @@ extern "C" int ps_hx_expand_experts(const void* slots, long long slot_stride, in
     PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_experts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     smem_set = true;
   }
-  hx_expand_experts_kernel<<<dim3(k * nb, parts), per_cta, smem, (cudaStream_t)stream>>>(
-      static_cast<const uint8_t*>(slots), slot_stride, hdr_word, mat_off, rows, K, static_cast<const uint32_t*>(lut),
+  const int grid = min(k * nb * parts, hx_grid_cap());
+  hx_expand_experts_kernel<<<grid, per_cta, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(slots), slot_stride, k, hdr_word, mat_off, rows, K, static_cast<const uint32_t*>(lut),
       static_cast<uint8_t*>(scratch), scratch_stride, out_off);
   PS_CHECK_LAUNCH();
   return PS_OK;
