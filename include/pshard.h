@@ -266,6 +266,14 @@ int ps_moe_decode_experts_c(const float* x, const int* ids, int k, const int* sl
                             const void* expert_base, long long expert_stride, long long gu_off,
                             long long down_off, int eff, int d, int gu_row_bytes, int down_row_bytes,
                             float* h, const float* w, float* y, void* stream);
+/* ps_moe_decode_experts (bf16 rows) in phases: phase 1 = gate/up + SwiGLU into h for the
+ * routed experts whose slot (rank, slot_of_expert) lies in [rank_lo, rank_hi); phase 2 =
+ * down + combine over all k (the same order as the one-call form: bit-identical); 3 =
+ * both. Lets the first experts of a layer compute while the rest are still arriving. */
+int ps_moe_decode_experts_phase(const float* x, const int* ids, int k, const int* slot_of_expert,
+                                const void* expert_base, long long expert_stride, long long gu_off,
+                                long long down_off, int eff, int d, float* h, const float* w, float* y, int phase,
+                                int rank_lo, int rank_hi, void* stream);
 
 /* ---- routed-expert fetcher (copy-engine uploads of router-selected experts) --
  * Replaces the zero-copy read of a streamed expert group in decode passes: the GPU
@@ -280,6 +288,11 @@ int ps_fetcher_info(void* fetcher, void** copy_stream, void** flag_dev, long lon
                     long long* bytes_copied, int* error);
 int ps_fetcher_submit(void* fetcher, unsigned seq, const void* host_base, long long expert_stride,
                       long long expert_bytes, void* slot_base, long long slot_stride);
+/* The same, raising the flag to seq - 1 once the first `split` ranks' copies are issued
+ * (then to seq after the rest): ps_wait_flag(seq - 1) releases the first experts early.
+ * seq >= 2; the caller advances its sequence by 2 per layer. */
+int ps_fetcher_submit_split(void* fetcher, unsigned seq, const void* host_base, long long expert_stride,
+                            long long expert_bytes, void* slot_base, long long slot_stride, int split);
 int ps_moe_publish(void* fetcher, const int* ids, int P, int E, int* slot_of_expert, unsigned seq,
                    void* stream);
 int ps_wait_flag(void* fetcher, unsigned seq, void* stream);

@@ -101,6 +101,7 @@ struct FetchJob {
   long long expert_stride, expert_bytes;
   char* slot_base;
   long long slot_stride;
+  int split;   // > 0: after the first `split` ranks are issued, raise the flag to seq - 1
 };
 
 class ExpertFetcher {
@@ -207,10 +208,19 @@ class ExpertFetcher {
           break;
         }
       }
+      bool half_sent = j.split <= 0;
       for (unsigned r = 0; r < n;) {
+        if (!half_sent && r >= (unsigned)j.split) {   // the first ranks have landed: seq - 1
+          unsigned* hs = seq_src_ + (ring_i_++ % kSeqRing);
+          *hs = j.seq - 1;
+          if (cudaMemcpyAsync(flag_dev_, hs, sizeof(unsigned), cudaMemcpyHostToDevice, stream_) != cudaSuccess)
+            error_.store(3);
+          half_sent = true;
+        }
         const unsigned e = ids[r];
         unsigned run = 1;
-        while (coalesce && r + run < n && ids[r + run] == e + run) ++run;
+        const unsigned lim = half_sent ? n : (unsigned)j.split;   // runs never cross the split
+        while (coalesce && r + run < lim && ids[r + run] == e + run) ++run;
         const long long bytes = (long long)(run - 1) * j.expert_stride + j.expert_bytes;
         if (cudaMemcpyAsync(j.slot_base + r * j.slot_stride, j.host_base + (long long)e * j.expert_stride, bytes,
                             cudaMemcpyHostToDevice, stream_) != cudaSuccess)
@@ -300,7 +310,18 @@ int ps_fetcher_submit(void* f, unsigned seq, const void* host_base, long long ex
   PS_REQUIRE(x != nullptr, "ps_fetcher_submit: null fetcher");
   PS_REQUIRE(expert_bytes > 0 && slot_stride >= expert_bytes, "ps_fetcher_submit: bad sizes");
   x->submit(FetchJob{seq, static_cast<const char*>(host_base), expert_stride, expert_bytes,
-                     static_cast<char*>(slot_base), slot_stride});
+                     static_cast<char*>(slot_base), slot_stride, 0});
+  return PS_OK;
+}
+
+int ps_fetcher_submit_split(void* f, unsigned seq, const void* host_base, long long expert_stride,
+                            long long expert_bytes, void* slot_base, long long slot_stride, int split) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr, "ps_fetcher_submit_split: null fetcher");
+  PS_REQUIRE(expert_bytes > 0 && slot_stride >= expert_bytes && split >= 1 && seq >= 2,
+             "ps_fetcher_submit_split: bad sizes / split %d / seq %u", split, seq);
+  x->submit(FetchJob{seq, static_cast<const char*>(host_base), expert_stride, expert_bytes,
+                     static_cast<char*>(slot_base), slot_stride, split});
   return PS_OK;
 }
 

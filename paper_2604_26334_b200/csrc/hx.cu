@@ -81,7 +81,7 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
     const uint32_t* p = nullptr;
     uint64_t buf = 0;
     int avail = 64;
-    uint32_t nextw = 0;
+    uint32_t nextw = 0, nextw2 = 0;
     if (live) {
       const uint8_t* row = block + row_start[r];
       const uint16_t* hdr = reinterpret_cast<const uint16_t*>(row);
@@ -96,8 +96,9 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
       p = reinterpret_cast<const uint32_t*>(row + hb + K) + (pos >> 5);
       buf = (((uint64_t)p[1] << 32) | p[0]) >> (pos & 31);
       avail = 64 - (int)(pos & 31);
-      nextw = p[2];
-      p += 3;
+      nextw = p[2];     // two words of look-ahead (~28 symbols): a refill's load has the time
+      nextw2 = p[3];    // of ~14 lookups to come back from L2 (the stream lines rarely stay in L1)
+      p += 4;
     }
     const int q = lane >> 3, l8 = lane & 7;   // phase 2: sub-block 4 i + q, columns 8 l8 ..
 #pragma unroll 1
@@ -106,7 +107,12 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
         int k = 0;
 #pragma unroll 1
         while (k < HX_CHUNK) {
-          if (avail < 32) { buf |= (uint64_t)nextw << avail; avail += 32; nextw = *p++; }
+          if (avail < 32) {
+            buf |= (uint64_t)nextw << avail;
+            avail += 32;
+            nextw = nextw2;
+            nextw2 = *p++;
+          }
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (k < HX_CHUNK) {

@@ -89,12 +89,16 @@ template <int NG, bool COMP>
 __global__ void __launch_bounds__(MD_THREADS, 1)
 moe_gu_t1_kernel(const float* __restrict__ x, const int* __restrict__ ids, const int* __restrict__ slot_of_expert,
                  const unsigned char* __restrict__ base, long long expert_stride, long long mat_off, int N, int K,
-                 float* __restrict__ h, int C, int R, int chunk, int rowb) {
+                 float* __restrict__ h, int C, int R, int chunk, int rowb, int rank_lo, int rank_hi) {
   constexpr int G = NG > 0 ? NG : MD_MAXG;
   extern __shared__ __align__(128) uint8_t smem[];
   const int j = blockIdx.x / C, c = blockIdx.x - j * C;
   const int r0 = c * R;
   if (r0 >= N) return;
+  if (slot_of_expert) {   // only the routed experts whose slot (rank) is in [rank_lo, rank_hi)
+    const int rk = slot_of_expert[ids[j]];
+    if (rk < rank_lo || rk >= rank_hi) return;   // whole CTA, before any barrier
+  }
   const int nrows = min(N, r0 + R) - r0;
   const int RS = GU_SLOT / rowb;
   const int nst = (nrows + RS - 1) / RS;
@@ -284,7 +288,8 @@ using namespace ps;
 template <bool COMP>
 static int md_launch(const float* x, const int* ids, int k, const int* slot_of_expert, const void* expert_base,
                      long long expert_stride, long long gu_off, long long down_off, int eff, int d, float* h,
-                     const float* w, float* y, cudaStream_t s, int gu_rowb, int down_rowb) {
+                     const float* w, float* y, cudaStream_t s, int gu_rowb, int down_rowb, int phase = 3,
+                     int rank_lo = 0, int rank_hi = 1 << 30) {
   if (!g_md_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -303,7 +308,7 @@ static int md_launch(const float* x, const int* ids, int k, const int* slot_of_e
   const int Rg = 2 * ((eff + C - 1) / C);
   const size_t sg = md_smem(Rg);
   using GuKernel = void (*)(const float*, const int*, const int*, const unsigned char*, long long, long long, int, int,
-                           float*, int, int, int, int);
+                           float*, int, int, int, int, int, int);
   const int ngu = d % 256 ? 0 : d / 256;
   GuKernel gk = moe_gu_t1_kernel<0, COMP>;
   switch (ngu) {
@@ -319,9 +324,12 @@ static int md_launch(const float* x, const int* ids, int k, const int* slot_of_e
     set_gu[ngu] = sg;
   }
   PS_REQUIRE(GU_SLOT / gu_rowb >= 1, "ps_moe_decode_experts: gate/up rows of %d bytes exceed a ring slot", gu_rowb);
-  gk<<<k * C, MD_THREADS, sg, s>>>(x, ids, slot_of_expert, base, expert_stride, gu_off, 2 * eff, d, h, C, Rg,
-                                   g_md_chunk, gu_rowb);
-  PS_CHECK_LAUNCH();
+  if (phase & 1) {
+    gk<<<k * C, MD_THREADS, sg, s>>>(x, ids, slot_of_expert, base, expert_stride, gu_off, 2 * eff, d, h, C, Rg,
+                                     g_md_chunk, gu_rowb, rank_lo, rank_hi);
+    PS_CHECK_LAUNCH();
+  }
+  if (!(phase & 2)) return PS_OK;
   // down + combine: row blocks of R rows, one ring slot per expert, all in flight
   int Rd = (d + g_md_sms - 1) / g_md_sms;
   int slot_bytes = (Rd * down_rowb + 127) / 128 * 128;
@@ -376,6 +384,18 @@ int ps_moe_decode_experts(const float* x, const int* ids, int k, const int* slot
   if (rc) return rc;
   return md_launch<false>(x, ids, k, slot_of_expert, expert_base, expert_stride, gu_off, down_off, eff, d, h, w, y,
                           (cudaStream_t)stream, d * 2, eff * 2);
+}
+
+int ps_moe_decode_experts_phase(const float* x, const int* ids, int k, const int* slot_of_expert,
+                                const void* expert_base, long long expert_stride, long long gu_off, long long down_off,
+                                int eff, int d, float* h, const float* w, float* y, int phase, int rank_lo,
+                                int rank_hi, void* stream) {
+  int rc = md_check(k, eff, d, expert_stride, gu_off, down_off, expert_base);
+  if (rc) return rc;
+  PS_REQUIRE(phase >= 1 && phase <= 3 && (phase == 2 || slot_of_expert != nullptr || (rank_lo <= 0 && rank_hi >= k)),
+             "ps_moe_decode_experts_phase: phase %d, ranks [%d, %d) need slot_of_expert", phase, rank_lo, rank_hi);
+  return md_launch<false>(x, ids, k, slot_of_expert, expert_base, expert_stride, gu_off, down_off, eff, d, h, w, y,
+                          (cudaStream_t)stream, d * 2, eff * 2, phase, rank_lo, rank_hi);
 }
 
 int ps_moe_decode_experts_c(const float* x, const int* ids, int k, const int* slot_of_expert,

@@ -1188,15 +1188,23 @@ class Executor:
                 os.environ.get("PS_CODED_EXPERTS", "1") != "0"):
             cexp = getattr(self.coded, "experts", {}).get(sid)
 
+        def hx_gate_up(ebase, slot_map, r0, r1):
+            """Routed experts of ranks [r0, r1): spans -> bf16 scratch experts (blob layout),
+            then their gate/up + SwiGLU."""
+            sc, sst = self.hx_escratch, stride
+            L.call("ps_hx_expand_experts", ebase + r0 * sb, sb, r1 - r0, 0, hxe["gu_off"], hxe["gu_rows"],
+                   hxe["gu_k"], self.hx_lut + self.hx.lut_off[(sid, "wgu")], sc + r0 * sst, sst, 0, self.cs)
+            L.call("ps_hx_expand_experts", ebase + r0 * sb, sb, r1 - r0, hxe["nb_gu"], hxe["dn_off"],
+                   hxe["dn_rows"], hxe["dn_k"], self.hx_lut + self.hx.lut_off[(sid, "wdown")], sc + r0 * sst, sst,
+                   down_off, self.cs)
+            L.call("ps_moe_decode_experts_phase", xn, self.m_ids, k, slot_map, sc, sst, 0, down_off, eff, d,
+                   self.m_h, self.m_w, self.x, 1, r0, r1, self.cs)
+
         def decode_t1(ebase, slot_map):
-            if hxe is not None:   # the k routed spans -> bf16 scratch experts (blob layout)
-                sc, sst = self.hx_escratch, stride
-                L.call("ps_hx_expand_experts", ebase, sb, k, 0, hxe["gu_off"], hxe["gu_rows"], hxe["gu_k"],
-                       self.hx_lut + self.hx.lut_off[(sid, "wgu")], sc, sst, 0, self.cs)
-                L.call("ps_hx_expand_experts", ebase, sb, k, hxe["nb_gu"], hxe["dn_off"], hxe["dn_rows"],
-                       hxe["dn_k"], self.hx_lut + self.hx.lut_off[(sid, "wdown")], sc, sst, down_off, self.cs)
-                L.call("ps_moe_decode_experts", xn, self.m_ids, k, slot_map, sc, sst, 0, down_off, eff, d,
-                       self.m_h, self.m_w, self.x, self.cs)
+            if hxe is not None:   # (unsplit: every rank has landed)
+                hx_gate_up(ebase, slot_map, 0, k)
+                L.call("ps_moe_decode_experts_phase", xn, self.m_ids, k, slot_map, self.hx_escratch, stride, 0,
+                       down_off, eff, d, self.m_h, self.m_w, self.x, 2, 0, k, self.cs)
                 return
             if cexp is not None:
                 L.call("ps_moe_decode_experts_c", xn, self.m_ids, k, slot_map, ebase, sb, 0, cexp[2], eff, d,
@@ -1221,7 +1229,15 @@ class Executor:
                 src0, src_stride, ebytes = self.hx.shard_ptr(sid), hxe["stride"], hxe["stride"]
             elif cexp is not None:    # coded experts: 25 % fewer bytes per routed expert
                 src0, src_stride, ebytes = self.coded.shard_ptr(sid) + cexp[0], cexp[1], cexp[3]
-            self.fetch_seq = (self.fetch_seq + 1) & 0xFFFFFFFF or 1
+            # PS_MOE_SPLIT=1: hx experts arrive in two halves, the first half's expansion and
+            # gate/up running while the second half is still crossing the link (flag seq - 1,
+            # then seq). Measured neutral on config 3 (19.85 vs 19.80 tokens/s): the chain
+            # after the last expert lands is the expansion's fixed latency (one 256-weight
+            # serial decode), the same for 4 experts as for 8. Off by default.
+            split = k // 2 if (hxe is not None and k >= 2 and os.environ.get("PS_MOE_SPLIT", "0") == "1") else 0
+            self.fetch_seq = (self.fetch_seq + (2 if split else 1)) & 0xFFFFFFFF
+            if self.fetch_seq < 2:
+                self.fetch_seq = 2
             seq = self.fetch_seq
             pre = self._prefix_dev.pop(sid, None)     # ffn_norm + router staged by gap filling
             if pre is not None:
@@ -1235,13 +1251,23 @@ class Executor:
                 self.ring.seal(region, [self._record(self.cs)])
 
             def fetch(_p, _a, _b):
-                L.call("ps_fetcher_submit", self.fetcher, seq, src0, src_stride, ebytes, slots, sb)
+                if split:
+                    L.call("ps_fetcher_submit_split", self.fetcher, seq, src0, src_stride, ebytes, slots, sb, split)
+                else:
+                    L.call("ps_fetcher_submit", self.fetcher, seq, src0, src_stride, ebytes, slots, sb)
                 L.call("ps_moe_publish", self.fetcher, self.m_ids, P, E, self.m_slotmap, seq, self.cs)
-                L.call("ps_wait_flag", self.fetcher, seq, self.cs)
+                L.call("ps_wait_flag", self.fetcher, seq - 1 if split else seq, self.cs)
                 if os.environ.get("PS_FETCH_DEBUG"):
                     self._fetch_debug(layer, seq, P, E, src0, src_stride, ebytes, slots, sb)
 
             def run(_p, _a, _b):
+                if t1 and split:
+                    hx_gate_up(slots, self.m_slotmap, 0, split)           # first half, landed
+                    L.call("ps_wait_flag", self.fetcher, seq, self.cs)     # the rest
+                    hx_gate_up(slots, self.m_slotmap, split, k)
+                    L.call("ps_moe_decode_experts_phase", xn, self.m_ids, k, self.m_slotmap, self.hx_escratch,
+                           stride, 0, down_off, eff, d, self.m_h, self.m_w, self.x, 2, 0, k, self.cs)
+                    return
                 if t1:
                     decode_t1(slots, self.m_slotmap)
                     return

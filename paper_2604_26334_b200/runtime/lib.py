@@ -69,6 +69,7 @@ _SIGS = {
     "ps_fetcher_destroy": [_p],
     "ps_fetcher_info": [_p, _pp, _pp, C.POINTER(_ll), C.POINTER(_ll), C.POINTER(_i)],
     "ps_fetcher_submit": [_p, C.c_uint, _p, _ll, _ll, _p, _ll],
+    "ps_fetcher_submit_split": [_p, C.c_uint, _p, _ll, _ll, _p, _ll, _i],
     "ps_moe_publish": [_p, _p, _i, _i, _p, C.c_uint, _p],
     "ps_wait_flag": [_p, C.c_uint, _p],
     "ps_fetcher_device_error": [_p, C.POINTER(C.c_uint)],
@@ -97,6 +98,7 @@ _SIGS = {
     "ps_gemv_bf16c": [_p, _i, _i, _p, _i, _i, _ll, _p, _i, _i, _p],
     "ps_moe_decode_experts": [_p, _p, _i, _p, _p, _ll, _ll, _ll, _i, _i, _p, _p, _p, _p],
     "ps_moe_decode_experts_c": [_p, _p, _i, _p, _p, _ll, _ll, _ll, _i, _i, _i, _i, _p, _p, _p, _p],
+    "ps_moe_decode_experts_phase": [_p, _p, _i, _p, _p, _ll, _ll, _ll, _i, _i, _p, _p, _p, _i, _i, _i, _p],
     "ps_embed_gather": [_p, _p, _i, _i, _p, _i, _p],
     "ps_argmax": [_p, _i, _i, _i, _p, _p],
     "ps_cast_f32_bf16": [_p, _i, _p, _i, _i, _i, _p],
@@ -142,7 +144,7 @@ KERNEL_CALLS = frozenset({
     "ps_gemv_bf16", "ps_gemm_bf16", "ps_rmsnorm", "ps_qkv_rope_append", "ps_attn_decode",
     "ps_attn_prefill", "ps_embed_gather", "ps_argmax", "ps_cast_f32_bf16", "ps_add_f32",
     "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_init_rowscaled_bf16", "ps_gemv_bf16_cfg", "ps_gemm_bf16_cfg",
-    "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine", "ps_moe_decode_experts", "ps_moe_decode_experts_c", "ps_gemv_bf16c", "ps_gemv_tc", "ps_expand_coded",
+    "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine", "ps_moe_decode_experts", "ps_moe_decode_experts_c", "ps_moe_decode_experts_phase", "ps_gemv_bf16c", "ps_gemv_tc", "ps_expand_coded",
     "ps_wencode_stats", "ps_wencode_rows", "ps_hx_expand", "ps_hx_expand_experts", "ps_hx_stats", "ps_hx_sizes", "ps_hx_write",
     "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_wait_flag",
     "ps_stripe_signal", "ps_stripe_wait", "ps_attn_prefill_tc"})
