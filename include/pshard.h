@@ -180,6 +180,11 @@ int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, 
 int ps_hx_expand_experts(const void* slots, long long slot_stride, int k, int hdr_word, long long mat_off, int rows,
                          int K, const void* lut, void* scratch, long long scratch_stride, long long out_off,
                          void* stream);
+/* Both matrices of the routed experts (A = gate/up, B = down) in one launch (the expansion
+ * is latency-bound: one launch's latency instead of two on the routing chain). */
+int ps_hx_expand_experts2(const void* slots, long long slot_stride, int k, int hdr_a, long long mat_a, int rows_a,
+                          int K_a, const void* lut_a, long long out_a, int hdr_b, long long mat_b, int rows_b, int K_b,
+                          const void* lut_b, long long out_b, void* scratch, long long scratch_stride, void* stream);
 int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist, void* stream);
 int ps_hx_sizes(const void* bits, int N, int K, long long ld, const int* rowmax, const unsigned* table,
                 unsigned short* sublen, unsigned* rowbytes, void* stream);

@@ -297,6 +297,43 @@ hx_write_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const in
   }
 }
 
+// Both matrices of the routed experts (gate/up, down) in ONE launch: the expansion is
+// latency-bound (a 256-weight serial decode per lane), so two back-to-back launches cost
+// two decode latencies on the routing chain; here CTAs [0, grid_a) expand matrix A with
+// its table, the rest matrix B with its own.
+struct HxExpertMat {
+  int hdr_word;
+  long long mat_off;
+  int rows, K;
+  const uint32_t* lut;
+  long long out_off;
+};
+
+__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
+hx_expand_experts2_kernel(const uint8_t* __restrict__ slots, long long slot_stride, int k, HxExpertMat a,
+                          HxExpertMat b, int grid_a, uint8_t* __restrict__ scratch, long long scratch_stride) {
+  __shared__ uint32_t lut[HX_LUT];
+  __shared__ uint32_t row_start[HX_BLOCK_ROWS];
+  extern __shared__ uint32_t hx_exps[];
+  auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);
+  const bool is_a = (int)blockIdx.x < grid_a;
+  const HxExpertMat& m = is_a ? a : b;
+  const int cta = is_a ? blockIdx.x : blockIdx.x - grid_a, ncta = is_a ? grid_a : gridDim.x - grid_a;
+  hx_load_lut(m.lut, lut);
+  const int parts = (HX_BLOCK_ROWS * (m.K / HX_SUB) + 32 * HX_EXP_WARPS - 1) / (32 * HX_EXP_WARPS);
+  const int nb = (m.rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
+  for (int item = cta; item < k * nb * parts; item += ncta) {
+    const int part = item % parts, jb = item / parts;
+    const int j = jb / nb, bb = jb - (jb / nb) * nb;
+    const uint8_t* span = slots + j * slot_stride;
+    const uint32_t off = reinterpret_cast<const uint32_t*>(span)[m.hdr_word + bb];
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(scratch + j * scratch_stride + m.out_off) +
+                       (long long)bb * HX_BLOCK_ROWS * m.K;
+    hx_expand_item(span + m.mat_off + off, min(HX_BLOCK_ROWS, m.rows - bb * HX_BLOCK_ROWS), m.K, part, lut,
+                   row_start, exps, o, m.K);
+  }
+}
+
 // resident CTAs of the expand kernels (8 per SM at ~25 KB of shared memory each)
 static int hx_grid_cap() {
   static int cap = 0;
@@ -362,6 +399,42 @@ extern "C" int ps_hx_expand_experts(const void* slots, long long slot_stride, in
   return PS_OK;
 }
 
+extern "C" int ps_hx_expand_experts2(const void* slots, long long slot_stride, int k, int hdr_a, long long mat_a,
+                                     int rows_a, int K_a, const void* lut_a, long long out_a, int hdr_b,
+                                     long long mat_b, int rows_b, int K_b, const void* lut_b, long long out_b,
+                                     void* scratch, long long scratch_stride, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K_a > 0 && K_a % HX_SUB == 0 && K_b > 0 && K_b % HX_SUB == 0 && rows_a > 0 && rows_b > 0 && k >= 0,
+             "ps_hx_expand_experts2: K %d / %d rows %d / %d k %d", K_a, K_b, rows_a, rows_b, k);
+  PS_REQUIRE(((uintptr_t)slots & 15) == 0 && (slot_stride & 255) == 0 && ((mat_a | mat_b) & 15) == 0 &&
+                 ((uintptr_t)scratch & 15) == 0 && (scratch_stride & 15) == 0 && ((out_a | out_b) & 15) == 0,
+             "ps_hx_expand_experts2: alignment");
+  if (k == 0) return PS_OK;
+  const int per_cta = 32 * HX_EXP_WARPS;
+  auto items = [&](int rows, int K) {
+    return k * ((rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS) * ((HX_BLOCK_ROWS * (K / HX_SUB) + per_cta - 1) / per_cta);
+  };
+  const int ia = items(rows_a, K_a), ib = items(rows_b, K_b);
+  const int cap = hx_grid_cap();
+  // resident CTAs split between the two matrices in proportion to their items
+  int ga = (int)((long long)cap * ia / (ia + ib));
+  ga = ga < 1 ? 1 : (ga > ia ? ia : ga);
+  int gb = cap - ga;
+  gb = gb < 1 ? 1 : (gb > ib ? ib : gb);
+  constexpr int smem = HX_EXP_WARPS * 32 * HX_EXP_ROW_WORDS * 4;
+  static bool smem_set = false;
+  if (!smem_set) {
+    PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_experts2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_set = true;
+  }
+  const HxExpertMat a{hdr_a, mat_a, rows_a, K_a, static_cast<const uint32_t*>(lut_a), out_a};
+  const HxExpertMat b{hdr_b, mat_b, rows_b, K_b, static_cast<const uint32_t*>(lut_b), out_b};
+  hx_expand_experts2_kernel<<<ga + gb, per_cta, smem, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(slots), slot_stride, k, a, b, ga, static_cast<uint8_t*>(scratch), scratch_stride);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
 extern "C" int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist,
                            void* stream) {
   using namespace ps;
@@ -402,5 +475,6 @@ int ps_preload_hx() {
   int n = 0;
   touch_kernel(hx_expand_kernel, n);
   touch_kernel(hx_expand_experts_kernel, n);
+  touch_kernel(hx_expand_experts2_kernel, n);
   return n;
 }

@@ -1192,11 +1192,10 @@ class Executor:
             """Routed experts of ranks [r0, r1): spans -> bf16 scratch experts (blob layout),
             then their gate/up + SwiGLU."""
             sc, sst = self.hx_escratch, stride
-            L.call("ps_hx_expand_experts", ebase + r0 * sb, sb, r1 - r0, 0, hxe["gu_off"], hxe["gu_rows"],
-                   hxe["gu_k"], self.hx_lut + self.hx.lut_off[(sid, "wgu")], sc + r0 * sst, sst, 0, self.cs)
-            L.call("ps_hx_expand_experts", ebase + r0 * sb, sb, r1 - r0, hxe["nb_gu"], hxe["dn_off"],
-                   hxe["dn_rows"], hxe["dn_k"], self.hx_lut + self.hx.lut_off[(sid, "wdown")], sc + r0 * sst, sst,
-                   down_off, self.cs)
+            L.call("ps_hx_expand_experts2", ebase + r0 * sb, sb, r1 - r0,
+                   0, hxe["gu_off"], hxe["gu_rows"], hxe["gu_k"], self.hx_lut + self.hx.lut_off[(sid, "wgu")], 0,
+                   hxe["nb_gu"], hxe["dn_off"], hxe["dn_rows"], hxe["dn_k"],
+                   self.hx_lut + self.hx.lut_off[(sid, "wdown")], down_off, sc + r0 * sst, sst, self.cs)
             L.call("ps_moe_decode_experts_phase", xn, self.m_ids, k, slot_map, sc, sst, 0, down_off, eff, d,
                    self.m_h, self.m_w, self.x, 1, r0, r1, self.cs)
 
