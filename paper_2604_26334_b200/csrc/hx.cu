@@ -18,6 +18,7 @@
 // weight and reads ~1.26), microseconds per piece against the milliseconds a piece takes
 // to cross PCIe; prefill passes run it ahead of the GEMM on every piece.
 #include "common.cuh"
+#include "wcodec.cuh"
 #include "../../include/pshard.h"
 
 namespace ps {
@@ -101,9 +102,21 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
       p += 4;
     }
     const int q = lane >> 3, l8 = lane & 7;   // phase 2: sub-block 4 i + q, columns 8 l8 ..
+    // phase-2 addresses of the (up to) 8 sub-blocks this lane assembles, once per item
+    const uint8_t* src8[8];
+    __nv_bfloat16* dst8[8];
+    uint32_t rmax4[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = 4 * i + q;
+      const int tj = task0 + min(j, ntask - 1), rj = tj / nsub, sj = tj - (tj / nsub) * nsub;
+      src8[i] = block + row_start[rj] + hb + sj * HX_SUB + 8 * l8;
+      dst8[i] = out + (long long)(r0 + rj) * ld_out + sj * HX_SUB + 8 * l8;
+      rmax4[i] = __shfl_sync(0xffffffffu, rowmax, min(j, 31)) * 0x01010101u;   // sub-block j's rowmax
+    }
 #pragma unroll 1
     for (int c0 = 0; c0 < HX_SUB; c0 += HX_CHUNK) {
-      if (live) {
+      if (live) {   // symbols (rowmax - exponent) of this lane's next 64 weights
         int k = 0;
 #pragma unroll 1
         while (k < HX_CHUNK) {
@@ -119,8 +132,8 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
               const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
               const bool both = (e >> 25) != 0u && k < HX_CHUNK - 1;
               const int len = both ? (int)((e >> 20) & 0x1Fu) : (int)((e >> 16) & 0xFu);
-              myb[k] = (uint8_t)(rowmax - (e & 0xFFu));
-              if (both) myb[k + 1] = (uint8_t)(rowmax - ((e >> 8) & 0xFFu));
+              myb[k] = (uint8_t)e;
+              if (both) myb[k + 1] = (uint8_t)(e >> 8);
               buf >>= len;
               avail -= len;
               k += both ? 2 : 1;
@@ -131,29 +144,23 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
       __syncwarp();
       uint2 mm[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int j = 4 * i + q;
-        const int tj = task0 + j, rj = tj / nsub, sj = tj - (tj / nsub) * nsub;
-        mm[i] = j < ntask ? *reinterpret_cast<const uint2*>(block + row_start[rj] + hb + sj * HX_SUB + c0 + 8 * l8)
-                          : make_uint2(0u, 0u);
-      }
+      for (int i = 0; i < 8; ++i)
+        mm[i] = 4 * i + q < ntask ? *reinterpret_cast<const uint2*>(src8[i] + c0) : make_uint2(0u, 0u);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int j = 4 * i + q;
         if (j < ntask) {
-          const int tj = task0 + j, rj = tj / nsub, sj = tj - (tj / nsub) * nsub;
-          const uint32_t e0 = exps[warp][j][2 * l8], e1 = exps[warp][j][2 * l8 + 1];
-          const uint32_t mw[2] = {mm[i].x, mm[i].y}, ew[2] = {e0, e1};
-          uint32_t w[4];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t b = (mw[u >> 2] >> (8 * (u & 3))) & 0xFFu;
-            const uint32_t ex = (ew[u >> 2] >> (8 * (u & 3))) & 0xFFu;
-            const uint32_t h = ((b & 0x80u) << 8) | (ex << 7) | (b & 0x7Fu);
-            if (u & 1) w[u >> 1] |= h << 16; else w[u >> 1] = h;
-          }
-          *reinterpret_cast<uint4*>(out + (long long)(r0 + rj) * ld_out + sj * HX_SUB + c0 + 8 * l8) =
-              make_uint4(w[0], w[1], w[2], w[3]);
+          // exponents = rowmax - symbol, four bytes per instruction; then two weights per
+          // word as in wcodec.cuh: a sign-replicating PRMT keeps sign << 15 | mantissa
+          // under & 0x807F807F, a PRMT spreads two exponents, a shift places them
+          const uint32_t e0 = __vsub4(rmax4[i], exps[warp][j][2 * l8]);
+          const uint32_t e1 = __vsub4(rmax4[i], exps[warp][j][2 * l8 + 1]);
+          uint4 w;
+          w.x = (prmt(mm[i].x, 0u, 0x9180u) & 0x807F807Fu) | (prmt(e0, 0u, 0x4140u) << 7);
+          w.y = (prmt(mm[i].x, 0u, 0xB3A2u) & 0x807F807Fu) | (prmt(e0, 0u, 0x4342u) << 7);
+          w.z = (prmt(mm[i].y, 0u, 0x9180u) & 0x807F807Fu) | (prmt(e1, 0u, 0x4140u) << 7);
+          w.w = (prmt(mm[i].y, 0u, 0xB3A2u) & 0x807F807Fu) | (prmt(e1, 0u, 0x4342u) << 7);
+          *reinterpret_cast<uint4*>(dst8[i] + c0) = w;
         }
       }
       __syncwarp();   // the next round overwrites the rows
