@@ -166,7 +166,7 @@ int ps_wencode_rows(const void* bits, int N, int K, long long ld, const int* bas
  * per bf16 weight, lossless. ps_hx_expand decodes `rows` rows (whole 64-row blocks;
  * block_off[b] = byte offset of block b from `piece`, device memory) to bf16 rows of
  * ld_out elements, with the matrix's 4096-entry lookup table (runtime/hxcodec.pair_table: uint32
- * s1 | s2 << 8 | len1 << 16 | (len1 + len2) << 20 | two << 25).
+ * s1 | s2 << 8 | bits << 16 | n << 24).
  * Encoder passes: ps_hx_stats (row max exponent + histogram of rowmax - exponent),
  * ps_hx_sizes (bits per 256-weight sub-block, bytes per row, given the code table
  * uint32 length << 16 | bit-reversed code), ps_hx_write (the coded rows at row_off into a

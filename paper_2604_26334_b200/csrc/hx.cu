@@ -83,6 +83,7 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
     uint64_t buf = 0;
     int avail = 64;
     uint32_t nextw = 0, nextw2 = 0;
+    int carry = -1;   // a symbol decoded past the previous round's end
     if (live) {
       const uint8_t* row = block + row_start[r];
       const uint16_t* hdr = reinterpret_cast<const uint16_t*>(row);
@@ -117,7 +118,12 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
 #pragma unroll 1
     for (int c0 = 0; c0 < HX_SUB; c0 += HX_CHUNK) {
       if (live) {   // symbols (rowmax - exponent) of this lane's next 64 weights
+        // A lookup always stores two symbol bytes and advances by the count it resolved
+        // (a lone symbol's second byte is overwritten by the next lookup); a pair that
+        // straddles the round's end leaves its second symbol in byte 64, carried to
+        // byte 0 of the next round. No per-lookup end test beyond the loop's.
         int k = 0;
+        if (carry >= 0) { myb[0] = (uint8_t)carry; k = 1; }
 #pragma unroll 1
         while (k < HX_CHUNK) {
           if (avail < 32) {
@@ -130,16 +136,16 @@ __device__ __forceinline__ void hx_expand_item(const uint8_t* __restrict__ block
           for (int t = 0; t < 2; ++t) {
             if (k < HX_CHUNK) {
               const uint32_t e = lut[(uint32_t)buf & (HX_LUT - 1)];
-              const bool both = (e >> 25) != 0u && k < HX_CHUNK - 1;
-              const int len = both ? (int)((e >> 20) & 0x1Fu) : (int)((e >> 16) & 0xFu);
+              const int len = (int)((e >> 16) & 0xFFu);
               myb[k] = (uint8_t)e;
-              if (both) myb[k + 1] = (uint8_t)(e >> 8);
+              myb[k + 1] = (uint8_t)(e >> 8);
               buf >>= len;
               avail -= len;
-              k += both ? 2 : 1;
+              k += (int)(e >> 24);
             }
           }
         }
+        carry = k > HX_CHUNK ? (int)myb[HX_CHUNK] : -1;
       }
       __syncwarp();
       uint2 mm[8];
@@ -182,7 +188,7 @@ __device__ __forceinline__ void hx_load_lut(const uint32_t* __restrict__ lut_g, 
 __global__ void __launch_bounds__(32 * HX_EXP_WARPS)
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
                  const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
-  __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | len1 << 16 | len1+len2 << 20 | two << 25
+  __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | bits << 16 | n << 24
   __shared__ uint32_t row_start[HX_BLOCK_ROWS];
   extern __shared__ uint32_t hx_exps[];   // [warp][lane][65] exponent rows (dynamic: > 48 KB static)
   auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);

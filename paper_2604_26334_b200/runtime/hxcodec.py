@@ -184,8 +184,8 @@ def decode(blob: np.ndarray, offs: np.ndarray, table: np.ndarray, n: int, k: int
 
 def pair_table(table: np.ndarray) -> np.ndarray:
     """The decoder's 4096-entry table (uint32) of `ps_hx_expand`: for every 12-bit
-    LSB-first window, s1 | s2 << 8 | len1 << 16 | (len1 + len2) << 20 | two << 25 — the
-    first symbol and, when the second code also lies inside the window, the second."""
+    LSB-first window, s1 | s2 << 8 | bits << 16 | n << 24 — the first symbol and, when the
+    second code also lies inside the window, the second (n = 2), with the bits they take."""
     single = lookup_table(table).astype(np.uint32)
     x = np.arange(1 << MAX_LEN, dtype=np.uint32)
     s1, l1 = single & 0xFF, single >> 8
@@ -193,8 +193,8 @@ def pair_table(table: np.ndarray) -> np.ndarray:
     e2 = single[rest]
     s2, l2 = e2 & 0xFF, e2 >> 8
     two = (l2 <= MAX_LEN - l1).astype(np.uint32)
-    return (s1 | (np.where(two, s2, 0) << 8) | (l1 << 16) | (np.where(two, l1 + l2, l1) << 20)
-            | (two << 25)).astype(np.uint32)
+    return (s1 | (np.where(two, s2, 0) << 8) | (np.where(two, l1 + l2, l1) << 16)
+            | ((1 + two) << 24)).astype(np.uint32)
 
 
 def lookup_table(table: np.ndarray) -> np.ndarray:

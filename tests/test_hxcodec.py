@@ -61,13 +61,13 @@ def test_pair_table_decodes_like_single_lookups():
     for x in rng.integers(0, 4096, 2000):
         s1, l1 = single[x] & 0xFF, single[x] >> 8
         e = pair[x]
-        assert e & 0xFF == s1 and (e >> 16) & 0xF == l1
-        if e >> 25:
+        assert e & 0xFF == s1
+        if e >> 24 == 2:
             rest = x >> l1
             s2, l2 = single[rest] & 0xFF, single[rest] >> 8
-            assert l1 + l2 <= hx.MAX_LEN and (e >> 8) & 0xFF == s2 and (e >> 20) & 0x1F == l1 + l2
+            assert l1 + l2 <= hx.MAX_LEN and (e >> 8) & 0xFF == s2 and (e >> 16) & 0xFF == l1 + l2
         else:
-            assert (single[x >> l1] >> 8) > hx.MAX_LEN - l1
+            assert e >> 24 == 1 and (e >> 16) & 0xFF == l1 and (single[x >> l1] >> 8) > hx.MAX_LEN - l1
 
 
 @pytest.mark.parametrize("dist", ["gaussian", "laplace", "student_t3"])
