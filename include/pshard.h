@@ -144,9 +144,19 @@ int ps_attn_tc_watchdog(unsigned* code, int reset);
 /* Device-side faults of every spin-wait with a timeout, in host-mapped memory (a plain
  * host load, no CUDA call, no synchronisation): words[0] = expert-fetch sequence the
  * wait gave up on, [1] = stripe sequence, [2] = tcgen05 attention barrier code,
- * [3] = host-side fetcher timeout (sequence never published). All zero = healthy;
+ * [3] = host-side fetcher timeout (sequence never published), [4] = pass sequence the
+ * early-head GEMV gave up waiting for. All zero = healthy;
  * reset clears them. The executor raises on any non-zero word after every pass. */
-int ps_fault_status(unsigned* words /* [4] */, int reset);
+int ps_fault_status(unsigned* words /* [5] */, int reset);
+
+/* "Early head" for one-token passes whose output head is CPU-placed (zero-copy): y[N] =
+ * x . W rows, launched on a side stream at the start of the pass with at most grid_cap
+ * CTAs; its producers stream W (bf16, or 12-bit coded rows with coded = 1 and ldw bytes)
+ * from host memory while the layers compute, its consumers wait for *xflag >= xseq.
+ * ps_set_flag writes the flag on the compute stream once x is final. */
+int ps_gemv_head_early(const float* x, int K, const void* W, int N, long long ldw, int coded, float* y, int grid_cap,
+                       const unsigned* xflag, unsigned xseq, void* stream);
+int ps_set_flag(unsigned* flag, unsigned value, void* stream);
 
 /* Coded rows (format of ps_gemv_bf16c, ld_in bytes each) -> bf16 rows (ld_out elements):
  * a GEMM pass that streams coded pieces expands each piece in VRAM for the tcgen05 GEMM. */

@@ -131,8 +131,9 @@ extern int g_pdl;   // ps_set_pdl(): launch_k() adds the PDL attribute while set
 // reads it with a plain load after every pass (ps_fault_status) and raises, so a
 // timed-out wait can never return wrong tokens silently. Slots: FAULT_FETCH (the
 // sequence number the expert wait gave up on), FAULT_STRIPE (stripe seq),
-// FAULT_ATTN (role/barrier code of tcgen05 attention), FAULT_HOST (host-side code).
-enum { FAULT_FETCH = 0, FAULT_STRIPE = 1, FAULT_ATTN = 2, FAULT_HOST = 3, FAULT_WORDS = 4 };
+// FAULT_ATTN (role/barrier code of tcgen05 attention), FAULT_HOST (host-side code),
+// FAULT_HEAD (pass sequence the early-head GEMV gave up waiting for).
+enum { FAULT_FETCH = 0, FAULT_STRIPE = 1, FAULT_ATTN = 2, FAULT_HOST = 3, FAULT_HEAD = 4, FAULT_WORDS = 5 };
 unsigned* fault_host();     // host address of the words (mapped, zero-initialised)
 unsigned* fault_dev();      // device alias of the same words
 __device__ __forceinline__ void raise_fault(unsigned* words, int slot, unsigned code) {

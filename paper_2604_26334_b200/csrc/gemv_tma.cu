@@ -111,10 +111,16 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[V], int lane) {
   }
 }
 
-template <int T, int EPI, bool COMP = false>
+// XF: the "early head" variant (executor: one-token passes reading a CPU-placed output
+// head zero-copy). Launched on a side stream at the start of the pass, its producers
+// stream the head rows from host memory while the layers compute on the other SMs; the
+// consumers wait for *xflag >= xseq (set on the compute stream once x is final) instead of
+// griddepcontrol.wait, and read x through L2 (a previous pass left stale L1 lines).
+template <int T, int EPI, bool COMP = false, bool XF = false>
 __global__ void __launch_bounds__(gt_threads(T), 1)
 gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat16* __restrict__ W, int N, int K,
-                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages) {
+                long long ldw, float* __restrict__ y, int ldy, int rows_per_cta, int stages,
+                const unsigned* __restrict__ xflag, unsigned xseq, unsigned* fault) {
   using S = GtShape<T, COMP>;
   constexpr int CPT = S::CPT, KC = S::KC, RS = S::RS, V = S::V, ROWB = S::ROWB;
   constexpr int GT_CONSUMERS = S::NC, GT_THREADS = gt_threads(T);
@@ -178,8 +184,26 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
   }
 
   // weights are never written inside a pass (the producer may stream them before
-  // the previous kernel finished); x and y are: consumers wait for it (PDL)
-  pdl_wait();
+  // the previous kernel finished); x and y are: consumers wait for it (PDL), or (XF) for
+  // the flag that says x is final
+  if constexpr (XF) {
+    if ((threadIdx.x & 31) == 0) {
+      unsigned long long t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      while ((int)(*reinterpret_cast<const volatile unsigned*>(xflag) - xseq) < 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 2000000000ull) {   // 2 s: record the fault (the host raises) instead of hanging
+          if (fault) raise_fault(fault, FAULT_HEAD, xseq);
+          break;
+        }
+        __nanosleep(256);
+      }
+      __threadfence();
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+  }
   const int j = threadIdx.x - 32;  // consumer thread 0..255
   const int cw = warp - 1;
   // value index this lane holds after the reduce-scatter, and whether it writes it
@@ -208,7 +232,14 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
         const int col = (h * GT_CONSUMERS * 32 + j) * 8;   // 8-column groups, consecutive threads adjacent
         if (col < kc && t < tt) {
           const float4* xp = reinterpret_cast<const float4*>(x + (long long)t * ldx + (long long)c * KC + col);
-          float4 a = __ldg(xp), b = __ldg(xp + 1);
+          float4 a, b;
+          if constexpr (XF) {
+            a = __ldcg(xp);
+            b = __ldcg(xp + 1);
+          } else {
+            a = __ldg(xp);
+            b = __ldg(xp + 1);
+          }
           xr[t][h * 4 + 0] = make_float2(a.x, a.y); xr[t][h * 4 + 1] = make_float2(a.z, a.w);
           xr[t][h * 4 + 2] = make_float2(b.x, b.y); xr[t][h * 4 + 3] = make_float2(b.z, b.w);
         } else {
@@ -346,9 +377,9 @@ gemv_tma_kernel(const float* __restrict__ x, int ldx, int tt, const __nv_bfloat1
 static int g_tma_sms = 0;
 static int g_tma_stages = 0;
 
-template <int T, int EPI, bool COMP = false>
+template <int T, int EPI, bool COMP = false, bool XF = false>
 static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, int N, int K, long long ldw, float* y,
-                      int ldy, cudaStream_t s, int grid_cap) {
+                      int ldy, cudaStream_t s, int grid_cap, const unsigned* xflag = nullptr, unsigned xseq = 0) {
   if (!g_tma_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -373,12 +404,17 @@ static int launch_tma(const float* x, int ldx, int tt, const __nv_bfloat16* W, i
   const size_t smem = (size_t)stages * (GT_STAGE_BYTES + 16) + (size_t)GT_CONSUMERS * rows_per_cta * T * 4;
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI, COMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+    PS_CHECK_CUDA(cudaFuncSetAttribute(gemv_tma_kernel<T, EPI, COMP, XF>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     smem_set = smem;
   }
-  launch_k(gemv_tma_kernel<T, EPI, COMP>, grid, GT_THREADS, smem, s, x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta,
-           stages);
+  if constexpr (XF) {   // side stream, plain launch: no programmatic dependency on anything
+    gemv_tma_kernel<T, EPI, COMP, XF><<<grid, GT_THREADS, smem, s>>>(x, ldx, tt, W, N, K, ldw, y, ldy, rows_per_cta,
+                                                                     stages, xflag, xseq, fault_dev());
+  } else {
+    launch_k(gemv_tma_kernel<T, EPI, COMP, XF>, grid, GT_THREADS, smem, s, x, ldx, tt, W, N, K, ldw, y, ldy,
+             rows_per_cta, stages, (const unsigned*)nullptr, 0u, (unsigned*)nullptr);
+  }
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -430,6 +466,37 @@ extern "C" int ps_gemv_bf16c(const float* x, int ldx, int t, const void* Wc, int
   return launch_tmac_epi<8>(epilogue, x, ldx, t, Wc, N, K, ldw, y, ldy, s);
 }
 
+extern "C" int ps_gemv_head_early(const float* x, int K, const void* W, int N, long long ldw, int coded, float* y,
+                                  int grid_cap, const unsigned* xflag, unsigned xseq, void* stream) {
+  using namespace ps;
+  PS_REQUIRE(K % 256 == 0 && ((uintptr_t)W & 15) == 0 && ((uintptr_t)x & 15) == 0 && xflag != nullptr,
+             "ps_gemv_head_early: K %d, alignment, flag", K);
+  if (N <= 0) return PS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto Wb = static_cast<const __nv_bfloat16*>(W);
+  if (coded) {
+    const long long tb = ldw - (long long)K * 3 / 2;
+    PS_REQUIRE(tb >= 16 && tb <= GT_TRAILER_MAX && tb % 16 == 0, "ps_gemv_head_early: coded row stride %lld", ldw);
+    return launch_tma<1, PS_EPI_STORE, true, true>(x, K, 1, Wb, N, K, ldw, y, N, s, grid_cap, xflag, xseq);
+  }
+  return launch_tma<1, PS_EPI_STORE, false, true>(x, K, 1, Wb, N, K, ldw, y, N, s, grid_cap, xflag, xseq);
+}
+
+namespace ps {
+__global__ void set_flag_kernel(unsigned* flag, unsigned v) {
+  __threadfence();   // this stream's earlier writes (x) before the flag
+  *reinterpret_cast<volatile unsigned*>(flag) = v;
+  __threadfence();
+}
+}  // namespace ps
+
+extern "C" int ps_set_flag(unsigned* flag, unsigned value, void* stream) {
+  using namespace ps;
+  set_flag_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag, value);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
 namespace ps {
 // Coded rows -> bf16 rows (GEMM passes that stream coded pieces: the tcgen05 GEMM reads
 // bf16 operands). One thread per 8 weights; rows of ld_in bytes in, K bf16 out.
@@ -479,5 +546,8 @@ int ps_preload_gemv_tma() {
   PS_T(1) PS_T(2) PS_T(4) PS_T(8)
 #undef PS_T
   touch_kernel(expand_coded_kernel, n);
+  touch_kernel(gemv_tma_kernel<1, PS_EPI_STORE, false, true>, n);
+  touch_kernel(gemv_tma_kernel<1, PS_EPI_STORE, true, true>, n);
+  touch_kernel(set_flag_kernel, n);
   return n;
 }

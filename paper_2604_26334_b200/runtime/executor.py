@@ -207,6 +207,12 @@ class Executor:
         self.h2d = L.stream_create()                    # copy engine, host -> device
         self.d2h = L.stream_create()                    # KV write-back, token readback
         self.events = EventPool()
+        # early head (one-token passes with a CPU-placed head, `_early_head`): a side
+        # stream, the "x is final" flag (pass sequence) and the events around it
+        self.hs = L.stream_create()
+        self.head_seq = 0
+        self._head_free = None    # dedicated events: the pool recycles its own within a pass
+        self._ev_head_done, self._ev_head_free = L.event_create(False), L.event_create(False)
 
         # host KV homes: [layer][position][slot][K|V heads] bf16, pinned + mapped
         self.kv_host = L.host_alloc(max(1, s.n_layers * self.kv_layer_bytes), mapped=True)
@@ -413,6 +419,8 @@ class Executor:
         self.i_rows = a.alloc_high("sample_rows", B * 4)
         self.i_bt = a.alloc_high("kv_block_table", B * self.pps * 4)
         self.i_tok_ring = a.alloc_high("sample_tok", 8 * B * 4)   # 8 rotating slots
+        self.head_flag = a.alloc_high("head_flag", 256)
+        L.call("ps_memset_async", self.head_flag, 0, 256, self.cs)
         self.tok_slot = 0
         self.i_tok = self.i_tok_ring
         rope = rope_table(self.arch, self.hd, self.cap)
@@ -458,6 +466,37 @@ class Executor:
         """One-token MoE passes fetch routed experts hx-coded (PS_HX_EXPERTS=0: off)."""
         return (T == 1 and self._hx_on and bool(getattr(self.hx, "experts", None)) and self.fetch_enabled and
                 os.environ.get("PS_HX_EXPERTS", "1") != "0")
+
+    def _early_head_plan(self, T: int, R: int):
+        """(final_norm ptr, head W ptr, ldw, coded) when this pass should read its CPU-placed
+        head early, else None. One-token passes of one sampled row whose head is read
+        zero-copy: the head GEMV is launched on a side stream at the start of the pass
+        (ps_gemv_head_early, half the SMs), streaming the head rows from host memory while
+        the layers compute on the other SMs, and computes once the compute stream flags x
+        final — meant to overlap the zero-copy read (~0.5 ms for config 1's 25 MB head)
+        with the ~0.25 ms of layers. Measured slower (1415 -> 1306 tokens/s on config 1):
+        the bulk-copy GEMV's stages are sized for 4096-column rows, so on the tiny head
+        (512 columns) half the SMs hold ~1 MB in flight and then stream the rest at half
+        rate. Off by default (PS_HEAD_EARLY=1 turns it on; tests keep it exact)."""
+        if T > GEMV_CORE_MAX_T or R != 1 or os.environ.get("PS_HEAD_EARLY", "0") != "1" or \
+                self.striper is not None or (self.stage_zc and self.stage_small):
+            return None
+        sid = self.by_layer_kind[(self.spec.n_layers, ShardKind.OUTPUT_HEAD)].id
+        if self.residency.get(sid, ("", 0))[0] != "zerocopy":
+            return None
+        blob = self.w.layout.blobs[sid]
+        if (self.coded is not None and sid in self.coded.tensors and getattr(self.coded, "mapped", False) and
+                (self.coded_only or os.environ.get("PS_CODED_ZEROCOPY", "1") != "0")):
+            meta = self.coded.tensors[sid]
+            base = self.coded.shard_ptr(sid)
+            off, rb, coded = meta["lm_head"]
+            return (base + meta["final_norm"][0], base + off, rb if coded else self.d, 1 if coded else 0,
+                    self.coded.shard_bytes[sid])
+        if not self.w.base:
+            return None
+        base = self.w.shard_ptr(sid)
+        return (base + blob.tensors["final_norm"].offset, base + blob.tensors["lm_head"].offset, self.d, 0,
+                blob.nbytes)
 
     def _zc_readable(self, sid: int) -> bool:
         """A CPU-placed shard can be read zero-copy: the bf16 blob or its 12-bit coded
@@ -807,6 +846,11 @@ class Executor:
             self.ring.striper.wait(seq, self.cs)
             return
         L.call("ps_stream_wait_event", self.cs, ev)
+
+    def _sm_count(self) -> int:
+        if not hasattr(self, "_sms"):
+            self._sms = int(L.device_info().get("sm_count", 148) or 148)
+        return self._sms
 
     def _record(self, stream: int) -> int:
         ev = self.events.next()
@@ -1506,6 +1550,16 @@ class Executor:
                 raise SpecError("a pass without ids must follow a pass that sampled the same slots")
             ids_ptr = self.i_tok          # the previous sampling pass's slot
         L.call("ps_embed_gather", self.w.embed, ids_ptr, T, d, self.x, d, self.cs)
+        early = self._early_head_plan(T, len(ps.sample))
+        if early is not None:
+            self.head_seq = (self.head_seq + 1) & 0x7FFFFFFF or 1
+            if self._head_free is not None:   # the previous pass's argmax has read the logits
+                L.call("ps_stream_wait_event", self.hs, self._head_free)
+            cap = max(1, self._sm_count() // 2)
+            L.call("ps_gemv_head_early", self.xs, d, early[1], self.V, early[2], early[3], self.logits, cap,
+                   self.head_flag, self.head_seq, self.hs)
+            L.call("ps_event_record", self._ev_head_done, self.hs)
+            self._stat.zero_copy_bytes += early[4]
 
         xn = self.xn32 if gemv else self.xn16
         att = self.att32 if gemv else self.att16
@@ -1618,8 +1672,19 @@ class Executor:
             def greedy(p, a, b):
                 L.call("ps_argmax", self.logits, R, self.V, self.V, self.i_tok, self.cs)
 
-            self._shard(head_sid, [Consumer("final_norm", hnorm), Consumer("lm_head", lm),
-                                   Consumer(None, greedy)], R)
+            if early is not None:
+                hnorm(early[0], 0, 1)                                       # x final ...
+                L.call("ps_set_flag", self.head_flag, self.head_seq, self.cs)   # ... says so
+                L.call("ps_stream_wait_event", self.cs, self._ev_head_done)
+                # a plain launch after the event wait: the argmax's programmatic dependency
+                # is on a kernel that itself started after the head GEMV finished
+                L.call("ps_set_flag", self.head_flag, self.head_seq, self.cs)
+                greedy(None, 0, 0)
+                L.call("ps_event_record", self._ev_head_free, self.cs)
+                self._head_free = self._ev_head_free
+            else:
+                self._shard(head_sid, [Consumer("final_norm", hnorm), Consumer("lm_head", lm),
+                                       Consumer(None, greedy)], R)
             L.call("ps_stream_wait_event", self.d2h, self._record(self.cs))
             dst = self.host_tok + (self.host_tok_i % 4096) * self.B * 4
             self.host_tok_i += 1
@@ -1666,7 +1731,7 @@ class Executor:
                                     "(1: routing never published, 2: bad expert id, 3: copy failed)")
 
     def synchronize(self) -> None:
-        for s in (self.cs, self.h2d, self.d2h):
+        for s in (self.cs, self.h2d, self.d2h, self.hs):
             L.call("ps_stream_synchronize", s)
 
     def close(self) -> None:

@@ -822,3 +822,29 @@ def test_moe_hx_experts_same_tokens_fewer_bytes(monkeypatch):
     assert np.array_equal(out["1"][1], out["0"][1])
     ref = RefModel(hp_from_spec(spec, arch_for(spec)), seed=0)
     assert_exact_parity(ref, prompt, np.array(out["1"][0]), out["1"][4])
+
+
+@pytest.mark.parametrize("frac", [0.5, 0.45])
+def test_early_head_same_tokens(monkeypatch, frac):
+    """One-token passes whose output head is CPU-placed read it early: the head GEMV runs
+    on a side stream from the start of the pass (half the SMs), streaming the head from
+    host memory while the layers compute, and waits for the compute stream's "x final"
+    flag (PS_HEAD_EARLY=1, off by default: measured slower on config 1). Same tokens and
+    logits as the in-order zero-copy head, with programmatic dependent launch on, across
+    the 12-bit and bf16 head forms."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    from paper_2604_26334_b200.runtime import lib as L
+    spec = catalog.builtin_model("tiny-llama")
+    prompt = _prompt(128, spec.vocab_size, seed=61)
+    for zc in ("1", "0"):
+        monkeypatch.setenv("PS_CODED_ZEROCOPY", zc)
+        out = {}
+        for he in ("0", "1"):
+            monkeypatch.setenv("PS_HEAD_EARLY", he)
+            eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160)
+            res = eng.generate([prompt], gen_len=24)
+            out[he] = (res.tokens[0].tolist(), eng.logits().copy())
+            eng.close()
+            assert not any(L.fault_status())
+        assert out["1"][0] == out["0"][0], zc
+        assert np.array_equal(out["1"][1], out["0"][1]), zc
