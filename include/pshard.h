@@ -184,14 +184,10 @@ int ps_wencode_rows(const void* bits, int N, int K, long long ld, const int* bas
 int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, const void* lut, void* out,
                  long long ld_out, void* stream);
 /* The k routed experts of a MoE layer fetched hx-coded into slots (rank j in slot j, slot
- * stride slot_stride): each slot's span carries the uint32 block offsets of the matrix at
- * word hdr_word and the matrix at mat_off; expands `rows` x K into scratch expert j at
- * out_off (bf16 rows of K), for the bf16 one-token expert kernels. */
-int ps_hx_expand_experts(const void* slots, long long slot_stride, int k, int hdr_word, long long mat_off, int rows,
-                         int K, const void* lut, void* scratch, long long scratch_stride, long long out_off,
-                         void* stream);
-/* Both matrices of the routed experts (A = gate/up, B = down) in one launch (the expansion
- * is latency-bound: one launch's latency instead of two on the routing chain). */
+ * stride slot_stride): each slot's span carries the uint32 block offsets of matrix A at
+ * word hdr_a and of B at hdr_b, the matrices at mat_a / mat_b; both are expanded in one
+ * launch (latency-bound: one launch's latency on the routing chain, not two) into scratch
+ * expert j at out_a / out_b (bf16 rows of K_a / K_b) for the bf16 one-token kernels. */
 int ps_hx_expand_experts2(const void* slots, long long slot_stride, int k, int hdr_a, long long mat_a, int rows_a,
                           int K_a, const void* lut_a, long long out_a, int hdr_b, long long mat_b, int rows_b, int K_b,
                           const void* lut_b, long long out_b, void* scratch, long long scratch_stride, void* stream);

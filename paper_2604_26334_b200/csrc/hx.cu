@@ -203,34 +203,6 @@ hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__
   }
 }
 
-// The routed experts of one MoE layer, fetched hx-coded into slots (expert rank j in slot
-// j): each slot holds a span [uint32 block offsets of the matrix][...][hx matrix], the
-// offsets at hdr_word (n_blocks of them), the matrix at mat_off. Item (j, b, part) expands
-// block b of expert j's matrix into scratch expert j (out_off bytes into it, rows of K
-// bf16): the bf16 one-token expert kernels then read the scratch slots.
-__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
-hx_expand_experts_kernel(const uint8_t* __restrict__ slots, long long slot_stride, int k, int hdr_word,
-                         long long mat_off, int rows, int K, const uint32_t* __restrict__ lut_g,
-                         uint8_t* __restrict__ scratch, long long scratch_stride, long long out_off) {
-  __shared__ uint32_t lut[HX_LUT];
-  __shared__ uint32_t row_start[HX_BLOCK_ROWS];
-  extern __shared__ uint32_t hx_exps[];
-  auto exps = reinterpret_cast<uint32_t (*)[32][HX_EXP_ROW_WORDS]>(hx_exps);
-  hx_load_lut(lut_g, lut);
-  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + 32 * HX_EXP_WARPS - 1) / (32 * HX_EXP_WARPS);
-  const int nb = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
-  for (int item = blockIdx.x; item < k * nb * parts; item += gridDim.x) {
-    const int part = item % parts, jb = item / parts;
-    const int j = jb / nb, b = jb - (jb / nb) * nb;
-    const uint8_t* span = slots + j * slot_stride;
-    const uint32_t off = reinterpret_cast<const uint32_t*>(span)[hdr_word + b];
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(scratch + j * scratch_stride + out_off) +
-                       (long long)b * HX_BLOCK_ROWS * K;
-    hx_expand_item(span + mat_off + off, min(HX_BLOCK_ROWS, rows - b * HX_BLOCK_ROWS), K, part, lut, row_start,
-                   exps, o, K);
-  }
-}
-
 __device__ __forceinline__ int hx_exp(uint16_t b) { return (b >> 7) & 0xFF; }
 
 __global__ void __launch_bounds__(HX_THREADS)
@@ -310,6 +282,10 @@ hx_write_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const in
   }
 }
 
+// The routed experts of one MoE layer, fetched hx-coded into slots (expert rank j in slot
+// j): each slot holds a span [uint32 block offsets of both matrices][...][hx matrices];
+// item (j, b, part) expands block b of expert j's matrix into scratch expert j (out_off
+// bytes into it, rows of K bf16) for the bf16 one-token expert kernels.
 // Both matrices of the routed experts (gate/up, down) in ONE launch: the expansion is
 // latency-bound (a 256-weight serial decode per lane), so two back-to-back launches cost
 // two decode latencies on the routing chain; here CTAs [0, grid_a) expand matrix A with
@@ -382,32 +358,6 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
   hx_expand_kernel<<<grid, per_cta, smem, (cudaStream_t)stream>>>(
       static_cast<const uint8_t*>(piece), block_off, rows, K, static_cast<const uint32_t*>(lut),
       static_cast<__nv_bfloat16*>(out), ld_out);
-  PS_CHECK_LAUNCH();
-  return PS_OK;
-}
-
-extern "C" int ps_hx_expand_experts(const void* slots, long long slot_stride, int k, int hdr_word,
-                                    long long mat_off, int rows, int K, const void* lut, void* scratch,
-                                    long long scratch_stride, long long out_off, void* stream) {
-  using namespace ps;
-  PS_REQUIRE(K > 0 && K % HX_SUB == 0 && rows > 0 && k >= 0, "ps_hx_expand_experts: K %d rows %d k %d", K, rows, k);
-  PS_REQUIRE(((uintptr_t)slots & 15) == 0 && (slot_stride & 255) == 0 && (mat_off & 15) == 0 &&
-             ((uintptr_t)scratch & 15) == 0 && (scratch_stride & 15) == 0 && (out_off & 15) == 0,
-             "ps_hx_expand_experts: alignment");
-  if (k == 0) return PS_OK;
-  const int nb = (rows + HX_BLOCK_ROWS - 1) / HX_BLOCK_ROWS;
-  const int per_cta = 32 * HX_EXP_WARPS;
-  const int parts = (HX_BLOCK_ROWS * (K / HX_SUB) + per_cta - 1) / per_cta;
-  constexpr int smem = HX_EXP_WARPS * 32 * HX_EXP_ROW_WORDS * 4;
-  static bool smem_set = false;
-  if (!smem_set) {
-    PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_experts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    smem_set = true;
-  }
-  const int grid = min(k * nb * parts, hx_grid_cap());
-  hx_expand_experts_kernel<<<grid, per_cta, smem, (cudaStream_t)stream>>>(
-      static_cast<const uint8_t*>(slots), slot_stride, k, hdr_word, mat_off, rows, K, static_cast<const uint32_t*>(lut),
-      static_cast<uint8_t*>(scratch), scratch_stride, out_off);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }
@@ -487,7 +437,6 @@ int ps_preload_hx() {
   using namespace ps;
   int n = 0;
   touch_kernel(hx_expand_kernel, n);
-  touch_kernel(hx_expand_experts_kernel, n);
   touch_kernel(hx_expand_experts2_kernel, n);
   return n;
 }

@@ -793,7 +793,7 @@ def test_hx_same_tokens_fewer_bytes(monkeypatch, frac, prompt_len, batch):
 def test_moe_hx_experts_same_tokens_fewer_bytes(monkeypatch):
     """One-token MoE decode with the routed experts fetched hx-coded (one Huffman code per
     matrix kind shared by a layer's experts, uniform-stride spans carrying their block
-    offsets) and expanded into bf16 scratch slots (ps_hx_expand_experts) ahead of the
+    offsets) and expanded into bf16 scratch slots (ps_hx_expand_experts2) ahead of the
     bf16 expert kernels: same tokens and logits as 12-bit experts (PS_HX_EXPERTS=0), fewer
     fetched bytes, decided-exact against the oracle."""
     import dataclasses
