@@ -848,3 +848,45 @@ def test_early_head_same_tokens(monkeypatch, frac):
             assert not any(L.fault_status())
         assert out["1"][0] == out["0"][0], zc
         assert np.array_equal(out["1"][1], out["0"][1]), zc
+
+
+@pytest.mark.parametrize("frac,prompt_len", [(0.5, 24), (0.35, 128)])
+def test_coding_on_heavy_tailed_checkpoint(monkeypatch, tmp_path, frac, prompt_len):
+    """The link / VRAM codings on weights that are not uniform-init: every tensor of a
+    tiny-llama checkpoint is redrawn Laplace-distributed with 1 % outliers x30 (trained-
+    weight-like, heavy-tailed exponents), written as safetensors and loaded back. hx (the
+    default), the 12-bit format (PS_HX=0) and bf16 (PS_CODED=0) generate the same tokens
+    and logits — the codings stay lossless whatever the exponent statistics."""
+    from paper_2604_26334_b200.runtime.engine import Engine
+    spec = catalog.builtin_model("tiny-llama")
+    budget = frac * total_model_bytes(spec)
+    eng = Engine(spec, budget_bytes=budget, context_len=160)
+    blob = eng.weights.blob_bytes().view(np.uint16)
+    rng = np.random.default_rng(7)
+    for b in eng.weights.layout.blobs.values():
+        for t in b.tensors.values():
+            n = t.rows * t.cols
+            w = rng.laplace(size=n).astype(np.float32) * (0.5 / np.sqrt(t.cols))
+            w[rng.random(n) < 0.01] *= 30.0
+            if t.rows == 1:
+                w = 1.0 + 0.1 * w                      # norm vectors near 1
+            o = (b.offset + t.offset) // 2
+            blob[o:o + n] = (w.view(np.uint32) >> 16).astype(np.uint16)
+    eng.weights.export(str(tmp_path))
+    eng.close()
+    prompt = _prompt(prompt_len, spec.vocab_size, seed=8)
+    out = {}
+    for name, env in (("hx", {"PS_HX_RESIDENT": "1", "PS_HX_STREAM": "1"}), ("c12", {"PS_HX": "0"}),
+                      ("bf16", {"PS_CODED": "0"})):
+        for k in ("PS_HX", "PS_CODED", "PS_HX_RESIDENT", "PS_HX_STREAM"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        e = Engine(None, budget_bytes=budget, context_len=160, checkpoint=str(tmp_path))
+        res = e.generate([prompt], gen_len=10)
+        out[name] = (res.tokens[0].tolist(), e.logits().copy(), getattr(e.weights, "hx", None) is not None)
+        e.close()
+    assert out["hx"][2], "the hx copy was not built"
+    for name in ("c12", "bf16"):
+        assert out[name][0] == out["hx"][0], name
+        assert np.array_equal(out[name][1], out["hx"][1]), name
