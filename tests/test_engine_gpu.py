@@ -871,7 +871,7 @@ def test_coding_on_heavy_tailed_checkpoint(monkeypatch, tmp_path, frac, prompt_l
             if t.rows == 1:
                 w = 1.0 + 0.1 * w                      # norm vectors near 1
             o = (b.offset + t.offset) // 2
-            blob[o:o + n] = (w.view(np.uint32) >> 16).astype(np.uint16)
+            blob[o:o + n] = (w.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
     eng.weights.export(str(tmp_path))
     eng.close()
     prompt = _prompt(prompt_len, spec.vocab_size, seed=8)
