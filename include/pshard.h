@@ -183,12 +183,14 @@ int ps_wencode_rows(const void* bits, int N, int K, long long ld, const int* bas
  * zeroed buffer). No reference counterpart: the link format is this build's. */
 int ps_hx_expand(const void* piece, const unsigned* block_off, int rows, int K, const void* lut, void* out,
                  long long ld_out, void* stream);
-/* The k routed experts of a MoE layer fetched hx-coded into slots (rank j in slot j, slot
- * stride slot_stride): each slot's span carries the uint32 block offsets of matrix A at
+/* The k routed experts of a MoE layer fetched hx-coded into slots (rank j in slot j, or in
+ * slot slot_of_rank[j] when non-null — ps_moe_publish_spec's placement; slot stride
+ * slot_stride): each slot's span carries the uint32 block offsets of matrix A at
  * word hdr_a and of B at hdr_b, the matrices at mat_a / mat_b; both are expanded in one
  * launch (latency-bound: one launch's latency on the routing chain, not two) into scratch
  * expert j at out_a / out_b (bf16 rows of K_a / K_b) for the bf16 one-token kernels. */
-int ps_hx_expand_experts2(const void* slots, long long slot_stride, int k, int hdr_a, long long mat_a, int rows_a,
+int ps_hx_expand_experts2(const void* slots, long long slot_stride, const int* slot_of_rank, int k, int hdr_a,
+                          long long mat_a, int rows_a,
                           int K_a, const void* lut_a, long long out_a, int hdr_b, long long mat_b, int rows_b, int K_b,
                           const void* lut_b, long long out_b, void* scratch, long long scratch_stride, void* stream);
 int ps_hx_stats(const void* bits, int N, int K, long long ld, int* rowmax, unsigned long long* hist, void* stream);
@@ -306,6 +308,27 @@ int ps_fetcher_submit_split(void* fetcher, unsigned seq, const void* host_base, 
                             long long expert_bytes, void* slot_base, long long slot_stride, int split);
 int ps_moe_publish(void* fetcher, const int* ids, int P, int E, int* slot_of_expert, unsigned seq,
                    void* stream);
+/* Speculative (pre-gated) prefetch. ps_moe_publish_spec publishes, for the job submitted
+ * with ps_fetcher_submit_spec (slots numbered 0 .. n_slots-1):
+ *  - this layer's routed experts NOT already in its prediction set spec_state[set_cur]
+ *    (set_cur = -1: no prediction), each into slot = its rank; a predicted expert stays
+ *    in slot k_base + set_cur * S + q. slot_of_rank[r] receives rank r's slot (for
+ *    ps_hx_expand_experts2);
+ *  - then, when set_next >= 0, the S experts pred[0..S) predicted for the next layer,
+ *    recorded in spec_state[set_next] and copied AFTER the flag is raised into slots
+ *    k_base + set_next * S + q (k_base >= P; the two sets alternate by layer).
+ * Predictions only move bytes earlier or waste them; every expert is read from the slot
+ * its bytes were copied into. Predictions are copied from the next layer's group
+ * (next_base / next_stride / next_bytes; null next_base: none are copied).
+ * ps_fetcher_seq_bytes: bytes the job of `seq` copied (-1: not processed yet), for the
+ * pass's link-byte count. */
+int ps_fetcher_submit_spec(void* fetcher, unsigned seq, const void* host_base, long long expert_stride,
+                           long long expert_bytes, void* slot_base, long long slot_stride, int n_slots,
+                           const void* next_base, long long next_stride, long long next_bytes);
+int ps_moe_publish_spec(void* fetcher, const int* ids, int P, int E, int* slot_of_expert, unsigned seq,
+                        const int* pred, int S, int* spec_state, int set_cur, int set_next, int k_base,
+                        int* slot_of_rank, void* stream);
+int ps_fetcher_seq_bytes(void* fetcher, unsigned seq, long long* bytes);
 int ps_wait_flag(void* fetcher, unsigned seq, void* stream);
 int ps_fetcher_device_error(void* fetcher, unsigned* seq_out);
 

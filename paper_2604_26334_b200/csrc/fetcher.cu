@@ -19,6 +19,16 @@
 // -1 otherwise), which the mapped expert kernels use to find each expert's
 // slot. The wait kernel gives up after a timeout and raises a device-side
 // error flag instead of hanging the GPU if the host thread ever stalls.
+//
+// Speculative (pre-gated) prefetch, ps_moe_publish_spec: the publish of layer i also
+// carries S experts PREDICTED for layer i+1 (the next router applied to layer i's
+// state). The host thread copies layer i's experts, raises the flag, then copies the
+// predictions into one of two spare slot sets, so they cross the link while layer i
+// computes and layer i+1 routes — time the link would otherwise idle. Layer i+1's
+// publish skips every routed expert already in its prediction set (a hit) and lists
+// only the misses; slot_of_rank[r] tells the expansion where rank r's bytes are.
+// Predictions that miss are wasted link bytes, never wrong results: every expert is
+// read from the slot its bytes were copied into.
 #include <stdint.h>
 #include <string.h>
 
@@ -35,16 +45,31 @@
 namespace ps {
 
 // publish block (host-mapped, 64-bit words tagged with the sequence number in the high
-// half): [0] = seq:count, [1 + r] = seq:expert id of rank r (ascending ids). Every word
-// carries its own tag, so the host can accept the block word by word and the GPU
-// needs no system-scope fence (which would queue behind the copy engines' PCIe reads).
+// half): [0] = seq:(count | nspec << 16), [1 + r] = seq:(expert id | slot << 16) for the
+// `count` copies of this layer (ascending ids), then the `nspec` speculative copies.
+// Every word carries its own tag, so the host can accept the block word by word and the
+// GPU needs no system-scope fence (which would queue behind the copy engines' PCIe reads).
 constexpr int PUB_HEADER = 1;
+constexpr int PUB_SPEC_MAX = 64;
 
+__device__ __forceinline__ unsigned long long pub_word(unsigned seq, int e, int slot) {
+  return ((unsigned long long)seq << 32) | (unsigned)e | ((unsigned)slot << 16);
+}
+
+// spec == false: every routed expert is copied into slot = its rank. spec == true (one
+// CTA, P <= blockDim): rank r's expert is looked up in this layer's prediction set
+// (spec_state[set_cur][0..S), set_cur < 0: none) — a hit is already in slot
+// k_base + set_cur * S + q and is not copied; a miss goes to slot r. Then the S
+// predictions for the next layer (pred[0..S), set_next >= 0) are recorded in
+// spec_state[set_next] and published for slots k_base + set_next * S + q.
 __global__ void __launch_bounds__(1024)
 moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ slot_of_expert,
-                   volatile unsigned long long* __restrict__ pub, unsigned seq) {
-  extern __shared__ int mark[];            // E flags, then 32 warp totals
+                   volatile unsigned long long* __restrict__ pub, unsigned seq, bool spec,
+                   const int* __restrict__ pred, int S, int* __restrict__ spec_state, int set_cur, int set_next,
+                   int k_base, int* __restrict__ slot_of_rank) {
+  extern __shared__ int mark[];            // E flags, then 32 warp totals, then E rank -> id
   int* warp_tot = mark + E;
+  int* rid = warp_tot + 32;
   __shared__ int base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int e = threadIdx.x; e < E; e += blockDim.x) mark[e] = 0;
@@ -68,11 +93,36 @@ moe_publish_kernel(const int* __restrict__ ids, int P, int E, int* __restrict__ 
     if (e < E) {
       const int rank = warp_tot[warp] + __popc(m & ((1u << lane) - 1));
       slot_of_expert[e] = hit ? rank : -1;
-      if (hit) pub[PUB_HEADER + rank] = ((unsigned long long)seq << 32) | (unsigned)e;
+      if (hit) {
+        if (spec) rid[rank] = e;
+        else pub[PUB_HEADER + rank] = pub_word(seq, e, rank);
+      }
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) pub[0] = ((unsigned long long)seq << 32) | (unsigned)base;
+  if (threadIdx.x != 0) return;
+  if (!spec) {
+    pub[0] = ((unsigned long long)seq << 32) | (unsigned)base;
+    return;
+  }
+  int cnt = 0;
+  for (int r = 0; r < base; ++r) {   // <= P entries, serial: a handful in a one-token pass
+    const int e = rid[r];
+    int slot = r;
+    if (set_cur >= 0)
+      for (int q = 0; q < S; ++q)
+        if (spec_state[set_cur * S + q] == e) slot = k_base + set_cur * S + q;
+    slot_of_rank[r] = slot;
+    if (slot == r) pub[PUB_HEADER + cnt++] = pub_word(seq, e, slot);
+  }
+  int ns = 0;
+  if (set_next >= 0)
+    for (int q = 0; q < S; ++q) {
+      const int e = pred[q];
+      spec_state[set_next * S + q] = e;
+      if (e >= 0 && e < E) pub[PUB_HEADER + cnt + ns++] = pub_word(seq, e, k_base + set_next * S + q);
+    }
+  pub[0] = ((unsigned long long)seq << 32) | (unsigned)(cnt | ns << 16);
 }
 
 __global__ void wait_flag_kernel(const volatile unsigned* __restrict__ flag, unsigned seq,
@@ -102,6 +152,10 @@ struct FetchJob {
   char* slot_base;
   long long slot_stride;
   int split;   // > 0: after the first `split` ranks are issued, raise the flag to seq - 1
+  int n_slots; // slots the published slot numbers may name
+  // predictions are experts of the NEXT layer: its group's host base, stride, bytes
+  const char* spec_base;
+  long long spec_stride, spec_bytes;
 };
 
 class ExpertFetcher {
@@ -109,9 +163,9 @@ class ExpertFetcher {
   ExpertFetcher(int max_experts) : max_experts_(max_experts) {}
 
   int init() {
-    PS_CHECK_CUDA(cudaHostAlloc(&pub_host_, (PUB_HEADER + max_experts_) * sizeof(unsigned long long),
-                                cudaHostAllocMapped));
-    memset((void*)pub_host_, 0, (PUB_HEADER + max_experts_) * sizeof(unsigned long long));
+    PS_CHECK_CUDA(cudaHostAlloc(&pub_host_, pub_words() * sizeof(unsigned long long), cudaHostAllocMapped));
+    memset((void*)pub_host_, 0, pub_words() * sizeof(unsigned long long));
+    for (auto& b : seq_bytes_) b.store(-1);
     PS_CHECK_CUDA(cudaHostGetDevicePointer((void**)&pub_dev_, (void*)pub_host_, 0));
     PS_CHECK_CUDA(cudaHostAlloc(&seq_src_, kSeqRing * sizeof(unsigned), cudaHostAllocDefault));
     PS_CHECK_CUDA(cudaMalloc(&flag_dev_, 2 * sizeof(unsigned)));   // [flag, error]
@@ -149,12 +203,17 @@ class ExpertFetcher {
   unsigned long long* pub_dev() const { return pub_dev_; }
   unsigned* flag_dev() const { return flag_dev_; }
   cudaStream_t stream() const { return stream_; }
+  int max_experts() const { return max_experts_; }
   long long experts_copied() const { return copied_.load(); }
+  // bytes the job of `seq` copies (-1: not processed yet; the slot is reused every kSeqRing seqs)
+  long long seq_bytes(unsigned seq) const {
+    return seq_tag_[seq % kSeqRing].load(std::memory_order_acquire) == seq ? seq_bytes_[seq % kSeqRing].load() : -1;
+  }
   long long bytes_copied() const { return bytes_.load(); }
   int error() const { return error_.load(); }
 
  private:
-  static constexpr int kSeqRing = 1024;
+  static constexpr int kSeqRing = 1 << 16;
 
   void run() {
     cudaSetDevice(device_);
@@ -190,50 +249,64 @@ class ExpertFetcher {
         if (fw && fw[FAULT_HOST] == 0) fw[FAULT_HOST] = j.seq ? j.seq : 1;
         continue;
       }
-      unsigned n = (unsigned)(pub_host_[0] & 0xffffffffu);
-      if (n > (unsigned)max_experts_) n = 0, error_.store(2);
-      // one copy per run of consecutive expert ids when host and slot strides agree
-      // (slots are in ascending-id order, so the run is contiguous on both sides)
-      const bool coalesce = j.expert_stride == j.slot_stride;
-      unsigned ids[4096];
-      for (unsigned r = 0; r < n; ++r) {      // each word carries the tag: wait for this seq's
+      const unsigned hdr = (unsigned)(pub_host_[0] & 0xffffffffu);
+      unsigned n = hdr & 0xffffu, ns = hdr >> 16;
+      if (n > (unsigned)max_experts_ || ns > (unsigned)PUB_SPEC_MAX) n = ns = 0, error_.store(2);
+      // one copy per run of consecutive expert ids into consecutive slots when host and
+      // slot strides agree (the run is contiguous on both sides)
+      unsigned ids[4096 + PUB_SPEC_MAX], slot[4096 + PUB_SPEC_MAX];
+      unsigned total = n + ns;
+      for (unsigned r = 0; r < total; ++r) {      // each word carries the tag: wait for this seq's
         unsigned long long w;
         while ((unsigned)((w = pub_host_[PUB_HEADER + r]) >> 32) != j.seq) {
           if (stopping()) break;
         }
-        ids[r] = (unsigned)(w & 0xffffffffu);
-        if (ids[r] >= (unsigned)max_experts_) {   // never copy outside the group
+        ids[r] = (unsigned)(w & 0xffffu);
+        slot[r] = (unsigned)((w >> 16) & 0xffffu);
+        if (ids[r] >= (unsigned)max_experts_ || slot[r] >= (unsigned)j.n_slots) {   // never copy outside
           error_.store(2);
-          n = r;
+          if (r < n) n = r, ns = 0; else ns = r - n;
+          total = n + ns;
           break;
         }
       }
+      const long long moved = (long long)n * j.expert_bytes + (long long)ns * j.spec_bytes;
+      copied_ += total;
+      bytes_ += moved;
+      seq_bytes_[j.seq % kSeqRing].store(moved);
+      seq_tag_[j.seq % kSeqRing].store(j.seq, std::memory_order_release);
       bool half_sent = j.split <= 0;
-      for (unsigned r = 0; r < n;) {
-        if (!half_sent && r >= (unsigned)j.split) {   // the first ranks have landed: seq - 1
-          unsigned* hs = seq_src_ + (ring_i_++ % kSeqRing);
-          *hs = j.seq - 1;
-          if (cudaMemcpyAsync(flag_dev_, hs, sizeof(unsigned), cudaMemcpyHostToDevice, stream_) != cudaSuccess)
+      auto copy_runs = [&](unsigned r, unsigned end, const char* hbase, long long hstride, long long hbytes) {
+        const bool coalesce = hstride == j.slot_stride;
+        while (r < end) {
+          if (!half_sent && r >= (unsigned)j.split) {   // the first ranks have landed: seq - 1
+            flag(j.seq - 1);
+            half_sent = true;
+          }
+          const unsigned e = ids[r];
+          unsigned run = 1;
+          const unsigned lim = half_sent ? end : (unsigned)j.split;   // runs never cross the split
+          while (coalesce && r + run < lim && ids[r + run] == e + run && slot[r + run] == slot[r] + run) ++run;
+          const long long bytes = (long long)(run - 1) * hstride + hbytes;
+          if (cudaMemcpyAsync(j.slot_base + (long long)slot[r] * j.slot_stride, hbase + (long long)e * hstride,
+                              bytes, cudaMemcpyHostToDevice, stream_) != cudaSuccess)
             error_.store(3);
-          half_sent = true;
+          r += run;
         }
-        const unsigned e = ids[r];
-        unsigned run = 1;
-        const unsigned lim = half_sent ? n : (unsigned)j.split;   // runs never cross the split
-        while (coalesce && r + run < lim && ids[r + run] == e + run) ++run;
-        const long long bytes = (long long)(run - 1) * j.expert_stride + j.expert_bytes;
-        if (cudaMemcpyAsync(j.slot_base + r * j.slot_stride, j.host_base + (long long)e * j.expert_stride, bytes,
-                            cudaMemcpyHostToDevice, stream_) != cudaSuccess)
-          error_.store(3);
-        r += run;
-      }
-      copied_ += n;
-      bytes_ += (long long)n * j.expert_bytes;
-      unsigned* src = seq_src_ + (ring_i_++ % kSeqRing);
-      *src = j.seq;
-      if (cudaMemcpyAsync(flag_dev_, src, sizeof(unsigned), cudaMemcpyHostToDevice, stream_) != cudaSuccess)
-        error_.store(3);
+      };
+      if (ns && !j.spec_base) error_.store(2);   // predictions published for a job that cannot copy them
+      copy_runs(0, n, j.host_base, j.expert_stride, j.expert_bytes);
+      flag(j.seq);
+      if (ns && j.spec_base)   // predictions for the next layer: behind the flag, link otherwise idle
+        copy_runs(n, total, j.spec_base, j.spec_stride, j.spec_bytes);
     }
+  }
+
+  void flag(unsigned v) {
+    unsigned* src = seq_src_ + (ring_i_++ % kSeqRing);
+    *src = v;
+    if (cudaMemcpyAsync(flag_dev_, src, sizeof(unsigned), cudaMemcpyHostToDevice, stream_) != cudaSuccess)
+      error_.store(3);
   }
 
   bool stopping() {
@@ -241,8 +314,12 @@ class ExpertFetcher {
     return stop_;
   }
 
+  int pub_words() const { return PUB_HEADER + max_experts_ + PUB_SPEC_MAX; }
+
   int max_experts_;
   int device_ = 0;
+  std::atomic<long long> seq_bytes_[kSeqRing];
+  std::atomic<unsigned> seq_tag_[kSeqRing] = {};
   volatile unsigned long long* pub_host_ = nullptr;
   unsigned long long* pub_dev_ = nullptr;
   unsigned* seq_src_ = nullptr;
@@ -310,7 +387,28 @@ int ps_fetcher_submit(void* f, unsigned seq, const void* host_base, long long ex
   PS_REQUIRE(x != nullptr, "ps_fetcher_submit: null fetcher");
   PS_REQUIRE(expert_bytes > 0 && slot_stride >= expert_bytes, "ps_fetcher_submit: bad sizes");
   x->submit(FetchJob{seq, static_cast<const char*>(host_base), expert_stride, expert_bytes,
-                     static_cast<char*>(slot_base), slot_stride, 0});
+                     static_cast<char*>(slot_base), slot_stride, 0, x->max_experts(), nullptr, 0, 0});
+  return PS_OK;
+}
+
+int ps_fetcher_submit_spec(void* f, unsigned seq, const void* host_base, long long expert_stride,
+                           long long expert_bytes, void* slot_base, long long slot_stride, int n_slots,
+                           const void* next_base, long long next_stride, long long next_bytes) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr, "ps_fetcher_submit_spec: null fetcher");
+  PS_REQUIRE(expert_bytes > 0 && slot_stride >= expert_bytes && n_slots >= 1 && n_slots <= 65535 &&
+                 (!next_base || (next_bytes > 0 && slot_stride >= next_bytes)),
+             "ps_fetcher_submit_spec: bad sizes / n_slots %d", n_slots);
+  x->submit(FetchJob{seq, static_cast<const char*>(host_base), expert_stride, expert_bytes,
+                     static_cast<char*>(slot_base), slot_stride, 0, n_slots, static_cast<const char*>(next_base),
+                     next_stride, next_bytes});
+  return PS_OK;
+}
+
+int ps_fetcher_seq_bytes(void* f, unsigned seq, long long* bytes) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr && bytes, "ps_fetcher_seq_bytes: null argument");
+  *bytes = x->seq_bytes(seq);
   return PS_OK;
 }
 
@@ -321,7 +419,7 @@ int ps_fetcher_submit_split(void* f, unsigned seq, const void* host_base, long l
   PS_REQUIRE(expert_bytes > 0 && slot_stride >= expert_bytes && split >= 1 && seq >= 2,
              "ps_fetcher_submit_split: bad sizes / split %d / seq %u", split, seq);
   x->submit(FetchJob{seq, static_cast<const char*>(host_base), expert_stride, expert_bytes,
-                     static_cast<char*>(slot_base), slot_stride, split});
+                     static_cast<char*>(slot_base), slot_stride, split, x->max_experts(), nullptr, 0, 0});
   return PS_OK;
 }
 
@@ -329,8 +427,24 @@ int ps_moe_publish(void* f, const int* ids, int P, int E, int* slot_of_expert, u
   auto* x = static_cast<ExpertFetcher*>(f);
   PS_REQUIRE(x != nullptr && P >= 1 && E >= 1, "ps_moe_publish: P=%d E=%d", P, E);
   const int threads = E >= 1024 ? 1024 : (E + 31) / 32 * 32;
-  moe_publish_kernel<<<1, threads, (E + 32) * sizeof(int), (cudaStream_t)stream>>>(ids, P, E, slot_of_expert,
-                                                                                   x->pub_dev(), seq);
+  moe_publish_kernel<<<1, threads, (2 * E + 32) * sizeof(int), (cudaStream_t)stream>>>(
+      ids, P, E, slot_of_expert, x->pub_dev(), seq, false, nullptr, 0, nullptr, -1, -1, 0, nullptr);
+  PS_CHECK_LAUNCH();
+  return PS_OK;
+}
+
+int ps_moe_publish_spec(void* f, const int* ids, int P, int E, int* slot_of_expert, unsigned seq, const int* pred,
+                        int S, int* spec_state, int set_cur, int set_next, int k_base, int* slot_of_rank,
+                        void* stream) {
+  auto* x = static_cast<ExpertFetcher*>(f);
+  PS_REQUIRE(x != nullptr && P >= 1 && E >= 1 && E <= x->max_experts() && P <= 1024 && S >= 0 &&
+                 S <= PUB_SPEC_MAX && set_cur >= -1 && set_cur <= 1 && set_next >= -1 && set_next <= 1 &&
+                 (S == 0 || spec_state) && slot_of_rank && (set_next < 0 || pred) && k_base >= P,
+             "ps_moe_publish_spec: P=%d E=%d S=%d sets %d/%d k_base %d", P, E, S, set_cur, set_next, k_base);
+  const int threads = E >= 1024 ? 1024 : (E + 31) / 32 * 32;
+  moe_publish_kernel<<<1, threads, (2 * E + 32) * sizeof(int), (cudaStream_t)stream>>>(
+      ids, P, E, slot_of_expert, x->pub_dev(), seq, true, pred, S, spec_state, set_cur, set_next, k_base,
+      slot_of_rank);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

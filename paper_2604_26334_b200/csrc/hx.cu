@@ -283,7 +283,7 @@ hx_write_kernel(const uint16_t* __restrict__ bits, int K, long long ld, const in
 }
 
 // The routed experts of one MoE layer, fetched hx-coded into slots (expert rank j in slot
-// j): each slot holds a span [uint32 block offsets of both matrices][...][hx matrices];
+// j, or slot_of_rank[j] when the fetcher placed it — a speculative prefetch hit): each slot holds a span [uint32 block offsets of both matrices][...][hx matrices];
 // item (j, b, part) expands block b of expert j's matrix into scratch expert j (out_off
 // bytes into it, rows of K bf16) for the bf16 one-token expert kernels.
 // Both matrices of the routed experts (gate/up, down) in ONE launch: the expansion is
@@ -299,8 +299,9 @@ struct HxExpertMat {
 };
 
 __global__ void __launch_bounds__(32 * HX_EXP_WARPS)
-hx_expand_experts2_kernel(const uint8_t* __restrict__ slots, long long slot_stride, int k, HxExpertMat a,
-                          HxExpertMat b, int grid_a, uint8_t* __restrict__ scratch, long long scratch_stride) {
+hx_expand_experts2_kernel(const uint8_t* __restrict__ slots, long long slot_stride, const int* __restrict__ slot_of_rank,
+                          int k, HxExpertMat a, HxExpertMat b, int grid_a, uint8_t* __restrict__ scratch,
+                          long long scratch_stride) {
   __shared__ uint32_t lut[HX_LUT];
   __shared__ uint32_t row_start[HX_BLOCK_ROWS];
   extern __shared__ uint32_t hx_exps[];
@@ -314,7 +315,7 @@ hx_expand_experts2_kernel(const uint8_t* __restrict__ slots, long long slot_stri
   for (int item = cta; item < k * nb * parts; item += ncta) {
     const int part = item % parts, jb = item / parts;
     const int j = jb / nb, bb = jb - (jb / nb) * nb;
-    const uint8_t* span = slots + j * slot_stride;
+    const uint8_t* span = slots + (long long)(slot_of_rank ? slot_of_rank[j] : j) * slot_stride;
     const uint32_t off = reinterpret_cast<const uint32_t*>(span)[m.hdr_word + bb];
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(scratch + j * scratch_stride + m.out_off) +
                        (long long)bb * HX_BLOCK_ROWS * m.K;
@@ -362,7 +363,8 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
   return PS_OK;
 }
 
-extern "C" int ps_hx_expand_experts2(const void* slots, long long slot_stride, int k, int hdr_a, long long mat_a,
+extern "C" int ps_hx_expand_experts2(const void* slots, long long slot_stride, const int* slot_of_rank, int k,
+                                     int hdr_a, long long mat_a,
                                      int rows_a, int K_a, const void* lut_a, long long out_a, int hdr_b,
                                      long long mat_b, int rows_b, int K_b, const void* lut_b, long long out_b,
                                      void* scratch, long long scratch_stride, void* stream) {
@@ -393,7 +395,8 @@ extern "C" int ps_hx_expand_experts2(const void* slots, long long slot_stride, i
   const HxExpertMat a{hdr_a, mat_a, rows_a, K_a, static_cast<const uint32_t*>(lut_a), out_a};
   const HxExpertMat b{hdr_b, mat_b, rows_b, K_b, static_cast<const uint32_t*>(lut_b), out_b};
   hx_expand_experts2_kernel<<<ga + gb, per_cta, smem, (cudaStream_t)stream>>>(
-      static_cast<const uint8_t*>(slots), slot_stride, k, a, b, ga, static_cast<uint8_t*>(scratch), scratch_stride);
+      static_cast<const uint8_t*>(slots), slot_stride, slot_of_rank, k, a, b, ga, static_cast<uint8_t*>(scratch),
+      scratch_stride);
   PS_CHECK_LAUNCH();
   return PS_OK;
 }

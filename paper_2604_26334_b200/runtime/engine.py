@@ -458,7 +458,7 @@ class Engine:
         if timing:
             ev1 = L.event_create(True)
             L.call("ps_event_record", ev1, ex.cs)
-        s.passes.append([tier, stats.T, ev0, ev1, stats.bytes_streamed,
+        s.passes.append([tier, stats.T, ev0, ev1, stats,   # bytes read after the final synchronize
                          step.context_consumed == 0 and step.decoded > 0, stats.zero_copy_bytes])
         if step.first_prompt_done and s.ttft is None:
             self._drain(ex, s.pending_host, s.out)   # first token is on the host
@@ -483,7 +483,8 @@ class Engine:
         total = time.perf_counter() - s.t_start
         decode_time, decode_tokens = 0.0, 0
         pass_rows = []
-        for tier, T, e0, e1, nbytes, is_decode, zc in s.passes:
+        for tier, T, e0, e1, st, is_decode, zc in s.passes:
+            nbytes = st.bytes_streamed    # settled: speculative fetches count what crossed
             secs = L.event_elapsed_ms(e0, e1) / 1e3 if timing else float("nan")
             # (tier, tokens, seconds, bytes via the copy engine, bytes read zero-copy)
             pass_rows.append((tier, T, secs, nbytes, zc))

@@ -30,7 +30,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -140,6 +140,9 @@ class PassStats:
     kv_writeback_bytes: int = 0
     zero_copy_bytes: int = 0
     kernel_calls: int = 0
+    fetch_seqs: list = field(default_factory=list)   # (seq, bytes counted) until settled
+    spec_hits: int = 0           # routed experts found prefetched (settled with the bytes)
+    spec_routed: int = 0         # routed experts of the layers that had a prediction set
 
 
 @dataclass
@@ -259,6 +262,7 @@ class Executor:
         self.d2d_bytes = 0                          # tier switches: weights relocated in VRAM
         self.tracer = None                          # runtime.tracer.Tracer when attached
         self.stats: list[PassStats] = []
+        self._unsettled: list[PassStats] = []   # passes with speculative fetches to settle
         self.host_tokens: list = []
         self._prev_sample_slots = None
         self._hx_res_on = self._hx_on
@@ -358,7 +362,12 @@ class Executor:
             spec += [("m_logits", "moe_logits", T * E * 4), ("m_ids", "moe_ids", P * 4),
                      ("m_w", "moe_w", P * 4), ("m_plan", "moe_plan", n_ints.value * 4),
                      ("m_h", "moe_h", P * eff * 4), ("m_out", "moe_out", P * d * 4),
-                     ("m_slotmap", "moe_slot_of_expert", E * 4)]
+                     ("m_slotmap", "moe_slot_of_expert", E * 4),
+                     # speculative prefetch: rank -> slot, predicted ids / weights, the two
+                     # prediction sets, the next layer's normalised input
+                     ("m_sor", "moe_slot_of_rank", P * 4), ("m_pids", "moe_pred_ids", 64 * 4),
+                     ("m_pw", "moe_pred_w", 64 * 4), ("m_spec", "moe_spec_state", 2 * 64 * 4),
+                     ("m_xp", "moe_pred_x", d * 4)]
         return spec
 
     def _hx_expand_bytes(self) -> int:
@@ -466,6 +475,24 @@ class Executor:
         """One-token MoE passes fetch routed experts hx-coded (PS_HX_EXPERTS=0: off)."""
         return (T == 1 and self._hx_on and bool(getattr(self.hx, "experts", None)) and self.fetch_enabled and
                 os.environ.get("PS_HX_EXPERTS", "1") != "0")
+
+    def _spec_n(self, T: int) -> int:
+        """_spec_want(T) when the carved expert slots have room for the two prediction
+        sets, else 0."""
+        S = self._spec_want(T)
+        if S and getattr(self, "expert_slot_count", 0) < T * self.moe.top_k + 2 * S:
+            return 0
+        return S
+
+    def _spec_want(self, T: int) -> int:
+        """Experts predicted per fetched MoE layer for the next one (speculative pre-gated
+        prefetch, csrc/fetcher.cu; PS_MOE_SPEC, default 2, 0: off): one-token passes that
+        fetch hx-coded experts. The next layer's router applied to this layer's
+        post-attention state picks ~78 % of its top-2 among the next layer's top-8 on
+        Qwen3-30B-A3B shapes (scratch measurement)."""
+        if self.moe is None or not self._hx_experts_on(T):
+            return 0
+        return max(0, min(int(os.environ.get("PS_MOE_SPEC", "2")), self.moe.top_k, 64))
 
     def _early_head_plan(self, T: int, R: int):
         """(final_norm ptr, head W ptr, ldw, coded) when this pass should read its CPU-placed
@@ -587,6 +614,8 @@ class Executor:
         _, _, _, ebytes = self._expert_geometry(groups[0], self.shards[groups[0]].layer_index)
         slot = (ebytes + 255) // 256 * 256
         n = min(self.moe.n_experts, T * self.moe.top_k)
+        if (n + 2 * self._spec_want(T)) * slot <= free // 4:
+            n += 2 * self._spec_want(T)   # the two prediction sets, when they fit as well
         if n * slot > free // 4:
             return 0, 0
         return n, slot
@@ -771,7 +800,7 @@ class Executor:
         the slots take at most a quarter of the free budget (decided before spare
         pinning, `_slot_bytes`); otherwise the expert kernels read the routed
         experts zero-copy."""
-        self.expert_slots, self.expert_slot_bytes = 0, 0
+        self.expert_slots, self.expert_slot_bytes, self.expert_slot_count = 0, 0, 0
         if modes is None:
             modes = {sid: m for sid, (m, _) in self.residency.items() if m != "pinned"}
         plan_free = self.arena.free_bytes + sum((self._phys_bytes(self.shards[sid]) + 255) // 256 * 256
@@ -781,7 +810,7 @@ class Executor:
             return
         # the spare pins were sized around these slots
         self.expert_slots = self.arena.alloc_high("expert_slots", n * slot)
-        self.expert_slot_bytes = slot
+        self.expert_slot_bytes, self.expert_slot_count = slot, n
         if self.fetcher is None:
             out = C.c_void_p()
             L.call("ps_fetcher_create", self.moe.n_experts, C.byref(out))
@@ -1232,11 +1261,15 @@ class Executor:
                 os.environ.get("PS_CODED_EXPERTS", "1") != "0"):
             cexp = getattr(self.coded, "experts", {}).get(sid)
 
+        spec_n = self._spec_n(T) if (t1 and fetched and hxe is not None) else 0
+
         def hx_gate_up(ebase, slot_map, r0, r1):
             """Routed experts of ranks [r0, r1): spans -> bf16 scratch experts (blob layout),
-            then their gate/up + SwiGLU."""
+            then their gate/up + SwiGLU. With speculative prefetch rank r's span is in slot
+            m_sor[r] (the fetcher's placement), else in slot r."""
             sc, sst = self.hx_escratch, stride
-            L.call("ps_hx_expand_experts2", ebase + r0 * sb, sb, r1 - r0,
+            span0, sor = (ebase, self.m_sor + r0 * 4) if spec_n else (ebase + r0 * sb, None)
+            L.call("ps_hx_expand_experts2", span0, sb, sor, r1 - r0,
                    0, hxe["gu_off"], hxe["gu_rows"], hxe["gu_k"], self.hx_lut + self.hx.lut_off[(sid, "wgu")], 0,
                    hxe["nb_gu"], hxe["dn_off"], hxe["dn_rows"], hxe["dn_k"],
                    self.hx_lut + self.hx.lut_off[(sid, "wdown")], down_off, sc + r0 * sst, sst, self.cs)
@@ -1277,7 +1310,8 @@ class Executor:
             # then seq). Measured neutral on config 3 (19.85 vs 19.80 tokens/s): the chain
             # after the last expert lands is the expansion's fixed latency (one 256-weight
             # serial decode), the same for 4 experts as for 8. Off by default.
-            split = k // 2 if (hxe is not None and k >= 2 and os.environ.get("PS_MOE_SPLIT", "0") == "1") else 0
+            split = k // 2 if (hxe is not None and k >= 2 and not spec_n and
+                               os.environ.get("PS_MOE_SPLIT", "0") == "1") else 0
             self.fetch_seq = (self.fetch_seq + (2 if split else 1)) & 0xFFFFFFFF
             if self.fetch_seq < 2:
                 self.fetch_seq = 2
@@ -1292,8 +1326,44 @@ class Executor:
             self._traced(f"L{layer}.router+topk", route, base)
             if pre is not None:
                 self.ring.seal(region, [self._record(self.cs)])
+            # speculative prefetch: this layer's hits sit in prediction set `set_cur`; the
+            # next layer's router (staged by gap filling) picks spec_n experts from this
+            # layer's post-attention state, copied into set `set_next` behind this layer's
+            # experts (csrc/fetcher.cu)
+            set_cur = set_next = -1
+            nxt_hx = None
+            if spec_n:
+                pend = self._spec_pending
+                set_cur = pend[1] if pend is not None and pend[0] == layer else -1
+                self._spec_pending = None
+                nxt = self.by_layer_kind.get((layer + 1, ShardKind.MOE_EXPERT_GROUP))
+                pre_n = self._prefix_dev.get(nxt.id) if nxt is not None else None
+                nxt_hx = self.hx.experts.get(nxt.id) if pre_n is not None else None
+                if nxt_hx is not None:
+                    set_next = 1 - set_cur if set_cur >= 0 else 0
+                    nblob = self.w.layout.blobs[nxt.id]
+                    _, nbase, narrived = pre_n
+                    self._wait(narrived)
+
+                    def predict(_p, _a, _b):
+                        L.call("ps_rmsnorm", self.x, d, 0, T, nbase + nblob.tensors[f"L{layer + 1}.ffn_norm"].offset,
+                               d, self.arch.rms_eps, self.m_xp, d, 0, self.cs)
+                        self._matmul(T, self.m_xp, nbase + nblob.tensors[f"L{layer + 1}.router"].offset, E, d,
+                                     self.m_logits, E, L.PS_EPI_STORE)
+                        L.call("ps_moe_route_topk", self.m_logits, E, T, E, spec_n, 1, self.m_pids, self.m_pw,
+                               self.cs)
+                    self._traced(f"L{layer}.predict L{layer + 1}", predict, 0, 0, 0)
+                    self._spec_pending = (layer + 1, set_next)
 
             def fetch(_p, _a, _b):
+                if spec_n:
+                    L.call("ps_fetcher_submit_spec", self.fetcher, seq, src0, src_stride, ebytes, slots, sb,
+                           self.expert_slot_count, self.hx.shard_ptr(nxt.id) if nxt_hx else None,
+                           nxt_hx["stride"] if nxt_hx else 0, nxt_hx["stride"] if nxt_hx else 0)
+                    L.call("ps_moe_publish_spec", self.fetcher, self.m_ids, P, E, self.m_slotmap, seq,
+                           self.m_pids, spec_n, self.m_spec, set_cur, set_next, P, self.m_sor, self.cs)
+                    L.call("ps_wait_flag", self.fetcher, seq, self.cs)
+                    return
                 if split:
                     L.call("ps_fetcher_submit_split", self.fetcher, seq, src0, src_stride, ebytes, slots, sb, split)
                 else:
@@ -1325,6 +1395,10 @@ class Executor:
             self._traced(f"L{layer}.experts", run, 0, 0, 0)
             self._stat.bytes_streamed += min(E, P) * ebytes
             self._stat.copies += min(E, P)
+            if spec_n:   # the fetcher decides what crosses the link: settled after the pass
+                self._stat.fetch_seqs.append((seq, min(E, P) * ebytes, ebytes,
+                                              spec_n * nxt_hx["stride"] if set_next >= 0 else 0,
+                                              min(E, P) if set_cur >= 0 else 0))
             if not t1:
                 L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
             return
@@ -1363,7 +1437,7 @@ class Executor:
         L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
 
     # ------------------------------------------------- gap filling (MoE decode)
-    def _plan_gapfill(self, gemv: bool, R: int) -> None:
+    def _plan_gapfill(self, gemv: bool, R: int, T: int = 0) -> None:
         """Zero-copy / fetched MoE decode leaves the host link idle between layers
         (expert kernels, the next layer's attention, router and top-k run while no
         expert byte can move yet). Two kinds of bytes are known in advance and fill
@@ -1377,6 +1451,7 @@ class Executor:
         Enabled only when nothing else in the pass uses the ring."""
         self._gapfill, self._piece_override, self._prefetched = None, {}, {}
         self._prefix_queue, self._prefix_dev = [], {}
+        self._spec_pending = None
         if not (gemv and R and self.moe is not None and self.ring is not None) or \
                 os.environ.get("PS_GAPFILL", "1") == "0":
             return
@@ -1409,6 +1484,8 @@ class Executor:
                              if self.residency[sid][0] == "stream")
             self._prefix_queue = [sid for _, sid in fetched]
             self._upload_prefix()
+            if self._spec_n(T):   # two ahead: the next layer's router predicts its experts
+                self._upload_prefix()
         # the pass opens with pinned layers and the first routing chain before any
         # expert byte can move: two head pieces keep the link busy meanwhile
         for _ in range(min(2, len(pieces))):
@@ -1501,6 +1578,7 @@ class Executor:
         if T > self.T_tier:
             raise SpecError(f"pass of {T} tokens exceeds the tier's {self.T_tier}-token buffers")
         nb = len(ps.slots)
+        self.settle()
         self._stat = PassStats(self.tier, T)
         calls0 = L.counters["kernel_calls"]
         gemv = T <= GEMV_MAX_T
@@ -1572,7 +1650,7 @@ class Executor:
         def norm(w_ptr):
             L.call("ps_rmsnorm", self.x, d, 0, T, w_ptr, d, eps, xn, d, 0 if gemv else 1, self.cs)
 
-        self._plan_gapfill(gemv, len(ps.sample))
+        self._plan_gapfill(gemv, len(ps.sample), T)
 
         for layer in range(self.spec.n_layers):
             attn_sid = self.by_layer_kind[(layer, ShardKind.ATTENTION)].id
@@ -1698,6 +1776,8 @@ class Executor:
             self.kv_len[slot] = max(self.kv_len[slot], p0 + n)
         self._stat.kernel_calls = L.counters["kernel_calls"] - calls0
         self.stats.append(self._stat)
+        if self._stat.fetch_seqs:
+            self._unsettled.append(self._stat)
         return self._stat
 
     # ------------------------------------------------------------------ results
@@ -1733,6 +1813,31 @@ class Executor:
     def synchronize(self) -> None:
         for s in (self.cs, self.h2d, self.d2h, self.hs):
             L.call("ps_stream_synchronize", s)
+        self.settle()
+
+    def settle(self) -> None:
+        """Replace the link bytes counted for speculatively fetched layers (k experts each)
+        by what the fetcher copied (misses + predictions), for every job the fetcher has
+        processed (all of them after a synchronize). Also called at each pass start, so the
+        fetcher's per-seq record (a ring of 65536 seqs) is read long before it wraps."""
+        keep = []
+        for st in self._unsettled:
+            rest = []
+            for seq, counted, ebytes, pred_bytes, routed in st.fetch_seqs:
+                got = C.c_longlong(-1)
+                L.call("ps_fetcher_seq_bytes", self.fetcher, seq, C.byref(got))
+                if got.value < 0:
+                    rest.append((seq, counted, ebytes, pred_bytes, routed))
+                    continue
+                st.bytes_streamed += got.value - counted
+                misses = (got.value - pred_bytes) // max(1, ebytes)
+                if routed:   # the routed experts that were not copied were prefetched hits
+                    st.spec_routed += routed
+                    st.spec_hits += routed - misses
+            st.fetch_seqs = rest
+            if rest:
+                keep.append(st)
+        self._unsettled = keep
 
     def close(self) -> None:
         if self.fetcher is not None:

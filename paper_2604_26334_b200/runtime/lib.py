@@ -71,6 +71,9 @@ _SIGS = {
     "ps_fetcher_submit": [_p, C.c_uint, _p, _ll, _ll, _p, _ll],
     "ps_fetcher_submit_split": [_p, C.c_uint, _p, _ll, _ll, _p, _ll, _i],
     "ps_moe_publish": [_p, _p, _i, _i, _p, C.c_uint, _p],
+    "ps_fetcher_submit_spec": [_p, C.c_uint, _p, _ll, _ll, _p, _ll, _i, _p, _ll, _ll],
+    "ps_moe_publish_spec": [_p, _p, _i, _i, _p, C.c_uint, _p, _i, _p, _i, _i, _i, _p, _p],
+    "ps_fetcher_seq_bytes": [_p, C.c_uint, C.POINTER(_ll)],
     "ps_wait_flag": [_p, C.c_uint, _p],
     "ps_fetcher_device_error": [_p, C.POINTER(C.c_uint)],
     "ps_stripe_ctl_bytes": [C.POINTER(_ll)],
@@ -91,7 +94,7 @@ _SIGS = {
     "ps_wencode_stats": [_p, _i, _i, _ll, _p, _p, _p],
     "ps_wencode_rows": [_p, _i, _i, _ll, _p, _i, _p, _ll, _p],
     "ps_hx_expand": [_p, _p, _i, _i, _p, _p, _ll, _p],
-    "ps_hx_expand_experts2": [_p, _ll, _i, _i, _ll, _i, _i, _p, _ll, _i, _ll, _i, _i, _p, _ll, _p, _ll, _p],
+    "ps_hx_expand_experts2": [_p, _ll, _p, _i, _i, _ll, _i, _i, _p, _ll, _i, _ll, _i, _i, _p, _ll, _p, _ll, _p],
     "ps_hx_stats": [_p, _i, _i, _ll, _p, _p, _p],
     "ps_hx_sizes": [_p, _i, _i, _ll, _p, _p, _p, _p, _p],
     "ps_hx_write": [_p, _i, _i, _ll, _p, _p, _p, _p, _p, _p, _p],
@@ -148,7 +151,7 @@ KERNEL_CALLS = frozenset({
     "ps_upload_small", "ps_init_uniform_bf16", "ps_init_interleaved_bf16", "ps_init_rowscaled_bf16", "ps_gemv_bf16_cfg", "ps_gemm_bf16_cfg",
     "ps_moe_route_topk", "ps_moe_plan", "ps_moe_expert_gu", "ps_moe_expert_down", "ps_moe_combine", "ps_moe_decode_experts", "ps_moe_decode_experts_c", "ps_moe_decode_experts_phase", "ps_gemv_bf16c", "ps_gemv_tc", "ps_expand_coded", "ps_gemv_head_early", "ps_set_flag",
     "ps_wencode_stats", "ps_wencode_rows", "ps_hx_expand", "ps_hx_expand_experts2", "ps_hx_stats", "ps_hx_sizes", "ps_hx_write",
-    "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_wait_flag",
+    "ps_moe_expert_gu_mapped", "ps_moe_expert_down_mapped", "ps_moe_publish", "ps_moe_publish_spec", "ps_wait_flag",
     "ps_stripe_signal", "ps_stripe_wait", "ps_attn_prefill_tc"})
 counters = {"kernel_calls": 0, "memcpy_calls": 0}
 

@@ -824,6 +824,46 @@ def test_moe_hx_experts_same_tokens_fewer_bytes(monkeypatch):
     assert_exact_parity(ref, prompt, np.array(out["1"][0]), out["1"][4])
 
 
+def test_moe_speculative_prefetch_same_tokens(monkeypatch):
+    """Speculative (pre-gated) expert prefetch: each fetched MoE layer publishes, with its
+    own routed experts, the top-2 experts the next layer's router picks from this layer's
+    state; the fetcher copies them (from the next layer's group) behind the flag and the
+    next layer copies only its misses. Same tokens and logits as without
+    (PS_MOE_SPEC=0) at every budget; at some budget predictions are made and some hit;
+    the pass rows carry the settled (fetcher-counted) link bytes."""
+    import dataclasses
+    from paper_2604_26334_b200.planning.graph import MoeSpec
+    from paper_2604_26334_b200.runtime.engine import Engine
+    base = catalog.builtin_model("tiny-moe")
+    # 64 experts of 256 (hx needs K % 256 == 0): expert slots (k + two prediction sets)
+    # stay within a quarter of the free budget
+    spec = dataclasses.replace(base, n_layers=4, moe=MoeSpec(64, base.moe.top_k, 256))
+    prompt = _prompt(24, spec.vocab_size, seed=18)
+    engaged = 0
+    for frac in (0.5, 0.7):
+        out = {}
+        for sp in ("0", "2"):
+            monkeypatch.setenv("PS_MOE_SPEC", sp)
+            eng = Engine(spec, budget_bytes=frac * total_model_bytes(spec), context_len=160)
+            res = eng.generate([prompt], gen_len=12)
+            ex = eng.executor
+            dec = [s for s in ex.stats if s.T == 1]
+            out[sp] = (res.tokens[0].tolist(), eng.logits().copy(), ex.fetcher_stats(),
+                       sum(s.spec_hits for s in dec), sum(s.spec_routed for s in dec),
+                       sum(s.bytes_streamed for s in ex.stats), sum(p[3] for p in res.passes),
+                       ex._spec_n(1), ex.expert_slot_count, ex._gapfill is not None)
+            eng.close()
+        print(frac, {sp: o[2:5] + o[7:] for sp, o in out.items()})
+        assert out["2"][0] == out["0"][0], frac
+        assert np.array_equal(out["2"][1], out["0"][1]), frac
+        assert out["0"][4] == 0
+        assert out["2"][5] == out["2"][6]     # pass rows carry the settled bytes
+        if out["2"][4]:
+            engaged += 1
+            assert 0 < out["2"][3] <= out["2"][4]
+    assert engaged, "no budget gave a pass with a prediction set"
+
+
 @pytest.mark.parametrize("frac", [0.5, 0.45])
 def test_early_head_same_tokens(monkeypatch, frac):
     """One-token passes whose output head is CPU-placed read it early: the head GEMV runs

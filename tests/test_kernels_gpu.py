@@ -492,6 +492,59 @@ def test_expert_fetcher_publish_copy_wait():
         lib.call("ps_fetcher_destroy", f)
 
 
+def test_expert_fetcher_speculative_slots():
+    """ps_moe_publish_spec: a layer's routed experts already in its prediction set are not
+    copied (slot_of_rank points at the prediction slot), misses go to slot = rank, and the
+    next layer's predictions are copied behind the flag into the other set; the per-seq
+    byte count is misses + predictions."""
+    import ctypes
+    lib = L()
+    E, k, S, nbytes = 16, 4, 2, 4096
+    n_slots = k + 2 * S
+    f = ctypes.c_void_p()
+    lib.call("ps_fetcher_create", E, ctypes.byref(f))
+    try:
+        host = lib.host_alloc(E * nbytes, mapped=True)
+        src = (np.arange(E * nbytes, dtype=np.uint32) % 251).astype(np.uint8).reshape(E, nbytes)
+        src[:, 0] = np.arange(E)
+        ctypes.memmove(host, src.ctypes.data, src.nbytes)
+        slots = torch.zeros(n_slots * nbytes, dtype=torch.uint8, device="cuda")
+        slotmap = torch.zeros(E, dtype=torch.int32, device="cuda")
+        sor = torch.full((k,), -7, dtype=torch.int32, device="cuda")
+        state = torch.full((2 * S,), -1, dtype=torch.int32, device="cuda")
+        # (routed ids, set_cur, predictions for the next layer, set_next, expected slot_of_rank, copies)
+        layers = [([3, 9, 1, 15], -1, [2, 9], 0, [0, 1, 2, 3], 6),
+                  ([9, 2, 5, 6], 0, [7, 8], 1, [4, 1, 2, 5], 4),
+                  ([7, 0, 8, 8], 1, None, -1, [0, 6, 7], 1)]
+        for seq, (ids, cur, pred, nxt, want, copies) in enumerate(layers, start=2):
+            dev_ids = torch.tensor(ids, dtype=torch.int32, device="cuda")
+            dev_pred = torch.tensor(pred or [0], dtype=torch.int32, device="cuda")
+            lib.call("ps_fetcher_submit_spec", f, seq, host, nbytes, nbytes, slots.data_ptr(), nbytes, n_slots,
+                     host, nbytes, nbytes)
+            lib.call("ps_moe_publish_spec", f, dev_ids.data_ptr(), k, E, slotmap.data_ptr(), seq,
+                     dev_pred.data_ptr(), S, state.data_ptr(), cur, nxt, k, sor.data_ptr(), stream())
+            lib.call("ps_wait_flag", f, seq, stream())
+            torch.cuda.synchronize()
+            routed = sorted(set(ids))
+            got_sor = sor.cpu().numpy()[:len(routed)].tolist()
+            assert got_sor == want, (seq, got_sor, want)
+            got = slots.cpu().numpy().reshape(n_slots, nbytes)
+            for r, e in enumerate(routed):
+                assert np.array_equal(got[got_sor[r]], src[e]), (seq, r, e)
+            m = slotmap.cpu().numpy()
+            for e in range(E):
+                assert m[e] == (routed.index(e) if e in routed else -1)
+            b = ctypes.c_longlong()
+            lib.call("ps_fetcher_seq_bytes", f, seq, ctypes.byref(b))
+            assert b.value == copies * nbytes, (seq, b.value)
+        n, b, err = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_int()
+        lib.call("ps_fetcher_info", f, None, None, ctypes.byref(n), ctypes.byref(b), ctypes.byref(err))
+        assert (n.value, err.value) == (11, 0)
+        lib.host_free(host)
+    finally:
+        lib.call("ps_fetcher_destroy", f)
+
+
 @pytest.mark.parametrize("N,K,t,epi", [(512, 4096, 1, 0), (1000, 2048, 2, 1), (640, 14336, 1, 0),
                                        (256, 4096, 8, 2), (300, 512, 4, 0), (4096, 768, 1, 1)])
 def test_gemv_coded_bit_identical(N, K, t, epi):
