@@ -490,6 +490,16 @@ def run_ours(args, rank: int, world: int) -> dict:
     # C-ABI kernel calls (each >= 1 launch of our sm_100a kernels) in the timed passes
     out["gpu_launches"] = int(sum(s.kernel_calls for s in timed_stats))
     out["copies_per_step"] = round(sum(s.copies for s in timed_stats) / max(1, len(timed_stats)), 1)
+    routed = sum(s.spec_routed for s in timed_stats)
+    if routed:   # speculative (pre-gated) expert prefetch, MoE one-token passes
+        out["moe_prefetch"] = {
+            "predicted_per_layer": eng.executor._spec_n(B),
+            "routed_with_prediction": routed,
+            "hits": int(sum(s.spec_hits for s in timed_stats)),
+            "hit_frac_of_routed": round(sum(s.spec_hits for s in timed_stats) / routed, 4),
+            "note": "the next layer's router applied to this layer's post-attention state picks "
+                    "experts copied behind this layer's; hits skip their copy, misses are wasted "
+                    "link bytes (counted in algorithmic_bytes_per_step); PS_MOE_SPEC=0: off"}
     out["prefill_passes"] = [{"tier": p[0], "tokens": p[1], "ms": round(p[2] * 1e3, 2),
                               "streamed_gb": round(p[3] / GB, 3), "zero_copy_gb": round(p[4] / GB, 3)}
                              for p in res.passes if p[1] != B][:4]
