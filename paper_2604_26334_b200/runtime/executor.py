@@ -388,6 +388,17 @@ class Executor:
             return self._hx_expand_bytes()
         return max(64 << 10, min(self.chunk_cap, int(self.arena.capacity) // 64)) // 256 * 256
 
+    def _hx_prefill_experts(self, sid: int) -> bool:
+        """GEMM passes stream this MoE group's experts hx-coded and expand them in VRAM
+        (PS_HX_PREFILL_EXPERTS=0: bf16). Needs the expansion buffer to hold one expert."""
+        if not (getattr(self, "_hx_on", False) and self.expand and os.environ.get("PS_HX_PREFILL_EXPERTS", "1") != "0"):
+            return False
+        hxg = getattr(self.hx, "experts", {}).get(sid)
+        if hxg is None:
+            return False
+        layer = self.shards[sid].layer_index
+        return self._expand_bytes() >= self._expert_geometry(sid, layer)[1] and self.ring.capacity >= hxg["stride"]
+
     def _coded_prefill(self) -> bool:
         """GEMM (prefill) passes stream coded pieces and expand them in VRAM (PS_CODED_PREFILL)."""
         return getattr(self, "coded", None) is not None and (
@@ -1415,6 +1426,42 @@ class Executor:
                 touched = min(E, P)
                 self._stat.zero_copy_bytes += e0.offset + touched * stride
                 self._gapfill_step()
+        elif self._hx_prefill_experts(sid):
+            # GEMM pass over a streamed group, hx-coded (~0.65 x the bf16 bytes): the bf16
+            # prefix (ffn_norm + router) first, then pieces of whole hx expert spans; each
+            # piece is expanded a few experts at a time into the expansion buffer (blob
+            # layout) and the expert kernels run on those experts, bit-identical to bf16
+            hxg = self.hx.experts[sid]
+            host, hs = self.w.shard_ptr(sid), hxg["stride"]
+            region, pdev, arrived = self.ring.upload(host, e0.offset, f"moe{sid} prefix")
+            self._stat.bytes_streamed += e0.offset
+            self._stat.copies += 1
+            self._wait(arrived)
+            self._traced(f"L{layer}.router+topk", route, pdev)
+            self.ring.seal(region, [self._record(self.cs)])
+            hx_base = self.hx.shard_ptr(sid)
+            lut_gu = self.hx_lut + self.hx.lut_off[(sid, "wgu")]
+            lut_dn = self.hx_lut + self.hx.lut_off[(sid, "wdown")]
+            per_piece = max(1, self.chunk // hs)
+            per_run = max(1, self._expand_bytes() // stride)
+
+            def expand_run(sp, a, b):
+                L.call("ps_hx_expand_experts2", sp, hs, None, b - a,
+                       0, hxg["gu_off"], hxg["gu_rows"], hxg["gu_k"], lut_gu, 0,
+                       hxg["nb_gu"], hxg["dn_off"], hxg["dn_rows"], hxg["dn_k"], lut_dn, down_off,
+                       self.expand, stride, self.cs)
+                experts(self.expand - a * stride, a, b)    # expert e at expand + (e - a) * stride
+
+            for lo in range(0, E, per_piece):
+                hi = min(E, lo + per_piece)
+                region, pdev, arrived = self.ring.upload(hx_base + lo * hs, (hi - lo) * hs, f"moe{sid}hx@{lo}")
+                self._stat.bytes_streamed += (hi - lo) * hs
+                self._stat.copies += 1
+                self._wait(arrived)
+                for a in range(lo, hi, per_run):
+                    b = min(hi, a + per_run)
+                    self._traced(f"L{layer}.experts[{a}:{b})", expand_run, pdev + (a - lo) * hs, a, b)
+                self.ring.seal(region, [self._record(self.cs)])
         else:
             host = self.w.shard_ptr(sid)
             per_piece = max(1, (self.chunk - e0.offset) // stride)

@@ -864,6 +864,30 @@ def test_moe_speculative_prefetch_same_tokens(monkeypatch):
     assert engaged, "no budget gave a pass with a prediction set"
 
 
+def test_moe_prefill_hx_experts_same_tokens(monkeypatch):
+    """GEMM (prefill) passes stream MoE expert groups hx-coded (prefix bf16, then whole hx
+    expert spans expanded a few experts at a time into the expansion buffer): same tokens
+    and logits as bf16 groups (PS_HX_PREFILL_EXPERTS=0), fewer prefill link bytes."""
+    import dataclasses
+    from paper_2604_26334_b200.planning.graph import MoeSpec
+    from paper_2604_26334_b200.runtime.engine import Engine
+    base = catalog.builtin_model("tiny-moe")
+    spec = dataclasses.replace(base, n_layers=4, moe=MoeSpec(64, base.moe.top_k, 256))
+    prompt = _prompt(96, spec.vocab_size, seed=23)
+    out = {}
+    for he in ("0", "1"):
+        monkeypatch.setenv("PS_HX_PREFILL_EXPERTS", he)
+        eng = Engine(spec, budget_bytes=0.5 * total_model_bytes(spec), context_len=160)
+        res = eng.generate([prompt], gen_len=8)
+        pre = [p for p in res.passes if p[1] > 32]
+        out[he] = (res.tokens[0].tolist(), eng.logits().copy(), sum(p[3] for p in pre))
+        eng.close()
+    print({he: o[2] for he, o in out.items()})
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert 0 < out["1"][2] < 0.8 * out["0"][2]
+
+
 @pytest.mark.parametrize("frac", [0.5, 0.45])
 def test_early_head_same_tokens(monkeypatch, frac):
     """One-token passes whose output head is CPU-placed read it early: the head GEMV runs
