@@ -1867,6 +1867,8 @@ class Executor:
         by what the fetcher copied (misses + predictions), for every job the fetcher has
         processed (all of them after a synchronize). Also called at each pass start, so the
         fetcher's per-seq record (a ring of 65536 seqs) is read long before it wraps."""
+        if self.fetcher is None or not self._unsettled:
+            return
         keep = []
         for st in self._unsettled:
             rest = []
