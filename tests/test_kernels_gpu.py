@@ -129,6 +129,26 @@ def test_rmsnorm_rows_and_bf16():
     assert rel_err(o16.float(), ref5) < 8e-3
 
 
+@pytest.mark.parametrize("n,d,ldx,gather", [(300, 4096, 4096, False), (257, 5120, 5128, True), (64, 8192, 8192, False),
+                                             (100, 2048, 2048, True)])
+def test_rmsnorm_bf16_many_rows(n, d, ldx, gather):
+    """GEMM-pass RMSNorm to bf16 (>= 64 rows: the vectorised kernel): within bf16 rounding
+    of the fp32 reference, every element; the row-gather form too."""
+    lib = L()
+    x = torch.randn(n, ldx, device="cuda")
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).to(torch.bfloat16)
+    rows = torch.randperm(n, device="cuda").to(torch.int32) if gather else None
+    o16 = torch.zeros(n, d + 8, device="cuda", dtype=torch.bfloat16)
+    lib.call("ps_rmsnorm", x.data_ptr(), ldx, rows.data_ptr() if gather else 0, n, w.data_ptr(), d, 1e-5,
+             o16.data_ptr(), d + 8, 1, stream())
+    xs = (x[rows.long()] if gather else x)[:, :d]
+    ref = xs * torch.rsqrt(xs.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    torch.cuda.synchronize()
+    got = o16[:, :d].float()
+    assert torch.all((got - ref).abs() <= ref.abs() * 2 ** -8 + 1e-6)
+    assert torch.all(o16[:, d:] == 0)
+
+
 def _rope_ref(x, pos, inv):
     hd = x.shape[-1]
     ang = pos.double()[:, None] * inv[None, :].double()
