@@ -126,3 +126,33 @@ def test_library_loads_and_exports_every_symbol():
     for name in L.EXPORTED:
         assert hasattr(lib, name), name
     assert lib.ps_abi_version() == 1
+
+
+def test_speculative_fetch_settlement(monkeypatch):
+    """Executor.settle (host bookkeeping of speculative expert prefetch, no GPU): a pass's
+    link bytes become what the fetcher copied (misses + predictions) once its job is
+    processed; routed experts that were not copied count as prefetch hits; jobs the
+    fetcher has not processed yet (-1) stay pending."""
+    from paper_2604_26334_b200.runtime import executor as X
+    copied = {10: 8 * 100, 11: 6 * 100 + 2 * 90, 12: -1}   # seq -> bytes (-1: not processed)
+
+    def fake_call(name, *args):
+        assert name == "ps_fetcher_seq_bytes"
+        args[2]._obj.value = copied[args[1]]
+        return 0
+    monkeypatch.setattr(X.L, "call", fake_call)
+    ex = X.Executor.__new__(X.Executor)
+    ex.fetcher = 1
+    st = X.PassStats(tier=1, T=1, bytes_streamed=3 * 800)
+    # (seq, bytes counted at enqueue, expert bytes, prediction bytes, routed experts with a set)
+    st.fetch_seqs = [(10, 800, 100, 0, 0), (11, 800, 100, 2 * 90, 8), (12, 800, 100, 2 * 90, 8)]
+    ex._unsettled = [st]
+    ex.settle()
+    assert st.bytes_streamed == 3 * 800 + (800 - 800) + (780 - 800)
+    assert (st.spec_routed, st.spec_hits) == (8, 2)
+    assert st.fetch_seqs == [(12, 800, 100, 180, 8)] and ex._unsettled == [st]
+    copied[12] = 5 * 100 + 2 * 90
+    ex.settle()
+    assert st.bytes_streamed == 3 * 800 - 20 - 120
+    assert (st.spec_routed, st.spec_hits) == (16, 5)
+    assert not st.fetch_seqs and ex._unsettled == []
