@@ -499,8 +499,8 @@ class Executor:
         """Experts predicted per fetched MoE layer for the next one (speculative pre-gated
         prefetch, csrc/fetcher.cu; PS_MOE_SPEC, default 2, 0: off): one-token passes that
         fetch hx-coded experts. The next layer's router applied to this layer's
-        post-attention state picks ~78 % of its top-2 among the next layer's top-8 on
-        Qwen3-30B-A3B shapes (scratch measurement)."""
+        post-attention state names one of the next layer's routed experts with ~90 % of
+        its top-2 picks on config 3 (bench `moe_prefetch`; sweep in DESIGN.md §5b)."""
         if self.moe is None or not self._hx_experts_on(T):
             return 0
         return max(0, min(int(os.environ.get("PS_MOE_SPEC", "2")), self.moe.top_k, 64))
