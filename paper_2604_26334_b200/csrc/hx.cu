@@ -185,7 +185,13 @@ __device__ __forceinline__ void hx_load_lut(const uint32_t* __restrict__ lut_g, 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
+// Minimum resident CTAs per SM the expansion kernels are compiled for (build-time
+// experiment knob: -DPS_HX_MIN_CTAS=6 trades ~20 spilled bytes for a sixth CTA per SM).
+#ifndef PS_HX_MIN_CTAS
+#define PS_HX_MIN_CTAS 1
+#endif
+
+__global__ void __launch_bounds__(32 * HX_EXP_WARPS, PS_HX_MIN_CTAS)
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
                  const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
   __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | bits << 16 | n << 24
@@ -298,7 +304,7 @@ struct HxExpertMat {
   long long out_off;
 };
 
-__global__ void __launch_bounds__(32 * HX_EXP_WARPS)
+__global__ void __launch_bounds__(32 * HX_EXP_WARPS, PS_HX_MIN_CTAS)
 hx_expand_experts2_kernel(const uint8_t* __restrict__ slots, long long slot_stride, const int* __restrict__ slot_of_rank,
                           int k, HxExpertMat a, HxExpertMat b, int grid_a, uint8_t* __restrict__ scratch,
                           long long scratch_stride) {
@@ -353,6 +359,9 @@ extern "C" int ps_hx_expand(const void* piece, const unsigned* block_off, int ro
   static bool smem_set = false;
   if (!smem_set) {
     PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (PS_HX_MIN_CTAS > 5)
+      PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared));
     smem_set = true;
   }
   const int grid = min(nblocks * parts, hx_grid_cap());
@@ -390,6 +399,9 @@ extern "C" int ps_hx_expand_experts2(const void* slots, long long slot_stride, c
   static bool smem_set = false;
   if (!smem_set) {
     PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_experts2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (PS_HX_MIN_CTAS > 5)
+      PS_CHECK_CUDA(cudaFuncSetAttribute(hx_expand_experts2_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared));
     smem_set = true;
   }
   const HxExpertMat a{hdr_a, mat_a, rows_a, K_a, static_cast<const uint32_t*>(lut_a), out_a};
