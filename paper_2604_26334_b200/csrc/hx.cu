@@ -187,11 +187,18 @@ __device__ __forceinline__ void hx_load_lut(const uint32_t* __restrict__ lut_g, 
 
 // Minimum resident CTAs per SM the expansion kernels are compiled for (build-time
 // experiment knob: -DPS_HX_MIN_CTAS=6 trades ~20 spilled bytes for a sixth CTA per SM).
+// (Default: the one-argument bound. `__launch_bounds__(128, 1)` is not equivalent in
+// practice: ptxas then takes 128 / 141 registers instead of 94 / 128.)
 #ifndef PS_HX_MIN_CTAS
 #define PS_HX_MIN_CTAS 1
 #endif
+#if PS_HX_MIN_CTAS > 1
+#define PS_HX_BOUNDS __launch_bounds__(32 * HX_EXP_WARPS, PS_HX_MIN_CTAS)
+#else
+#define PS_HX_BOUNDS __launch_bounds__(32 * HX_EXP_WARPS)
+#endif
 
-__global__ void __launch_bounds__(32 * HX_EXP_WARPS, PS_HX_MIN_CTAS)
+__global__ void PS_HX_BOUNDS
 hx_expand_kernel(const uint8_t* __restrict__ piece, const uint32_t* __restrict__ blk, int rows, int K,
                  const uint32_t* __restrict__ lut_g, __nv_bfloat16* __restrict__ out, long long ld_out) {
   __shared__ uint32_t lut[HX_LUT];   // s1 | s2 << 8 | bits << 16 | n << 24
@@ -304,7 +311,7 @@ struct HxExpertMat {
   long long out_off;
 };
 
-__global__ void __launch_bounds__(32 * HX_EXP_WARPS, PS_HX_MIN_CTAS)
+__global__ void PS_HX_BOUNDS
 hx_expand_experts2_kernel(const uint8_t* __restrict__ slots, long long slot_stride, const int* __restrict__ slot_of_rank,
                           int k, HxExpertMat a, HxExpertMat b, int grid_a, uint8_t* __restrict__ scratch,
                           long long scratch_stride) {
