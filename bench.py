@@ -497,13 +497,26 @@ def run_ours(args, rank: int, world: int) -> dict:
             "routed_with_prediction": routed,
             "hits": int(sum(s.spec_hits for s in timed_stats)),
             "hit_frac_of_routed": round(sum(s.spec_hits for s in timed_stats) / routed, 4),
+            "predicted": int(sum(s.spec_predicted for s in timed_stats)),
+            # predictions no later layer used: moved (inside algorithmic_bytes_per_step) but wasted
+            "mispredicted_bytes_per_step": int(max(0, sum(s.spec_predicted for s in timed_stats) -
+                                                   sum(s.spec_hits for s in timed_stats)) *
+                                               sum(s.spec_pred_bytes for s in timed_stats) /
+                                               max(1, sum(s.spec_predicted for s in timed_stats)) /
+                                               max(1, len(timed_stats))),
+            "useful_link_frac": None,
             "note": "the next layer's router applied to this layer's post-attention state picks "
-                    "experts copied behind this layer's; hits skip their copy, misses are wasted "
-                    "link bytes (counted in algorithmic_bytes_per_step); PS_MOE_SPEC=0: off"}
+                    "experts copied behind this layer's; hits skip their copy, wrong predictions are "
+                    "wasted link bytes (counted in algorithmic_bytes_per_step, excluded from "
+                    "useful_link_frac); PS_MOE_SPEC=0: off"}
     out["prefill_passes"] = [{"tier": p[0], "tokens": p[1], "ms": round(p[2] * 1e3, 2),
                               "streamed_gb": round(p[3] / GB, 3), "zero_copy_gb": round(p[4] / GB, 3)}
                              for p in res.passes if p[1] != B][:4]
     out["roofline"]["zero_copy_bytes_per_step"] = int(zero_copy)
+    if "moe_prefetch" in out and out["roofline"].get("algorithmic_bytes_per_step"):
+        mp, rl = out["moe_prefetch"], out["roofline"]
+        mp["useful_link_frac"] = round(rl["frac"] * (1 - mp["mispredicted_bytes_per_step"] /
+                                                     rl["algorithmic_bytes_per_step"]), 4)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(eng, args.cpu_sample_steps)

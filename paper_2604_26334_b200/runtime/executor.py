@@ -143,6 +143,8 @@ class PassStats:
     fetch_seqs: list = field(default_factory=list)   # (seq, bytes counted) until settled
     spec_hits: int = 0           # routed experts found prefetched (settled with the bytes)
     spec_routed: int = 0         # routed experts of the layers that had a prediction set
+    spec_predicted: int = 0      # experts copied as predictions for a next layer
+    spec_pred_bytes: int = 0     # their bytes
 
 
 @dataclass
@@ -1409,7 +1411,7 @@ class Executor:
             if spec_n:   # the fetcher decides what crosses the link: settled after the pass
                 self._stat.fetch_seqs.append((seq, min(E, P) * ebytes, ebytes,
                                               spec_n * nxt_hx["stride"] if set_next >= 0 else 0,
-                                              min(E, P) if set_cur >= 0 else 0))
+                                              min(E, P) if set_cur >= 0 else 0, spec_n if set_next >= 0 else 0))
             if not t1:
                 L.call("ps_moe_combine", self.m_out, self.m_plan, E, P, self.m_w, T, k, d, self.x, d, self.cs)
             return
@@ -1872,13 +1874,16 @@ class Executor:
         keep = []
         for st in self._unsettled:
             rest = []
-            for seq, counted, ebytes, pred_bytes, routed in st.fetch_seqs:
+            for job in st.fetch_seqs:
+                seq, counted, ebytes, pred_bytes, routed, npred = job
                 got = C.c_longlong(-1)
                 L.call("ps_fetcher_seq_bytes", self.fetcher, seq, C.byref(got))
                 if got.value < 0:
-                    rest.append((seq, counted, ebytes, pred_bytes, routed))
+                    rest.append(job)
                     continue
                 st.bytes_streamed += got.value - counted
+                st.spec_predicted += npred
+                st.spec_pred_bytes += pred_bytes
                 misses = (got.value - pred_bytes) // max(1, ebytes)
                 if routed:   # the routed experts that were not copied were prefetched hits
                     st.spec_routed += routed

@@ -144,15 +144,18 @@ def test_speculative_fetch_settlement(monkeypatch):
     ex = X.Executor.__new__(X.Executor)
     ex.fetcher = 1
     st = X.PassStats(tier=1, T=1, bytes_streamed=3 * 800)
-    # (seq, bytes counted at enqueue, expert bytes, prediction bytes, routed experts with a set)
-    st.fetch_seqs = [(10, 800, 100, 0, 0), (11, 800, 100, 2 * 90, 8), (12, 800, 100, 2 * 90, 8)]
+    # (seq, bytes counted at enqueue, expert bytes, prediction bytes, routed experts with a
+    # prediction set, predictions made)
+    st.fetch_seqs = [(10, 800, 100, 0, 0, 0), (11, 800, 100, 2 * 90, 8, 2), (12, 800, 100, 2 * 90, 8, 2)]
     ex._unsettled = [st]
     ex.settle()
     assert st.bytes_streamed == 3 * 800 + (800 - 800) + (780 - 800)
     assert (st.spec_routed, st.spec_hits) == (8, 2)
-    assert st.fetch_seqs == [(12, 800, 100, 180, 8)] and ex._unsettled == [st]
+    assert st.fetch_seqs == [(12, 800, 100, 180, 8, 2)] and ex._unsettled == [st]
+    assert (st.spec_predicted, st.spec_pred_bytes) == (2, 180)
     copied[12] = 5 * 100 + 2 * 90
     ex.settle()
     assert st.bytes_streamed == 3 * 800 - 20 - 120
     assert (st.spec_routed, st.spec_hits) == (16, 5)
+    assert (st.spec_predicted, st.spec_pred_bytes) == (4, 360)
     assert not st.fetch_seqs and ex._unsettled == []
