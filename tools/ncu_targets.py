@@ -5,7 +5,7 @@ targets: gemv_bf16 | gemv_coded (28672 x 4096, t = 1, SwiGLU: the bench's kernel
 matrix), gemv_tc_bf16 | gemv_tc_coded (same matrix, t = 32), moe_coded (Qwen3-30B-A3B
 one-token experts, k = 8, coded), attn_tc (Llama-3.3-70B 4096-token causal prefill over a
 paged cache), expand (8192 x 4096 coded piece -> bf16), hx_expand (one 32 MB run of the
-235 MB matrix, Huffman-coded -> bf16)."""
+235 MB matrix, Huffman-coded -> bf16), rmsnorm_vec (16384 x 4096 GEMM-pass RMSNorm to bf16)."""
 import ctypes
 import math
 import os
@@ -113,6 +113,13 @@ elif target == "attn_tc":
         L.call("ps_attn_prefill_tc", q.data_ptr(), (h + 2 * kv) * hd, 1, qs.data_ptr(), p0.data_ptr(), 0, n, h, kv,
                hd, pool.data_ptr(), 2 * kv * hd, perm.data_ptr(), pps, 64, pps, 1 / math.sqrt(hd), out.data_ptr(),
                h * hd, 1, s)
+elif target == "rmsnorm_vec":   # the config-4 prefill shape: 16384 rows x 4096, fp32 -> bf16
+    n, d = 16384, 4096
+    x = torch.randn(n, d, device="cuda")
+    w = torch.ones(d, device="cuda").to(torch.bfloat16)
+    o = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    for _ in range(reps):
+        L.call("ps_rmsnorm", x.data_ptr(), d, None, n, w.data_ptr(), d, 1e-5, o.data_ptr(), d, 1, s)
 else:
     raise SystemExit(f"unknown target {target}")
 torch.cuda.synchronize()
